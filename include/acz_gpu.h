@@ -1,0 +1,192 @@
+/*
+ * acz_gpu.h -- C-ABI of the B200-native activation compressor (arXiv 2011.09017).
+ *
+ * This is the drop-in boundary under the reference's codec API. Every entry point takes
+ * plain pointers and sizes (no C++ or torch types) and returns an int status; the C++
+ * host layer (paper_2011_09017_b200/cpp/acz_b200.hpp) rethrows the matching acz::Error
+ * subclass, so callers such as Controller::wrap_forward / unwrap_backward
+ * (ref proj/core/src/controller.cpp:194-249) keep their behaviour.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj/core):
+ *   acz_gpu_compress          <- CompressedTensor compress(const Tensor&, const CodecParams&)
+ *                                include/acz/codec.hpp:54, src/codec.cpp:61-120
+ *   acz_gpu_decompress        <- Tensor decompress(const CompressedTensor&, bool zero_filter)
+ *                                include/acz/codec.hpp:59, src/codec.cpp:122-171
+ *   acz_gpu_blob_info         <- CompressedTensor::{shape, params, compressed_bytes, ...},
+ *                                compression_ratio()  include/acz/codec.hpp:32-47,61
+ *   acz_gpu_blob_to_host      <- std::vector<uint8_t> blob_to_bytes(const CompressedTensor&)
+ *                                include/acz/codec.hpp:69, src/codec.cpp:177-199
+ *   acz_gpu_blob_from_host    <- CompressedTensor blob_from_bytes(const uint8_t*, size_t)
+ *                                include/acz/codec.hpp:70, src/codec.cpp:201-262
+ *   acz_gpu_nonzero_ratio     <- double nonzero_ratio(const Tensor&)  include/acz/tensor.hpp:91-99
+ *   acz_gpu_mean_abs          <- double mean_abs(const Tensor&)       include/acz/tensor.hpp:82-89
+ *   acz_gpu_zero_bitmap       <- (north_star "fused ReLU zero-bitmap and sparsity pass";
+ *                                the predicate is nonzero_ratio's v != 0)
+ *   acz_gpu_huffman_encode    <- HuffmanCode huffman_encode(const std::vector<uint32_t>&)
+ *                                include/acz/huffman.hpp:26, src/huffman.cpp:107-135
+ *   acz_gpu_huffman_decode    <- std::vector<uint32_t> huffman_decode(...)
+ *                                include/acz/huffman.hpp:30-32, src/huffman.cpp:137-189
+ *   acz_gpu_compress_host / acz_gpu_decompress_host
+ *                             <- compress/decompress on host tensors (the reference's own
+ *                                calling convention, host buffers in and out)
+ *
+ * Status codes map one-to-one onto the reference exception hierarchy
+ * (include/acz/error.hpp:9-53). No exception ever crosses this boundary.
+ *
+ * Threading: one context per (device, caller thread); calls on one context are not
+ * reentrant; distinct contexts are independent (ref SPEC.md:157-158). All work is
+ * stream-ordered on the caller's cudaStream_t (passed as void*; NULL = legacy default).
+ *
+ * Data layout: tensors are dense row-major fp32 in device memory; the codec scans the
+ * trailing two dimensions as planes (ref src/codec.cpp:17-34). A device blob owns its
+ * device buffers: canonical codebook, MSB-first Huffman bitstream (byte-identical to the
+ * ACZ1 bitstream section), outlier (index, value) arrays and a decode sidecar (bit offset,
+ * outlier prefix and chain state every `interval` symbols) that makes decompression
+ * chunk-parallel. The sidecar is NOT part of ACZ1; compressed_bytes is the ACZ1 size.
+ */
+#ifndef ACZ_GPU_H
+#define ACZ_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (one per acz::Error subclass, include/acz/error.hpp) ---- */
+#define ACZ_OK 0
+#define ACZ_ERR_PARAM 1    /* acz::ParamError  : eb <= 0 / non-finite, bad quant_radius  */
+#define ACZ_ERR_DOMAIN 2   /* acz::DomainError : empty tensor, non-finite element         */
+#define ACZ_ERR_FORMAT 3   /* acz::FormatError : codebook > 65535, malformed blob         */
+#define ACZ_ERR_DECODE 4   /* acz::DecodeError : code length > 64, truncated bitstream    */
+#define ACZ_ERR_SHAPE 5    /* acz::ShapeError  : zero extent, size mismatch               */
+#define ACZ_ERR_CUDA 6     /* CUDA runtime failure (no reference counterpart)             */
+#define ACZ_ERR_NOMEM 7    /* allocation failure                                          */
+#define ACZ_ERR_INVALID 8  /* bad handle / null pointer (programming error)               */
+
+#define ACZ_PRED_PREV 0     /* Predictor::PrevValue  (include/acz/codec.hpp:13) */
+#define ACZ_PRED_LORENZO2D 1 /* Predictor::Lorenzo2d (include/acz/codec.hpp:14) */
+
+#define ACZ_MAX_RANK 16
+
+typedef struct acz_gpu_ctx acz_gpu_ctx;
+typedef struct acz_gpu_blob acz_gpu_blob;
+
+/* Host-visible description of a device blob (mirrors CompressedTensor's scalar fields). */
+typedef struct {
+    uint32_t rank;
+    uint64_t shape[ACZ_MAX_RANK];
+    double eb;
+    uint32_t quant_radius;
+    uint32_t predictor;
+    uint64_t element_count;
+    uint32_t codebook_size;
+    uint64_t bit_length;
+    uint64_t outlier_count;
+    uint64_t uncompressed_bytes; /* 4 * element_count                              */
+    uint64_t compressed_bytes;   /* exact ACZ1 serialisation size (blob_to_bytes)   */
+    uint64_t device_bytes;       /* device memory held by the blob incl. sidecar    */
+    uint64_t sidecar_bytes;      /* size of the serialised sidecar (acz_gpu_sidecar_to_host) */
+    uint32_t max_code_length;
+} acz_gpu_blob_info_t;
+
+/* ---- context ---- */
+int acz_gpu_ctx_create(int device, acz_gpu_ctx** ctx);
+int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx);
+/* Message of the last failing call on this context ("" if none). */
+const char* acz_gpu_last_error(const acz_gpu_ctx* ctx);
+/* Library version string. */
+const char* acz_gpu_version(void);
+
+/* ---- codec (device buffers) ---- */
+/* Compress a dense fp32 tensor resident in device memory. Synchronises the stream once
+ * (to size the blob). On success *out owns a device blob; free with acz_gpu_blob_free. */
+int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape, uint32_t rank,
+                     double eb, uint32_t quant_radius, uint32_t predictor, void* stream,
+                     acz_gpu_blob** out);
+/* Decompress into d_out (element_count floats). zero_filter: |v| <= eb -> 0 on output
+ * (ref src/codec.cpp:162-164). Stream-ordered, no host synchronisation. */
+int acz_gpu_decompress(acz_gpu_ctx* ctx, const acz_gpu_blob* blob, int zero_filter, float* d_out,
+                       void* stream);
+int acz_gpu_blob_info(const acz_gpu_blob* blob, acz_gpu_blob_info_t* info);
+int acz_gpu_blob_free(acz_gpu_blob* blob);
+
+/* ACZ1 serialisation (bit-exact with ref blob_to_bytes). dst must hold compressed_bytes.
+ * Synchronises the stream. */
+int acz_gpu_blob_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* blob, uint8_t* dst, uint64_t cap,
+                         uint64_t* written, void* stream);
+/* Parse + validate ACZ1 bytes (ref blob_from_bytes checks) into a device blob. When a
+ * sidecar produced by acz_gpu_sidecar_to_host for the same blob is supplied, decode is
+ * chunk-parallel immediately; otherwise the sidecar is rebuilt on the GPU. */
+int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
+                           const uint8_t* sidecar, uint64_t sidecar_size, void* stream,
+                           acz_gpu_blob** out);
+/* Serialise the decode sidecar ("ACZS": interval, per-chunk bit offset, outlier prefix,
+ * chain state). dst must hold info.sidecar_bytes. Synchronises the stream. */
+int acz_gpu_sidecar_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* blob, uint8_t* dst,
+                            uint64_t cap, uint64_t* written, void* stream);
+
+/* ---- codec (host buffers): the reference's own calling convention ---- */
+/* compress(host tensor) -> ACZ1 bytes (+ optional sidecar). *acz1 / *sidecar are
+ * malloc'd; free with acz_gpu_host_free. */
+int acz_gpu_compress_host(acz_gpu_ctx* ctx, const float* h_in, const uint64_t* shape,
+                          uint32_t rank, double eb, uint32_t quant_radius, uint32_t predictor,
+                          uint8_t** acz1, uint64_t* acz1_size, uint8_t** sidecar,
+                          uint64_t* sidecar_size);
+/* decompress(ACZ1 bytes [+ sidecar]) -> host tensor of n floats. */
+int acz_gpu_decompress_host(acz_gpu_ctx* ctx, const uint8_t* acz1, uint64_t acz1_size,
+                            const uint8_t* sidecar, uint64_t sidecar_size, int zero_filter,
+                            float* h_out, uint64_t n);
+void acz_gpu_host_free(void* p);
+
+/* ---- sparsity / statistics (controller inputs, ref src/controller.cpp:133-135) ---- */
+/* Fused pass: bitmap bit (i%32) of word i/32 = (x[i] != 0); *nonzero = count; returns
+ * ACZ_ERR_DOMAIN if any element is non-finite. d_bitmap may be NULL (count only). */
+int acz_gpu_zero_bitmap(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, uint32_t* d_bitmap,
+                        uint64_t* nonzero, void* stream);
+int acz_gpu_nonzero_ratio(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void* stream,
+                          double* ratio);
+/* Sum of |x| in double (parallel order: equal to the reference's sequential sum within
+ * 1e-12 relative, not bit-exact). */
+int acz_gpu_mean_abs(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void* stream,
+                     double* mean);
+
+/* ---- Huffman coder on arbitrary u32 symbol streams (ref include/acz/huffman.hpp) ---- */
+/* Encodes n device symbols; writes the canonical book (host arrays, capacity book_cap)
+ * and the MSB-first bitstream (host, capacity bits_cap bytes). */
+int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t n,
+                           uint32_t* book_sym, uint8_t* book_len, uint32_t book_cap,
+                           uint32_t* book_size, uint8_t* bits, uint64_t bits_cap,
+                           uint64_t* bit_length, void* stream);
+/* Decodes count symbols of a host (book, bitstream) into d_out (device). */
+int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uint8_t* book_len,
+                           uint32_t book_size, const uint8_t* bits, uint64_t bit_length,
+                           uint64_t count, uint32_t* d_out, void* stream);
+
+/* ---- profiling ---- */
+/* Kernel classes timed by acz_gpu_profile_* (CUDA events on the launching stream). */
+#define ACZ_K_STATS 0     /* K1 zero bitmap / sparsity                     */
+#define ACZ_K_QUANT 1     /* K2 quantiser                                  */
+#define ACZ_K_HIST 2      /* K3 histogram                                  */
+#define ACZ_K_BOOK 3      /* K4 codebook                                   */
+#define ACZ_K_ENCODE 4    /* K5 encode                                     */
+#define ACZ_K_DECODE 5    /* K6+K7 decode / reconstruct                    */
+#define ACZ_K_SCAN 6      /* sequential sidecar rebuild (foreign blobs)    */
+#define ACZ_K_COUNT 7
+/* Enable (1) / disable (0) per-launch event timing; enabling resets the accumulators. */
+int acz_gpu_profile_enable(acz_gpu_ctx* ctx, int on);
+/* Synchronises pending events; writes ACZ_K_COUNT accumulated milliseconds and launch
+ * counts. */
+int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches);
+
+/* ---- parity / debug ---- */
+/* Copy the quantisation symbols of the last compress on this context (device, n u32). */
+int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, void* stream);
+/* Number of CUDA kernel launches issued by this context since creation. */
+uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACZ_GPU_H */

@@ -1,0 +1,14 @@
+"""B200-native activation compressor (arXiv 2011.09017, "acz"): the reference's SZ-style
+error-bounded codec for fp32 activations re-built as hand-written sm_100a CUDA kernels
+behind a C-ABI (include/acz_gpu.h). See DESIGN.md.
+
+Python surface mirrors ref proj/core/include/acz/codec.hpp (see codec.py).
+"""
+from .codec import (CodebookEntry, CodecParams, CompressedTensor, Context, CudaError,
+                    DecodeError, DomainError, Error, FormatError, HuffmanCode, Outlier,
+                    ParamError, Predictor, ShapeError, blob_from_bytes, blob_to_bytes, compress,
+                    compress_host, compression_ratio, debug_last_symbols, decompress,
+                    decompress_host, default_context, huffman_decode, huffman_encode, mean_abs,
+                    nonzero_ratio, parse_acz1, zero_bitmap)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

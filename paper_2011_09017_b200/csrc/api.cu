@@ -1,0 +1,1180 @@
+// C-ABI implementation (include/acz_gpu.h): host orchestration of the device codec.
+//
+// compress  (ref src/codec.cpp:61-120):  K2 quant -> K3 histogram -> K4 codebook ->
+//            [one stream sync: book size, total bits, outlier count, error flags] ->
+//            blob allocation -> K5 encode (bitstream + outliers + decode sidecar).
+// decompress (ref src/codec.cpp:122-171): K6+K7 fused chunk-parallel decode/reconstruct.
+// ACZ1 (ref src/codec.cpp:177-262): header assembled on the host, bitstream copied
+//            device->host straight into place (device bytes already are ACZ1 order).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace acz_b200;
+
+// ------------------------------------------------------------------------- structs --
+struct acz_gpu_ctx {
+    int device = 0;
+    int sms = 148;
+    std::string err;
+    uint64_t launches = 0;
+    cudaStream_t own = nullptr;  // stream used by the host-buffer entry points
+    // workspace (grown on demand)
+    void* ws_sym = nullptr;
+    size_t ws_sym_cap = 0;
+    void* ws_hist = nullptr;
+    size_t ws_hist_cap = 0;
+    void* ws_enc = nullptr;
+    size_t ws_enc_cap = 0;
+    void* ws_cb = nullptr;
+    size_t ws_cb_cap = 0;
+    void* ws_status = nullptr;
+    size_t ws_status_cap = 0;
+    void* ws_row = nullptr;
+    size_t ws_row_cap = 0;
+    void* ws_io = nullptr;  // host-API staging (input / output floats)
+    size_t ws_io_cap = 0;
+    void* ws_aux = nullptr;  // sequential-decode scratch (symbols, plane prefixes)
+    size_t ws_aux_cap = 0;
+    void* ws_book = nullptr;  // codebook output (sym u32 + len u8) before the blob exists
+    size_t ws_book_cap = 0;
+    void* ws_side = nullptr;  // sidecar chain states produced by K2
+    size_t ws_side_cap = 0;
+    // small fixed device block
+    struct Small {
+        BookInfo info;
+        unsigned int flags;
+        unsigned int ticket;
+        unsigned long long nnz;
+        double sumabs;
+        unsigned int maxsym;
+        unsigned int pad;
+        CanonTables canon;
+        uint32_t lut[kLutSize];
+    };
+    Small* d_small = nullptr;
+    Small* h_small = nullptr;  // pinned mirror
+    uint64_t last_n = 0;
+    // profiling: events recorded around every launch when enabled
+    bool prof = false;
+    struct Pending {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double prof_ms[ACZ_K_COUNT] = {0};
+    uint64_t prof_n[ACZ_K_COUNT] = {0};
+};
+
+namespace {
+cudaEvent_t take_event(acz_gpu_ctx* c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+// RAII timer around one kernel launch (no-op unless profiling is on).
+struct KTimer {
+    acz_gpu_ctx* c;
+    int cls;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    KTimer(acz_gpu_ctx* c_, int cls_, cudaStream_t s_) : c(c_), cls(cls_), s(s_) {
+        if (c->prof) {
+            a = take_event(c);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~KTimer() {
+        if (c->prof && a) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, s);
+            c->pending.push_back({cls, a, b});
+        }
+    }
+};
+}  // namespace
+
+struct acz_gpu_blob {
+    acz_gpu_blob_info_t info{};
+    uint64_t interval = 0, nchunks = 0, nwords = 0;
+    uint32_t max_len = 0;
+    // device arena
+    void* arena = nullptr;
+    size_t arena_bytes = 0;
+    uint32_t* book_sym = nullptr;
+    uint8_t* book_len = nullptr;
+    uint32_t* words = nullptr;
+    unsigned long long* out_index = nullptr;
+    float* out_value = nullptr;
+    unsigned long long* side_bitoff = nullptr;
+    uint32_t* side_outl = nullptr;
+    float* side_state = nullptr;
+    uint32_t* lut = nullptr;
+    CanonTables* canon = nullptr;
+    cudaStream_t stream = nullptr;
+    int invalid = 0;  // deferred decompress failure (foreign blobs), ACZ_ERR_*
+    std::string invalid_msg;
+};
+
+namespace acz_b200 {
+PlaneGeom plane_geom(const uint64_t* shape, uint32_t rank) {
+    PlaneGeom g{1, 1, 1, 1, 0};
+    if (rank == 0) {
+        g.n = 0;
+        return g;
+    }
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < rank; ++i) n *= shape[i];
+    g.n = n;
+    if (rank == 1) {
+        g.cols = shape[0];
+    } else {
+        g.rows = shape[rank - 2];
+        g.cols = shape[rank - 1];
+        for (uint32_t i = 0; i + 2 < rank; ++i) g.planes *= shape[i];
+    }
+    g.plane_size = g.rows * g.cols;
+    return g;
+}
+}  // namespace acz_b200
+
+namespace {
+
+const char* kVersion = "acz-b200 0.1 (sm_100a)";
+
+int fail(acz_gpu_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_fail(acz_gpu_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, ACZ_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                   \
+    do {                                                           \
+        cudaError_t _e = (expr);                                   \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);   \
+    } while (0)
+
+cudaError_t grow(void** p, size_t* cap, size_t need) {
+    if (need <= *cap && *p) return cudaSuccess;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    size_t want = std::max<size_t>(need, 256);
+    cudaError_t e = cudaMalloc(p, want);
+    if (e == cudaSuccess) *cap = want;
+    return e;
+}
+
+bool params_ok(double eb, uint32_t radius) {
+    // ref src/codec.cpp:54-59
+    return (eb > 0.0) && std::isfinite(eb) && radius >= 2 && radius <= (1u << 24) &&
+           (radius & (radius - 1)) == 0;
+}
+
+const char* param_msg(double eb) {
+    return (!(eb > 0.0) || !std::isfinite(eb)) ? "error bound must be positive"
+                                               : "quant_radius must be a power of two in [2, 2^24]";
+}
+
+uint64_t sidecar_interval_default() {
+    static uint64_t v = [] {
+        const char* s = std::getenv("ACZ_SIDECAR_INTERVAL");
+        uint64_t x = s ? std::strtoull(s, nullptr, 10) : 0;
+        return x ? x : (uint64_t)256;
+    }();
+    return v;
+}
+
+uint64_t acz1_size(uint32_t rank, uint32_t book, uint64_t bits, uint64_t nout) {
+    // ref src/codec.cpp:177-199
+    return 4 + 1 + 1 + 1 + 8ull * rank + 8 + 4 + 4 + 2 + 5ull * book + 8 + (bits + 7) / 8 +
+           12ull * nout;
+}
+
+size_t al(size_t v) { return (v + 255) & ~size_t(255); }
+
+// Allocates the blob arena for the given sizes and carves the pointers.
+cudaError_t blob_alloc(acz_gpu_blob* b, uint32_t book, uint64_t nwords, uint64_t nout,
+                       uint64_t nchunks, cudaStream_t s) {
+    size_t off = 0;
+    const size_t o_sym = off; off += al(4ull * std::max<uint32_t>(book, 1));
+    const size_t o_len = off; off += al(std::max<uint32_t>(book, 1));
+    const size_t o_words = off; off += al(4ull * (nwords + 4));
+    const size_t o_oidx = off; off += al(8ull * std::max<uint64_t>(nout, 1));
+    const size_t o_oval = off; off += al(4ull * std::max<uint64_t>(nout, 1));
+    const size_t o_sb = off; off += al(8ull * std::max<uint64_t>(nchunks, 1));
+    const size_t o_so = off; off += al(4ull * std::max<uint64_t>(nchunks, 1));
+    const size_t o_ss = off; off += al(4ull * std::max<uint64_t>(nchunks, 1));
+    const size_t o_lut = off; off += al(4ull * kLutSize);
+    const size_t o_canon = off; off += al(sizeof(CanonTables));
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, off, s);
+    if (e != cudaSuccess) return e;
+    char* c = static_cast<char*>(p);
+    b->arena = p;
+    b->arena_bytes = off;
+    b->book_sym = reinterpret_cast<uint32_t*>(c + o_sym);
+    b->book_len = reinterpret_cast<uint8_t*>(c + o_len);
+    b->words = reinterpret_cast<uint32_t*>(c + o_words);
+    b->out_index = reinterpret_cast<unsigned long long*>(c + o_oidx);
+    b->out_value = reinterpret_cast<float*>(c + o_oval);
+    b->side_bitoff = reinterpret_cast<unsigned long long*>(c + o_sb);
+    b->side_outl = reinterpret_cast<uint32_t*>(c + o_so);
+    b->side_state = reinterpret_cast<float*>(c + o_ss);
+    b->lut = reinterpret_cast<uint32_t*>(c + o_lut);
+    b->canon = reinterpret_cast<CanonTables*>(c + o_canon);
+    b->stream = s;
+    return cudaSuccess;
+}
+
+uint64_t sidecar_bytes(uint64_t nchunks) { return 4 + 4 + 8 * 6 + nchunks * (8 + 4 + 4); }
+
+uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h = 1469598103934665603ull) {
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+// Binds a sidecar to its blob: header + codebook + bit length + outlier count.
+uint64_t blob_binding(const acz_gpu_blob_info_t& in) {
+    uint64_t h = fnv1a(reinterpret_cast<const uint8_t*>(&in.rank), sizeof(in.rank));
+    h = fnv1a(reinterpret_cast<const uint8_t*>(in.shape), 8ull * in.rank, h);
+    h = fnv1a(reinterpret_cast<const uint8_t*>(&in.eb), 8, h);
+    h = fnv1a(reinterpret_cast<const uint8_t*>(&in.quant_radius), 4, h);
+    h = fnv1a(reinterpret_cast<const uint8_t*>(&in.predictor), 4, h);
+    h = fnv1a(reinterpret_cast<const uint8_t*>(&in.codebook_size), 4, h);
+    h = fnv1a(reinterpret_cast<const uint8_t*>(&in.bit_length), 8, h);
+    h = fnv1a(reinterpret_cast<const uint8_t*>(&in.outlier_count), 8, h);
+    return h;
+}
+
+int ensure_small(acz_gpu_ctx* ctx) {
+    if (ctx->d_small) return ACZ_OK;
+    CK(cudaMalloc(&ctx->d_small, sizeof(acz_gpu_ctx::Small)));
+    CK(cudaMallocHost(&ctx->h_small, sizeof(acz_gpu_ctx::Small)));
+    return ACZ_OK;
+}
+
+// Runs the fused stats pass and returns non-finite / nnz / sum|x|.
+int run_stats(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, uint32_t* d_bitmap,
+              cudaStream_t s, unsigned* flags, uint64_t* nnz, double* sumabs) {
+    int rc = ensure_small(ctx);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(&ctx->d_small->flags, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(&ctx->d_small->nnz, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(&ctx->d_small->sumabs, 0, sizeof(double), s));
+    {
+        KTimer kt(ctx, ACZ_K_STATS, s);
+        CK(launch_stats(d_in, n, d_bitmap, &ctx->d_small->nnz, &ctx->d_small->flags,
+                        &ctx->d_small->sumabs, ctx->sms, s, &ctx->launches));
+    }
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, offsetof(acz_gpu_ctx::Small, canon),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (flags) *flags = ctx->h_small->flags;
+    if (nnz) *nnz = ctx->h_small->nnz;
+    if (sumabs) *sumabs = ctx->h_small->sumabs;
+    return ACZ_OK;
+}
+
+int validate_shape(acz_gpu_ctx* ctx, const uint64_t* shape, uint32_t rank, uint64_t* n) {
+    if (rank > ACZ_MAX_RANK) return fail(ctx, ACZ_ERR_SHAPE, "rank exceeds ACZ_MAX_RANK");
+    if (rank && !shape) return fail(ctx, ACZ_ERR_INVALID, "null shape");
+    uint64_t v = rank ? 1 : 0;
+    for (uint32_t i = 0; i < rank; ++i) {
+        if (shape[i] == 0) return fail(ctx, ACZ_ERR_SHAPE, "tensor extents must be positive");
+        v *= shape[i];
+    }
+    *n = v;
+    return ACZ_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------ context --
+extern "C" {
+
+const char* acz_gpu_version(void) { return kVersion; }
+
+int acz_gpu_ctx_create(int device, acz_gpu_ctx** out) {
+    if (!out) return ACZ_ERR_INVALID;
+    *out = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return ACZ_ERR_CUDA;
+    acz_gpu_ctx* ctx = new (std::nothrow) acz_gpu_ctx();
+    if (!ctx) return ACZ_ERR_NOMEM;
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    // keep freed blob memory cached in the stream-ordered pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return ACZ_ERR_CUDA;
+    }
+    if (ensure_small(ctx) != ACZ_OK) {
+        delete ctx;
+        return ACZ_ERR_CUDA;
+    }
+    *out = ctx;
+    return ACZ_OK;
+}
+
+int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    cudaDeviceSynchronize();
+    for (void* p : {ctx->ws_sym, ctx->ws_hist, ctx->ws_enc, ctx->ws_cb, ctx->ws_status,
+                    ctx->ws_row, ctx->ws_io, ctx->ws_aux, ctx->ws_book, ctx->ws_side})
+        if (p) cudaFree(p);
+    if (ctx->d_small) cudaFree(ctx->d_small);
+    if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    for (auto& p : ctx->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    delete ctx;
+    return ACZ_OK;
+}
+
+const char* acz_gpu_last_error(const acz_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"
+
+// ----------------------------------------------------------------------- compress --
+namespace {
+
+// Blob-side finalisation shared by compress and the generic Huffman encoder: after the
+// codebook sync, allocates the blob, copies the tables and runs K5.
+int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const uint32_t* d_sym, uint64_t n,
+                  const float* d_x, uint64_t interval, cudaStream_t s) {
+    const BookInfo& bi = ctx->h_small->info;
+    const uint64_t nwords = (bi.total_bits + 31) / 32;
+    const uint64_t nout = d_x ? bi.n_escapes : 0;
+    const uint64_t nchunks = interval ? (n + interval - 1) / interval : 0;
+    CK(blob_alloc(b, bi.book_size, nwords, nout, nchunks, s));
+    b->nwords = nwords;
+    b->interval = interval;
+    b->nchunks = nchunks;
+    b->max_len = bi.max_len;
+    CK(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 4), s));
+    const uint32_t* wb_sym = static_cast<const uint32_t*>(ctx->ws_book);
+    const uint8_t* wb_len =
+        reinterpret_cast<const uint8_t*>(wb_sym + std::max<uint64_t>(ctx->ws_book_cap / 5, 1));
+    CK(cudaMemcpyAsync(b->book_sym, wb_sym, 4ull * bi.book_size, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(b->book_len, wb_len, bi.book_size, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(b->lut, ctx->d_small->lut, 4ull * kLutSize, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(b->canon, &ctx->d_small->canon, sizeof(CanonTables),
+                       cudaMemcpyDeviceToDevice, s));
+    if (nchunks && d_x)
+        CK(cudaMemcpyAsync(b->side_state, ctx->ws_side, 4ull * nchunks, cudaMemcpyDeviceToDevice,
+                           s));
+    EncodeArgs ea;
+    ea.sym = d_sym;
+    ea.n = n;
+    ea.enc = static_cast<const unsigned long long*>(ctx->ws_enc);
+    ea.x = d_x;
+    ea.words = b->words;
+    ea.nwords = nwords;
+    ea.out_index = b->out_index;
+    ea.out_value = b->out_value;
+    ea.side_bitoff = nchunks ? b->side_bitoff : nullptr;
+    ea.side_outl = b->side_outl;
+    ea.interval = interval ? interval : 1;
+    ea.max_len = bi.max_len;
+    ea.status = static_cast<TileStatus*>(ctx->ws_status);
+    ea.ticket = &ctx->d_small->ticket;
+    {
+        KTimer kt(ctx, ACZ_K_ENCODE, s);
+        CK(launch_encode(ea, ctx->sms, s, &ctx->launches));
+    }
+    return ACZ_OK;
+}
+
+// Histogram + codebook + the single synchronisation. Leaves BookInfo in h_small.
+int build_book(acz_gpu_ctx* ctx, const uint32_t* d_sym, uint64_t n, uint32_t alphabet,
+               uint32_t center, cudaStream_t s) {
+    const uint64_t max_leaves = std::min<uint64_t>(alphabet, n);
+    CK(grow(&ctx->ws_hist, &ctx->ws_hist_cap, 8ull * alphabet));
+    CK(grow(&ctx->ws_enc, &ctx->ws_enc_cap, 8ull * alphabet));
+    CK(grow(&ctx->ws_cb, &ctx->ws_cb_cap, codebook_scratch_bytes(max_leaves)));
+    CK(grow(&ctx->ws_book, &ctx->ws_book_cap, 5ull * max_leaves + 64));
+    const uint64_t tiles = (n + kEncTile - 1) / kEncTile;
+    CK(grow(&ctx->ws_status, &ctx->ws_status_cap, sizeof(TileStatus) * tiles));
+    {
+    KTimer kt(ctx, ACZ_K_HIST, s);
+    CK(launch_histogram(d_sym, n, alphabet, center,
+                        static_cast<unsigned long long*>(ctx->ws_hist), ctx->sms, s,
+                        &ctx->launches));
+    }
+    uint32_t* wb_sym = static_cast<uint32_t*>(ctx->ws_book);
+    uint8_t* wb_len = reinterpret_cast<uint8_t*>(wb_sym + std::max<uint64_t>(ctx->ws_book_cap / 5, 1));
+    {
+    KTimer kt(ctx, ACZ_K_BOOK, s);
+    CK(launch_codebook(static_cast<unsigned long long*>(ctx->ws_hist), alphabet, max_leaves,
+                       ctx->ws_cb, wb_sym, wb_len, static_cast<unsigned long long*>(ctx->ws_enc),
+                       &ctx->d_small->canon, ctx->d_small->lut, &ctx->d_small->info, s,
+                       &ctx->launches));
+    }
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, offsetof(acz_gpu_ctx::Small, canon),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape, uint32_t rank,
+                     double eb, uint32_t quant_radius, uint32_t predictor, void* stream,
+                     acz_gpu_blob** out) {
+    if (!ctx || !out) return ACZ_ERR_INVALID;
+    *out = nullptr;
+    ctx->err.clear();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint64_t n = 0;
+    int rc = validate_shape(ctx, shape, rank, &n);
+    if (rc) return rc;
+    if (n && !d_in) return fail(ctx, ACZ_ERR_INVALID, "null input");
+    if (predictor > 1) return fail(ctx, ACZ_ERR_PARAM, "unknown predictor");
+    if (!params_ok(eb, quant_radius)) {
+        // The reference builds the Tensor (finiteness check) before compress validates.
+        if (n) {
+            unsigned fl = 0;
+            rc = run_stats(ctx, d_in, n, nullptr, s, &fl, nullptr, nullptr);
+            if (rc) return rc;
+            if (fl & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
+        }
+        return fail(ctx, ACZ_ERR_PARAM, param_msg(eb));
+    }
+    if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "compress: empty tensor");
+    const PlaneGeom g = plane_geom(shape, rank);
+    const uint32_t alphabet = 2u * quant_radius;
+    const uint64_t interval = predictor == ACZ_PRED_PREV
+                                  ? std::min<uint64_t>(sidecar_interval_default(), n)
+                                  : g.plane_size;
+    const uint64_t nchunks = (n + interval - 1) / interval;
+
+    CK(grow(&ctx->ws_sym, &ctx->ws_sym_cap, 4ull * n));
+    CK(grow(&ctx->ws_side, &ctx->ws_side_cap, 4ull * nchunks));
+    if (predictor == ACZ_PRED_LORENZO2D)
+        CK(grow(&ctx->ws_row, &ctx->ws_row_cap, 4ull * g.planes * g.cols));
+    ctx->last_n = n;
+
+    acz_gpu_ctx::Small* sm = ctx->d_small;
+    CK(cudaMemsetAsync(&sm->flags, 0, sizeof(unsigned), s));
+    QuantArgs qa;
+    qa.x = d_in;
+    qa.g = g;
+    qa.eb = eb;
+    qa.step = 2.0 * eb;
+    qa.radius = quant_radius;
+    qa.predictor = predictor;
+    qa.sym = static_cast<uint32_t*>(ctx->ws_sym);
+    qa.side_state = static_cast<float*>(ctx->ws_side);
+    qa.interval = interval;
+    qa.row_scratch = static_cast<float*>(ctx->ws_row);
+    qa.flags = &sm->flags;
+    {
+        KTimer kt(ctx, ACZ_K_QUANT, s);
+        CK(launch_quant(qa, ctx->sms, s, &ctx->launches));
+    }
+    rc = build_book(ctx, qa.sym, n, alphabet, quant_radius, s);
+    if (rc) return rc;
+    const BookInfo bi = ctx->h_small->info;
+    const unsigned flags = ctx->h_small->flags | bi.flags;
+    // precedence follows the reference: Tensor ctor (DomainError), huffman_encode
+    // (DecodeError), then the codebook limit in compress (FormatError).
+    if (flags & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
+    if (flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
+    if (bi.book_size > kMaxBook)
+        return fail(ctx, ACZ_ERR_FORMAT, "codebook exceeds the 65535-entry limit of the blob format");
+    if (flags & kFlagLenTooLong) return fail(ctx, ACZ_ERR_FORMAT, "code length > 56 bits unsupported");
+
+    acz_gpu_blob* b = new (std::nothrow) acz_gpu_blob();
+    if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
+    rc = finish_encode(ctx, b, qa.sym, n, d_in, interval, s);
+    if (rc) {
+        if (b->arena) cudaFreeAsync(b->arena, s);
+        delete b;
+        return rc;
+    }
+    acz_gpu_blob_info_t& in = b->info;
+    in.rank = rank;
+    for (uint32_t i = 0; i < rank; ++i) in.shape[i] = shape[i];
+    in.eb = eb;
+    in.quant_radius = quant_radius;
+    in.predictor = predictor;
+    in.element_count = n;
+    in.codebook_size = bi.book_size;
+    in.bit_length = bi.total_bits;
+    in.outlier_count = bi.n_escapes;
+    in.uncompressed_bytes = 4ull * n;
+    in.compressed_bytes = acz1_size(rank, bi.book_size, bi.total_bits, bi.n_escapes);
+    in.device_bytes = b->arena_bytes;
+    in.sidecar_bytes = sidecar_bytes(b->nchunks);
+    in.max_code_length = bi.max_len;
+    *out = b;
+    return ACZ_OK;
+}
+
+int acz_gpu_decompress(acz_gpu_ctx* ctx, const acz_gpu_blob* b, int zero_filter, float* d_out,
+                       void* stream) {
+    if (!ctx || !b || !d_out) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    if (b->invalid) return fail(ctx, b->invalid, b->invalid_msg);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const acz_gpu_blob_info_t& in = b->info;
+    const PlaneGeom g = plane_geom(in.shape, in.rank);
+    if (in.predictor == ACZ_PRED_LORENZO2D)
+        CK(grow(&ctx->ws_row, &ctx->ws_row_cap, 4ull * g.planes * g.cols));
+    DecodeArgs a;
+    a.words = b->words;
+    a.nwords = b->nwords;
+    a.bit_length = in.bit_length;
+    a.lut = b->lut;
+    a.canon = b->canon;
+    a.book_sym = b->book_sym;
+    a.book_size = in.codebook_size;
+    a.side_bitoff = b->side_bitoff;
+    a.side_outl = b->side_outl;
+    a.side_state = b->side_state;
+    a.interval = b->interval;
+    a.nchunks = b->nchunks;
+    a.out_index = b->out_index;
+    a.out_value = b->out_value;
+    a.n_outliers = in.outlier_count;
+    a.g = g;
+    a.eb = in.eb;
+    a.step = 2.0 * in.eb;
+    a.radius = in.quant_radius;
+    a.predictor = in.predictor;
+    a.zero_filter = zero_filter;
+    a.out = d_out;
+    a.row_scratch = static_cast<float*>(ctx->ws_row);
+    {
+        KTimer kt(ctx, ACZ_K_DECODE, s);
+        CK(launch_decode(a, ctx->sms, s, &ctx->launches));
+    }
+    return ACZ_OK;
+}
+
+int acz_gpu_blob_info(const acz_gpu_blob* b, acz_gpu_blob_info_t* info) {
+    if (!b || !info) return ACZ_ERR_INVALID;
+    *info = b->info;
+    return ACZ_OK;
+}
+
+int acz_gpu_blob_free(acz_gpu_blob* b) {
+    if (!b) return ACZ_ERR_INVALID;
+    if (b->arena) cudaFreeAsync(b->arena, b->stream);
+    delete b;
+    return ACZ_OK;
+}
+
+// ------------------------------------------------------------------ serialisation --
+int acz_gpu_blob_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
+                         uint64_t* written, void* stream) {
+    if (!ctx || !b || !dst) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    const acz_gpu_blob_info_t& in = b->info;
+    if (cap < in.compressed_bytes) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t k = in.codebook_size;
+    const uint64_t nout = in.outlier_count;
+    std::vector<uint32_t> bsym(k);
+    std::vector<uint8_t> blen(k);
+    std::vector<unsigned long long> oidx(nout);
+    std::vector<float> oval(nout);
+    // header: ref src/codec.cpp:179-191
+    uint8_t* p = dst;
+    auto put = [&](uint64_t v, int bytes) {
+        for (int i = 0; i < bytes; ++i) *p++ = (uint8_t)(v >> (8 * i));
+    };
+    std::memcpy(p, "ACZ1", 4);
+    p += 4;
+    put(1, 1);
+    put(in.predictor, 1);
+    put(in.rank, 1);
+    for (uint32_t i = 0; i < in.rank; ++i) put(in.shape[i], 8);
+    uint64_t ebits;
+    std::memcpy(&ebits, &in.eb, 8);
+    put(ebits, 8);
+    put(in.quant_radius, 4);
+    put(nout, 4);
+    put(k, 2);
+    uint8_t* book_at = p;
+    p += 5ull * k;
+    put(in.bit_length, 8);
+    const uint64_t nbytes = (in.bit_length + 7) / 8;
+    CK(cudaMemcpyAsync(p, b->words, nbytes, cudaMemcpyDeviceToHost, s));
+    p += nbytes;
+    if (k) {
+        CK(cudaMemcpyAsync(bsym.data(), b->book_sym, 4ull * k, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(blen.data(), b->book_len, k, cudaMemcpyDeviceToHost, s));
+    }
+    if (nout) {
+        CK(cudaMemcpyAsync(oidx.data(), b->out_index, 8ull * nout, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(oval.data(), b->out_value, 4ull * nout, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    uint8_t* q = book_at;
+    for (uint32_t i = 0; i < k; ++i) {
+        for (int j = 0; j < 4; ++j) *q++ = (uint8_t)(bsym[i] >> (8 * j));
+        *q++ = blen[i];
+    }
+    for (uint64_t i = 0; i < nout; ++i) {
+        put(oidx[i], 8);
+        uint32_t vb;
+        std::memcpy(&vb, &oval[i], 4);
+        put(vb, 4);
+    }
+    if ((uint64_t)(p - dst) != in.compressed_bytes)
+        return fail(ctx, ACZ_ERR_FORMAT, "internal: ACZ1 size mismatch");
+    if (written) *written = in.compressed_bytes;
+    return ACZ_OK;
+}
+
+int acz_gpu_sidecar_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
+                            uint64_t* written, void* stream) {
+    if (!ctx || !b || !dst) return ACZ_ERR_INVALID;
+    const uint64_t need = sidecar_bytes(b->nchunks);
+    if (cap < need) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint8_t* p = dst;
+    std::memcpy(p, "ACZS", 4);
+    p += 4;
+    const uint32_t ver = 1;
+    std::memcpy(p, &ver, 4);
+    p += 4;
+    const uint64_t hdr[6] = {b->info.element_count, b->info.bit_length, b->interval, b->nchunks,
+                             blob_binding(b->info), 0};
+    std::memcpy(p, hdr, sizeof(hdr));
+    p += sizeof(hdr);
+    CK(cudaMemcpyAsync(p, b->side_bitoff, 8ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+    p += 8ull * b->nchunks;
+    CK(cudaMemcpyAsync(p, b->side_outl, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+    p += 4ull * b->nchunks;
+    CK(cudaMemcpyAsync(p, b->side_state, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (written) *written = need;
+    return ACZ_OK;
+}
+
+int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
+                           const uint8_t* sidecar, uint64_t sidecar_size, void* stream,
+                           acz_gpu_blob** out) {
+    if (!ctx || !out || (!src && size)) return ACZ_ERR_INVALID;
+    *out = nullptr;
+    ctx->err.clear();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // ---- ref src/codec.cpp:201-262 (blob_from_bytes), same checks and order ----
+    uint64_t pos = 0;
+    bool trunc = false;
+    auto get = [&](int bytes) -> uint64_t {
+        if (trunc || pos + (uint64_t)bytes > size) {
+            trunc = true;
+            return 0;
+        }
+        uint64_t v = 0;
+        for (int i = 0; i < bytes; ++i) v |= (uint64_t)src[pos + i] << (8 * i);
+        pos += (uint64_t)bytes;
+        return v;
+    };
+#define NEED()                                                                       \
+    do {                                                                             \
+        if (trunc) return fail(ctx, ACZ_ERR_FORMAT, "unexpected end of stream");     \
+    } while (0)
+    if (size < 4) return fail(ctx, ACZ_ERR_FORMAT, "unexpected end of stream at offset 0");
+    if (std::memcmp(src, "ACZ1", 4) != 0)
+        return fail(ctx, ACZ_ERR_FORMAT, "bad blob magic at offset 0 (expected \"ACZ1\")");
+    pos = 4;
+    const uint64_t version = get(1);
+    NEED();
+    if (version != 1) return fail(ctx, ACZ_ERR_FORMAT, "unsupported blob version");
+    const uint64_t pred = get(1);
+    NEED();
+    if (pred > 1) return fail(ctx, ACZ_ERR_FORMAT, "unknown predictor id");
+    const uint64_t rank = get(1);
+    NEED();
+    if (rank == 0) return fail(ctx, ACZ_ERR_FORMAT, "blob rank must be >= 1");
+    if (rank > ACZ_MAX_RANK) return fail(ctx, ACZ_ERR_FORMAT, "blob rank exceeds ACZ_MAX_RANK");
+    acz_gpu_blob_info_t in{};
+    in.rank = (uint32_t)rank;
+    in.predictor = (uint32_t)pred;
+    uint64_t count = 1;
+    for (uint64_t i = 0; i < rank; ++i) {
+        in.shape[i] = get(8);
+        NEED();
+        if (in.shape[i] == 0) return fail(ctx, ACZ_ERR_FORMAT, "zero extent in blob header");
+        count *= in.shape[i];
+    }
+    const uint64_t ebits = get(8);
+    in.quant_radius = (uint32_t)get(4);
+    NEED();
+    std::memcpy(&in.eb, &ebits, 8);
+    if (!params_ok(in.eb, in.quant_radius)) return fail(ctx, ACZ_ERR_PARAM, param_msg(in.eb));
+    const uint64_t nout = get(4);
+    const uint64_t k = get(2);
+    NEED();
+    if (k == 0) return fail(ctx, ACZ_ERR_FORMAT, "empty codebook");
+    std::vector<uint32_t> bsym(k);
+    std::vector<uint8_t> blen(k);
+    for (uint64_t i = 0; i < k; ++i) {
+        bsym[i] = (uint32_t)get(4);
+        blen[i] = (uint8_t)get(1);
+    }
+    const uint64_t bit_length = get(8);
+    NEED();
+    const uint64_t nbytes = bit_length / 8 + ((bit_length & 7) ? 1 : 0);
+    if (nbytes > size - pos) return fail(ctx, ACZ_ERR_FORMAT, "unexpected end of stream");
+    const uint8_t* bits = src + pos;
+    pos += nbytes;
+    std::vector<unsigned long long> oidx(nout);
+    std::vector<float> oval(nout);
+    for (uint64_t i = 0; i < nout; ++i) {
+        oidx[i] = get(8);
+        const uint32_t vb = (uint32_t)get(4);
+        NEED();
+        std::memcpy(&oval[i], &vb, 4);
+        if (oidx[i] >= count) return fail(ctx, ACZ_ERR_FORMAT, "outlier index out of range");
+        if (i > 0 && oidx[i] <= oidx[i - 1])
+            return fail(ctx, ACZ_ERR_FORMAT, "outlier indices are not strictly increasing");
+    }
+    if (pos != size) return fail(ctx, ACZ_ERR_FORMAT, "trailing bytes after blob");
+#undef NEED
+    in.element_count = count;
+    in.codebook_size = (uint32_t)k;
+    in.bit_length = bit_length;
+    in.outlier_count = nout;
+    in.uncompressed_bytes = 4ull * count;
+    in.compressed_bytes = size;
+    uint32_t maxl = 0;
+    for (uint64_t i = 0; i < k; ++i) maxl = std::max<uint32_t>(maxl, blen[i]);
+    in.max_code_length = maxl;
+
+    // deferred (decompress-time) checks of the reference: huffman_decode book validation
+    int deferred = 0;
+    std::string dmsg;
+    for (uint64_t i = 1; i < k && !deferred; ++i)
+        if (blen[i - 1] > blen[i] || (blen[i - 1] == blen[i] && bsym[i - 1] >= bsym[i])) {
+            deferred = ACZ_ERR_DECODE;
+            dmsg = "codebook entries are not in canonical order";
+        }
+    for (uint64_t i = 0; i < k && !deferred; ++i)
+        if (blen[i] == 0 || blen[i] > 64) {
+            deferred = ACZ_ERR_DECODE;
+            dmsg = "invalid code length in codebook";
+        }
+    const PlaneGeom g = plane_geom(in.shape, in.rank);
+    const uint64_t interval = pred == ACZ_PRED_PREV ? std::min<uint64_t>(sidecar_interval_default(), count)
+                                                    : g.plane_size;
+    // sidecar supplied?
+    bool have_side = false;
+    uint64_t side_interval = interval, side_chunks = (count + interval - 1) / interval;
+    if (sidecar && sidecar_size >= 56 && std::memcmp(sidecar, "ACZS", 4) == 0) {
+        uint64_t hdr[6];
+        std::memcpy(hdr, sidecar + 8, sizeof(hdr));
+        if (hdr[0] == count && hdr[1] == bit_length && hdr[2] > 0 &&
+            hdr[3] == (count + hdr[2] - 1) / hdr[2] && hdr[4] == blob_binding(in) &&
+            sidecar_size == sidecar_bytes(hdr[3]) &&
+            (pred == ACZ_PRED_PREV || hdr[2] == g.plane_size)) {
+            have_side = true;
+            side_interval = hdr[2];
+            side_chunks = hdr[3];
+        }
+    }
+    acz_gpu_blob* b = new (std::nothrow) acz_gpu_blob();
+    if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
+    b->info = in;
+    const uint64_t nwords = (bit_length + 31) / 32;
+    cudaError_t e = blob_alloc(b, (uint32_t)k, nwords, nout, side_chunks, s);
+    if (e != cudaSuccess) {
+        delete b;
+        return cuda_fail(ctx, e, "blob_alloc");
+    }
+    b->nwords = nwords;
+    b->interval = side_interval;
+    b->nchunks = side_chunks;
+    b->max_len = maxl;
+    b->info.device_bytes = b->arena_bytes;
+    b->info.sidecar_bytes = sidecar_bytes(side_chunks);
+    auto cleanup = [&](int rc) {
+        cudaFreeAsync(b->arena, s);
+        delete b;
+        return rc;
+    };
+#define CKB(expr)                                                                  \
+    do {                                                                           \
+        cudaError_t _e = (expr);                                                   \
+        if (_e != cudaSuccess) return cleanup(cuda_fail(ctx, _e, #expr));          \
+    } while (0)
+    CKB(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 4), s));
+    CKB(cudaMemcpyAsync(b->words, bits, nbytes, cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(b->book_sym, bsym.data(), 4ull * k, cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(b->book_len, blen.data(), k, cudaMemcpyHostToDevice, s));
+    if (nout) {
+        CKB(cudaMemcpyAsync(b->out_index, oidx.data(), 8ull * nout, cudaMemcpyHostToDevice, s));
+        CKB(cudaMemcpyAsync(b->out_value, oval.data(), 4ull * nout, cudaMemcpyHostToDevice, s));
+    }
+    if (deferred) {
+        CKB(cudaStreamSynchronize(s));
+        b->invalid = deferred;
+        b->invalid_msg = dmsg;
+        *out = b;
+        return ACZ_OK;
+    }
+    CKB(launch_build_tables(b->book_sym, b->book_len, (uint32_t)k, b->canon, b->lut, nullptr, s,
+                            &ctx->launches));
+    if (have_side) {
+        const uint8_t* p = sidecar + 56;
+        CKB(cudaMemcpyAsync(b->side_bitoff, p, 8ull * side_chunks, cudaMemcpyHostToDevice, s));
+        p += 8ull * side_chunks;
+        CKB(cudaMemcpyAsync(b->side_outl, p, 4ull * side_chunks, cudaMemcpyHostToDevice, s));
+        p += 4ull * side_chunks;
+        CKB(cudaMemcpyAsync(b->side_state, p, 4ull * side_chunks, cudaMemcpyHostToDevice, s));
+        CKB(cudaStreamSynchronize(s));  // host vectors go out of scope
+        *out = b;
+        return ACZ_OK;
+    }
+    // rebuild the sidecar on the GPU: sequential decode + validation, then chain states
+    const bool prev = pred == ACZ_PRED_PREV;
+    const size_t aux = (prev ? 4ull * count : 0) + 8ull * (g.planes + 1) + 256;
+    CKB(grow(&ctx->ws_aux, &ctx->ws_aux_cap, aux));
+    unsigned long long* plane_outl = static_cast<unsigned long long*>(ctx->ws_aux);
+    uint32_t* syms = prev ? reinterpret_cast<uint32_t*>(plane_outl + g.planes + 1) : nullptr;
+    CKB(cudaMemsetAsync(&ctx->d_small->flags, 0, sizeof(unsigned), s));
+    ScanArgs sa;
+    sa.words = b->words;
+    sa.nwords = nwords;
+    sa.bit_length = bit_length;
+    sa.n = count;
+    sa.lut = b->lut;
+    sa.canon = b->canon;
+    sa.book_sym = b->book_sym;
+    sa.out_index = b->out_index;
+    sa.n_outliers = nout;
+    sa.interval = side_interval;
+    sa.side_bitoff = b->side_bitoff;
+    sa.side_outl = b->side_outl;
+    sa.sym_out = syms;
+    sa.plane_outl = plane_outl;
+    sa.plane_size = g.plane_size;
+    sa.flags = &ctx->d_small->flags;
+    {
+        KTimer kt(ctx, ACZ_K_SCAN, s);
+        CKB(launch_scan_decode(sa, s, &ctx->launches));
+    }
+    CKB(cudaMemcpyAsync(&ctx->h_small->flags, &ctx->d_small->flags, sizeof(unsigned),
+                        cudaMemcpyDeviceToHost, s));
+    CKB(cudaStreamSynchronize(s));
+    const unsigned fl = ctx->h_small->flags;
+    if (fl) {
+        b->invalid = (fl & (kDecTruncated | kDecNoMatch)) ? ACZ_ERR_DECODE : ACZ_ERR_FORMAT;
+        b->invalid_msg = (fl & kDecTruncated)        ? "truncated bitstream"
+                         : (fl & kDecNoMatch)        ? "no codeword matches bitstream"
+                         : (fl & kDecOutlierMissing) ? "escape symbol without a matching outlier record"
+                         : (fl & kDecOutlierIndex)   ? "outlier index does not match scan position"
+                                                     : "blob contains unused outlier records";
+        *out = b;
+        return ACZ_OK;
+    }
+    if (prev) {
+        CKB(launch_chain_states(syms, plane_outl, b->out_value, g, 2.0 * in.eb, in.quant_radius,
+                                side_interval, b->side_state, ctx->sms, s, &ctx->launches));
+    }
+    CKB(cudaStreamSynchronize(s));
+#undef CKB
+    *out = b;
+    return ACZ_OK;
+}
+
+// ------------------------------------------------------------------- host buffers --
+void acz_gpu_host_free(void* p) { std::free(p); }
+
+int acz_gpu_compress_host(acz_gpu_ctx* ctx, const float* h_in, const uint64_t* shape,
+                          uint32_t rank, double eb, uint32_t quant_radius, uint32_t predictor,
+                          uint8_t** acz1, uint64_t* acz1_size, uint8_t** sidecar,
+                          uint64_t* sidecar_size) {
+    if (!ctx || !acz1 || !acz1_size) return ACZ_ERR_INVALID;
+    *acz1 = nullptr;
+    if (sidecar) *sidecar = nullptr;
+    uint64_t n = 0;
+    int rc = validate_shape(ctx, shape, rank, &n);
+    if (rc) return rc;
+    cudaStream_t s = ctx->own;
+    if (n) {
+        CK(grow(&ctx->ws_io, &ctx->ws_io_cap, 4ull * n));
+        CK(cudaMemcpyAsync(ctx->ws_io, h_in, 4ull * n, cudaMemcpyHostToDevice, s));
+    }
+    acz_gpu_blob* b = nullptr;
+    rc = acz_gpu_compress(ctx, static_cast<const float*>(ctx->ws_io), shape, rank, eb,
+                          quant_radius, predictor, s, &b);
+    if (rc) return rc;
+    const uint64_t sz = b->info.compressed_bytes;
+    uint8_t* buf = static_cast<uint8_t*>(std::malloc(sz));
+    if (!buf) {
+        acz_gpu_blob_free(b);
+        return fail(ctx, ACZ_ERR_NOMEM, "host buffer");
+    }
+    rc = acz_gpu_blob_to_host(ctx, b, buf, sz, nullptr, s);
+    if (!rc && sidecar) {
+        const uint64_t ss = b->info.sidecar_bytes;
+        *sidecar = static_cast<uint8_t*>(std::malloc(ss));
+        if (!*sidecar) rc = fail(ctx, ACZ_ERR_NOMEM, "host buffer");
+        else rc = acz_gpu_sidecar_to_host(ctx, b, *sidecar, ss, sidecar_size, s);
+    }
+    acz_gpu_blob_free(b);
+    if (rc) {
+        std::free(buf);
+        if (sidecar && *sidecar) {
+            std::free(*sidecar);
+            *sidecar = nullptr;
+        }
+        return rc;
+    }
+    *acz1 = buf;
+    *acz1_size = sz;
+    return ACZ_OK;
+}
+
+int acz_gpu_decompress_host(acz_gpu_ctx* ctx, const uint8_t* acz1, uint64_t acz1_size,
+                            const uint8_t* sidecar, uint64_t sidecar_size, int zero_filter,
+                            float* h_out, uint64_t n) {
+    if (!ctx || !h_out) return ACZ_ERR_INVALID;
+    cudaStream_t s = ctx->own;
+    acz_gpu_blob* b = nullptr;
+    int rc = acz_gpu_blob_from_host(ctx, acz1, acz1_size, sidecar, sidecar_size, s, &b);
+    if (rc) return rc;
+    if (b->info.element_count != n) {
+        acz_gpu_blob_free(b);
+        return fail(ctx, ACZ_ERR_SHAPE, "output size mismatch");
+    }
+    int grc = (int)grow(&ctx->ws_io, &ctx->ws_io_cap, 4ull * n);
+    if (grc != cudaSuccess) {
+        acz_gpu_blob_free(b);
+        return cuda_fail(ctx, (cudaError_t)grc, "grow");
+    }
+    rc = acz_gpu_decompress(ctx, b, zero_filter, static_cast<float*>(ctx->ws_io), s);
+    if (!rc) {
+        cudaError_t e = cudaMemcpyAsync(h_out, ctx->ws_io, 4ull * n, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = cuda_fail(ctx, e, "d2h");
+    }
+    acz_gpu_blob_free(b);
+    return rc;
+}
+
+// ---------------------------------------------------------------------- statistics --
+int acz_gpu_zero_bitmap(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, uint32_t* d_bitmap,
+                        uint64_t* nonzero, void* stream) {
+    if (!ctx || (!d_in && n)) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "nonzero_ratio: empty tensor");
+    unsigned fl = 0;
+    uint64_t nz = 0;
+    int rc = run_stats(ctx, d_in, n, d_bitmap, static_cast<cudaStream_t>(stream), &fl, &nz, nullptr);
+    if (rc) return rc;
+    if (nonzero) *nonzero = nz;
+    if (fl & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
+    return ACZ_OK;
+}
+
+int acz_gpu_nonzero_ratio(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void* stream,
+                          double* ratio) {
+    uint64_t nz = 0;
+    int rc = acz_gpu_zero_bitmap(ctx, d_in, n, nullptr, &nz, stream);
+    if (rc) return rc;
+    if (ratio) *ratio = (double)nz / (double)n;  // ref include/acz/tensor.hpp:98
+    return ACZ_OK;
+}
+
+int acz_gpu_mean_abs(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void* stream,
+                     double* mean) {
+    if (!ctx || (!d_in && n)) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "mean_abs: empty tensor");
+    unsigned fl = 0;
+    double sa = 0;
+    int rc = run_stats(ctx, d_in, n, nullptr, static_cast<cudaStream_t>(stream), &fl, nullptr, &sa);
+    if (rc) return rc;
+    if (fl & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
+    if (mean) *mean = sa / (double)n;
+    return ACZ_OK;
+}
+
+// ------------------------------------------------------------------------- Huffman --
+int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t n,
+                           uint32_t* book_sym, uint8_t* book_len, uint32_t book_cap,
+                           uint32_t* book_size, uint8_t* bits, uint64_t bits_cap,
+                           uint64_t* bit_length, void* stream) {
+    if (!ctx || !book_size || !bit_length) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    *book_size = 0;
+    *bit_length = 0;
+    if (n == 0) return ACZ_OK;  // ref src/huffman.cpp:108
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // alphabet = max symbol + 1 (dense GPU histogram; alphabets beyond 2^26 unsupported)
+    uint32_t maxsym = 0;
+    {
+        std::vector<uint32_t> tmp;  // small reduction on device via the stats path is overkill
+        const uint64_t chunk = 1 << 24;
+        tmp.resize(std::min<uint64_t>(n, chunk));
+        for (uint64_t o = 0; o < n; o += chunk) {
+            const uint64_t m = std::min<uint64_t>(chunk, n - o);
+            CK(cudaMemcpyAsync(tmp.data(), d_symbols + o, 4ull * m, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (uint64_t i = 0; i < m; ++i) maxsym = std::max(maxsym, tmp[i]);
+        }
+    }
+    if (maxsym >= (1u << 26)) return fail(ctx, ACZ_ERR_PARAM, "symbol alphabet beyond 2^26 unsupported");
+    const uint32_t alphabet = maxsym + 1;
+    int rc = build_book(ctx, d_symbols, n, alphabet, 0, s);
+    if (rc) return rc;
+    const BookInfo bi = ctx->h_small->info;
+    if (bi.flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
+    if (bi.flags & kFlagLenTooLong) return fail(ctx, ACZ_ERR_FORMAT, "code length > 56 bits unsupported");
+    if (bi.book_size > book_cap) return fail(ctx, ACZ_ERR_INVALID, "book capacity too small");
+    if ((bi.total_bits + 7) / 8 > bits_cap) return fail(ctx, ACZ_ERR_INVALID, "bits capacity too small");
+    acz_gpu_blob tmpb;
+    rc = finish_encode(ctx, &tmpb, d_symbols, n, nullptr, 0, s);
+    if (rc) {
+        if (tmpb.arena) cudaFreeAsync(tmpb.arena, s);
+        return rc;
+    }
+    CK(cudaMemcpyAsync(book_sym, tmpb.book_sym, 4ull * bi.book_size, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(book_len, tmpb.book_len, bi.book_size, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(bits, tmpb.words, (bi.total_bits + 7) / 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(tmpb.arena, s));
+    CK(cudaStreamSynchronize(s));
+    *book_size = bi.book_size;
+    *bit_length = bi.total_bits;
+    return ACZ_OK;
+}
+
+int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uint8_t* book_len,
+                           uint32_t book_size, const uint8_t* bits, uint64_t bit_length,
+                           uint64_t count, uint32_t* d_out, void* stream) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    if (count == 0) return ACZ_OK;  // ref src/huffman.cpp:140
+    if (book_size == 0) return fail(ctx, ACZ_ERR_DECODE, "empty codebook");
+    for (uint32_t i = 1; i < book_size; ++i)
+        if (book_len[i - 1] > book_len[i] ||
+            (book_len[i - 1] == book_len[i] && book_sym[i - 1] >= book_sym[i]))
+            return fail(ctx, ACZ_ERR_DECODE, "codebook entries are not in canonical order");
+    for (uint32_t i = 0; i < book_size; ++i)
+        if (book_len[i] == 0 || book_len[i] > 64)
+            return fail(ctx, ACZ_ERR_DECODE, "invalid code length in codebook");
+    for (uint32_t i = 0; i < book_size; ++i)
+        if (book_sym[i] >= (1u << 27))
+            return fail(ctx, ACZ_ERR_PARAM, "symbol beyond 2^27 unsupported by the GPU decoder");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    acz_gpu_blob tmpb;
+    const uint64_t nwords = (bit_length + 31) / 32;
+    CK(blob_alloc(&tmpb, book_size, nwords, 0, 0, s));
+    CK(cudaMemsetAsync(tmpb.words, 0, 4ull * (nwords + 4), s));
+    CK(cudaMemcpyAsync(tmpb.words, bits, (bit_length + 7) / 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(tmpb.book_sym, book_sym, 4ull * book_size, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(tmpb.book_len, book_len, book_size, cudaMemcpyHostToDevice, s));
+    CK(launch_build_tables(tmpb.book_sym, tmpb.book_len, book_size, tmpb.canon, tmpb.lut, nullptr,
+                           s, &ctx->launches));
+    CK(cudaMemsetAsync(&ctx->d_small->flags, 0, sizeof(unsigned), s));
+    ScanArgs sa{};
+    sa.words = tmpb.words;
+    sa.nwords = nwords;
+    sa.bit_length = bit_length;
+    sa.n = count;
+    sa.lut = tmpb.lut;
+    sa.canon = tmpb.canon;
+    sa.book_sym = tmpb.book_sym;
+    sa.out_index = nullptr;
+    sa.n_outliers = 0;
+    sa.interval = count;
+    sa.side_bitoff = nullptr;
+    sa.side_outl = nullptr;
+    sa.sym_out = d_out;
+    sa.plane_outl = nullptr;
+    sa.plane_size = count;
+    sa.flags = &ctx->d_small->flags;
+    CK(launch_scan_decode(sa, s, &ctx->launches));
+    CK(cudaMemcpyAsync(&ctx->h_small->flags, &ctx->d_small->flags, sizeof(unsigned),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(tmpb.arena, s));
+    CK(cudaStreamSynchronize(s));
+    const unsigned fl = ctx->h_small->flags;
+    if (fl & kDecTruncated) return fail(ctx, ACZ_ERR_DECODE, "truncated bitstream");
+    if (fl & kDecNoMatch) return fail(ctx, ACZ_ERR_DECODE, "no codeword matches bitstream");
+    return ACZ_OK;
+}
+
+// ----------------------------------------------------------------------- profiling --
+int acz_gpu_profile_enable(acz_gpu_ctx* ctx, int on) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    double ms[ACZ_K_COUNT];
+    uint64_t n[ACZ_K_COUNT];
+    acz_gpu_profile_read(ctx, ms, n);
+    for (int i = 0; i < ACZ_K_COUNT; ++i) {
+        ctx->prof_ms[i] = 0;
+        ctx->prof_n[i] = 0;
+    }
+    ctx->prof = on != 0;
+    return ACZ_OK;
+}
+
+int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    for (auto& p : ctx->pending) {
+        cudaEventSynchronize(p.b);
+        float t = 0;
+        if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) {
+            ctx->prof_ms[p.cls] += t;
+            ctx->prof_n[p.cls] += 1;
+        }
+        ctx->event_pool.push_back(p.a);
+        ctx->event_pool.push_back(p.b);
+    }
+    ctx->pending.clear();
+    for (int i = 0; i < ACZ_K_COUNT; ++i) {
+        if (ms) ms[i] = ctx->prof_ms[i];
+        if (launches) launches[i] = ctx->prof_n[i];
+    }
+    return ACZ_OK;
+}
+
+// --------------------------------------------------------------------------- debug --
+int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, void* stream) {
+    if (!ctx || !d_out) return ACZ_ERR_INVALID;
+    if (n != ctx->last_n || !ctx->ws_sym) return fail(ctx, ACZ_ERR_SHAPE, "no symbols of that size");
+    CK(cudaMemcpyAsync(d_out, ctx->ws_sym, 4ull * n, cudaMemcpyDeviceToDevice,
+                       static_cast<cudaStream_t>(stream)));
+    return ACZ_OK;
+}
+
+}  // extern "C"

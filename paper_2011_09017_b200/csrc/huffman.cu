@@ -1,0 +1,719 @@
+// K3 histogram, K4 codebook, K5 encode: the canonical Huffman coder of the reference
+// (ref src/huffman.cpp:22-135), bit-exact.
+//
+// K3  k_histogram   : shared-memory privatised histogram over a window of 8192 bins
+//                     centred on the zero-residual symbol (quant_radius); out-of-window
+//                     symbols go straight to global u64 atomics.
+// K4  k_codebook    : single 1024-thread CTA. Compaction of non-zero bins (ascending
+//                     symbol order == the reference's std::map order, huffman.cpp:110),
+//                     stable LSD radix sort of the leaves by frequency, two-queue merge
+//                     (leaf wins frequency ties, internal nodes FIFO) which reproduces the
+//                     reference heap's (freq, creation-index) pop order exactly
+//                     (huffman.cpp:25-54), depths by pointer jumping, canonical
+//                     (length, symbol) order by a stable counting sort (huffman.cpp:116-125),
+//                     canonical codes (huffman.cpp:75-86), decode LUT.
+// K5  k_encode      : 4096 symbols per CTA; per-thread code lengths, CTA scan, decoupled
+//                     look-back over tiles for the global bit offset and escape count,
+//                     bit concatenation in shared memory, coalesced word stores (boundary
+//                     words by atomicOr). Also writes the outlier list and the decode
+//                     sidecar (bit offset / outlier prefix every `interval` symbols).
+#include "internal.h"
+
+namespace acz_b200 {
+
+namespace {
+
+constexpr int kHistWindow = 8192;
+
+// --------------------------------------------------------------------------- K3 ----
+__global__ void __launch_bounds__(512) k_histogram(const uint32_t* __restrict__ sym, uint64_t n,
+                                                   uint32_t alphabet, uint32_t win_lo,
+                                                   uint32_t win_n,
+                                                   unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int bins[kHistWindow];
+    for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) bins[i] = 0;
+    __syncthreads();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t n4 = ((reinterpret_cast<uintptr_t>(sym) & 15) == 0) ? n / 4 : 0;
+    const uint4* s4 = reinterpret_cast<const uint4*>(sym);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        uint4 v = __ldcs(s4 + i);
+        uint32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t o = e[k] - win_lo;
+            if (o < win_n) atomicAdd(&bins[o], 1u);
+            else if (e[k] < alphabet) atomicAdd(&hist[e[k]], 1ull);
+        }
+    }
+    for (uint64_t i = n4 * 4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += stride) {
+        uint32_t e = sym[i];
+        uint32_t o = e - win_lo;
+        if (o < win_n) atomicAdd(&bins[o], 1u);
+        else if (e < alphabet) atomicAdd(&hist[e], 1ull);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x)
+        if (bins[i]) atomicAdd(&hist[win_lo + i], (unsigned long long)bins[i]);
+}
+
+// --------------------------------------------------------------------------- K4 ----
+constexpr int kCbThreads = 1024;
+constexpr int kCbWarps = kCbThreads / 32;
+constexpr int kRadixBits = 4;
+constexpr int kRadixBuckets = 1 << kRadixBits;
+constexpr uint64_t kSmemQueue = 16384;  // internal-node FIFO kept in shared memory
+
+struct CbScratch {
+    uint32_t* leaf_sym;           // k, ascending symbol
+    unsigned long long* leaf_freq;
+    unsigned long long* key_a;    // radix ping-pong (freq)
+    unsigned long long* key_b;
+    uint32_t* val_a;              // leaf ids
+    uint32_t* val_b;
+    unsigned long long* ifreq;    // internal-node frequencies (global fallback)
+    uint32_t* anc_a;              // 2k-1 nodes
+    uint32_t* anc_b;
+    uint32_t* dist_a;
+    uint32_t* dist_b;
+};
+
+__host__ __device__ inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+__host__ __device__ inline CbScratch carve(void* base, uint64_t k) {
+    char* p = static_cast<char*>(base);
+    CbScratch s;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char* r = p + off;
+        off += align256(bytes);
+        return r;
+    };
+    s.leaf_sym = reinterpret_cast<uint32_t*>(take(4 * k));
+    s.leaf_freq = reinterpret_cast<unsigned long long*>(take(8 * k));
+    s.key_a = reinterpret_cast<unsigned long long*>(take(8 * k));
+    s.key_b = reinterpret_cast<unsigned long long*>(take(8 * k));
+    s.val_a = reinterpret_cast<uint32_t*>(take(4 * k));
+    s.val_b = reinterpret_cast<uint32_t*>(take(4 * k));
+    s.ifreq = reinterpret_cast<unsigned long long*>(take(8 * k));
+    s.anc_a = reinterpret_cast<uint32_t*>(take(4 * 2 * k));
+    s.anc_b = reinterpret_cast<uint32_t*>(take(4 * 2 * k));
+    s.dist_a = reinterpret_cast<uint32_t*>(take(4 * 2 * k));
+    s.dist_b = reinterpret_cast<uint32_t*>(take(4 * 2 * k));
+    return s;
+}
+
+// Block-wide exclusive scan of one u32 per thread (1024 threads). Returns the exclusive
+// prefix; *total receives the block sum. `tmp` holds kCbWarps + 1 words.
+__device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* tmp, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) tmp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kCbWarps ? tmp[lane] : 0;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < kCbWarps) tmp[lane] = wi - w;
+        if (lane == kCbWarps - 1) tmp[kCbWarps] = wi;
+    }
+    __syncthreads();
+    uint32_t res = tmp[warp] + inc - v;
+    *total = tmp[kCbWarps];
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(kCbThreads, 1) k_codebook(
+    const unsigned long long* __restrict__ hist, uint32_t alphabet, uint64_t max_leaves,
+    void* scratch, uint32_t* __restrict__ book_sym, uint8_t* __restrict__ book_len,
+    unsigned long long* __restrict__ enc, CanonTables* __restrict__ canon,
+    uint32_t* __restrict__ lut, BookInfo* __restrict__ info) {
+    extern __shared__ unsigned long long dyn[];  // radix table / internal FIFO
+    __shared__ uint32_t scan_tmp[kCbWarps + 1];
+    __shared__ unsigned long long s_first_code[65];
+    __shared__ uint32_t s_count[65], s_first_index[65], s_base[65];
+    __shared__ uint32_t s_wcnt[kCbWarps][65];
+    __shared__ unsigned long long s_total_bits;
+    __shared__ uint32_t s_max_len, s_flags;
+
+    const int tid = threadIdx.x;
+    CbScratch S = carve(scratch, max_leaves);
+
+    // (1) compaction of non-zero bins, ascending symbol order --------------------------
+    uint32_t k = 0;
+    for (uint64_t base = 0; base < alphabet; base += kCbThreads) {
+        const uint64_t s = base + tid;
+        const unsigned long long f = s < alphabet ? hist[s] : 0ull;
+        uint32_t tot;
+        const uint32_t pos = block_scan_u32(f != 0, scan_tmp, &tot);
+        if (f != 0 && k + pos < max_leaves) {
+            S.leaf_sym[k + pos] = (uint32_t)s;
+            S.leaf_freq[k + pos] = f;
+        }
+        k += tot;
+    }
+    if (tid == 0) {
+        s_flags = 0;
+        s_total_bits = 0;
+        s_max_len = 0;
+    }
+    __syncthreads();
+    if (k == 0 || k > max_leaves) {
+        if (tid == 0) {
+            info->book_size = k;
+            info->total_bits = 0;
+            info->n_escapes = alphabet ? hist[0] : 0;
+            info->max_len = 0;
+            info->flags = k > max_leaves ? kFlagBookTooBig : 0;
+        }
+        return;
+    }
+
+    // (2) stable LSD radix sort of leaf ids by frequency ------------------------------
+    unsigned long long maxf = 0;
+    for (uint32_t i = tid; i < k; i += kCbThreads) {
+        S.key_a[i] = S.leaf_freq[i];
+        S.val_a[i] = i;
+        maxf = max(maxf, S.leaf_freq[i]);
+    }
+    // block max via shared
+    {
+        __shared__ unsigned long long s_maxf;
+        if (tid == 0) s_maxf = 0;
+        __syncthreads();
+        atomicMax(&s_maxf, maxf);
+        __syncthreads();
+        maxf = s_maxf;
+    }
+    const int key_bits = 64 - __clzll(maxf | 1ull);
+    const int passes = (key_bits + kRadixBits - 1) / kRadixBits;
+    uint32_t* table = reinterpret_cast<uint32_t*>(dyn);  // [kRadixBuckets][kCbThreads]
+    unsigned long long *kin = S.key_a, *kout = S.key_b;
+    uint32_t *vin = S.val_a, *vout = S.val_b;
+    const uint32_t seg = (k + kCbThreads - 1) / kCbThreads;
+    const uint32_t lo = min(k, tid * seg), hi = min(k, lo + seg);
+    for (int p = 0; p < passes; ++p) {
+        const int shift = p * kRadixBits;
+        uint32_t cnt[kRadixBuckets];
+#pragma unroll
+        for (int d = 0; d < kRadixBuckets; ++d) cnt[d] = 0;
+        for (uint32_t i = lo; i < hi; ++i) cnt[(kin[i] >> shift) & (kRadixBuckets - 1)]++;
+#pragma unroll
+        for (int d = 0; d < kRadixBuckets; ++d) table[d * kCbThreads + tid] = cnt[d];
+        __syncthreads();
+        // exclusive scan over the digit-major table: thread t scans 16 consecutive cells
+        uint32_t local[kRadixBuckets];
+        uint32_t run = 0;
+#pragma unroll
+        for (int j = 0; j < kRadixBuckets; ++j) {
+            local[j] = table[tid * kRadixBuckets + j];
+            run += local[j];
+        }
+        uint32_t tot;
+        uint32_t pre = block_scan_u32(run, scan_tmp, &tot);
+#pragma unroll
+        for (int j = 0; j < kRadixBuckets; ++j) {
+            table[tid * kRadixBuckets + j] = pre;
+            pre += local[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int d = 0; d < kRadixBuckets; ++d) cnt[d] = table[d * kCbThreads + tid];
+        for (uint32_t i = lo; i < hi; ++i) {
+            const int d = (kin[i] >> shift) & (kRadixBuckets - 1);
+            const uint32_t o = cnt[d]++;
+            kout[o] = kin[i];
+            vout[o] = vin[i];
+        }
+        __syncthreads();
+        unsigned long long* tk = kin;
+        kin = kout;
+        kout = tk;
+        uint32_t* tv = vin;
+        vin = vout;
+        vout = tv;
+        __threadfence_block();
+        __syncthreads();
+    }
+    // sorted: kin (freq), vin (leaf id)
+
+    // (3) two-queue Huffman merge (single thread) --------------------------------------
+    //     node ids: leaf j -> j, internal m -> k + m; anc_a[] receives parents.
+    const uint32_t root = 2 * k - 2;
+    if (tid == 0) {
+        if (k == 1) {
+            S.anc_a[0] = 0;
+        } else {
+            unsigned long long* q = (k - 1 <= kSmemQueue) ? dyn : S.ifreq;
+            uint32_t li = 0, ii = 0;
+            unsigned long long lf = kin[0];
+            for (uint32_t m = 0; m < k - 1; ++m) {
+                unsigned long long fa, fb;
+                uint32_t ida, idb;
+                // pop a
+                if (li < k && (ii >= m || lf <= q[ii])) {
+                    fa = lf;
+                    ida = vin[li++];
+                    lf = li < k ? kin[li] : 0;
+                } else {
+                    fa = q[ii];
+                    ida = k + ii++;
+                }
+                // pop b
+                if (li < k && (ii >= m || lf <= q[ii])) {
+                    fb = lf;
+                    idb = vin[li++];
+                    lf = li < k ? kin[li] : 0;
+                } else {
+                    fb = q[ii];
+                    idb = k + ii++;
+                }
+                S.anc_a[ida] = k + m;
+                S.anc_a[idb] = k + m;
+                q[m] = fa + fb;
+            }
+            S.anc_a[root] = root;
+        }
+    }
+    __syncthreads();
+
+    // (4) depths by pointer jumping over 2k-1 nodes -------------------------------------
+    const uint32_t nodes = k == 1 ? 1 : 2 * k - 1;
+    uint32_t *ain = S.anc_a, *aout = S.anc_b, *din = S.dist_a, *dout = S.dist_b;
+    for (uint32_t i = tid; i < nodes; i += kCbThreads) din[i] = (k == 1) ? 1 : (i == root ? 0 : 1);
+    __syncthreads();
+    if (k > 1) {
+        for (int it = 0; it < 40; ++it) {
+            int changed = 0;
+            for (uint32_t i = tid; i < nodes; i += kCbThreads) {
+                const uint32_t a = ain[i];
+                if (a != root) {
+                    dout[i] = din[i] + din[a];
+                    aout[i] = ain[a];
+                    changed = 1;
+                } else {
+                    dout[i] = din[i];
+                    aout[i] = a;
+                }
+            }
+            const int any = __syncthreads_or(changed);
+            uint32_t* t = ain;
+            ain = aout;
+            aout = t;
+            t = din;
+            din = dout;
+            dout = t;
+            if (!any) break;
+        }
+    }
+    // leaf j length = din[j]
+
+    // (5) canonical order: stable counting sort by length over ascending symbols --------
+    if (tid < 65) {
+        s_count[tid] = 0;
+        s_base[tid] = 0;
+    }
+    __syncthreads();
+    unsigned long long bits_part = 0;
+    uint32_t maxl = 0;
+    bool too_deep = false;
+    for (uint32_t i = tid; i < k; i += kCbThreads) {
+        uint32_t l = din[i];
+        if (l > 64) {
+            too_deep = true;
+            l = 64;
+        }
+        atomicAdd(&s_count[l], 1u);
+        bits_part += S.leaf_freq[i] * l;
+        maxl = max(maxl, l);
+    }
+    atomicAdd(&s_total_bits, bits_part);
+    atomicMax(&s_max_len, maxl);
+    if (too_deep) atomicOr(&s_flags, kFlagDepth64);
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long code = 0;
+        uint32_t prev = 0, idx = 0;
+        for (int l = 1; l <= 64; ++l) {
+            s_first_index[l] = idx;
+            if (s_count[l]) {
+                code <<= (l - prev);
+                s_first_code[l] = code;
+                code += s_count[l];
+                prev = l;
+                idx += s_count[l];
+            } else {
+                s_first_code[l] = 0;
+            }
+        }
+        s_first_code[0] = 0;
+        s_first_index[0] = 0;
+        if (s_max_len > 56) s_flags |= kFlagLenTooLong;
+    }
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5;
+    const unsigned lanemask_lt = (1u << lane) - 1;
+    for (uint32_t base = 0; base < k; base += kCbThreads) {
+        const uint32_t i = base + tid;
+        const bool valid = i < k;
+        const uint32_t l = valid ? min(din[i], 64u) : 0xFFu;
+        const unsigned same = __match_any_sync(0xffffffffu, l);
+        const uint32_t rank_w = __popc(same & lanemask_lt);
+        for (int j = lane; j < 65; j += 32) s_wcnt[warp][j] = 0;
+        __syncwarp();
+        if (valid && rank_w == 0) s_wcnt[warp][l] = __popc(same);
+        __syncthreads();
+        // prefix over warps per length (thread t < 65 handles length t)
+        if (tid < 65) {
+            uint32_t run = s_base[tid];
+            for (int w = 0; w < kCbWarps; ++w) {
+                const uint32_t c = s_wcnt[w][tid];
+                s_wcnt[w][tid] = run;
+                run += c;
+            }
+            s_base[tid] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t rank = s_wcnt[warp][l] + rank_w;
+            const uint32_t pos = s_first_index[l] + rank;
+            const uint32_t sym = S.leaf_sym[i];
+            book_sym[pos] = sym;
+            book_len[pos] = (uint8_t)l;
+            const unsigned long long code = s_first_code[l] + rank;
+            enc[sym] = (code << 8) | l;
+        }
+        __syncthreads();
+    }
+    // (6) decode tables ----------------------------------------------------------------
+    if (tid < 65) {
+        canon->first_code[tid] = s_first_code[tid];
+        canon->first_index[tid] = s_first_index[tid];
+        canon->count[tid] = s_count[tid];
+    }
+    __syncthreads();
+    __threadfence_block();
+    for (uint32_t v = tid; v < kLutSize; v += kCbThreads) {
+        uint32_t e = 0;
+        for (int l = 1; l <= kLutBits; ++l) {
+            if (!s_count[l]) continue;
+            const unsigned long long c = v >> (kLutBits - l);
+            if (c >= s_first_code[l] && c - s_first_code[l] < s_count[l]) {
+                // symbol of canonical entry first_index + (c - first_code)
+                e = (book_sym[s_first_index[l] + (uint32_t)(c - s_first_code[l])] << 5) | l;
+                break;
+            }
+        }
+        lut[v] = e;
+    }
+    if (tid == 0) {
+        info->book_size = k;
+        info->total_bits = s_total_bits;
+        info->n_escapes = S.leaf_sym[0] == 0 ? S.leaf_freq[0] : 0;
+        info->max_len = s_max_len;
+        info->flags = s_flags | (k > kMaxBook ? kFlagBookTooBig : 0);
+    }
+}
+
+// Builds the LUT + canonical tables for an existing canonical book (foreign blobs).
+__global__ void __launch_bounds__(1024) k_build_tables(const uint32_t* __restrict__ book_sym,
+                                                       const uint8_t* __restrict__ book_len,
+                                                       uint32_t book_size,
+                                                       CanonTables* __restrict__ canon,
+                                                       uint32_t* __restrict__ lut,
+                                                       unsigned int* flags) {
+    __shared__ unsigned long long s_first_code[65];
+    __shared__ uint32_t s_count[65], s_first_index[65];
+    const int tid = threadIdx.x;
+    if (tid < 65) s_count[tid] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < book_size; i += blockDim.x) atomicAdd(&s_count[book_len[i]], 1u);
+    __syncthreads();
+    if (tid == 0) {
+        // canonical order was validated on the host; codes follow ref huffman.cpp:75-86
+        unsigned long long code = 0;
+        uint32_t prev = 0, idx = 0;
+        for (int l = 1; l <= 64; ++l) {
+            s_first_index[l] = idx;
+            s_first_code[l] = 0;
+            if (s_count[l]) {
+                code <<= (l - prev);
+                s_first_code[l] = code;
+                code += s_count[l];
+                prev = l;
+                idx += s_count[l];
+            }
+        }
+        s_first_code[0] = 0;
+        s_first_index[0] = 0;
+    }
+    __syncthreads();
+    if (tid < 65) {
+        canon->first_code[tid] = s_first_code[tid];
+        canon->first_index[tid] = s_first_index[tid];
+        canon->count[tid] = s_count[tid];
+    }
+    for (uint32_t v = tid; v < kLutSize; v += blockDim.x) {
+        uint32_t e = 0;
+        for (int l = 1; l <= kLutBits; ++l) {
+            if (!s_count[l]) continue;
+            const unsigned long long c = v >> (kLutBits - l);
+            if (c >= s_first_code[l] && c - s_first_code[l] < s_count[l]) {
+                e = (book_sym[s_first_index[l] + (uint32_t)(c - s_first_code[l])] << 5) | l;
+                break;
+            }
+        }
+        lut[v] = e;
+    }
+    (void)flags;
+}
+
+// --------------------------------------------------------------------------- K5 ----
+__device__ __forceinline__ void smem_put_bits(uint32_t* w, uint64_t p, unsigned long long code,
+                                              uint32_t len) {
+    // MSB-first: stream bit p is bit (31 - p%32) of word p/32.
+    const uint32_t o = (uint32_t)(p & 31);
+    const uint64_t wi = p >> 5;
+    if (o + len <= 64) {
+        const unsigned long long v = code << (64 - o - len);
+        const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+        if (hi) atomicOr(&w[wi], hi);
+        if (lo) atomicOr(&w[wi + 1], lo);
+    } else {
+        const uint32_t l2 = o + len - 64;  // bits spilling into the third word
+        const unsigned long long v = code >> l2;  // first 64 - o bits
+        const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+        if (hi) atomicOr(&w[wi], hi);
+        if (lo) atomicOr(&w[wi + 1], lo);
+        const uint32_t tail = (uint32_t)(code & ((1ull << l2) - 1)) << (32 - l2);
+        if (tail) atomicOr(&w[wi + 2], tail);
+    }
+}
+
+__global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
+    extern __shared__ uint32_t stage[];
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_prefix_bits, s_prefix_esc;
+    __shared__ uint32_t s_warp_bits[kEncThreads / 32], s_warp_esc[kEncThreads / 32];
+    __shared__ uint32_t s_tile_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t t0 = (uint64_t)tile * kEncTile;
+    if (t0 >= a.n) return;
+    const uint64_t my0 = t0 + (uint64_t)tid * kEncPer;
+
+    unsigned long long codes[kEncPer];
+    uint32_t lens[kEncPer];
+    uint32_t my_bits = 0, my_esc = 0, escmask = 0;
+#pragma unroll
+    for (int i = 0; i < kEncPer; ++i) {
+        const uint64_t g = my0 + i;
+        if (g < a.n) {
+            const uint32_t s = a.sym[g];
+            const unsigned long long e = __ldg(a.enc + s);
+            codes[i] = e >> 8;
+            lens[i] = (uint32_t)(e & 0xFF);
+            if (s == 0) {
+                ++my_esc;
+                escmask |= 1u << i;
+            }
+        } else {
+            codes[i] = 0;
+            lens[i] = 0;
+        }
+        my_bits += lens[i];
+    }
+    // CTA exclusive scan of (bits, escapes)
+    uint32_t ib = my_bits, ie = my_esc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t tb = __shfl_up_sync(0xffffffffu, ib, o);
+        const uint32_t te = __shfl_up_sync(0xffffffffu, ie, o);
+        if (lane >= o) {
+            ib += tb;
+            ie += te;
+        }
+    }
+    if (lane == 31) {
+        s_warp_bits[warp] = ib;
+        s_warp_esc[warp] = ie;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t rb = 0, re = 0;
+        for (int w = 0; w < kEncThreads / 32; ++w) {
+            const uint32_t b = s_warp_bits[w], e = s_warp_esc[w];
+            s_warp_bits[w] = rb;
+            s_warp_esc[w] = re;
+            rb += b;
+            re += e;
+        }
+        s_tile_total = rb;
+        // decoupled look-back over tiles (serial walk by one thread)
+        TileStatus* st = a.status;
+        volatile TileStatus* vst = st;
+        unsigned long long pb = 0, pe = 0;
+        st[tile].agg_bits = rb;
+        st[tile].agg_esc = re;
+        if (tile == 0) {
+            st[tile].incl_bits = rb;
+            st[tile].incl_esc = re;
+            __threadfence();
+            atomicExch(&st[tile].flag, 2u);
+        } else {
+            __threadfence();
+            atomicExch(&st[tile].flag, 1u);
+            int64_t j = (int64_t)tile - 1;
+            while (j >= 0) {
+                unsigned f;
+                do {
+                    f = vst[j].flag;
+                } while (f == 0);
+                __threadfence();
+                if (f == 2) {
+                    pb += vst[j].incl_bits;
+                    pe += vst[j].incl_esc;
+                    break;
+                }
+                pb += vst[j].agg_bits;
+                pe += vst[j].agg_esc;
+                --j;
+            }
+            st[tile].incl_bits = pb + rb;
+            st[tile].incl_esc = pe + re;
+            __threadfence();
+            atomicExch(&st[tile].flag, 2u);
+        }
+        s_prefix_bits = pb;
+        s_prefix_esc = pe;
+    }
+    __syncthreads();
+    const unsigned long long tile_bit0 = s_prefix_bits;
+    const unsigned long long tile_esc0 = s_prefix_esc;
+    const uint32_t total = s_tile_total;
+    const uint32_t s0 = (uint32_t)(tile_bit0 & 31);
+    const uint32_t nw = (s0 + total + 31) / 32;
+    for (uint32_t i = tid; i < nw + 3; i += kEncThreads) stage[i] = 0;
+    __syncthreads();
+    const uint32_t excl_bits = s_warp_bits[warp] + (ib - my_bits);
+    uint64_t off = (uint64_t)s0 + excl_bits;
+    unsigned long long gbit = tile_bit0 + excl_bits;
+    unsigned long long gesc = tile_esc0 + s_warp_esc[warp] + (ie - my_esc);
+    // next sidecar point at or after my0
+    uint64_t next_side = a.side_bitoff ? ((my0 + a.interval - 1) / a.interval) * a.interval : ~0ull;
+#pragma unroll
+    for (int i = 0; i < kEncPer; ++i) {
+        const uint64_t g = my0 + i;
+        if (g >= a.n) break;
+        if (g == next_side) {
+            a.side_bitoff[g / a.interval] = gbit;
+            a.side_outl[g / a.interval] = (uint32_t)gesc;
+            next_side += a.interval;
+        }
+        smem_put_bits(stage, off, codes[i], lens[i]);
+        if ((escmask >> i) & 1u) {
+            if (a.x) {
+                a.out_index[gesc] = g;
+                a.out_value[gesc] = a.x[g];
+            }
+            ++gesc;
+        }
+        off += lens[i];
+        gbit += lens[i];
+    }
+    __syncthreads();
+    const uint64_t gw0 = tile_bit0 >> 5;
+    for (uint32_t i = tid; i < nw; i += kEncThreads) {
+        const uint64_t gw = gw0 + i;
+        if (gw >= a.nwords) break;
+        const uint32_t v = bswap32(stage[i]);
+        if (i == 0 || i == nw - 1) {
+            if (v) atomicOr(&a.words[gw], v);
+        } else {
+            a.words[gw] = v;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_histogram(const uint32_t* sym, uint64_t n, uint32_t alphabet,
+                             uint32_t center, unsigned long long* hist, int sms, cudaStream_t s,
+                             uint64_t* launches) {
+    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * alphabet, s);
+    if (e != cudaSuccess) return e;
+    uint32_t win_lo = center > kHistWindow / 2 ? center - kHistWindow / 2 : 0;
+    uint32_t win_n = alphabet - win_lo < (uint32_t)kHistWindow ? alphabet - win_lo : kHistWindow;
+    uint64_t blocks = (n / 4 + 511) / 512;
+    const uint64_t cap = (uint64_t)sms * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) blocks = 1;
+    k_histogram<<<(unsigned)blocks, 512, 0, s>>>(sym, n, alphabet, win_lo, win_n, hist);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+size_t codebook_scratch_bytes(uint64_t k) {
+    return align256(4 * k) + 5 * align256(8 * k) + 2 * align256(4 * k) + 4 * align256(8 * k) +
+           4096;
+}
+
+cudaError_t launch_codebook(const unsigned long long* hist, uint32_t alphabet, uint64_t max_leaves,
+                            void* scratch, uint32_t* book_sym, uint8_t* book_len,
+                            unsigned long long* enc, CanonTables* canon, uint32_t* lut,
+                            BookInfo* info, cudaStream_t s, uint64_t* launches) {
+    const size_t smem = kSmemQueue * sizeof(unsigned long long);  // 128 KiB (>= radix table)
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_codebook<<<1, kCbThreads, smem, s>>>(hist, alphabet, max_leaves, scratch, book_sym, book_len,
+                                           enc, canon, lut, info);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_tables(const uint32_t* book_sym, const uint8_t* book_len,
+                                uint32_t book_size, CanonTables* canon, uint32_t* lut,
+                                unsigned int* flags, cudaStream_t s, uint64_t* launches) {
+    k_build_tables<<<1, 1024, 0, s>>>(book_sym, book_len, book_size, canon, lut, flags);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t* launches) {
+    (void)sms;
+    const uint64_t tiles = (a.n + kEncTile - 1) / kEncTile;
+    cudaError_t e = cudaMemsetAsync(a.status, 0, sizeof(TileStatus) * tiles, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    const size_t smem = ((size_t)kEncTile * (a.max_len ? a.max_len : 1) / 32 + 8) * 4;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        e = cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    k_encode<<<(unsigned)tiles, kEncThreads, smem, s>>>(a);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace acz_b200

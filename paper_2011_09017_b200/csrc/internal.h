@@ -1,0 +1,144 @@
+// Internal (non-ABI) interface between the C-ABI layer (api.cu) and the kernel
+// translation units. Host-side launchers return cudaError_t; every launcher counts its
+// kernel launches into *launches so acz_gpu_launch_count can report them.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "acz_gpu.h"
+#include "common.cuh"
+
+namespace acz_b200 {
+
+// Tile-status record for decoupled look-back prefix sums (encode kernel).
+struct TileStatus {
+    unsigned long long agg_bits, agg_esc;    // this tile's aggregates
+    unsigned long long incl_bits, incl_esc;  // inclusive prefixes
+    unsigned int flag;                       // 0 none, 1 aggregate, 2 inclusive
+    unsigned int pad[3];
+};
+
+// Geometry of the plane scan (ref src/codec.cpp:21-34).
+struct PlaneGeom {
+    uint64_t planes, rows, cols, plane_size, n;
+};
+
+PlaneGeom plane_geom(const uint64_t* shape, uint32_t rank);
+
+// ---- stats.cu ----
+cudaError_t launch_stats(const float* x, uint64_t n, uint32_t* bitmap,
+                         unsigned long long* d_nnz, unsigned int* d_flags, double* d_sumabs,
+                         int sms, cudaStream_t s, uint64_t* launches);
+
+// ---- quant.cu ----
+struct QuantArgs {
+    const float* x;
+    PlaneGeom g;
+    double eb, step;
+    uint32_t radius;
+    uint32_t predictor;
+    uint32_t* sym;            // n symbols out
+    float* side_state;        // chain state before every `interval`-th element (PrevValue)
+    uint64_t interval;        // sidecar interval (power of two for PrevValue, plane size for Lorenzo2d)
+    float* row_scratch;       // planes*cols floats (Lorenzo2d only)
+    unsigned int* flags;      // kFlagNonFinite
+};
+cudaError_t launch_quant(const QuantArgs& a, int sms, cudaStream_t s, uint64_t* launches);
+
+// ---- huffman.cu ----
+cudaError_t launch_histogram(const uint32_t* sym, uint64_t n, uint32_t alphabet,
+                             uint32_t center, unsigned long long* hist, int sms, cudaStream_t s,
+                             uint64_t* launches);
+// Workspace needed by launch_codebook for an alphabet of `alphabet` symbols and at most
+// `max_leaves` distinct symbols.
+size_t codebook_scratch_bytes(uint64_t max_leaves);
+cudaError_t launch_codebook(const unsigned long long* hist, uint32_t alphabet, uint64_t max_leaves,
+                            void* scratch, uint32_t* book_sym, uint8_t* book_len,
+                            unsigned long long* enc, CanonTables* canon, uint32_t* lut,
+                            BookInfo* info, cudaStream_t s, uint64_t* launches);
+struct EncodeArgs {
+    const uint32_t* sym;
+    uint64_t n;
+    const unsigned long long* enc;   // dense symbol -> (code << 8 | len)
+    const float* x;                  // for outlier values (nullptr: no outlier output)
+    uint32_t* words;                 // bitstream, big-endian bit order, stored byte-swapped
+    uint64_t nwords;
+    unsigned long long* out_index;
+    float* out_value;
+    unsigned long long* side_bitoff;
+    uint32_t* side_outl;
+    uint64_t interval;
+    uint32_t max_len;
+    TileStatus* status;              // ceil(n / kEncTile) entries, zeroed by the launcher
+    unsigned int* ticket;            // zeroed by the launcher
+};
+constexpr int kEncThreads = 256;
+constexpr int kEncPer = 16;
+constexpr int kEncTile = kEncThreads * kEncPer;
+cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t* launches);
+
+// ---- decode.cu ----
+struct DecodeArgs {
+    const uint32_t* words;
+    uint64_t nwords;
+    uint64_t bit_length;
+    const uint32_t* lut;
+    const CanonTables* canon;
+    const uint32_t* book_sym;
+    uint32_t book_size;
+    const unsigned long long* side_bitoff;
+    const uint32_t* side_outl;
+    const float* side_state;
+    uint64_t interval, nchunks;
+    const unsigned long long* out_index;
+    const float* out_value;
+    uint64_t n_outliers;
+    PlaneGeom g;
+    double eb, step;
+    uint32_t radius;
+    uint32_t predictor;
+    int zero_filter;
+    float* out;
+    float* row_scratch;              // Lorenzo2d
+};
+cudaError_t launch_decode(const DecodeArgs& a, int sms, cudaStream_t s, uint64_t* launches);
+
+// Sequential GPU decode of a whole stream (foreign blobs / generic Huffman decode):
+// records sidecar bit offsets + outlier prefixes every `interval` symbols, optional
+// symbols out, validates against the outlier list. flags: kDec* below.
+constexpr unsigned kDecTruncated = 1u;   // DecodeError "truncated bitstream"
+constexpr unsigned kDecNoMatch = 2u;     // DecodeError "no codeword matches bitstream"
+constexpr unsigned kDecOutlierMissing = 4u;  // FormatError escape without outlier
+constexpr unsigned kDecOutlierIndex = 8u;    // FormatError index mismatch
+constexpr unsigned kDecOutlierUnused = 16u;  // FormatError unused outliers
+struct ScanArgs {
+    const uint32_t* words;
+    uint64_t nwords, bit_length, n;
+    const uint32_t* lut;
+    const CanonTables* canon;
+    const uint32_t* book_sym;
+    const unsigned long long* out_index;  // nullptr: no outlier validation
+    uint64_t n_outliers;
+    uint64_t interval;
+    unsigned long long* side_bitoff;      // may be nullptr
+    uint32_t* side_outl;                  // may be nullptr
+    uint32_t* sym_out;                    // may be nullptr
+    unsigned long long* plane_outl;       // outlier prefix at every plane start (may be nullptr)
+    uint64_t plane_size;
+    unsigned int* flags;
+};
+cudaError_t launch_scan_decode(const ScanArgs& a, cudaStream_t s, uint64_t* launches);
+// Rebuild per-chunk chain states (PrevValue) from decoded symbols: thread per plane.
+cudaError_t launch_chain_states(const uint32_t* sym, const unsigned long long* plane_outl,
+                                const float* out_value, PlaneGeom g, double step,
+                                uint32_t radius, uint64_t interval, float* side_state,
+                                int sms, cudaStream_t s, uint64_t* launches);
+// Build LUT + canonical tables for a given canonical book (device arrays).
+cudaError_t launch_build_tables(const uint32_t* book_sym, const uint8_t* book_len,
+                                uint32_t book_size, CanonTables* canon, uint32_t* lut,
+                                unsigned int* flags, cudaStream_t s, uint64_t* launches);
+
+}  // namespace acz_b200
