@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libacz_gpu.so")
-SOURCES = ["stats.cu", "quant.cu", "huffman.cu", "decode.cu", "api.cu"]
+SOURCES = ["stats.cu", "quant.cu", "quant_spec.cu", "huffman.cu", "decode.cu", "api.cu"]
 HEADERS = ["common.cuh", "internal.h"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")

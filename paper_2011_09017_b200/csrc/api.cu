@@ -47,6 +47,8 @@ struct acz_gpu_ctx {
     size_t ws_book_cap = 0;
     void* ws_side = nullptr;  // sidecar chain states produced by K2
     size_t ws_side_cap = 0;
+    void* ws_qs = nullptr;  // speculative quantiser scratch (look-back status, anchors)
+    size_t ws_qs_cap = 0;
     // small fixed device block
     struct Small {
         BookInfo info;
@@ -346,7 +348,7 @@ int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
     if (!ctx) return ACZ_ERR_INVALID;
     cudaDeviceSynchronize();
     for (void* p : {ctx->ws_sym, ctx->ws_hist, ctx->ws_enc, ctx->ws_cb, ctx->ws_status,
-                    ctx->ws_row, ctx->ws_io, ctx->ws_aux, ctx->ws_book, ctx->ws_side})
+                    ctx->ws_row, ctx->ws_io, ctx->ws_aux, ctx->ws_book, ctx->ws_side, ctx->ws_qs})
         if (p) cudaFree(p);
     if (ctx->d_small) cudaFree(ctx->d_small);
     if (ctx->h_small) cudaFreeHost(ctx->h_small);
@@ -503,7 +505,12 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
     qa.flags = &sm->flags;
     {
         KTimer kt(ctx, ACZ_K_QUANT, s);
-        CK(launch_quant(qa, ctx->sms, s, &ctx->launches));
+        if (quant_spec_applicable(predictor, g.plane_size) && !std::getenv("ACZ_SERIAL_QUANT")) {
+            CK(grow(&ctx->ws_qs, &ctx->ws_qs_cap, quant_spec_scratch_bytes(g.planes, g.plane_size)));
+            CK(launch_quant_spec(qa, ctx->ws_qs, s, &ctx->launches));
+        } else {
+            CK(launch_quant(qa, ctx->sms, s, &ctx->launches));
+        }
     }
     rc = build_book(ctx, qa.sym, n, alphabet, quant_radius, s);
     if (rc) return rc;

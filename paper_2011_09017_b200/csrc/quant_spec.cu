@@ -1,0 +1,598 @@
+// K2 (long planes): exact PrevValue quantiser by speculation + certified walk.
+//
+// The reference recurrence (src/codec.cpp:76-104) is serial per plane: every prediction
+// reads the previous element's reconstructed float, computed in double and rounded to
+// float. Bit-exact symbols need that recurrence, so this kernel
+// reproduces it exactly with intra-plane parallelism (design validated by
+// tools/proto/walk2.cpp on CPU):
+//
+// Segment = up to 2048 elements of one plane, owned by one warp (CTA = 32 threads).
+// Phase A (speculate, all lanes): lane l owns the range that starts right after the first
+//   "anchor" (|x| in the tensor's top frequent binade B) of its 64-element window. The
+//   range's speculative chain starts from the lattice guess g = RN32(lam + K*step) of the
+//   anchor. Because the anchor's true output lies on the same coarse float grid, the true
+//   chain differs from the speculative one by an offset D that is a multiple of that grid,
+//   and translation by D commutes with every rounding in the recurrence except at a few
+//   statically detectable "candidate" elements: fragile decision/acceptance margins
+//   (<= 2*Tmax), outputs above the anchor binade or near a binade edge, exact RNE ties,
+//   collapse re-expansions without a certificate, escapes, range starts, sidecar points.
+// Phase B (walk, warp-parallel): the exact offset is carried range to range (D of range k
+//   = exit of range k-1 - g_k). Lanes evaluate 32 candidate events at once with the exact
+//   reference step from the true pre-state (s + D, or the true collapsed residual); the
+//   first lane whose exact result is not the translated speculative one applies its state
+//   change, the rest of the batch is re-evaluated. Too-large or too-fine offsets switch to
+//   dense mode (every element visited); a lattice change at a range start (after an escape)
+//   re-speculates the remaining ranges from the exact state ("rebase").
+// Segments of one plane chain their exact exit states through a decoupled look-back in
+// ticket order (deadlock-free).
+#include "internal.h"
+
+namespace acz_b200 {
+
+namespace {
+
+constexpr int kW = 32;
+constexpr int kL = 64;
+constexpr int kSeg = kW * kL;
+constexpr int kExt = 2 * kL;
+constexpr int kCap = kSeg + kExt;
+constexpr int kCapW = (kCap + 31) / 32;
+
+struct SP {
+    double eb, step, radius_d, Tmax;
+    long long R;
+    float anchor_min;
+    int B;  // anchor binade exponent
+    uint64_t P, nseg, interval;
+};
+
+struct XS {
+    uint32_t sym;
+    float out;
+    double pre;
+    double t, q;
+};
+
+// The reference step, exactly (ref src/codec.cpp:80-101).
+__device__ __forceinline__ XS xstep(float xf, double pred, const SP& p) {
+    XS r;
+    const double orig = (double)xf;
+    r.t = __ddiv_rn(__dsub_rn(orig, pred), p.step);
+    r.q = round(r.t);
+    r.sym = 0;
+    r.out = xf;
+    r.pre = 0.0;
+    if (fabs(r.q) < p.radius_d) {
+        const double y = __dadd_rn(pred, __dmul_rn(r.q, p.step));
+        const float cand = __double2float_rn(y);
+        if (isfinite(cand) && fabs(__dsub_rn(orig, (double)cand)) <= p.eb) {
+            r.sym = (uint32_t)((long long)r.q + p.R);
+            r.out = cand;
+            r.pre = y;
+        }
+    }
+    return r;
+}
+
+__device__ __forceinline__ int fexp(double v) {  // floor(log2 |v|), v != 0 finite
+    return ((__double2hiint(v) >> 20) & 0x7FF) - 1023;
+}
+
+// exponent of the lowest set bit of D (granularity); huge for 0
+__device__ __forceinline__ int gran(double D) {
+    if (D == 0.0) return 100000;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(D);
+    const int e = (int)((b >> 52) & 0x7FF);
+    const unsigned long long m = (b & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+    return e - 1075 + __ffsll((long long)m) - 1;
+}
+
+__device__ __forceinline__ bool is_anchor(float v, float amin) { return fabsf(v) >= amin; }
+
+__device__ __forceinline__ float lattice_guess(double lam, float xa, const SP& p) {
+    const double K = round(__ddiv_rn(__dsub_rn((double)xa, lam), p.step));
+    return __double2float_rn(__dadd_rn(lam, __dmul_rn(K, p.step)));
+}
+
+// First range start of segment j of a plane (plane coordinates), see phase A notes.
+__device__ __forceinline__ uint64_t seg_bound(const float* xp, uint64_t j, const SP& p) {
+    if (j == 0) return 0;
+    const uint64_t b = j * kSeg;
+    if (b >= p.P) return p.P;
+    const uint64_t e = min(p.P, b + kExt);
+    for (uint64_t i = b; i < e; ++i)
+        if (is_anchor(__ldg(xp + i), p.anchor_min)) return i + 1;
+    return e;
+}
+
+struct Smem {
+    float s[kCap];
+    uint32_t sym[kCap];
+    uint32_t cand[kCapW];
+    int rstart[kW + 1];   // segment-relative range starts (sorted), rstart[nr] = len
+    float guess[kW];      // speculative entry state of each range
+    float send[kW];       // speculative exit (state after the last element)
+    double C[kW];         // prefix of (send[k-1] - guess[k])
+    int nr;
+    int forced[kW];       // range start is not an anchor-aligned guess
+};
+
+// Speculative chain over range k (phase A) from its guess; writes s, sym, candidate bits.
+__device__ void spec_range(Smem& S, const float* xp, uint64_t seg0, int k, const SP& p,
+                           uint64_t plane_flat0, unsigned* flags) {
+    const int b = S.rstart[k], e = S.rstart[k + 1];
+    float r = S.guess[k];
+    bool collapsed = false;
+    double ycol = 0.0;
+    bool bad = false;
+    for (int i = b; i < e; ++i) {
+        const uint64_t pi = seg0 + (uint64_t)i;  // plane index
+        const float xf = __ldg(xp + pi);
+        bad |= !isfinite(xf);
+        const double pred = pi == 0 ? 0.0 : (double)r;
+        const XS o = xstep(xf, pred, p);
+        bool c = (i == b);
+        if (o.sym == 0) {
+            c = true;
+            collapsed = false;
+        } else {
+            const double dm = (0.5 - fabs(o.t - o.q)) * p.step;
+            const double am = p.eb - fabs((double)xf - (double)o.out);
+            if (fmin(dm, am) <= 2.0 * p.Tmax) c = true;
+            if (fabs(o.q) >= p.radius_d - 1.0) c = true;
+            if (o.q == 0.0 && collapsed) {
+                // identity inside a collapsed run
+            } else if (fabs((double)o.out) < p.eb) {
+                collapsed = true;
+                ycol = o.pre;
+                // the lazy collapse formula RN32(pre + D) needs pre == prev + q*step exactly
+                if (__dsub_rn(o.pre, pred) != __dmul_rn(o.q, p.step)) c = true;
+            } else {
+                const int ex = fexp((double)o.out);
+                if (ex > p.B) c = true;
+                const double a = fabs((double)o.out), lo = ldexp(1.0, ex);
+                if (a - lo <= 2.0 * p.Tmax || 2.0 * lo - a <= 2.0 * p.Tmax) c = true;
+                const double half = ldexp(1.0, fexp(o.pre) - 24);
+                if (fabs(o.pre - (double)o.out) == half) c = true;  // exact RNE tie
+                if (collapsed) {
+                    // re-expansion certificate for any |D| <= Tmax
+                    const double dmax =
+                        ldexp(1.0, fexp(2.0 * fmax(fabs(ycol), 2.0 * p.Tmax)) - 22);
+                    const double u = ldexp(1.0, fexp(o.pre) - 23);
+                    const double fr = fabs(fmod(fabs(o.pre), u) - 0.5 * u);
+                    if (!(fr > dmax + ldexp(fabs(o.pre), -50))) c = true;
+                }
+                collapsed = false;
+            }
+        }
+        if (((plane_flat0 + pi) % p.interval) == 0) c = true;  // sidecar point
+        S.s[i] = o.out;
+        S.sym[i] = o.sym;
+        if (c) atomicOr(&S.cand[i >> 5], 1u << (i & 31));
+        r = o.out;
+    }
+    S.send[k] = r;
+    if (bad) atomicOr(flags, kFlagNonFinite);
+}
+
+// Phase A for ranges k0.. with lattice origin lam (all lanes participate).
+__device__ void phase_a(Smem& S, const float* xp, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
+                        float k0_entry, const SP& p, uint64_t plane_flat0, unsigned* flags) {
+    const int lane = threadIdx.x;
+    // clear candidate bits of the affected span
+    const int b0 = S.rstart[k0];
+    for (int w = (b0 >> 5) + lane; w < kCapW; w += kW) {
+        uint32_t keep = 0;
+        if (w == (b0 >> 5)) keep = (b0 & 31) ? ((1u << (b0 & 31)) - 1) : 0u;
+        S.cand[w] &= keep;
+    }
+    __syncwarp();
+    for (int k = k0 + lane; k < S.nr; k += kW) {
+        const int st = S.rstart[k];
+        if (k == k0 && lam_exact_k0) {
+            S.guess[k] = k0_entry;
+        } else if (seg0 + (uint64_t)st == 0) {
+            S.guess[k] = 0.0f;
+        } else {
+            S.guess[k] = lattice_guess(lam, __ldg(xp + seg0 + st - 1), p);
+        }
+        spec_range(S, xp, seg0, k, p, plane_flat0, flags);
+    }
+    __syncwarp();
+    // prefix C[k] = sum_{j<=k, j>0} (send[j-1] - guess[j])
+    if (lane == 0) {
+        double acc = 0.0;
+        for (int k = 0; k < S.nr; ++k) {
+            if (k > 0) acc += (double)S.send[k - 1] - (double)S.guess[k];
+            S.C[k] = acc;
+        }
+    }
+    __syncwarp();
+}
+
+// Top frequent binade of a tensor from a strided sample: the largest e with
+// #(|x| >= 2^e) >= max(1, nonzero/32). Writes B to *out (one CTA).
+__global__ void __launch_bounds__(256) k_anchor_binade(const float* __restrict__ x, uint64_t n,
+                                                      int* out) {
+    __shared__ unsigned cnt[300];
+    for (int i = threadIdx.x; i < 300; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const uint64_t samples = n < 65536 ? n : 65536;
+    const uint64_t stride = n / samples;
+    for (uint64_t s = threadIdx.x; s < samples; s += blockDim.x) {
+        const float v = fabsf(__ldg(x + s * stride));
+        if (v > 0.0f && isfinite(v)) {
+            int e = ((__float_as_int(v) >> 23) & 0xFF) - 127;
+            atomicAdd(&cnt[e + 150], 1u);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int i = 0; i < 300; ++i) tot += cnt[i];
+        const unsigned need = tot / 32 > 0 ? tot / 32 : 1;
+        unsigned acc = 0;
+        int B = -126;
+        for (int i = 299; i >= 0; --i) {
+            acc += cnt[i];
+            if (acc >= need) {
+                B = i - 150;
+                break;
+            }
+        }
+        *out = B;
+    }
+}
+
+__global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, SP p, const int* dB,
+                                                   uint32_t* __restrict__ sym_out,
+                                                   float* __restrict__ side_state,
+                                                   unsigned int* __restrict__ status,
+                                                   float* __restrict__ exits,
+                                                   unsigned int* ticket, unsigned int* flags,
+                                                   unsigned long long total_segs) {
+    __shared__ Smem S;
+    __shared__ unsigned s_tk;
+    const int lane = threadIdx.x;
+    {
+        const int B = *dB;
+        p.B = B;
+        p.anchor_min = ldexpf(1.0f, B) * (1.0f + 1.0f / 64.0f);
+        p.Tmax = fmin(ldexp(1.0, B - 23) * 32.0, p.eb / 8.0);
+    }
+    if (lane == 0) s_tk = atomicAdd(ticket, 1u);
+    __syncwarp();
+    const unsigned long long seg_id = s_tk;
+    if (seg_id >= total_segs) return;
+    const uint64_t plane = seg_id / p.nseg, j = seg_id % p.nseg;
+    const float* xp = x + plane * p.P;
+    const uint64_t plane_flat0 = plane * p.P;
+
+    // ---- segment geometry -------------------------------------------------------
+    const uint64_t b0 = seg_bound(xp, j, p);           // first range start
+    const uint64_t b1 = seg_bound(xp, j + 1, p);       // next segment's first start
+    const uint64_t seg0 = b0;
+    const int len = (int)(b1 - b0);
+    if (len <= 0) {
+        // empty segment (plane too short for this index): pass the state through
+        if (lane == 0) {
+            float tin = 0.0f;
+            if (j > 0) {
+                volatile unsigned* vf = status + seg_id - 1;
+                while (*vf == 0) {
+                }
+                __threadfence();
+                tin = *((volatile float*)exits + seg_id - 1);
+            }
+            exits[seg_id] = tin;
+            __threadfence();
+            atomicExch(status + seg_id, 1u);
+        }
+        return;
+    }
+    // lane windows: lane l > 0 starts after the first anchor in
+    // [max(j*Seg + l*L, b0), j*Seg + (l+1)*L) if that start lies before b1
+    int my_start = -1;
+    if (lane == 0) {
+        my_start = 0;
+    } else {
+        const uint64_t w0 = max(j * kSeg + (uint64_t)lane * kL, b0);
+        const uint64_t w1 = min(j * kSeg + (uint64_t)(lane + 1) * kL, b1);
+        for (uint64_t i = w0; i < w1; ++i)
+            if (is_anchor(__ldg(xp + i), p.anchor_min)) {
+                if (i + 1 < b1) my_start = (int)(i + 1 - seg0);
+                break;
+            }
+    }
+    const unsigned has = __ballot_sync(0xffffffffu, my_start >= 0);
+    const int nr = __popc(has);
+    const int my_k = __popc(has & ((1u << lane) - 1));
+    if (my_start >= 0) {
+        S.rstart[my_k] = my_start;
+        S.forced[my_k] = 0;
+    }
+    if (lane == 0) {
+        S.nr = nr;
+        S.rstart[nr] = len;
+        // the segment's first range starts at a forced (non-anchor) boundary?
+        bool forced = false;
+        if (j > 0) {
+            const float xa = __ldg(xp + b0 - 1);
+            forced = !is_anchor(xa, p.anchor_min);
+        }
+        S.forced[0] = forced ? 1 : 0;
+    }
+    for (int w = lane; w < kCapW; w += kW) S.cand[w] = 0;
+    __syncwarp();
+
+    // ---- phase A: speculate all ranges (lattice origin 0: plane-start lattice) ----
+    phase_a(S, xp, seg0, 0, 0.0, false, 0.0f, p, plane_flat0, flags);
+
+    // ---- entry state from the predecessor segment (decoupled look-back) ----------
+    float tin = 0.0f;
+    if (j > 0) {
+        if (lane == 0) {
+            volatile unsigned* vf = status + seg_id - 1;
+            while (*vf == 0) {
+            }
+            __threadfence();
+            tin = *((volatile float*)exits + seg_id - 1);
+        }
+        tin = __shfl_sync(0xffffffffu, tin, 0);
+    }
+    // offset of range 0
+    double D = (j == 0) ? 0.0 : __dsub_rn((double)tin, (double)S.guess[0]);
+    if (j > 0 && (fabs(D) > p.Tmax || gran(D) < p.B - 23)) {
+        // lattice differs (escape upstream) or guess too far: re-speculate from tin
+        phase_a(S, xp, seg0, 0, (double)tin, true, tin, p, plane_flat0, flags);
+        D = 0.0;
+    }
+    int rcur = 0;          // range the offset D refers to
+    bool exact_mode = false;  // EXACT: the true state T is tracked explicitly
+    float T = 0.0f;
+    int pos = 0;           // next position to consider
+    __shared__ int s_vis[kW];
+
+    auto range_of = [&](int q) {
+        int k = 0;
+        while (k + 1 < S.nr && S.rstart[k + 1] <= q) ++k;
+        return k;
+    };
+    auto okD = [&](double d) {
+        return d == 0.0 || (fabs(d) <= p.Tmax && gran(d) >= p.B - 23);
+    };
+    // spec pre-value of element c of range kc: RN64(prev + q*step)
+    auto spec_pre = [&](int c, int kc) -> double {
+        const double prev = (c == S.rstart[kc]) ? (double)S.guess[kc] : (double)S.s[c - 1];
+        const double q = (double)((long long)S.sym[c] - p.R);
+        return __dadd_rn(prev, __dmul_rn(q, p.step));
+    };
+    auto is_coll = [&](int c) { return S.sym[c] != 0 && fabs((double)S.s[c]) < p.eb; };
+
+    while (pos < len) {
+        if (exact_mode) {
+            const int k = range_of(pos);
+            if (pos == S.rstart[k] && pos > 0) {
+                // exact entry T at a range start: resume translation (rebase if needed)
+                const double Dk = __dsub_rn((double)T, (double)S.guess[k]);
+                if (!okD(Dk)) {
+                    phase_a(S, xp, seg0, k, (double)T, true, T, p, plane_flat0, flags);
+                    D = 0.0;
+                } else {
+                    D = Dk;
+                }
+                rcur = k;
+                exact_mode = false;
+                continue;
+            }
+            const uint64_t pi = seg0 + (uint64_t)pos;
+            const float tprev = T;
+            const XS ex = xstep(__ldg(xp + pi), pi == 0 ? 0.0 : (double)tprev, p);
+            if (lane == 0) {
+                S.sym[pos] = ex.sym;
+                const uint64_t flat = plane_flat0 + pi;
+                if (flat % p.interval == 0) side_state[flat / p.interval] = pi == 0 ? 0.0f : tprev;
+            }
+            __syncwarp();
+            T = ex.out;
+            const float ss = S.s[pos];
+            if (fabs((double)T) >= p.eb && fabs((double)ss) >= p.eb) {
+                const double Dn = __dsub_rn((double)T, (double)ss);
+                if (okD(Dn)) {
+                    D = Dn;
+                    rcur = k;
+                    exact_mode = false;
+                }
+            }
+            ++pos;
+            continue;
+        }
+        // ---- TRANSLATE: gather the next 32 candidate positions -----------------------
+        {
+            const int w = (pos >> 5) + lane;
+            uint32_t bits = (w < kCapW) ? S.cand[w] : 0u;
+            if (lane == 0) bits &= ~((1u << (pos & 31)) - 1u);
+            const int c = __popc(bits);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            int r = incl - c;
+            while (bits && r < kW) {
+                const int b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                s_vis[r++] = (w << 5) + b;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            __syncwarp();
+            if (lane >= total) s_vis[lane] = len;
+            __syncwarp();
+            if (total == 0) {
+                // no candidates in this 1024-position window: skip it
+                pos = min(len, (((pos >> 5) + kW) << 5));
+                continue;
+            }
+        }
+        int vp = s_vis[lane];
+        if (vp > len) vp = len;
+        const bool active = vp < len;
+        bool ok = true, rebase = false;
+        XS ex;
+        ex.sym = 0;
+        ex.out = 0.0f;
+        float tprev = 0.0f;
+        double Dp = D;
+        int kv = rcur;
+        if (active) {
+            kv = range_of(vp);
+            Dp = __dadd_rn(D, __dsub_rn(S.C[kv], S.C[rcur]));
+            const uint64_t pi = seg0 + (uint64_t)vp;
+            if (vp == S.rstart[kv] && kv > 0 && !okD(Dp)) {
+                ok = false;
+                rebase = true;
+                tprev = __double2float_rn(__dadd_rn((double)S.guess[kv], Dp));
+            } else {
+                bool prev_coll = false;
+                if (vp == S.rstart[kv]) {
+                    tprev = (pi == 0) ? 0.0f
+                                      : __double2float_rn(__dadd_rn((double)S.guess[kv], Dp));
+                } else if (is_coll(vp - 1)) {
+                    int c = vp - 1;
+                    while (c > S.rstart[kv] && S.sym[c] == (uint32_t)p.R && is_coll(c - 1)) --c;
+                    prev_coll = true;
+                    tprev = __double2float_rn(__dadd_rn(spec_pre(c, kv), Dp));
+                } else {
+                    tprev = __double2float_rn(__dadd_rn((double)S.s[vp - 1], Dp));
+                }
+                ex = xstep(__ldg(xp + pi), pi == 0 ? 0.0 : (double)tprev, p);
+                const uint32_t ssym = S.sym[vp];
+                const float ss = S.s[vp];
+                if (ex.sym != ssym) {
+                    ok = false;
+                } else if (ex.sym == 0) {
+                    ok = Dp == 0.0;  // both escape to x; the offset becomes 0
+                } else if (fabs((double)ex.out) < p.eb) {
+                    if (fabs((double)ss) >= p.eb) ok = false;
+                    else if (ssym == (uint32_t)p.R && prev_coll) ok = ex.out == tprev;
+                    else ok = ex.out == __double2float_rn(__dadd_rn(spec_pre(vp, kv), Dp));
+                } else {
+                    ok = fabs((double)ss) >= p.eb &&
+                         __dsub_rn((double)ex.out, (double)ss) == Dp;
+                }
+            }
+        }
+        const unsigned fail = __ballot_sync(0xffffffffu, active && !ok);
+        const int f = fail ? __ffs(fail) - 1 : 32;
+        if (active && lane < f) {
+            const uint64_t flat = plane_flat0 + seg0 + (uint64_t)vp;
+            if (flat % p.interval == 0) side_state[flat / p.interval] = (seg0 + vp == 0) ? 0.0f : tprev;
+        }
+        if (f < 32) {
+            const int fvp = __shfl_sync(0xffffffffu, vp, f);
+            const int fk = __shfl_sync(0xffffffffu, kv, f);
+            const int frb = __shfl_sync(0xffffffffu, (int)rebase, f);
+            const float ftp = __shfl_sync(0xffffffffu, tprev, f);
+            if (frb) {
+                // lattice changed at range start fk: re-speculate ranges >= fk from the
+                // exact entry state and re-evaluate from fvp
+                phase_a(S, xp, seg0, fk, (double)ftp, true, ftp, p, plane_flat0, flags);
+                D = 0.0;
+                rcur = fk;
+                pos = fvp;
+                continue;
+            }
+            const float fout = __shfl_sync(0xffffffffu, ex.out, f);
+            const uint32_t fsym = __shfl_sync(0xffffffffu, ex.sym, f);
+            if (lane == f) {
+                S.sym[fvp] = fsym;
+                const uint64_t flat = plane_flat0 + seg0 + (uint64_t)fvp;
+                if (flat % p.interval == 0) side_state[flat / p.interval] = (seg0 + fvp == 0) ? 0.0f : ftp;
+            }
+            __syncwarp();
+            const float fss = S.s[fvp];
+            rcur = fk;
+            const double Dn = __dsub_rn((double)fout, (double)fss);
+            if (fabs((double)fout) >= p.eb && fabs((double)fss) >= p.eb && okD(Dn)) {
+                D = Dn;
+            } else {
+                exact_mode = true;
+                T = fout;
+            }
+            pos = fvp + 1;
+        } else {
+            const unsigned act = __ballot_sync(0xffffffffu, active);
+            if (!act) break;
+            const int hl = 31 - __clz(act);
+            pos = __shfl_sync(0xffffffffu, vp, hl) + 1;
+        }
+    }
+    // ---- exit state ----------------------------------------------------------------
+    float texit;
+    if (exact_mode) {
+        texit = T;
+    } else {
+        const int kl = S.nr - 1;
+        const double Dl = __dadd_rn(D, __dsub_rn(S.C[kl], S.C[rcur]));
+        const int last = len - 1;
+        if (is_coll(last)) {
+            int c = last;
+            while (c > S.rstart[kl] && S.sym[c] == (uint32_t)p.R && is_coll(c - 1)) --c;
+            texit = __double2float_rn(__dadd_rn(spec_pre(c, kl), Dl));
+        } else {
+            texit = __double2float_rn(__dadd_rn((double)S.s[last], Dl));
+        }
+    }
+    if (lane == 0) {
+        exits[seg_id] = texit;
+        __threadfence();
+        atomicExch(status + seg_id, 1u);
+    }
+    // ---- symbols out (coalesced) ----------------------------------------------------
+    uint32_t* so = sym_out + plane_flat0 + seg0;
+    for (int i = lane; i < len; i += kW) so[i] = S.sym[i];
+}
+
+}  // namespace
+
+// Host launcher. `scratch` must hold quant_spec_scratch_bytes(planes, plane_size).
+cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
+                              uint64_t* launches) {
+    SP p;
+    p.eb = a.eb;
+    p.step = a.step;
+    p.radius_d = (double)a.radius;
+    p.R = a.radius;
+    p.B = 0;
+    p.anchor_min = 1.0f;
+    p.Tmax = 0.0;
+    p.P = a.g.plane_size;
+    p.nseg = (p.P + kSeg - 1) / kSeg;
+    p.interval = a.interval;
+    const unsigned long long total = (unsigned long long)a.g.planes * p.nseg;
+    char* sc = static_cast<char*>(scratch);
+    int* dB = reinterpret_cast<int*>(sc);
+    unsigned* ticket = reinterpret_cast<unsigned*>(sc + 16);
+    unsigned* status = reinterpret_cast<unsigned*>(sc + 256);
+    float* exits = reinterpret_cast<float*>(sc + 256 + ((4 * total + 255) & ~255ull));
+    cudaError_t e = cudaMemsetAsync(sc, 0, 256 + ((4 * total + 255) & ~255ull), s);
+    if (e != cudaSuccess) return e;
+    k_anchor_binade<<<1, 256, 0, s>>>(a.x, a.g.n, dB);
+    ++*launches;
+    k_quant_spec<<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym, a.side_state, status, exits,
+                                                ticket, a.flags, total);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+size_t quant_spec_scratch_bytes(uint64_t planes, uint64_t plane_size) {
+    const uint64_t total = planes * ((plane_size + kSeg - 1) / kSeg);
+    return 256 + 2 * ((4 * total + 255) & ~255ull);
+}
+
+bool quant_spec_applicable(uint32_t predictor, uint64_t plane_size) {
+    return predictor == ACZ_PRED_PREV && plane_size > 1024;
+}
+
+}  // namespace acz_b200
