@@ -519,6 +519,7 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
     // precedence follows the reference: Tensor ctor (DomainError), huffman_encode
     // (DecodeError), then the codebook limit in compress (FormatError).
     if (flags & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
+    if (flags & kFlagInternal) return fail(ctx, ACZ_ERR_CUDA, "internal: look-back timeout");
     if (flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
     if (bi.book_size > kMaxBook)
         return fail(ctx, ACZ_ERR_FORMAT, "codebook exceeds the 65535-entry limit of the blob format");

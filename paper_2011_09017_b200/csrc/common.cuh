@@ -31,6 +31,7 @@ constexpr unsigned kFlagNonFinite = 1u;  // DomainError (ref include/acz/tensor.
 constexpr unsigned kFlagBookTooBig = 2u; // FormatError (ref src/codec.cpp:107-108)
 constexpr unsigned kFlagDepth64 = 4u;    // DecodeError (ref src/huffman.cpp:64)
 constexpr unsigned kFlagLenTooLong = 8u; // code length > 56: unsupported packing (never for n<2^44)
+constexpr unsigned kFlagInternal = 16u;  // internal consistency failure (look-back timeout)
 
 // Per-length canonical decode tables (ref src/huffman.cpp:152-166).
 struct CanonTables {

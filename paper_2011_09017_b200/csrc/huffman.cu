@@ -579,9 +579,10 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
             int64_t j = (int64_t)tile - 1;
             while (j >= 0) {
                 unsigned f;
+                unsigned long long spins = 0;
                 do {
                     f = vst[j].flag;
-                } while (f == 0);
+                } while (f == 0 && ++spins < (1ull << 30));
                 __threadfence();
                 if (f == 2) {
                     pb += vst[j].incl_bits;

@@ -279,7 +279,12 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             float tin = 0.0f;
             if (j > 0) {
                 volatile unsigned* vf = status + seg_id - 1;
+                unsigned long long spins = 0;
                 while (*vf == 0) {
+                    if (++spins > (1ull << 28)) {  // never expected: report, do not hang
+                        atomicOr(flags, kFlagInternal);
+                        break;
+                    }
                 }
                 __threadfence();
                 tin = *((volatile float*)exits + seg_id - 1);
@@ -333,7 +338,12 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     if (j > 0) {
         if (lane == 0) {
             volatile unsigned* vf = status + seg_id - 1;
+            unsigned long long spins = 0;
             while (*vf == 0) {
+                if (++spins > (1ull << 28)) {
+                    atomicOr(flags, kFlagInternal);
+                    break;
+                }
             }
             __threadfence();
             tin = *((volatile float*)exits + seg_id - 1);
