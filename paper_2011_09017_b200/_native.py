@@ -61,6 +61,7 @@ SIGNATURES = [
                                          _vp, _vp]),
     ("acz_gpu_profile_enable", C.c_int, [_vp, C.c_int]),
     ("acz_gpu_profile_read", C.c_int, [_vp, C.POINTER(C.c_double), _u64p]),
+    ("acz_gpu_debug_counters", C.c_int, [_vp, _u64p, C.c_uint32, C.c_int]),
     ("acz_gpu_debug_last_symbols", C.c_int, [_vp, _vp, C.c_uint64, _vp]),
     ("acz_gpu_launch_count", C.c_uint64, [_vp]),
 ]

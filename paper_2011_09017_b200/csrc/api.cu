@@ -198,7 +198,10 @@ uint64_t sidecar_interval_default() {
     static uint64_t v = [] {
         const char* s = std::getenv("ACZ_SIDECAR_INTERVAL");
         uint64_t x = s ? std::strtoull(s, nullptr, 10) : 0;
-        return x ? x : (uint64_t)256;
+        if (!x) x = 256;
+        uint64_t p2 = 1;
+        while (p2 * 2 <= x) p2 *= 2;  // power of two (mask arithmetic in the kernels)
+        return p2;
     }();
     return v;
 }
@@ -478,9 +481,7 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
     if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "compress: empty tensor");
     const PlaneGeom g = plane_geom(shape, rank);
     const uint32_t alphabet = 2u * quant_radius;
-    const uint64_t interval = predictor == ACZ_PRED_PREV
-                                  ? std::min<uint64_t>(sidecar_interval_default(), n)
-                                  : g.plane_size;
+    const uint64_t interval = predictor == ACZ_PRED_PREV ? sidecar_interval_default() : g.plane_size;
     const uint64_t nchunks = (n + interval - 1) / interval;
 
     CK(grow(&ctx->ws_sym, &ctx->ws_sym_cap, 4ull * n));
@@ -801,8 +802,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
             dmsg = "invalid code length in codebook";
         }
     const PlaneGeom g = plane_geom(in.shape, in.rank);
-    const uint64_t interval = pred == ACZ_PRED_PREV ? std::min<uint64_t>(sidecar_interval_default(), count)
-                                                    : g.plane_size;
+    const uint64_t interval = pred == ACZ_PRED_PREV ? sidecar_interval_default() : g.plane_size;
     // sidecar supplied?
     bool have_side = false;
     uint64_t side_interval = interval, side_chunks = (count + interval - 1) / interval;
@@ -1177,6 +1177,14 @@ int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches) {
 }
 
 // --------------------------------------------------------------------------- debug --
+int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset) {
+    if (!ctx || !out || n < 8) return ACZ_ERR_INVALID;
+    unsigned long long v[8];
+    CK(quant_spec_stats(v, reset != 0));
+    for (int i = 0; i < 8; ++i) out[i] = v[i];
+    return ACZ_OK;
+}
+
 int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, void* stream) {
     if (!ctx || !d_out) return ACZ_ERR_INVALID;
     if (n != ctx->last_n || !ctx->ws_sym) return fail(ctx, ACZ_ERR_SHAPE, "no symbols of that size");

@@ -96,37 +96,141 @@ __device__ __forceinline__ void load_tables(const uint32_t* lut, const CanonTabl
     __syncthreads();
 }
 
+// Exact RN32 of a double kept in a double register (no F2F on the dependency chain):
+// adding and subtracting 1.5 * 2^(e+29) rounds y to 24 significant bits, ties to even.
+// Valid for y in the float normal range; other inputs take the conversion path.
+__device__ __forceinline__ double rn32_in_double(double y) {
+    const int hi = __double2hiint(y);
+    const int ex = (hi >> 20) & 0x7FF;
+    if (ex < 1023 - 126 || ex > 1023 + 127) return (double)__double2float_rn(y);
+    const double M = __hiloint2double((ex << 20) + ((29 << 20) | (1 << 19)), 0);
+    return __dsub_rn(__dadd_rn(y, M), M);
+}
+
+// Canonical decode limits (left-aligned): the code length of a 64-bit window w is the
+// smallest l with (w >> (64 - l)) < limit[l]; codes of length l are [nc[l], limit[l]).
+struct Limits {
+    unsigned long long nc[65];
+    unsigned long long lim[65];
+    int maxlen;
+};
+
+__device__ __forceinline__ void build_limits(const CanonTables& ct, Limits* L) {
+    if (threadIdx.x == 0) {
+        unsigned long long nc = 0;
+        L->nc[0] = 0;
+        L->lim[0] = 0;
+        for (int l = 1; l <= 64; ++l) {
+            nc = (l == 1) ? 0 : ((L->nc[l - 1] + ct.count[l - 1]) << 1);
+            L->nc[l] = nc;
+            L->lim[l] = nc + ct.count[l];
+            if (ct.count[l]) L->maxlen = l;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128) k_decode_prev(DecodeArgs a) {
     __shared__ uint32_t s_lut[kLutSize];
     __shared__ CanonTables s_ct;
+    __shared__ Limits s_lim;
     load_tables(a.lut, a.canon, s_lut, &s_ct);
+    build_limits(s_ct, &s_lim);
+    __syncthreads();
     const uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (chunk >= a.nchunks) return;
     const uint64_t start = chunk * a.interval;
     const uint64_t end = min(a.g.n, start + a.interval);
     uint64_t pos = a.side_bitoff[chunk];
     uint32_t oi = a.side_outl[chunk];
-    float r = a.side_state[chunk];
+    double r = (double)a.side_state[chunk];
     const uint64_t P = a.g.plane_size;
     uint64_t pin = start % P;
-    const long long R = a.radius;
-    BitReader br;
-    br.init(a.words, a.nwords, pos);
-    for (uint64_t flat = start; flat < end; ++flat) {
-        uint32_t sym = 0;
-        decode_one(br, pos, s_lut, s_ct, a.book_sym, &sym);
+    const int R = (int)a.radius;
+    const double step = a.step, eb = a.eb;
+    const bool zf = a.zero_filter != 0;
+    // bit reader: 64-bit MSB-aligned buffer; words are stored byte-swapped (ACZ1 order)
+    const uint32_t* W = a.words;
+    const bool short_codes = s_lim.maxlen <= 32;  // buffer always holds a whole code
+    uint64_t wi = pos >> 5;
+    const int off = (int)(pos & 31);
+    unsigned long long buf =
+        ((((unsigned long long)bswap32(__ldg(W + wi))) << 32) | bswap32(__ldg(W + wi + 1))) << off;
+    int nb = 64 - off;
+    wi += 2;
+    float ob[8];
+    uint64_t flat = start;
+    while (flat < end) {
+        // decode one symbol
+        if (nb <= 32) {
+            if ((wi & 31) == 0 && wi + 32 < a.nwords)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(W + wi + 32));
+            buf |= (unsigned long long)bswap32(__ldg(W + wi)) << (32 - nb);
+            ++wi;
+            nb += 32;
+        }
+        const uint32_t e = s_lut[(uint32_t)(buf >> (64 - kLutBits))];
+        uint32_t len = e & 31, sym;
+        if (len) {
+            sym = e >> 5;
+        } else {
+            // long code: canonical limit search (window has >= 33 valid bits; codes longer
+            // than the buffer use an absolute 64-bit window)
+            unsigned long long w = buf;
+            if (!short_codes) {
+                const uint64_t ap = (wi << 5) - (uint64_t)nb;  // absolute position of buf's MSB
+                const uint64_t i = ap >> 5;
+                const int o = (int)(ap & 31);
+                const unsigned long long x0 = bswap32(__ldg(W + i)), x1 = bswap32(__ldg(W + i + 1)),
+                                         x2 = bswap32(__ldg(W + i + 2));
+                const unsigned long long h = (x0 << 32) | x1;
+                w = o ? (h << o) | (x2 << o >> 32) : h;
+            }
+            len = kLutBits + 1;
+            while (len < 64 && (w >> (64 - len)) >= s_lim.lim[len]) ++len;
+            const unsigned long long c = w >> (64 - len);
+            sym = __ldg(a.book_sym + s_ct.first_index[len] + (uint32_t)(c - s_lim.nc[len]));
+        }
+        if (len >= 64) {
+            buf = 0;
+        } else {
+            buf <<= len;
+        }
+        nb -= (int)len;
+        if (nb < 0) {
+            // consumed beyond the buffer (code longer than the valid bits): re-sync
+            const uint64_t ap = (wi << 5) - (uint64_t)(nb + (int)len) + len;
+            wi = ap >> 5;
+            const int o2 = (int)(ap & 31);
+            buf = ((((unsigned long long)bswap32(__ldg(W + wi))) << 32) | bswap32(__ldg(W + wi + 1))) << o2;
+            nb = 64 - o2;
+            wi += 2;
+        }
+        // reconstruct (ref src/codec.cpp:143-164); r stays an exact float value in double
         float v;
         if (sym == 0) {
             v = __ldg(a.out_value + oi);
             ++oi;
+            r = (double)v;
         } else {
-            const double pred = pin == 0 ? 0.0 : (double)r;
-            v = recon_value(pred, (double)((long long)sym - R), a.step);
+            const double pred = pin == 0 ? 0.0 : r;
+            const double y = __dadd_rn(pred, __dmul_rn((double)((int)sym - R), step));
+            r = rn32_in_double(y);
+            v = (float)r;
         }
-        r = v;
-        a.out[flat] = (a.zero_filter && fabs((double)v) <= a.eb) ? 0.0f : v;
+        const float o = (zf && fabs(r) <= eb) ? 0.0f : v;
+        const int slot = (int)(flat & 7);
+        ob[slot] = o;
+        ++flat;
         if (++pin == P) pin = 0;
+        if (slot == 7) {
+            float4* dst = reinterpret_cast<float4*>(a.out + flat - 8);
+            dst[0] = make_float4(ob[0], ob[1], ob[2], ob[3]);
+            dst[1] = make_float4(ob[4], ob[5], ob[6], ob[7]);
+        }
     }
+    // tail (chunk end not 8-aligned: only the tensor's last chunk)
+    const int rem = (int)(flat & 7);
+    for (int t = 0; t < rem; ++t) a.out[flat - rem + t] = ob[t];
 }
 
 __global__ void __launch_bounds__(128) k_decode_lorenzo(DecodeArgs a) {

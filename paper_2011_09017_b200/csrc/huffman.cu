@@ -248,43 +248,119 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook(
     }
     // sorted: kin (freq), vin (leaf id)
 
-    // (3) two-queue Huffman merge (single thread) --------------------------------------
-    //     node ids: leaf j -> j, internal m -> k + m; anc_a[] receives parents.
-    const uint32_t root = 2 * k - 2;
-    if (tid == 0) {
-        if (k == 1) {
-            S.anc_a[0] = 0;
-        } else {
-            unsigned long long* q = (k - 1 <= kSmemQueue) ? dyn : S.ifreq;
-            uint32_t li = 0, ii = 0;
-            unsigned long long lf = kin[0];
-            for (uint32_t m = 0; m < k - 1; ++m) {
-                unsigned long long fa, fb;
-                uint32_t ida, idb;
-                // pop a
-                if (li < k && (ii >= m || lf <= q[ii])) {
-                    fa = lf;
-                    ida = vin[li++];
-                    lf = li < k ? kin[li] : 0;
-                } else {
-                    fa = q[ii];
-                    ida = k + ii++;
-                }
-                // pop b
-                if (li < k && (ii >= m || lf <= q[ii])) {
-                    fb = lf;
-                    idb = vin[li++];
-                    lf = li < k ? kin[li] : 0;
-                } else {
-                    fb = q[ii];
-                    idb = k + ii++;
-                }
-                S.anc_a[ida] = k + m;
-                S.anc_a[idb] = k + m;
-                q[m] = fa + fb;
-            }
-            S.anc_a[root] = root;
+    // (3) Huffman tree by parallel rounds ----------------------------------------------
+    //     Equivalent to the two-queue merge (leaf wins frequency ties, internals FIFO),
+    //     itself equivalent to the reference heap order (ref src/huffman.cpp:42-54).
+    //     A round pops the two smallest items a, b -> internal X; every pending item with
+    //     key < key(X) (all queued internals, leaves with freq <= f(X)) is popped before X,
+    //     in merged order, pairwise -> new internals Y_j (all > X); an odd leftover pairs
+    //     with X. ~20 rounds for activation histograms instead of k-1 serial merges.
+    //     node ids: leaf j -> j, internal t -> k + t; S.anc_a[] receives parents.
+    const uint32_t root = k == 1 ? 0 : 2 * k - 2;
+    {
+        __shared__ uint32_t sh_li, sh_ii, sh_m, sh_nl, sh_ni, sh_xm, sh_done;
+        unsigned long long* If = S.ifreq;               // internal freqs, creation order
+        unsigned long long* Sf = kout;                  // merged S (freq)
+        uint32_t* Sid = vout;                           // merged S (node id)
+        if (tid == 0) {
+            sh_li = 0;
+            sh_ii = 0;
+            sh_m = 0;
+            sh_done = 0;
+            if (k == 1) S.anc_a[0] = 0;
         }
+        __syncthreads();
+        while (k > 1) {
+            if (tid == 0) {
+                uint32_t li = sh_li, ii = sh_ii, m = sh_m;
+                if ((k - li) + (m - ii) <= 1) {
+                    sh_done = 1;
+                } else {
+                    unsigned long long f2[2];
+                    uint32_t id2[2];
+                    for (int t = 0; t < 2; ++t) {
+                        if (li < k && (ii >= m || kin[li] <= If[ii])) {
+                            f2[t] = kin[li];
+                            id2[t] = vin[li++];
+                        } else {
+                            f2[t] = If[ii];
+                            id2[t] = k + ii++;
+                        }
+                    }
+                    const unsigned long long fx = f2[0] + f2[1];
+                    If[m] = fx;
+                    S.anc_a[id2[0]] = k + m;
+                    S.anc_a[id2[1]] = k + m;
+                    // leaves with freq <= fx
+                    uint32_t lo = li, hi = k;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (kin[mid] <= fx) lo = mid + 1; else hi = mid;
+                    }
+                    sh_nl = lo - li;
+                    sh_ni = m - ii;
+                    sh_xm = m;
+                    sh_li = li;
+                    sh_ii = ii;
+                    sh_m = m + 1;
+                }
+            }
+            __syncthreads();
+            if (sh_done) break;
+            const uint32_t li = sh_li, ii = sh_ii, nl = sh_nl, ni = sh_ni, xm = sh_xm;
+            const uint32_t ns = nl + ni;
+            const unsigned long long* A = kin + li;
+            const uint32_t* Aid = vin + li;
+            const unsigned long long* Bf = If + ii;
+            // merge path: thread t writes outputs [d0, d1)
+            const uint32_t per = (ns + kCbThreads - 1) / kCbThreads;
+            const uint32_t d0 = min(ns, tid * per), d1 = min(ns, d0 + per);
+            if (d0 < d1) {
+                uint32_t lo = d0 > ni ? d0 - ni : 0, hi = min(d0, nl);
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (A[mid] <= Bf[d0 - mid - 1]) lo = mid + 1; else hi = mid;
+                }
+                uint32_t ia = lo, ib = d0 - lo;
+                for (uint32_t d = d0; d < d1; ++d) {
+                    if (ia < nl && (ib >= ni || A[ia] <= Bf[ib])) {
+                        Sf[d] = A[ia];
+                        Sid[d] = Aid[ia];
+                        ++ia;
+                    } else {
+                        Sf[d] = Bf[ib];
+                        Sid[d] = k + ii + ib;
+                        ++ib;
+                    }
+                }
+            }
+            __syncthreads();
+            const uint32_t m1 = xm + 1;  // first id slot after X
+            const uint32_t np = ns >> 1;
+            for (uint32_t q = tid; q < np; q += kCbThreads) {
+                If[m1 + q] = Sf[2 * q] + Sf[2 * q + 1];
+                S.anc_a[Sid[2 * q]] = k + m1 + q;
+                S.anc_a[Sid[2 * q + 1]] = k + m1 + q;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t m = m1 + np;
+                uint32_t iin = xm;  // X becomes the queue front
+                if (ns & 1) {
+                    // leftover pairs with X
+                    If[m] = Sf[ns - 1] + If[xm];
+                    S.anc_a[Sid[ns - 1]] = k + m;
+                    S.anc_a[k + xm] = k + m;
+                    ++m;
+                    iin = xm + 1;
+                }
+                sh_li = li + nl;
+                sh_ii = iin;
+                sh_m = m;
+            }
+            __syncthreads();
+        }
+        if (tid == 0 && k > 1) S.anc_a[root] = root;
     }
     __syncthreads();
 
@@ -515,26 +591,19 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     if (t0 >= a.n) return;
     const uint64_t my0 = t0 + (uint64_t)tid * kEncPer;
 
-    unsigned long long codes[kEncPer];
-    uint32_t lens[kEncPer];
+    // pass 1: code lengths and escapes of my 16 symbols
     uint32_t my_bits = 0, my_esc = 0, escmask = 0;
 #pragma unroll
     for (int i = 0; i < kEncPer; ++i) {
         const uint64_t g = my0 + i;
         if (g < a.n) {
-            const uint32_t s = a.sym[g];
-            const unsigned long long e = __ldg(a.enc + s);
-            codes[i] = e >> 8;
-            lens[i] = (uint32_t)(e & 0xFF);
-            if (s == 0) {
+            const uint32_t sy = a.sym[g];
+            my_bits += (uint32_t)(__ldg(a.enc + sy) & 0xFF);
+            if (sy == 0) {
                 ++my_esc;
                 escmask |= 1u << i;
             }
-        } else {
-            codes[i] = 0;
-            lens[i] = 0;
         }
-        my_bits += lens[i];
     }
     // CTA exclusive scan of (bits, escapes)
     uint32_t ib = my_bits, ie = my_esc;
@@ -552,54 +621,87 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
         s_warp_esc[warp] = ie;
     }
     __syncthreads();
-    if (tid == 0) {
-        uint32_t rb = 0, re = 0;
-        for (int w = 0; w < kEncThreads / 32; ++w) {
-            const uint32_t b = s_warp_bits[w], e = s_warp_esc[w];
-            s_warp_bits[w] = rb;
-            s_warp_esc[w] = re;
-            rb += b;
-            re += e;
+    if (warp == 0) {
+        uint32_t wb = lane < kEncThreads / 32 ? s_warp_bits[lane] : 0;
+        uint32_t we = lane < kEncThreads / 32 ? s_warp_esc[lane] : 0;
+        uint32_t xb = wb, xe = we;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t tb = __shfl_up_sync(0xffffffffu, xb, o);
+            const uint32_t te = __shfl_up_sync(0xffffffffu, xe, o);
+            if (lane >= o) {
+                xb += tb;
+                xe += te;
+            }
         }
-        s_tile_total = rb;
-        // decoupled look-back over tiles (serial walk by one thread)
+        if (lane < kEncThreads / 32) {
+            s_warp_bits[lane] = xb - wb;
+            s_warp_esc[lane] = xe - we;
+        }
+        const uint32_t rb = __shfl_sync(0xffffffffu, xb, kEncThreads / 32 - 1);
+        const uint32_t re = __shfl_sync(0xffffffffu, xe, kEncThreads / 32 - 1);
+        // decoupled look-back, 32 predecessors per probe
         TileStatus* st = a.status;
         volatile TileStatus* vst = st;
         unsigned long long pb = 0, pe = 0;
-        st[tile].agg_bits = rb;
-        st[tile].agg_esc = re;
-        if (tile == 0) {
-            st[tile].incl_bits = rb;
-            st[tile].incl_esc = re;
-            __threadfence();
-            atomicExch(&st[tile].flag, 2u);
-        } else {
-            __threadfence();
-            atomicExch(&st[tile].flag, 1u);
-            int64_t j = (int64_t)tile - 1;
-            while (j >= 0) {
-                unsigned f;
-                unsigned long long spins = 0;
-                do {
-                    f = vst[j].flag;
-                } while (f == 0 && ++spins < (1ull << 30));
-                __threadfence();
-                if (f == 2) {
-                    pb += vst[j].incl_bits;
-                    pe += vst[j].incl_esc;
-                    break;
-                }
-                pb += vst[j].agg_bits;
-                pe += vst[j].agg_esc;
-                --j;
+        if (lane == 0) {
+            st[tile].agg_bits = rb;
+            st[tile].agg_esc = re;
+            if (tile == 0) {
+                st[tile].incl_bits = rb;
+                st[tile].incl_esc = re;
             }
-            st[tile].incl_bits = pb + rb;
-            st[tile].incl_esc = pe + re;
             __threadfence();
-            atomicExch(&st[tile].flag, 2u);
+            atomicExch(&st[tile].flag, tile == 0 ? 2u : 1u);
         }
-        s_prefix_bits = pb;
-        s_prefix_esc = pe;
+        if (tile > 0) {
+            int64_t base = (int64_t)tile - 1;
+            for (;;) {
+                const int64_t j = base - lane;
+                unsigned f = 2;
+                unsigned long long vb = 0, ve = 0;
+                if (j >= 0) {
+                    unsigned long long spins = 0;
+                    do {
+                        f = vst[j].flag;
+                    } while (f == 0 && ++spins < (1ull << 30));
+                    __threadfence();
+                    if (f == 2) {
+                        vb = vst[j].incl_bits;
+                        ve = vst[j].incl_esc;
+                    } else {
+                        vb = vst[j].agg_bits;
+                        ve = vst[j].agg_esc;
+                    }
+                }
+                const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
+                const int stop = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
+                if (lane > stop) {
+                    vb = 0;
+                    ve = 0;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    vb += __shfl_xor_sync(0xffffffffu, vb, o);
+                    ve += __shfl_xor_sync(0xffffffffu, ve, o);
+                }
+                pb += vb;
+                pe += ve;
+                if (incl) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                st[tile].incl_bits = pb + rb;
+                st[tile].incl_esc = pe + re;
+                __threadfence();
+                atomicExch(&st[tile].flag, 2u);
+            }
+        }
+        if (lane == 0) {
+            s_prefix_bits = pb;
+            s_prefix_esc = pe;
+            s_tile_total = rb;
+        }
     }
     __syncthreads();
     const unsigned long long tile_bit0 = s_prefix_bits;
@@ -613,18 +715,20 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     uint64_t off = (uint64_t)s0 + excl_bits;
     unsigned long long gbit = tile_bit0 + excl_bits;
     unsigned long long gesc = tile_esc0 + s_warp_esc[warp] + (ie - my_esc);
-    // next sidecar point at or after my0
     uint64_t next_side = a.side_bitoff ? ((my0 + a.interval - 1) / a.interval) * a.interval : ~0ull;
-#pragma unroll
+    // pass 2: write codes (re-fetched from the L1-resident table)
+#pragma unroll 4
     for (int i = 0; i < kEncPer; ++i) {
         const uint64_t g = my0 + i;
         if (g >= a.n) break;
+        const unsigned long long e = __ldg(a.enc + a.sym[g]);
+        const uint32_t len = (uint32_t)(e & 0xFF);
         if (g == next_side) {
             a.side_bitoff[g / a.interval] = gbit;
             a.side_outl[g / a.interval] = (uint32_t)gesc;
             next_side += a.interval;
         }
-        smem_put_bits(stage, off, codes[i], lens[i]);
+        smem_put_bits(stage, off, e >> 8, len);
         if ((escmask >> i) & 1u) {
             if (a.x) {
                 a.out_index[gesc] = g;
@@ -632,8 +736,8 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
             }
             ++gesc;
         }
-        off += lens[i];
-        gbit += lens[i];
+        off += len;
+        gbit += len;
     }
     __syncthreads();
     const uint64_t gw0 = tile_bit0 >> 5;

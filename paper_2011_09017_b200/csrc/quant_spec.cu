@@ -38,12 +38,16 @@ constexpr int kExt = 2 * kL;
 constexpr int kCap = kSeg + kExt;
 constexpr int kCapW = (kCap + 31) / 32;
 
+// Walk statistics (debug; read with acz_gpu_debug_counters): batches, state changes,
+// exact-mode steps, rebases, phase-A elements, walk visits.
+__device__ unsigned long long g_qstats[8];
+
 struct SP {
-    double eb, step, radius_d, Tmax;
+    double eb, step, inv_step, radius_d, Tmax;
     long long R;
     float anchor_min;
     int B;  // anchor binade exponent
-    uint64_t P, nseg, interval;
+    uint64_t P, nseg, interval, planes;
 };
 
 struct XS {
@@ -57,8 +61,14 @@ struct XS {
 __device__ __forceinline__ XS xstep(float xf, double pred, const SP& p) {
     XS r;
     const double orig = (double)xf;
-    r.t = __ddiv_rn(__dsub_rn(orig, pred), p.step);
+    const double d = __dsub_rn(orig, pred);
+    r.t = __dmul_rn(d, p.inv_step);
     r.q = round(r.t);
+    // round(RN64(d/step)) == round(t) unless t is within a few ulps of a half-integer
+    if (0.5 - fabs(r.t - r.q) <= fabs(r.t) * 0x1p-44 + 0x1p-60) {
+        r.t = __ddiv_rn(d, p.step);
+        r.q = round(r.t);
+    }
     r.sym = 0;
     r.out = xf;
     r.pre = 0.0;
@@ -87,6 +97,10 @@ __device__ __forceinline__ int gran(double D) {
     return e - 1075 + __ffsll((long long)m) - 1;
 }
 
+__device__ __forceinline__ double pow2(int k) {  // 2^k for normal k
+    return __hiloint2double((k + 1023) << 20, 0);
+}
+
 __device__ __forceinline__ bool is_anchor(float v, float amin) { return fabsf(v) >= amin; }
 
 __device__ __forceinline__ float lattice_guess(double lam, float xa, const SP& p) {
@@ -94,20 +108,11 @@ __device__ __forceinline__ float lattice_guess(double lam, float xa, const SP& p
     return __double2float_rn(__dadd_rn(lam, __dmul_rn(K, p.step)));
 }
 
-// First range start of segment j of a plane (plane coordinates), see phase A notes.
-__device__ __forceinline__ uint64_t seg_bound(const float* xp, uint64_t j, const SP& p) {
-    if (j == 0) return 0;
-    const uint64_t b = j * kSeg;
-    if (b >= p.P) return p.P;
-    const uint64_t e = min(p.P, b + kExt);
-    for (uint64_t i = b; i < e; ++i)
-        if (is_anchor(__ldg(xp + i), p.anchor_min)) return i + 1;
-    return e;
-}
-
+template <typename SymT>
 struct Smem {
     float s[kCap];
-    uint32_t sym[kCap];
+    SymT sym[kCap];
+    uint32_t abits[kSeg / 32];  // anchor bitmap of the segment's nominal span
     uint32_t cand[kCapW];
     int rstart[kW + 1];   // segment-relative range starts (sorted), rstart[nr] = len
     float guess[kW];      // speculative entry state of each range
@@ -118,7 +123,8 @@ struct Smem {
 };
 
 // Speculative chain over range k (phase A) from its guess; writes s, sym, candidate bits.
-__device__ void spec_range(Smem& S, const float* xp, uint64_t seg0, int k, const SP& p,
+template <typename SymT>
+__device__ void spec_range(Smem<SymT>& S, const float* xp, uint64_t seg0, int k, const SP& p,
                            uint64_t plane_flat0, unsigned* flags) {
     const int b = S.rstart[k], e = S.rstart[k + 1];
     float r = S.guess[k];
@@ -150,33 +156,34 @@ __device__ void spec_range(Smem& S, const float* xp, uint64_t seg0, int k, const
             } else {
                 const int ex = fexp((double)o.out);
                 if (ex > p.B) c = true;
-                const double a = fabs((double)o.out), lo = ldexp(1.0, ex);
+                const double a = fabs((double)o.out), lo = pow2(ex);
                 if (a - lo <= 2.0 * p.Tmax || 2.0 * lo - a <= 2.0 * p.Tmax) c = true;
-                const double half = ldexp(1.0, fexp(o.pre) - 24);
-                if (fabs(o.pre - (double)o.out) == half) c = true;  // exact RNE tie
+                // distance of the pre-value to the nearest rounding midpoint of its grid
+                const double half = pow2(fexp(o.pre) - 24);
+                const double fr = half - fabs(o.pre - (double)o.out);
+                if (fr == 0.0) c = true;  // exact RNE tie
                 if (collapsed) {
                     // re-expansion certificate for any |D| <= Tmax
-                    const double dmax =
-                        ldexp(1.0, fexp(2.0 * fmax(fabs(ycol), 2.0 * p.Tmax)) - 22);
-                    const double u = ldexp(1.0, fexp(o.pre) - 23);
-                    const double fr = fabs(fmod(fabs(o.pre), u) - 0.5 * u);
-                    if (!(fr > dmax + ldexp(fabs(o.pre), -50))) c = true;
+                    const double dmax = pow2(fexp(2.0 * fmax(fabs(ycol), 2.0 * p.Tmax)) - 22);
+                    if (!(fr > dmax + fabs(o.pre) * 0x1p-50)) c = true;
                 }
                 collapsed = false;
             }
         }
-        if (((plane_flat0 + pi) % p.interval) == 0) c = true;  // sidecar point
+        if (((plane_flat0 + pi) & (p.interval - 1)) == 0) c = true;  // sidecar point
         S.s[i] = o.out;
-        S.sym[i] = o.sym;
+        S.sym[i] = (SymT)o.sym;
         if (c) atomicOr(&S.cand[i >> 5], 1u << (i & 31));
         r = o.out;
     }
     S.send[k] = r;
+    atomicAdd(&g_qstats[4], (unsigned long long)(e - b));
     if (bad) atomicOr(flags, kFlagNonFinite);
 }
 
 // Phase A for ranges k0.. with lattice origin lam (all lanes participate).
-__device__ void phase_a(Smem& S, const float* xp, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
+template <typename SymT>
+__device__ void phase_a(Smem<SymT>& S, const float* xp, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
                         float k0_entry, const SP& p, uint64_t plane_flat0, unsigned* flags) {
     const int lane = threadIdx.x;
     // clear candidate bits of the affected span
@@ -244,6 +251,28 @@ __global__ void __launch_bounds__(256) k_anchor_binade(const float* __restrict__
     }
 }
 
+// Warp-cooperative: first anchor in [b, e) (plane coordinates), or e if none.
+__device__ __forceinline__ uint64_t first_anchor(const float* xp, uint64_t b, uint64_t e, float amin) {
+    for (uint64_t base = b; base < e; base += 32) {
+        const uint64_t i = base + threadIdx.x;
+        const bool a = i < e && is_anchor(__ldg(xp + i), amin);
+        const unsigned m = __ballot_sync(0xffffffffu, a);
+        if (m) return base + __ffs(m) - 1;
+    }
+    return e;
+}
+
+// First range start of segment j (warp-cooperative version of seg_bound).
+__device__ __forceinline__ uint64_t seg_bound_w(const float* xp, uint64_t j, const SP& p) {
+    if (j == 0) return 0;
+    const uint64_t b = j * kSeg;
+    if (b >= p.P) return p.P;
+    const uint64_t e = min(p.P, b + kExt);
+    const uint64_t a = first_anchor(xp, b, e, p.anchor_min);
+    return a < e ? a + 1 : e;
+}
+
+template <typename SymT>
 __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, SP p, const int* dB,
                                                    uint32_t* __restrict__ sym_out,
                                                    float* __restrict__ side_state,
@@ -251,7 +280,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
                                                    float* __restrict__ exits,
                                                    unsigned int* ticket, unsigned int* flags,
                                                    unsigned long long total_segs) {
-    __shared__ Smem S;
+    __shared__ Smem<SymT> S;
     __shared__ unsigned s_tk;
     const int lane = threadIdx.x;
     {
@@ -264,13 +293,16 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     __syncwarp();
     const unsigned long long seg_id = s_tk;
     if (seg_id >= total_segs) return;
-    const uint64_t plane = seg_id / p.nseg, j = seg_id % p.nseg;
+    // segment-major order: all planes' segment j before any segment j+1, so a segment's
+    // predecessor (same plane, j-1) always holds an earlier ticket and is usually done
+    const uint64_t j = seg_id / p.planes, plane = seg_id % p.planes;
+    const uint64_t sidx = plane * p.nseg + j;  // status/exit slot
     const float* xp = x + plane * p.P;
     const uint64_t plane_flat0 = plane * p.P;
 
     // ---- segment geometry -------------------------------------------------------
-    const uint64_t b0 = seg_bound(xp, j, p);           // first range start
-    const uint64_t b1 = seg_bound(xp, j + 1, p);       // next segment's first start
+    const uint64_t b0 = seg_bound_w(xp, j, p);         // first range start
+    const uint64_t b1 = seg_bound_w(xp, j + 1, p);     // next segment's first start
     const uint64_t seg0 = b0;
     const int len = (int)(b1 - b0);
     if (len <= 0) {
@@ -278,36 +310,53 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         if (lane == 0) {
             float tin = 0.0f;
             if (j > 0) {
-                volatile unsigned* vf = status + seg_id - 1;
+                volatile unsigned* vf = status + sidx - 1;
                 unsigned long long spins = 0;
                 while (*vf == 0) {
-                    if (++spins > (1ull << 28)) {  // never expected: report, do not hang
+                    __nanosleep(64);
+                    if (++spins > (1ull << 26)) {  // never expected: report, do not hang
                         atomicOr(flags, kFlagInternal);
                         break;
                     }
                 }
                 __threadfence();
-                tin = *((volatile float*)exits + seg_id - 1);
+                tin = *((volatile float*)exits + sidx - 1);
             }
-            exits[seg_id] = tin;
+            exits[sidx] = tin;
             __threadfence();
-            atomicExch(status + seg_id, 1u);
+            atomicExch(status + sidx, 1u);
         }
         return;
     }
     // lane windows: lane l > 0 starts after the first anchor in
     // [max(j*Seg + l*L, b0), j*Seg + (l+1)*L) if that start lies before b1
+    {
+        const uint64_t nb = j * kSeg;
+        for (int w = 0; w < kSeg / 32; ++w) {
+            const uint64_t i = nb + (uint64_t)w * 32 + lane;
+            const bool a = i < p.P && is_anchor(__ldg(xp + i), p.anchor_min);
+            const unsigned m = __ballot_sync(0xffffffffu, a);
+            if (lane == 0) S.abits[w] = m;
+        }
+        __syncwarp();
+    }
     int my_start = -1;
     if (lane == 0) {
         my_start = 0;
     } else {
-        const uint64_t w0 = max(j * kSeg + (uint64_t)lane * kL, b0);
-        const uint64_t w1 = min(j * kSeg + (uint64_t)(lane + 1) * kL, b1);
-        for (uint64_t i = w0; i < w1; ++i)
-            if (is_anchor(__ldg(xp + i), p.anchor_min)) {
-                if (i + 1 < b1) my_start = (int)(i + 1 - seg0);
+        const uint64_t nb = j * kSeg;
+        const uint64_t w0 = max(nb + (uint64_t)lane * kL, b0);
+        const uint64_t w1 = min(nb + (uint64_t)(lane + 1) * kL, b1);
+        for (uint64_t i = w0; i < w1;) {
+            const int off = (int)(i - nb);
+            uint32_t bits = S.abits[off >> 5] & (~0u << (off & 31));
+            if (bits) {
+                const uint64_t a = nb + (uint64_t)((off & ~31) + __ffs(bits) - 1);
+                if (a < w1 && a + 1 < b1) my_start = (int)(a + 1 - seg0);
                 break;
             }
+            i = nb + (uint64_t)((off & ~31) + 32);
+        }
     }
     const unsigned has = __ballot_sync(0xffffffffu, my_start >= 0);
     const int nr = __popc(has);
@@ -337,16 +386,17 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     float tin = 0.0f;
     if (j > 0) {
         if (lane == 0) {
-            volatile unsigned* vf = status + seg_id - 1;
+            volatile unsigned* vf = status + sidx - 1;
             unsigned long long spins = 0;
             while (*vf == 0) {
-                if (++spins > (1ull << 28)) {
+                __nanosleep(64);
+                if (++spins > (1ull << 26)) {
                     atomicOr(flags, kFlagInternal);
                     break;
                 }
             }
             __threadfence();
-            tin = *((volatile float*)exits + seg_id - 1);
+            tin = *((volatile float*)exits + sidx - 1);
         }
         tin = __shfl_sync(0xffffffffu, tin, 0);
     }
@@ -381,6 +431,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
 
     while (pos < len) {
         if (exact_mode) {
+            if (lane == 0) atomicAdd(&g_qstats[2], 1ull);
             const int k = range_of(pos);
             if (pos == S.rstart[k] && pos > 0) {
                 // exact entry T at a range start: resume translation (rebase if needed)
@@ -399,9 +450,9 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             const float tprev = T;
             const XS ex = xstep(__ldg(xp + pi), pi == 0 ? 0.0 : (double)tprev, p);
             if (lane == 0) {
-                S.sym[pos] = ex.sym;
+                S.sym[pos] = (SymT)ex.sym;
                 const uint64_t flat = plane_flat0 + pi;
-                if (flat % p.interval == 0) side_state[flat / p.interval] = pi == 0 ? 0.0f : tprev;
+                if ((flat & (p.interval - 1)) == 0) side_state[flat / p.interval] = pi == 0 ? 0.0f : tprev;
             }
             __syncwarp();
             T = ex.out;
@@ -477,7 +528,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
                     tprev = __double2float_rn(__dadd_rn((double)S.s[vp - 1], Dp));
                 }
                 ex = xstep(__ldg(xp + pi), pi == 0 ? 0.0 : (double)tprev, p);
-                const uint32_t ssym = S.sym[vp];
+                const uint32_t ssym = (uint32_t)S.sym[vp];
                 const float ss = S.s[vp];
                 if (ex.sym != ssym) {
                     ok = false;
@@ -495,9 +546,17 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         }
         const unsigned fail = __ballot_sync(0xffffffffu, active && !ok);
         const int f = fail ? __ffs(fail) - 1 : 32;
+        {
+            const int nact = __popc(__ballot_sync(0xffffffffu, active));
+            if (lane == 0) {
+                atomicAdd(&g_qstats[0], 1ull);
+                if (f < 32) atomicAdd(&g_qstats[1], 1ull);
+                atomicAdd(&g_qstats[5], (unsigned long long)min(f + 1, nact));
+            }
+        }
         if (active && lane < f) {
             const uint64_t flat = plane_flat0 + seg0 + (uint64_t)vp;
-            if (flat % p.interval == 0) side_state[flat / p.interval] = (seg0 + vp == 0) ? 0.0f : tprev;
+            if ((flat & (p.interval - 1)) == 0) side_state[flat / p.interval] = (seg0 + vp == 0) ? 0.0f : tprev;
         }
         if (f < 32) {
             const int fvp = __shfl_sync(0xffffffffu, vp, f);
@@ -505,6 +564,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             const int frb = __shfl_sync(0xffffffffu, (int)rebase, f);
             const float ftp = __shfl_sync(0xffffffffu, tprev, f);
             if (frb) {
+                if (lane == 0) atomicAdd(&g_qstats[3], 1ull);
                 // lattice changed at range start fk: re-speculate ranges >= fk from the
                 // exact entry state and re-evaluate from fvp
                 phase_a(S, xp, seg0, fk, (double)ftp, true, ftp, p, plane_flat0, flags);
@@ -516,9 +576,9 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             const float fout = __shfl_sync(0xffffffffu, ex.out, f);
             const uint32_t fsym = __shfl_sync(0xffffffffu, ex.sym, f);
             if (lane == f) {
-                S.sym[fvp] = fsym;
+                S.sym[fvp] = (SymT)fsym;
                 const uint64_t flat = plane_flat0 + seg0 + (uint64_t)fvp;
-                if (flat % p.interval == 0) side_state[flat / p.interval] = (seg0 + fvp == 0) ? 0.0f : ftp;
+                if ((flat & (p.interval - 1)) == 0) side_state[flat / p.interval] = (seg0 + fvp == 0) ? 0.0f : ftp;
             }
             __syncwarp();
             const float fss = S.s[fvp];
@@ -555,13 +615,13 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         }
     }
     if (lane == 0) {
-        exits[seg_id] = texit;
+        exits[sidx] = texit;
         __threadfence();
-        atomicExch(status + seg_id, 1u);
+        atomicExch(status + sidx, 1u);
     }
     // ---- symbols out (coalesced) ----------------------------------------------------
     uint32_t* so = sym_out + plane_flat0 + seg0;
-    for (int i = lane; i < len; i += kW) so[i] = S.sym[i];
+    for (int i = lane; i < len; i += kW) so[i] = (uint32_t)S.sym[i];
 }
 
 }  // namespace
@@ -580,6 +640,8 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     p.P = a.g.plane_size;
     p.nseg = (p.P + kSeg - 1) / kSeg;
     p.interval = a.interval;
+    p.planes = a.g.planes;
+    p.inv_step = 1.0 / a.step;
     const unsigned long long total = (unsigned long long)a.g.planes * p.nseg;
     char* sc = static_cast<char*>(scratch);
     int* dB = reinterpret_cast<int*>(sc);
@@ -590,10 +652,23 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     if (e != cudaSuccess) return e;
     k_anchor_binade<<<1, 256, 0, s>>>(a.x, a.g.n, dB);
     ++*launches;
-    k_quant_spec<<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym, a.side_state, status, exits,
-                                                ticket, a.flags, total);
+    if (a.radius <= 32768)
+        k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym, a.side_state,
+                                                              status, exits, ticket, a.flags, total);
+    else
+        k_quant_spec<uint32_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym, a.side_state,
+                                                              status, exits, ticket, a.flags, total);
     ++*launches;
     return cudaGetLastError();
+}
+
+cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_qstats, sizeof(g_qstats));
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[8] = {0};
+        e = cudaMemcpyToSymbol(g_qstats, z, sizeof(z));
+    }
+    return e;
 }
 
 size_t quant_spec_scratch_bytes(uint64_t planes, uint64_t plane_size) {

@@ -1,0 +1,41 @@
+"""Times compress/decompress per kernel class for given shapes and prints the speculative
+quantiser's walk counters (development tool)."""
+import ctypes as C
+import sys
+import time
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import torch
+
+import paper_2011_09017_b200 as acz
+from paper_2011_09017_b200 import _native, workloads as W
+
+lib = _native.load()
+ctx = acz.default_context()
+shapes = {"conv1": (256, 3, 227, 227, False), "config1": (64, 64, 56, 56, True),
+          "conv2": (256, 96, 27, 27, True), "conv3": (256, 256, 13, 13, True),
+          "vgg_conv2": (16, 64, 224, 224, True)}
+which = sys.argv[1:] or list(shapes)
+for nm in which:
+    b, c, h, w, relu = shapes[nm]
+    x = W.make_tensor((b, c, h, w), relu, 7)
+    p = acz.CodecParams(1e-3)
+    for _ in range(2):
+        blob = acz.compress(x, p)
+    v = (C.c_uint64 * 8)()
+    lib.acz_gpu_debug_counters(ctx.handle, v, 8, 1)
+    lib.acz_gpu_profile_enable(ctx.handle, 1)
+    blob = acz.compress(x, p)
+    out = acz.decompress(blob, True)
+    torch.cuda.synchronize()
+    ms = (C.c_double * 7)()
+    cnt = (C.c_uint64 * 7)()
+    lib.acz_gpu_profile_read(ctx.handle, ms, cnt)
+    lib.acz_gpu_profile_enable(ctx.handle, 0)
+    lib.acz_gpu_debug_counters(ctx.handle, v, 8, 1)
+    names = ["stats", "quant", "hist", "book", "encode", "decode", "scan"]
+    print(nm, x.shape, "ratio %.3f" % acz.compression_ratio(blob),
+          {names[i]: round(ms[i], 3) for i in range(7) if cnt[i]})
+    n = x.numel()
+    print("   walk: batches %d (%.4f/elem) changes %d (%.4f) exact %d (%.4f) rebases %d spec %.2f/elem visits %.4f/elem" % (
+        v[0], v[0] / n, v[1], v[1] / n, v[2], v[2] / n, v[3], v[4] / n, v[5] / n))
