@@ -183,8 +183,12 @@ int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches);
 /* ---- parity / debug ---- */
 /* Copy the quantisation symbols of the last compress on this context (device, n u32). */
 int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, void* stream);
-/* Speculative-quantiser walk counters (8 values: batches, state changes, exact steps,
- * rebases, speculated elements, visits); reset != 0 clears them. */
+/* Debug counters; reset != 0 clears them. out[0..7]: speculative-quantiser walk counters
+ * (batches, state changes, exact steps, rebases, speculated elements, visits); when n >= 16,
+ * out[8..15]: codebook phase cycles (compaction, sort, rounds, depths, canonical, tables),
+ * round count, calls; when n >= 20, out[16..19]: speculative-quantiser cycles summed over
+ * segments (phase A, look-back wait, walk, output); when n >= 24, out[20..23]: decoder
+ * cycles summed over warps (table prologue, stream staging, symbol loop) and warp count. */
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset);
 /* Number of CUDA kernel launches issued by this context since creation. */
 uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx);

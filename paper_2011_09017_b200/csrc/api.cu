@@ -29,8 +29,9 @@ struct acz_gpu_ctx {
     // workspace (grown on demand)
     void* ws_sym = nullptr;
     size_t ws_sym_cap = 0;
-    void* ws_hist = nullptr;
+    void* ws_hist = nullptr;  // u64 bins x alphabet + touched bitmap; kept zero between calls
     size_t ws_hist_cap = 0;
+    bool hist_clean = false;
     void* ws_enc = nullptr;
     size_t ws_enc_cap = 0;
     void* ws_cb = nullptr;
@@ -64,6 +65,7 @@ struct acz_gpu_ctx {
     Small* d_small = nullptr;
     Small* h_small = nullptr;  // pinned mirror
     uint64_t last_n = 0;
+    bool last_sym16 = false;
     // profiling: events recorded around every launch when enabled
     bool prof = false;
     struct Pending {
@@ -198,7 +200,7 @@ uint64_t sidecar_interval_default() {
     static uint64_t v = [] {
         const char* s = std::getenv("ACZ_SIDECAR_INTERVAL");
         uint64_t x = s ? std::strtoull(s, nullptr, 10) : 0;
-        if (!x) x = 256;
+        if (x < 32) x = 128;  // the decoder's output tiles need a multiple of 32
         uint64_t p2 = 1;
         while (p2 * 2 <= x) p2 *= 2;  // power of two (mask arithmetic in the kernels)
         return p2;
@@ -216,15 +218,15 @@ size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
 // Allocates the blob arena for the given sizes and carves the pointers.
 cudaError_t blob_alloc(acz_gpu_blob* b, uint32_t book, uint64_t nwords, uint64_t nout,
-                       uint64_t nchunks, cudaStream_t s) {
+                       uint64_t nchunks, bool with_outl, cudaStream_t s) {
     size_t off = 0;
     const size_t o_sym = off; off += al(4ull * std::max<uint32_t>(book, 1));
     const size_t o_len = off; off += al(std::max<uint32_t>(book, 1));
-    const size_t o_words = off; off += al(4ull * (nwords + 4));
+    const size_t o_words = off; off += al(4ull * (nwords + 32));  // decoder reads 3 blocks ahead
     const size_t o_oidx = off; off += al(8ull * std::max<uint64_t>(nout, 1));
     const size_t o_oval = off; off += al(4ull * std::max<uint64_t>(nout, 1));
     const size_t o_sb = off; off += al(8ull * std::max<uint64_t>(nchunks, 1));
-    const size_t o_so = off; off += al(4ull * std::max<uint64_t>(nchunks, 1));
+    const size_t o_so = off; off += with_outl ? al(4ull * std::max<uint64_t>(nchunks, 1)) : 0;
     const size_t o_ss = off; off += al(4ull * std::max<uint64_t>(nchunks, 1));
     const size_t o_lut = off; off += al(4ull * kLutSize);
     const size_t o_canon = off; off += al(sizeof(CanonTables));
@@ -240,7 +242,7 @@ cudaError_t blob_alloc(acz_gpu_blob* b, uint32_t book, uint64_t nwords, uint64_t
     b->out_index = reinterpret_cast<unsigned long long*>(c + o_oidx);
     b->out_value = reinterpret_cast<float*>(c + o_oval);
     b->side_bitoff = reinterpret_cast<unsigned long long*>(c + o_sb);
-    b->side_outl = reinterpret_cast<uint32_t*>(c + o_so);
+    b->side_outl = with_outl ? reinterpret_cast<uint32_t*>(c + o_so) : nullptr;
     b->side_state = reinterpret_cast<float*>(c + o_ss);
     b->lut = reinterpret_cast<uint32_t*>(c + o_lut);
     b->canon = reinterpret_cast<CanonTables*>(c + o_canon);
@@ -248,7 +250,11 @@ cudaError_t blob_alloc(acz_gpu_blob* b, uint32_t book, uint64_t nwords, uint64_t
     return cudaSuccess;
 }
 
-uint64_t sidecar_bytes(uint64_t nchunks) { return 4 + 4 + 8 * 6 + nchunks * (8 + 4 + 4); }
+// ACZS v2: "ACZS" u32 version, u64 {count, bit_length, interval, nchunks, binding, has_outl},
+// u64 bit offset x nchunks, [u32 outlier prefix x nchunks if has_outl], f32 state x nchunks.
+uint64_t sidecar_bytes(uint64_t nchunks, bool has_outl) {
+    return 4 + 4 + 8 * 6 + nchunks * (8 + (has_outl ? 4 : 0) + 4);
+}
 
 uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h = 1469598103934665603ull) {
     for (size_t i = 0; i < n; ++i) {
@@ -376,18 +382,18 @@ namespace {
 
 // Blob-side finalisation shared by compress and the generic Huffman encoder: after the
 // codebook sync, allocates the blob, copies the tables and runs K5.
-int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const uint32_t* d_sym, uint64_t n,
-                  const float* d_x, uint64_t interval, cudaStream_t s) {
+int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const void* d_sym, int sym16, uint64_t n,
+                  const float* d_x, uint64_t interval, bool with_outl, cudaStream_t s) {
     const BookInfo& bi = ctx->h_small->info;
     const uint64_t nwords = (bi.total_bits + 31) / 32;
     const uint64_t nout = d_x ? bi.n_escapes : 0;
     const uint64_t nchunks = interval ? (n + interval - 1) / interval : 0;
-    CK(blob_alloc(b, bi.book_size, nwords, nout, nchunks, s));
+    CK(blob_alloc(b, bi.book_size, nwords, nout, nchunks, with_outl, s));
     b->nwords = nwords;
     b->interval = interval;
     b->nchunks = nchunks;
     b->max_len = bi.max_len;
-    CK(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 4), s));
+    CK(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 32), s));
     const uint32_t* wb_sym = static_cast<const uint32_t*>(ctx->ws_book);
     const uint8_t* wb_len =
         reinterpret_cast<const uint8_t*>(wb_sym + std::max<uint64_t>(ctx->ws_book_cap / 5, 1));
@@ -401,6 +407,7 @@ int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const uint32_t* d_sym, uint
                            s));
     EncodeArgs ea;
     ea.sym = d_sym;
+    ea.sym16 = sym16;
     ea.n = n;
     ea.enc = static_cast<const unsigned long long*>(ctx->ws_enc);
     ea.x = d_x;
@@ -422,10 +429,18 @@ int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const uint32_t* d_sym, uint
 }
 
 // Histogram + codebook + the single synchronisation. Leaves BookInfo in h_small.
-int build_book(acz_gpu_ctx* ctx, const uint32_t* d_sym, uint64_t n, uint32_t alphabet,
+int build_book(acz_gpu_ctx* ctx, const void* d_sym, int sym16, uint64_t n, uint32_t alphabet,
                uint32_t center, cudaStream_t s) {
     const uint64_t max_leaves = std::min<uint64_t>(alphabet, n);
-    CK(grow(&ctx->ws_hist, &ctx->ws_hist_cap, 8ull * alphabet));
+    const size_t hist_bytes = 8ull * alphabet + 4ull * ((alphabet + 31) / 32);
+    if (hist_bytes > ctx->ws_hist_cap) ctx->hist_clean = false;
+    CK(grow(&ctx->ws_hist, &ctx->ws_hist_cap, hist_bytes));
+    if (!ctx->hist_clean) {
+        CK(cudaMemsetAsync(ctx->ws_hist, 0, ctx->ws_hist_cap, s));
+        ctx->hist_clean = true;
+    }
+    unsigned long long* hist = static_cast<unsigned long long*>(ctx->ws_hist);
+    uint32_t* touched = reinterpret_cast<uint32_t*>(hist + alphabet);
     CK(grow(&ctx->ws_enc, &ctx->ws_enc_cap, 8ull * alphabet));
     CK(grow(&ctx->ws_cb, &ctx->ws_cb_cap, codebook_scratch_bytes(max_leaves)));
     CK(grow(&ctx->ws_book, &ctx->ws_book_cap, 5ull * max_leaves + 64));
@@ -433,19 +448,19 @@ int build_book(acz_gpu_ctx* ctx, const uint32_t* d_sym, uint64_t n, uint32_t alp
     CK(grow(&ctx->ws_status, &ctx->ws_status_cap, sizeof(TileStatus) * tiles));
     {
     KTimer kt(ctx, ACZ_K_HIST, s);
-    CK(launch_histogram(d_sym, n, alphabet, center,
-                        static_cast<unsigned long long*>(ctx->ws_hist), ctx->sms, s,
+    ctx->hist_clean = false;  // until the codebook kernels have consumed the bins
+    CK(launch_histogram(d_sym, sym16, n, alphabet, center, hist, touched, ctx->sms, s,
                         &ctx->launches));
     }
     uint32_t* wb_sym = static_cast<uint32_t*>(ctx->ws_book);
     uint8_t* wb_len = reinterpret_cast<uint8_t*>(wb_sym + std::max<uint64_t>(ctx->ws_book_cap / 5, 1));
     {
     KTimer kt(ctx, ACZ_K_BOOK, s);
-    CK(launch_codebook(static_cast<unsigned long long*>(ctx->ws_hist), alphabet, max_leaves,
-                       ctx->ws_cb, wb_sym, wb_len, static_cast<unsigned long long*>(ctx->ws_enc),
-                       &ctx->d_small->canon, ctx->d_small->lut, &ctx->d_small->info, s,
-                       &ctx->launches));
+    CK(launch_codebook(hist, touched, alphabet, max_leaves, ctx->ws_cb, wb_sym, wb_len,
+                       static_cast<unsigned long long*>(ctx->ws_enc), &ctx->d_small->canon,
+                       ctx->d_small->lut, &ctx->d_small->info, s, &ctx->launches));
     }
+    ctx->hist_clean = true;
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, offsetof(acz_gpu_ctx::Small, canon),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -499,7 +514,10 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
     qa.step = 2.0 * eb;
     qa.radius = quant_radius;
     qa.predictor = predictor;
-    qa.sym = static_cast<uint32_t*>(ctx->ws_sym);
+    const int sym16 = (predictor == ACZ_PRED_PREV && quant_radius <= 32768) ? 1 : 0;
+    ctx->last_sym16 = sym16 != 0;
+    qa.sym = sym16 ? nullptr : static_cast<uint32_t*>(ctx->ws_sym);
+    qa.sym16 = sym16 ? static_cast<uint16_t*>(ctx->ws_sym) : nullptr;
     qa.side_state = static_cast<float*>(ctx->ws_side);
     qa.interval = interval;
     qa.row_scratch = static_cast<float*>(ctx->ws_row);
@@ -513,7 +531,7 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
             CK(launch_quant(qa, ctx->sms, s, &ctx->launches));
         }
     }
-    rc = build_book(ctx, qa.sym, n, alphabet, quant_radius, s);
+    rc = build_book(ctx, ctx->ws_sym, sym16, n, alphabet, quant_radius, s);
     if (rc) return rc;
     const BookInfo bi = ctx->h_small->info;
     const unsigned flags = ctx->h_small->flags | bi.flags;
@@ -528,7 +546,8 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
 
     acz_gpu_blob* b = new (std::nothrow) acz_gpu_blob();
     if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
-    rc = finish_encode(ctx, b, qa.sym, n, d_in, interval, s);
+    rc = finish_encode(ctx, b, ctx->ws_sym, sym16, n, d_in, interval,
+                       predictor == ACZ_PRED_LORENZO2D, s);
     if (rc) {
         if (b->arena) cudaFreeAsync(b->arena, s);
         delete b;
@@ -547,7 +566,7 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
     in.uncompressed_bytes = 4ull * n;
     in.compressed_bytes = acz1_size(rank, bi.book_size, bi.total_bits, bi.n_escapes);
     in.device_bytes = b->arena_bytes;
-    in.sidecar_bytes = sidecar_bytes(b->nchunks);
+    in.sidecar_bytes = sidecar_bytes(b->nchunks, b->side_outl != nullptr);
     in.max_code_length = bi.max_len;
     *out = b;
     return ACZ_OK;
@@ -673,23 +692,26 @@ int acz_gpu_blob_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, 
 int acz_gpu_sidecar_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
                             uint64_t* written, void* stream) {
     if (!ctx || !b || !dst) return ACZ_ERR_INVALID;
-    const uint64_t need = sidecar_bytes(b->nchunks);
+    const bool has_outl = b->side_outl != nullptr;
+    const uint64_t need = sidecar_bytes(b->nchunks, has_outl);
     if (cap < need) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     uint8_t* p = dst;
     std::memcpy(p, "ACZS", 4);
     p += 4;
-    const uint32_t ver = 1;
+    const uint32_t ver = 2;
     std::memcpy(p, &ver, 4);
     p += 4;
     const uint64_t hdr[6] = {b->info.element_count, b->info.bit_length, b->interval, b->nchunks,
-                             blob_binding(b->info), 0};
+                             blob_binding(b->info), has_outl ? 1ull : 0ull};
     std::memcpy(p, hdr, sizeof(hdr));
     p += sizeof(hdr);
     CK(cudaMemcpyAsync(p, b->side_bitoff, 8ull * b->nchunks, cudaMemcpyDeviceToHost, s));
     p += 8ull * b->nchunks;
-    CK(cudaMemcpyAsync(p, b->side_outl, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
-    p += 4ull * b->nchunks;
+    if (has_outl) {
+        CK(cudaMemcpyAsync(p, b->side_outl, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+        p += 4ull * b->nchunks;
+    }
     CK(cudaMemcpyAsync(p, b->side_state, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (written) *written = need;
@@ -806,12 +828,17 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
     // sidecar supplied?
     bool have_side = false;
     uint64_t side_interval = interval, side_chunks = (count + interval - 1) / interval;
-    if (sidecar && sidecar_size >= 56 && std::memcmp(sidecar, "ACZS", 4) == 0) {
+    const bool want_outl = pred == ACZ_PRED_LORENZO2D;
+    uint32_t sver = 0;
+    if (sidecar && sidecar_size >= 56) std::memcpy(&sver, sidecar + 4, 4);
+    if (sidecar && sidecar_size >= 56 && std::memcmp(sidecar, "ACZS", 4) == 0 && sver == 2) {
         uint64_t hdr[6];
         std::memcpy(hdr, sidecar + 8, sizeof(hdr));
         if (hdr[0] == count && hdr[1] == bit_length && hdr[2] > 0 &&
+            (pred != ACZ_PRED_PREV || (hdr[2] % 32 == 0)) &&
             hdr[3] == (count + hdr[2] - 1) / hdr[2] && hdr[4] == blob_binding(in) &&
-            sidecar_size == sidecar_bytes(hdr[3]) &&
+            hdr[5] == (want_outl ? 1ull : 0ull) &&
+            sidecar_size == sidecar_bytes(hdr[3], want_outl) &&
             (pred == ACZ_PRED_PREV || hdr[2] == g.plane_size)) {
             have_side = true;
             side_interval = hdr[2];
@@ -822,7 +849,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
     if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
     b->info = in;
     const uint64_t nwords = (bit_length + 31) / 32;
-    cudaError_t e = blob_alloc(b, (uint32_t)k, nwords, nout, side_chunks, s);
+    cudaError_t e = blob_alloc(b, (uint32_t)k, nwords, nout, side_chunks, want_outl, s);
     if (e != cudaSuccess) {
         delete b;
         return cuda_fail(ctx, e, "blob_alloc");
@@ -832,7 +859,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
     b->nchunks = side_chunks;
     b->max_len = maxl;
     b->info.device_bytes = b->arena_bytes;
-    b->info.sidecar_bytes = sidecar_bytes(side_chunks);
+    b->info.sidecar_bytes = sidecar_bytes(side_chunks, want_outl);
     auto cleanup = [&](int rc) {
         cudaFreeAsync(b->arena, s);
         delete b;
@@ -843,7 +870,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
         cudaError_t _e = (expr);                                                   \
         if (_e != cudaSuccess) return cleanup(cuda_fail(ctx, _e, #expr));          \
     } while (0)
-    CKB(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 4), s));
+    CKB(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 32), s));
     CKB(cudaMemcpyAsync(b->words, bits, nbytes, cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(b->book_sym, bsym.data(), 4ull * k, cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(b->book_len, blen.data(), k, cudaMemcpyHostToDevice, s));
@@ -864,8 +891,10 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
         const uint8_t* p = sidecar + 56;
         CKB(cudaMemcpyAsync(b->side_bitoff, p, 8ull * side_chunks, cudaMemcpyHostToDevice, s));
         p += 8ull * side_chunks;
-        CKB(cudaMemcpyAsync(b->side_outl, p, 4ull * side_chunks, cudaMemcpyHostToDevice, s));
-        p += 4ull * side_chunks;
+        if (want_outl) {
+            CKB(cudaMemcpyAsync(b->side_outl, p, 4ull * side_chunks, cudaMemcpyHostToDevice, s));
+            p += 4ull * side_chunks;
+        }
         CKB(cudaMemcpyAsync(b->side_state, p, 4ull * side_chunks, cudaMemcpyHostToDevice, s));
         CKB(cudaStreamSynchronize(s));  // host vectors go out of scope
         *out = b;
@@ -1063,7 +1092,7 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
     }
     if (maxsym >= (1u << 26)) return fail(ctx, ACZ_ERR_PARAM, "symbol alphabet beyond 2^26 unsupported");
     const uint32_t alphabet = maxsym + 1;
-    int rc = build_book(ctx, d_symbols, n, alphabet, 0, s);
+    int rc = build_book(ctx, d_symbols, 0, n, alphabet, 0, s);
     if (rc) return rc;
     const BookInfo bi = ctx->h_small->info;
     if (bi.flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
@@ -1071,7 +1100,7 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
     if (bi.book_size > book_cap) return fail(ctx, ACZ_ERR_INVALID, "book capacity too small");
     if ((bi.total_bits + 7) / 8 > bits_cap) return fail(ctx, ACZ_ERR_INVALID, "bits capacity too small");
     acz_gpu_blob tmpb;
-    rc = finish_encode(ctx, &tmpb, d_symbols, n, nullptr, 0, s);
+    rc = finish_encode(ctx, &tmpb, d_symbols, 0, n, nullptr, 0, false, s);
     if (rc) {
         if (tmpb.arena) cudaFreeAsync(tmpb.arena, s);
         return rc;
@@ -1106,8 +1135,8 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     acz_gpu_blob tmpb;
     const uint64_t nwords = (bit_length + 31) / 32;
-    CK(blob_alloc(&tmpb, book_size, nwords, 0, 0, s));
-    CK(cudaMemsetAsync(tmpb.words, 0, 4ull * (nwords + 4), s));
+    CK(blob_alloc(&tmpb, book_size, nwords, 0, 0, false, s));
+    CK(cudaMemsetAsync(tmpb.words, 0, 4ull * (nwords + 32), s));
     CK(cudaMemcpyAsync(tmpb.words, bits, (bit_length + 7) / 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(tmpb.book_sym, book_sym, 4ull * book_size, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(tmpb.book_len, book_len, book_size, cudaMemcpyHostToDevice, s));
@@ -1179,17 +1208,33 @@ int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches) {
 // --------------------------------------------------------------------------- debug --
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset) {
     if (!ctx || !out || n < 8) return ACZ_ERR_INVALID;
-    unsigned long long v[8];
+    unsigned long long v[12];
     CK(quant_spec_stats(v, reset != 0));
     for (int i = 0; i < 8; ++i) out[i] = v[i];
+    if (n >= 16) {
+        unsigned long long c[8];
+        CK(codebook_stats(c, reset != 0));
+        for (int i = 0; i < 8; ++i) out[8 + i] = c[i];
+    }
+    if (n >= 20)
+        for (int i = 0; i < 4; ++i) out[16 + i] = v[8 + i];
+    if (n >= 24) {
+        unsigned long long d[4];
+        CK(decode_stats(d, reset != 0));
+        for (int i = 0; i < 4; ++i) out[20 + i] = d[i];
+    }
     return ACZ_OK;
 }
 
 int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, void* stream) {
     if (!ctx || !d_out) return ACZ_ERR_INVALID;
     if (n != ctx->last_n || !ctx->ws_sym) return fail(ctx, ACZ_ERR_SHAPE, "no symbols of that size");
-    CK(cudaMemcpyAsync(d_out, ctx->ws_sym, 4ull * n, cudaMemcpyDeviceToDevice,
-                       static_cast<cudaStream_t>(stream)));
+    if (ctx->last_sym16)
+        CK(launch_widen_u16(static_cast<const uint16_t*>(ctx->ws_sym), d_out, n, ctx->sms,
+                            static_cast<cudaStream_t>(stream), &ctx->launches));
+    else
+        CK(cudaMemcpyAsync(d_out, ctx->ws_sym, 4ull * n, cudaMemcpyDeviceToDevice,
+                           static_cast<cudaStream_t>(stream)));
     return ACZ_OK;
 }
 

@@ -13,7 +13,8 @@
 
 namespace acz_b200 {
 
-constexpr int kLutBits = 12;             // decode lookup table: 4096 entries
+constexpr int kLutBits = 14;             // decode lookup table: 16384 entries (64 KiB smem);
+                                         // codes > 14 bits are ~2% of activation symbols
 constexpr int kLutSize = 1 << kLutBits;
 constexpr uint32_t kMaxBook = 0xFFFF;    // ACZ1 u16 codebook size (ref src/codec.cpp:107)
 
@@ -25,7 +26,7 @@ struct BookInfo {
     unsigned int book_size;          // number of distinct symbols
     unsigned int max_len;
     unsigned int flags;              // kFlag* bits below
-    unsigned int pad;
+    unsigned int slow;               // 1: more leaves than the shared-memory codebook holds
 };
 constexpr unsigned kFlagNonFinite = 1u;  // DomainError (ref include/acz/tensor.hpp:69-73)
 constexpr unsigned kFlagBookTooBig = 2u; // FormatError (ref src/codec.cpp:107-108)
@@ -41,6 +42,20 @@ struct CanonTables {
 };
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+// Asynchronous global -> shared copies (LDGSTS): a loop of these issues every load before
+// any completes, unlike a load/store loop whose iterations each wait out the memory latency.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // Exact reference arithmetic ------------------------------------------------------------
 
@@ -65,6 +80,71 @@ __device__ __forceinline__ uint32_t quant_step(float xf, double pred, double ste
     }
     *value = xf;
     return 0u;
+}
+
+// Exact (double)(float)y for a double y, without the F2F pipe (7.4 conversions / clk / SM
+// measured vs 62.5 DADD): adding and subtracting M = 1.5 * 2^(e+29) rounds y to 24
+// significant bits, ties to even, exactly like the F32 conversion. Valid when the result is
+// a normal float below 2^127; other exponents (zero, subnormal, overflow) take the
+// conversion path so inf/denormal behaviour is the reference's.
+__device__ __forceinline__ double rn32d(double y) {
+    const int hi = __double2hiint(y);
+    const int ex = (hi >> 20) & 0x7FF;
+    if (ex < 1023 - 126 || ex > 1023 + 126) return (double)__double2float_rn(y);
+    const double M = __hiloint2double((ex << 20) + ((29 << 20) | (1 << 19)), 0);
+    return __dsub_rn(__dadd_rn(y, M), M);
+}
+
+// Parameters of the reference quantisation step.
+struct QParams {
+    double eb, step, inv_step, radius_d;
+    long long R;
+    int exact_div;  // 1/step not usable (absurdly small eb): always divide
+};
+
+// The reference quantisation step (ref src/codec.cpp:80-101), bit-exact:
+//   q = round((x - pred) / step)   ties away from zero, correctly rounded quotient
+//   accept iff |q| < R, cand = fl32(pred + q*step) finite, |x - cand| <= eb
+// The quotient is a reciprocal multiply; round(RN(d/step)) can differ from round(d*inv)
+// only within a few ulps of a half-integer, where the guard falls back to __ddiv_rn.
+// Rounding to an integer uses the 1.5*2^52 magic add, whose low word is q itself (no F2I);
+// the guard is evaluated off the dependency chain and only consulted at the end.
+// Returns the symbol (0 = escape); *r receives the chain value (a float, as a double).
+// The fragile-quotient fallback is inline and branched around (a call on the chain costs
+// ~120 cycles per step on B200: tools/microbench/qchain.cu).
+__device__ __forceinline__ uint32_t qstep(double orig, float xf, double pred, const QParams& p,
+                                          double* r) {
+    (void)xf;
+    const double d = __dsub_rn(orig, pred);
+    const double t = __dmul_rn(d, p.inv_step);
+    const double M52 = 6755399441055744.0;  // 1.5 * 2^52
+    double tm = __dadd_rn(t, M52);
+    double q = __dsub_rn(tm, M52);
+    // plain F2F round trip: the shortest dependent chain measured on B200
+    // (tools/microbench/qchain.cu: 162 cycles/step vs 190-282 for magic-add rounding)
+    float cf = __double2float_rn(__dadd_rn(pred, __dmul_rn(q, p.step)));
+    const bool fragile = p.exact_div || 0.5 - fabs(t - q) <= fabs(t) * 0x1p-44 + 0x1p-60;
+    if (fragile) {
+        q = round(__ddiv_rn(d, p.step));
+        tm = fabs(q) < 0x1p51 ? __dadd_rn(q, M52) : M52;
+        cf = __double2float_rn(__dadd_rn(pred, __dmul_rn(q, p.step)));
+    }
+    const double c = (double)cf;
+    const bool ok = fabs(q) < p.radius_d && isfinite(cf) && fabs(__dsub_rn(orig, c)) <= p.eb;
+    *r = ok ? c : orig;
+    return ok ? (uint32_t)(__double2loint(tm) + (int)p.R) : 0u;
+}
+
+__host__ inline QParams make_qparams(double eb, uint32_t radius) {
+    QParams p;
+    p.eb = eb;
+    p.step = 2.0 * eb;
+    p.inv_step = 1.0 / p.step;
+    p.radius_d = (double)radius;
+    p.R = radius;
+    // the reciprocal path needs a finite, normal 1/step and |t| well inside 2^51
+    p.exact_div = !(p.inv_step < 1e300 && p.step < 1e300) ? 1 : 0;
+    return p;
 }
 
 }  // namespace acz_b200

@@ -41,7 +41,7 @@ struct BitReader {
             nb += 32;
         }
     }
-    __device__ __forceinline__ uint32_t peek12() const { return (uint32_t)(buf >> (64 - kLutBits)); }
+    __device__ __forceinline__ uint32_t peek() const { return (uint32_t)(buf >> (64 - kLutBits)); }
     __device__ __forceinline__ void skip(int k) {
         buf <<= k;
         nb -= k;
@@ -62,7 +62,7 @@ __device__ __forceinline__ uint32_t decode_one(BitReader& br, uint64_t& pos,
                                                const uint32_t* s_lut, const CanonTables& ct,
                                                const uint32_t* book_sym, uint32_t* sym) {
     br.refill();
-    const uint32_t e = s_lut[br.peek12()];
+    const uint32_t e = s_lut[br.peek()];
     uint32_t len = e & 31;
     if (len) {
         *sym = e >> 5;
@@ -87,24 +87,16 @@ __device__ __forceinline__ uint32_t decode_one(BitReader& br, uint64_t& pos,
 
 __device__ __forceinline__ void load_tables(const uint32_t* lut, const CanonTables* canon,
                                             uint32_t* s_lut, CanonTables* s_ct) {
-    for (int i = threadIdx.x; i < kLutSize; i += blockDim.x) s_lut[i] = __ldg(lut + i);
+    // 64 KiB LUT: asynchronous 16-byte copies, all in flight at once
+    for (int i = threadIdx.x; i < kLutSize / 4; i += blockDim.x) cp_async16(s_lut + 4 * i, lut + 4 * i);
+    cp_async_commit();
     for (int i = threadIdx.x; i < 65; i += blockDim.x) {
         s_ct->first_code[i] = canon->first_code[i];
         s_ct->first_index[i] = canon->first_index[i];
         s_ct->count[i] = canon->count[i];
     }
+    cp_async_wait<0>();
     __syncthreads();
-}
-
-// Exact RN32 of a double kept in a double register (no F2F on the dependency chain):
-// adding and subtracting 1.5 * 2^(e+29) rounds y to 24 significant bits, ties to even.
-// Valid for y in the float normal range; other inputs take the conversion path.
-__device__ __forceinline__ double rn32_in_double(double y) {
-    const int hi = __double2hiint(y);
-    const int ex = (hi >> 20) & 0x7FF;
-    if (ex < 1023 - 126 || ex > 1023 + 127) return (double)__double2float_rn(y);
-    const double M = __hiloint2double((ex << 20) + ((29 << 20) | (1 << 19)), 0);
-    return __dsub_rn(__dadd_rn(y, M), M);
 }
 
 // Canonical decode limits (left-aligned): the code length of a 64-bit window w is the
@@ -129,112 +121,172 @@ __device__ __forceinline__ void build_limits(const CanonTables& ct, Limits* L) {
     }
 }
 
-__global__ void __launch_bounds__(128) k_decode_prev(DecodeArgs a) {
-    __shared__ uint32_t s_lut[kLutSize];
-    __shared__ CanonTables s_ct;
-    __shared__ Limits s_lim;
-    load_tables(a.lut, a.canon, s_lut, &s_ct);
-    build_limits(s_ct, &s_lim);
-    __syncthreads();
-    const uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (chunk >= a.nchunks) return;
-    const uint64_t start = chunk * a.interval;
-    const uint64_t end = min(a.g.n, start + a.interval);
-    uint64_t pos = a.side_bitoff[chunk];
-    uint32_t oi = a.side_outl[chunk];
-    double r = (double)a.side_state[chunk];
-    const uint64_t P = a.g.plane_size;
-    uint64_t pin = start % P;
+// K6+K7 (PrevValue). A task = 32 consecutive sidecar chunks (`interval` symbols each, a
+// multiple of 32); a warp takes one task at a time, lane = chunk. Persistent CTAs (one per SM,
+// kDW warps) load the 64 KiB decode LUT and the long-code book entries once. Per task the
+// warp stages the contiguous bitstream span of its 32 chunks into shared memory with
+// asynchronous 16-byte copies; every lane then decodes its chunk from its sidecar bit offset
+// with two shared loads + a funnel shift per symbol and reconstructs it with the exact
+// reference expression from the sidecar chain state (ref src/codec.cpp:143-164). Outputs go
+// through a transposed 32x32 shared tile, so every global store is one coalesced 128-byte
+// line of one chunk. The outlier cursor of a chunk is found by binary search over the
+// (sorted) outlier indices at its first escape. A span larger than the staging window
+// (very long codes) decodes from global memory through the same code.
+constexpr int kDW = 12;           // warps per CTA (one CTA per SM)
+constexpr int kDStage = 1792;     // staged stream words per warp (7 KiB, a multiple of 4:
+                                  // 32 x 128 symbols at up to 14 bits/symbol)
+constexpr int kLongCap = 6144;    // book entries of codes longer than kLutBits kept in smem
+constexpr size_t kDecSmem = 4ull * kLutSize + 4ull * kLongCap + 4ull * kDW * (kDStage + 32 * 33);
+__device__ unsigned long long g_dclk[4];  // debug: prologue, staging, loop cycles; tasks
+
+__device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
+                                                    unsigned long long key) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <bool kStaged, typename PosT>
+__device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t* bits, PosT p,
+                                             const uint32_t* s_lut, const uint32_t* lbook,
+                                             uint32_t lfirst, const Limits& lim,
+                                             const CanonTables& ct, uint32_t cnt,
+                                             uint64_t start, double r, uint32_t to_reset,
+                                             float* tile, float (*s_out)[33], uint64_t chunk0,
+                                             int lane) {
+    const uint32_t I = (uint32_t)a.interval;
+    const uint32_t P32 = (uint32_t)min(a.g.plane_size, (uint64_t)0xFFFFFFFFu);
     const int R = (int)a.radius;
     const double step = a.step, eb = a.eb;
     const bool zf = a.zero_filter != 0;
-    // bit reader: 64-bit MSB-aligned buffer; words are stored byte-swapped (ACZ1 order)
-    const uint32_t* W = a.words;
-    const bool short_codes = s_lim.maxlen <= 32;  // buffer always holds a whole code
-    uint64_t wi = pos >> 5;
-    const int off = (int)(pos & 31);
-    unsigned long long buf =
-        ((((unsigned long long)bswap32(__ldg(W + wi))) << 32) | bswap32(__ldg(W + wi + 1))) << off;
-    int nb = 64 - off;
-    wi += 2;
-    float ob[8];
-    uint64_t flat = start;
-    while (flat < end) {
-        // decode one symbol
-        if (nb <= 32) {
-            if ((wi & 31) == 0 && wi + 32 < a.nwords)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(W + wi + 32));
-            buf |= (unsigned long long)bswap32(__ldg(W + wi)) << (32 - nb);
-            ++wi;
-            nb += 32;
-        }
-        const uint32_t e = s_lut[(uint32_t)(buf >> (64 - kLutBits))];
-        uint32_t len = e & 31, sym;
-        if (len) {
-            sym = e >> 5;
-        } else {
-            // long code: canonical limit search (window has >= 33 valid bits; codes longer
-            // than the buffer use an absolute 64-bit window)
-            unsigned long long w = buf;
-            if (!short_codes) {
-                const uint64_t ap = (wi << 5) - (uint64_t)nb;  // absolute position of buf's MSB
-                const uint64_t i = ap >> 5;
-                const int o = (int)(ap & 31);
-                const unsigned long long x0 = bswap32(__ldg(W + i)), x1 = bswap32(__ldg(W + i + 1)),
-                                         x2 = bswap32(__ldg(W + i + 2));
-                const unsigned long long h = (x0 << 32) | x1;
-                w = o ? (h << o) | (x2 << o >> 32) : h;
+    uint32_t oi = 0xFFFFFFFFu;  // outlier cursor, found at the first escape
+    auto word = [&](PosT i) -> uint32_t {
+        return bswap32(kStaged ? bits[i] : __ldg(bits + i));
+    };
+    for (uint32_t t0 = 0; t0 < I; t0 += 32) {
+        if (t0 < cnt) {
+            const uint32_t m = min(32u, cnt - t0);
+            for (uint32_t j = 0; j < m; ++j) {
+                const PosT i = p >> 5;
+                const uint32_t o = (uint32_t)p & 31u;
+                const uint32_t w0 = word(i), w1 = word(i + 1);
+                const uint32_t top = __funnelshift_l(w1, w0, o);  // stream bits [p, p+32)
+                const uint32_t e = s_lut[top >> (32 - kLutBits)];
+                uint32_t len = e & 31, sym = e >> 5;
+                if (!len) {
+                    // long code: canonical limit search on a 64-bit window
+                    const uint32_t w2 = word(i + 2);
+                    const unsigned long long win =
+                        ((unsigned long long)top << 32) | __funnelshift_l(w2, w1, o);
+                    len = kLutBits + 1;
+                    while (len < 64 && (win >> (64 - len)) >= lim.lim[len]) ++len;
+                    const unsigned long long c = win >> (64 - len);
+                    const uint32_t idx = ct.first_index[len] + (uint32_t)(c - lim.nc[len]);
+                    sym = lbook ? lbook[idx - lfirst] : __ldg(a.book_sym + idx);
+                }
+                p += len;
+                // reconstruct (ref src/codec.cpp:143-164); r is an exact float in a double
+                float v;
+                if (sym == 0) {
+                    if (oi == 0xFFFFFFFFu)
+                        oi = lower_bound_u64(a.out_index, (uint32_t)a.n_outliers, start + t0 + j);
+                    v = __ldg(a.out_value + oi);
+                    ++oi;
+                } else {
+                    const double pred = to_reset == 0 ? 0.0 : r;
+                    v = __double2float_rn(__dadd_rn(pred, __dmul_rn((double)((int)sym - R), step)));
+                }
+                r = (double)v;
+                tile[j] = (zf && fabs(r) <= eb) ? 0.0f : v;
+                to_reset = to_reset + 1 == P32 ? 0u : to_reset + 1;
             }
-            len = kLutBits + 1;
-            while (len < 64 && (w >> (64 - len)) >= s_lim.lim[len]) ++len;
-            const unsigned long long c = w >> (64 - len);
-            sym = __ldg(a.book_sym + s_ct.first_index[len] + (uint32_t)(c - s_lim.nc[len]));
         }
-        if (len >= 64) {
-            buf = 0;
-        } else {
-            buf <<= len;
+        __syncwarp();
+        // coalesced stores: line c of the tile = elements [t0, t0+32) of chunk chunk0 + c
+        {
+            float* dst = a.out + chunk0 * I + t0 + lane;
+            const float* src = &s_out[0][lane];
+            if ((chunk0 + 32) * I <= a.g.n) {  // all 32 chunks complete (every task but the last)
+#pragma unroll 8
+                for (int c = 0; c < 32; ++c, dst += I, src += 33) *dst = *src;
+            } else {
+                for (int c = 0; c < 32; ++c, dst += I, src += 33) {
+                    const uint64_t e = (chunk0 + c) * I + t0 + lane;
+                    if (e < a.g.n) *dst = *src;
+                }
+            }
         }
-        nb -= (int)len;
-        if (nb < 0) {
-            // consumed beyond the buffer (code longer than the valid bits): re-sync
-            const uint64_t ap = (wi << 5) - (uint64_t)(nb + (int)len) + len;
-            wi = ap >> 5;
-            const int o2 = (int)(ap & 31);
-            buf = ((((unsigned long long)bswap32(__ldg(W + wi))) << 32) | bswap32(__ldg(W + wi + 1))) << o2;
-            nb = 64 - o2;
-            wi += 2;
-        }
-        // reconstruct (ref src/codec.cpp:143-164); r stays an exact float value in double
-        float v;
-        if (sym == 0) {
-            v = __ldg(a.out_value + oi);
-            ++oi;
-            r = (double)v;
-        } else {
-            const double pred = pin == 0 ? 0.0 : r;
-            const double y = __dadd_rn(pred, __dmul_rn((double)((int)sym - R), step));
-            r = rn32_in_double(y);
-            v = (float)r;
-        }
-        const float o = (zf && fabs(r) <= eb) ? 0.0f : v;
-        const int slot = (int)(flat & 7);
-        ob[slot] = o;
-        ++flat;
-        if (++pin == P) pin = 0;
-        if (slot == 7) {
-            float4* dst = reinterpret_cast<float4*>(a.out + flat - 8);
-            dst[0] = make_float4(ob[0], ob[1], ob[2], ob[3]);
-            dst[1] = make_float4(ob[4], ob[5], ob[6], ob[7]);
-        }
+        __syncwarp();
     }
-    // tail (chunk end not 8-aligned: only the tensor's last chunk)
-    const int rem = (int)(flat & 7);
-    for (int t = 0; t < rem; ++t) a.out[flat - rem + t] = ob[t];
+}
+
+__global__ void __launch_bounds__(kDW * 32, 1) k_decode_prev(DecodeArgs a) {
+    extern __shared__ uint32_t dsm[];
+    const long long tk0 = clock64();
+    uint32_t* s_lut = dsm;                // 64 KiB
+    uint32_t* s_lbook = dsm + kLutSize;   // book entries of long codes (canonical order)
+    __shared__ CanonTables s_ct;
+    __shared__ Limits s_lim;
+    const uint32_t lfirst = __ldg(&a.canon->first_index[kLutBits + 1]);
+    const bool lstaged = a.book_size - lfirst <= (uint32_t)kLongCap;
+    if (lstaged)
+        for (uint32_t i = threadIdx.x; i < a.book_size - lfirst; i += blockDim.x)
+            cp_async4(s_lbook + i, a.book_sym + lfirst + i);
+    load_tables(a.lut, a.canon, s_lut, &s_ct);  // commits and waits for all async copies
+    build_limits(s_ct, &s_lim);
+    __syncthreads();
+    const uint32_t* lbook = lstaged ? s_lbook : nullptr;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* s_bits = dsm + kLutSize + kLongCap + w * (kDStage + 32 * 33);
+    float(*s_out)[33] = reinterpret_cast<float(*)[33]>(s_bits + kDStage);
+    float* tile = s_out[lane];
+    if (lane == 0) atomicAdd(&g_dclk[0], (unsigned long long)(clock64() - tk0));
+    const uint64_t ntasks = (a.nchunks + 31) / 32;
+    const uint64_t I = a.interval;
+    for (uint64_t task = (uint64_t)blockIdx.x * kDW + w; task < ntasks;
+         task += (uint64_t)gridDim.x * kDW) {
+        const long long tk1 = clock64();
+        const uint64_t chunk0 = task * 32;
+        const uint64_t chunk = chunk0 + lane;
+        const bool active = chunk < a.nchunks;
+        const uint64_t start = chunk * I;
+        const uint32_t cnt = active ? (uint32_t)min(I, a.g.n - start) : 0u;
+        const uint64_t pos = active ? a.side_bitoff[chunk] : 0;
+        const double r = active ? (double)a.side_state[chunk] : 0.0;
+        const uint32_t pin = (uint32_t)(start % a.g.plane_size);
+        // the task's stream span [b0, b1) in bits, staged as words [w0, w0 + nw)
+        const uint64_t b0 = __shfl_sync(0xffffffffu, pos, 0);
+        const uint64_t b1 = chunk0 + 32 < a.nchunks ? a.side_bitoff[chunk0 + 32] : a.bit_length;
+        const uint64_t w0 = (b0 >> 5) & ~3ull;         // 16-byte aligned start
+        const uint64_t nw = ((b1 + 31) >> 5) + 3 - w0;  // + 3 words of look-ahead
+        if (nw <= (uint64_t)kDStage) {
+            // the words array is padded by 32 words, so the rounded-up tail is readable
+            for (uint64_t i = lane; i < (nw + 3) / 4; i += 32)
+                cp_async16(s_bits + 4 * i, a.words + w0 + 4 * i);
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncwarp();
+            const long long tk2 = clock64();
+            decode_chunk<true, uint32_t>(a, s_bits, (uint32_t)(pos - w0 * 32), s_lut, lbook, lfirst,
+                                         s_lim, s_ct, cnt, start, r, pin, tile, s_out, chunk0, lane);
+            if (lane == 0) {
+                atomicAdd(&g_dclk[1], (unsigned long long)(tk2 - tk1));
+                atomicAdd(&g_dclk[2], (unsigned long long)(clock64() - tk2));
+                atomicAdd(&g_dclk[3], 1ull);
+            }
+        } else {
+            decode_chunk<false, uint64_t>(a, a.words, pos, s_lut, lbook, lfirst, s_lim, s_ct, cnt,
+                                          start, r, pin, tile, s_out, chunk0, lane);
+        }
+        __syncwarp();
+    }
 }
 
 __global__ void __launch_bounds__(128) k_decode_lorenzo(DecodeArgs a) {
-    __shared__ uint32_t s_lut[kLutSize];
+    extern __shared__ uint32_t s_lut[];
     __shared__ CanonTables s_ct;
     load_tables(a.lut, a.canon, s_lut, &s_ct);
     const uint64_t plane = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -275,7 +327,7 @@ __global__ void __launch_bounds__(128) k_decode_lorenzo(DecodeArgs a) {
 
 // Single-thread sequential decode of the whole stream (foreign blobs, generic Huffman).
 __global__ void k_scan_decode(ScanArgs a) {
-    __shared__ uint32_t s_lut[kLutSize];
+    extern __shared__ uint32_t s_lut[];
     __shared__ CanonTables s_ct;
     load_tables(a.lut, a.canon, s_lut, &s_ct);
     if (threadIdx.x != 0) return;
@@ -289,7 +341,7 @@ __global__ void k_scan_decode(ScanArgs a) {
         if (flat == next_side) {
             if (a.side_bitoff) {
                 a.side_bitoff[flat / a.interval] = pos;
-                a.side_outl[flat / a.interval] = (uint32_t)oi;
+                if (a.side_outl) a.side_outl[flat / a.interval] = (uint32_t)oi;
             }
             next_side += a.interval;
         }
@@ -354,22 +406,51 @@ __global__ void __launch_bounds__(128) k_chain_states(const uint32_t* __restrict
 
 }  // namespace
 
+cudaError_t set_decode_attrs() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_decode_prev, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kDecSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_decode_lorenzo, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 4 * kLutSize);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_scan_decode, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 4 * kLutSize);
+    done = e == cudaSuccess;
+    return e;
+}
+
 cudaError_t launch_decode(const DecodeArgs& a, int sms, cudaStream_t s, uint64_t* launches) {
-    (void)sms;
+    cudaError_t e = set_decode_attrs();
+    if (e != cudaSuccess) return e;
     const unsigned threads = 128;
     if (a.predictor == ACZ_PRED_PREV) {
-        const uint64_t blocks = (a.nchunks + threads - 1) / threads;
-        k_decode_prev<<<(unsigned)blocks, threads, 0, s>>>(a);
+        const uint64_t tasks = (a.nchunks + 31) / 32;
+        uint64_t blocks = (tasks + kDW - 1) / kDW;
+        if (blocks > (uint64_t)sms) blocks = sms;  // persistent: one CTA per SM
+        k_decode_prev<<<(unsigned)blocks, kDW * 32, kDecSmem, s>>>(a);
     } else {
         const uint64_t blocks = (a.g.planes + threads - 1) / threads;
-        k_decode_lorenzo<<<(unsigned)blocks, threads, 0, s>>>(a);
+        k_decode_lorenzo<<<(unsigned)blocks, threads, 4 * kLutSize, s>>>(a);
     }
     ++*launches;
     return cudaGetLastError();
 }
 
+cudaError_t decode_stats(unsigned long long* out, bool reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_dclk, sizeof(g_dclk));
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[4] = {0};
+        e = cudaMemcpyToSymbol(g_dclk, z, sizeof(z));
+    }
+    return e;
+}
+
 cudaError_t launch_scan_decode(const ScanArgs& a, cudaStream_t s, uint64_t* launches) {
-    k_scan_decode<<<1, 128, 0, s>>>(a);
+    cudaError_t e = set_decode_attrs();
+    if (e != cudaSuccess) return e;
+    k_scan_decode<<<1, 128, 4 * kLutSize, s>>>(a);
     ++*launches;
     return cudaGetLastError();
 }

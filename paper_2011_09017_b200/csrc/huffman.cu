@@ -26,36 +26,64 @@ namespace {
 constexpr int kHistWindow = 8192;
 
 // --------------------------------------------------------------------------- K3 ----
-__global__ void __launch_bounds__(512) k_histogram(const uint32_t* __restrict__ sym, uint64_t n,
+// The histogram buffer is self-cleaning: the codebook kernel zeroes every bin it reads and
+// the `touched` bitmap, so no per-call memset of the 2R-bin table is needed.
+template <typename SymT>
+__global__ void __launch_bounds__(512) k_histogram(const SymT* __restrict__ sym, uint64_t n,
                                                    uint32_t alphabet, uint32_t win_lo,
-                                                   uint32_t win_n,
-                                                   unsigned long long* __restrict__ hist) {
+                                                   uint32_t win_n, uint32_t center,
+                                                   unsigned long long* __restrict__ hist,
+                                                   uint32_t* __restrict__ touched) {
     __shared__ unsigned int bins[kHistWindow];
-    for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x) bins[i] = 0;
+    for (uint32_t i = threadIdx.x; i < kHistWindow; i += blockDim.x) bins[i] = 0;
     __syncthreads();
+    // the zero-residual symbol (about half of all ReLU activations) is counted in a register:
+    // no shared-memory atomic contention on the hottest bin
+    uint32_t c0 = 0;
+    auto count = [&](uint32_t e) {
+        if (e == center) {
+            ++c0;
+            return;
+        }
+        const uint32_t o = e - win_lo;
+        if (o < win_n) {
+            atomicAdd(&bins[o], 1u);
+        } else if (e < alphabet) {
+            atomicAdd(&hist[e], 1ull);
+            atomicOr(&touched[e >> 5], 1u << (e & 31));
+        }
+    };
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t n4 = ((reinterpret_cast<uintptr_t>(sym) & 15) == 0) ? n / 4 : 0;
+    constexpr int V = 16 / sizeof(SymT);  // symbols per 128-bit load
+    const uint64_t nv = ((reinterpret_cast<uintptr_t>(sym) & 15) == 0) ? n / V : 0;
     const uint4* s4 = reinterpret_cast<const uint4*>(sym);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
-        uint4 v = __ldcs(s4 + i);
-        uint32_t e[4] = {v.x, v.y, v.z, v.w};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 v = __ldcs(s4 + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            uint32_t o = e[k] - win_lo;
-            if (o < win_n) atomicAdd(&bins[o], 1u);
-            else if (e[k] < alphabet) atomicAdd(&hist[e[k]], 1ull);
+            if (sizeof(SymT) == 2) {
+                count(w[k] & 0xFFFFu);
+                count(w[k] >> 16);
+            } else {
+                count(w[k]);
+            }
         }
     }
-    for (uint64_t i = n4 * 4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += stride) {
-        uint32_t e = sym[i];
-        uint32_t o = e - win_lo;
-        if (o < win_n) atomicAdd(&bins[o], 1u);
-        else if (e < alphabet) atomicAdd(&hist[e], 1ull);
-    }
+    for (uint64_t i = nv * V + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += stride)
+        count((uint32_t)sym[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+    if ((threadIdx.x & 31) == 0 && c0) atomicAdd(&bins[center - win_lo], c0);
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < win_n; i += blockDim.x)
-        if (bins[i]) atomicAdd(&hist[win_lo + i], (unsigned long long)bins[i]);
+    // flush: win_lo is a multiple of 32, so a warp's 32 consecutive bins are one bitmap word
+    for (uint32_t i = threadIdx.x; i < kHistWindow; i += blockDim.x) {
+        const uint32_t b = i < win_n ? bins[i] : 0u;
+        if (b) atomicAdd(&hist[win_lo + i], (unsigned long long)b);
+        const unsigned m = __ballot_sync(0xffffffffu, b != 0);
+        if ((threadIdx.x & 31) == 0 && m) atomicOr(&touched[(win_lo + i) >> 5], m);
+    }
 }
 
 // --------------------------------------------------------------------------- K4 ----
@@ -134,11 +162,424 @@ __device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* tmp, ui
     return res;
 }
 
-__global__ void __launch_bounds__(kCbThreads, 1) k_codebook(
-    const unsigned long long* __restrict__ hist, uint32_t alphabet, uint64_t max_leaves,
-    void* scratch, uint32_t* __restrict__ book_sym, uint8_t* __restrict__ book_len,
-    unsigned long long* __restrict__ enc, CanonTables* __restrict__ canon,
-    uint32_t* __restrict__ lut, BookInfo* __restrict__ info) {
+// Canonical decode tables + LUT from per-length counts (shared by both codebook paths and
+// the foreign-blob table builder). Canonical codes (ref src/huffman.cpp:75-86): the first
+// code of length l is end(l-1) << 1, end(l) = first(l) + count(l). A LUT index v (the next
+// kLutBits stream bits) decodes to the smallest l with v < end(l) << (kLutBits - l) -- a
+// 4-step binary search over the left-justified limits; v beyond them is a long code (0).
+__device__ void write_tables(const uint32_t* s_count, const unsigned long long* s_first_code,
+                             const uint32_t* s_first_index, const uint32_t* book_sym,
+                             CanonTables* canon, uint32_t* lut) {
+    __shared__ uint32_t s_lj[kLutBits + 1];
+    __shared__ uint32_t s_start[kLutBits + 1];
+    const int tid = threadIdx.x;
+    if (tid < 65) {
+        canon->first_code[tid] = s_first_code[tid];
+        canon->first_index[tid] = s_first_index[tid];
+        canon->count[tid] = s_count[tid];
+    }
+    if (tid == 0) {
+        unsigned long long end = 0;
+        s_lj[0] = 0;
+        for (int l = 1; l <= kLutBits; ++l) {
+            const unsigned long long st = end << 1;
+            end = st + s_count[l];
+            s_start[l] = (uint32_t)st;
+            s_lj[l] = (uint32_t)min(end << (kLutBits - l), (unsigned long long)kLutSize);
+        }
+    }
+    __syncthreads();
+    for (uint32_t v = tid; v < kLutSize; v += blockDim.x) {
+        uint32_t e = 0;
+        if (v < s_lj[kLutBits]) {
+            int lo = 1, hi = kLutBits;  // smallest l with v < lj[l]
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (v < s_lj[mid]) hi = mid; else lo = mid + 1;
+            }
+            const uint32_t c = v >> (kLutBits - lo);
+            e = (book_sym[s_first_index[lo] + (c - s_start[lo])] << 5) | (uint32_t)lo;
+        }
+        lut[v] = e;
+    }
+}
+
+// Fast K4: every structure of the tree build lives in shared memory (books of up to
+// kFastLeaves symbols -- all activation books at eb >= ~3e-4). Steps (ref
+// src/huffman.cpp:22-86, 113-125):
+//   1. compaction of the touched bins (bitmap written by K3), ascending symbol order
+//      == the reference's std::map iteration order; the bins are zeroed on the way;
+//   2. bitonic sort of the 64-bit keys (freq << 16 | leaf index): ascending frequency,
+//      ties by symbol == the reference heap's (freq, creation index) order for leaves;
+//   3. Huffman tree by parallel rounds (see k_codebook_slow, step 3) with S-positions
+//      computed by binary search instead of a materialised merge;
+//   4. depths by pointer jumping; 5. canonical (length, symbol) order; 6. decode tables.
+constexpr int kFastLeaves = 8192;
+// phase timing of the fast codebook (debug; acz_gpu_debug_counters slots 8..15):
+// compaction, sort, rounds, depths, canonical, tables (SM cycles), round count, calls
+__device__ unsigned long long g_cbstats[8];
+constexpr size_t kFastSmem = kFastLeaves * 8 /*keys*/ + kFastLeaves * 8 /*ifreq*/ +
+                             2 * kFastLeaves * 2 /*parent*/ + 2 * kFastLeaves /*depth*/;
+
+__global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
+    unsigned long long* __restrict__ hist, uint32_t* __restrict__ touched, uint32_t alphabet,
+    uint32_t* __restrict__ leaf_sym, uint32_t* __restrict__ book_sym,
+    uint8_t* __restrict__ book_len, unsigned long long* __restrict__ enc,
+    CanonTables* __restrict__ canon, uint32_t* __restrict__ lut, BookInfo* __restrict__ info) {
+    extern __shared__ unsigned long long dyn[];
+    unsigned long long* key = dyn;                         // [kFastLeaves]
+    unsigned long long* ifreq = dyn + kFastLeaves;         // [kFastLeaves]
+    uint16_t* par = reinterpret_cast<uint16_t*>(dyn + 2 * kFastLeaves);  // [2*kFastLeaves]
+    uint8_t* dep = reinterpret_cast<uint8_t*>(par + 2 * kFastLeaves);    // [2*kFastLeaves]
+    __shared__ uint32_t scan_tmp[kCbWarps + 1];
+    __shared__ unsigned long long s_first_code[65];
+    __shared__ uint32_t s_count[65], s_first_index[65], s_base[65];
+    __shared__ uint32_t s_wcnt[kCbWarps][65];
+    __shared__ unsigned long long s_total_bits, s_esc;
+    __shared__ uint32_t s_max_len, s_flags;
+    __shared__ uint32_t sh_li, sh_ii, sh_m, sh_nl, sh_ni, sh_xm, sh_done;
+    const int tid = threadIdx.x;
+    long long tclk = clock64();
+    auto phase = [&](int slot) {
+        if (tid == 0) {
+            const long long t = clock64();
+            atomicAdd(&g_cbstats[slot], (unsigned long long)(t - tclk));
+            tclk = t;
+        }
+    };
+
+    // (1) compaction -------------------------------------------------------------------
+    // warp wp owns bitmap words [wp*per, (wp+1)*per); lane b of a word loads bin b
+    // (coalesced, independent loads); positions = block prefix of set bits.
+    const int lane = tid & 31, warp = tid >> 5;
+    const uint32_t nwords = (alphabet + 31) / 32;
+    const uint32_t per = (nwords + kCbWarps - 1) / kCbWarps;
+    const uint32_t w0 = min(nwords, warp * per), w1 = min(nwords, w0 + per);
+    uint32_t mine = 0;
+    for (uint32_t w = w0 + lane; w < w1; w += 32) mine += __popc(touched[w]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (tid == 0) {
+        s_flags = 0;
+        s_total_bits = 0;
+        s_max_len = 0;
+        s_esc = 0;
+    }
+    uint32_t k;
+    uint32_t pos = block_scan_u32(lane == 0 ? mine : 0u, scan_tmp, &k);
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (k > kFastLeaves) {
+        if (tid == 0) info->slow = 1;  // k_codebook_slow takes over (bins left intact)
+        return;
+    }
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll 4
+    for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t m = touched[w];
+        if ((m >> lane) & 1u) {
+            const uint32_t p = pos + __popc(m & lt);
+            const uint32_t sy = w * 32 + lane;
+            const unsigned long long f = hist[sy];
+            leaf_sym[p] = sy;
+            key[p] = (f << 16) | p;
+            if (sy == 0) s_esc = f;
+        }
+        pos += __popc(m);
+    }
+    __syncthreads();
+    // self-cleaning: zero the consumed bins and the bitmap (no longer read)
+    for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t m = touched[w];
+        if ((m >> lane) & 1u) hist[w * 32 + lane] = 0;
+    }
+    __syncwarp();
+    for (uint32_t w = w0 + lane; w < w1; w += 32) touched[w] = 0;
+    uint32_t p2 = 2;
+    while (p2 < k) p2 <<= 1;
+    for (uint32_t i = k + tid; i < p2; i += kCbThreads) key[i] = ~0ull;
+    __syncthreads();
+    phase(0);
+    if (k == 0) {
+        if (tid == 0) {
+            info->book_size = 0;
+            info->total_bits = 0;
+            info->n_escapes = 0;
+            info->max_len = 0;
+            info->flags = 0;
+            info->slow = 0;
+        }
+        return;
+    }
+
+    // (2) bitonic sort of the keys -------------------------------------------------------
+    for (uint32_t size = 2; size <= p2; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < p2 / 2; i += kCbThreads) {
+                const uint32_t lo = 2 * i - (i & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool asc = (lo & size) == 0;
+                const unsigned long long a = key[lo], b = key[hi];
+                if ((a > b) == asc) {
+                    key[lo] = b;
+                    key[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    phase(1);
+    // (3) tree by parallel rounds -------------------------------------------------------
+    // node ids: leaf (symbol-order index) j -> j, internal t -> k + t; par[] = parent id.
+    const uint32_t root = k == 1 ? 0 : 2 * k - 2;
+    if (tid == 0) {
+        sh_li = 0;
+        sh_ii = 0;
+        sh_m = 0;
+        sh_done = 0;
+        if (k == 1) par[0] = 0;
+    }
+    __syncthreads();
+    while (k > 1) {
+        if (tid == 0) {
+            uint32_t li = sh_li, ii = sh_ii, m = sh_m;
+            if ((k - li) + (m - ii) <= 1) {
+                sh_done = 1;
+            } else {
+                unsigned long long f2[2];
+                uint32_t id2[2];
+                for (int t = 0; t < 2; ++t) {
+                    const unsigned long long fl = li < k ? (key[li] >> 16) : ~0ull;
+                    if (li < k && (ii >= m || fl <= ifreq[ii])) {  // leaf wins ties
+                        f2[t] = fl;
+                        id2[t] = (uint32_t)(key[li] & 0xFFFF);
+                        ++li;
+                    } else {
+                        f2[t] = ifreq[ii];
+                        id2[t] = k + ii;
+                        ++ii;
+                    }
+                }
+                const unsigned long long fx = f2[0] + f2[1];
+                atomicAdd(&g_cbstats[6], 1ull);
+                ifreq[m] = fx;
+                par[id2[0]] = (uint16_t)(k + m);
+                par[id2[1]] = (uint16_t)(k + m);
+                // leaves with freq <= fx (their keys precede X's)
+                uint32_t lo = li, hi = k;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if ((key[mid] >> 16) <= fx) lo = mid + 1; else hi = mid;
+                }
+                sh_nl = lo - li;
+                sh_ni = m - ii;  // queued internals (all precede X)
+                sh_xm = m;
+                sh_li = li;
+                sh_ii = ii;
+                sh_m = m + 1;
+            }
+        }
+        __syncthreads();
+        if (sh_done) break;
+        const uint32_t li = sh_li, ii = sh_ii, nl = sh_nl, ni = sh_ni, xm = sh_xm;
+        const uint32_t ns = nl + ni, np = ns >> 1, m1 = xm + 1;
+        const bool odd = ns & 1;
+        for (uint32_t q = tid; q < np + (odd ? 1u : 0u); q += kCbThreads) ifreq[m1 + q] = 0;
+        __syncthreads();
+        // S = merge(leaves[li, li+nl), internals[ii, ii+ni)) by key; S[2q], S[2q+1] -> Y_q;
+        // an odd last element pairs with X.
+        for (uint32_t t = tid; t < ns; t += kCbThreads) {
+            unsigned long long f;
+            uint32_t node, p;
+            if (t < nl) {
+                f = key[li + t] >> 16;
+                node = (uint32_t)(key[li + t] & 0xFFFF);
+                uint32_t lo = 0, hi = ni;  // internals with freq < f precede the leaf
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (ifreq[ii + mid] < f) lo = mid + 1; else hi = mid;
+                }
+                p = t + lo;
+            } else {
+                const uint32_t i = t - nl;
+                f = ifreq[ii + i];
+                node = k + ii + i;
+                uint32_t lo = 0, hi = nl;  // leaves with freq <= f precede the internal
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if ((key[li + mid] >> 16) <= f) lo = mid + 1; else hi = mid;
+                }
+                p = i + lo;
+            }
+            const uint32_t q = p >> 1;  // p == ns - 1 with odd ns -> q == np (pairs with X)
+            par[node] = (uint16_t)(k + m1 + q);
+            atomicAdd(&ifreq[m1 + q], f);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t m = m1 + np;
+            uint32_t iin = xm;  // X becomes the queue front
+            if (odd) {
+                atomicAdd(&ifreq[m], ifreq[xm]);
+                par[k + xm] = (uint16_t)(k + m);
+                ++m;
+                iin = xm + 1;
+            }
+            sh_li = li + nl;
+            sh_ii = iin;
+            sh_m = m;
+        }
+        __syncthreads();
+    }
+    if (tid == 0 && k > 1) par[root] = (uint16_t)root;
+    __syncthreads();
+    phase(2);
+
+    // (4) depths by pointer jumping (register-staged, in place) --------------------------
+    const uint32_t nodes = k == 1 ? 1 : 2 * k - 1;
+    constexpr int kNpt = 2 * kFastLeaves / kCbThreads;  // nodes per thread
+    for (uint32_t i = tid; i < nodes; i += kCbThreads) dep[i] = (k == 1) ? 1 : (i == root ? 0 : 1);
+    __syncthreads();
+    if (k > 1) {
+        for (int it = 0; it < 16; ++it) {
+            uint16_t na[kNpt];
+            uint8_t nd[kNpt];
+            int changed = 0;
+#pragma unroll
+            for (int j = 0; j < kNpt; ++j) {
+                const uint32_t i = tid + j * kCbThreads;
+                if (i < nodes) {
+                    const uint32_t a = par[i];
+                    if (a != root) {
+                        nd[j] = (uint8_t)min(255u, (uint32_t)dep[i] + dep[a]);
+                        na[j] = par[a];
+                        changed = 1;
+                    } else {
+                        nd[j] = dep[i];
+                        na[j] = (uint16_t)a;
+                    }
+                }
+            }
+            const int any = __syncthreads_or(changed);
+#pragma unroll
+            for (int j = 0; j < kNpt; ++j) {
+                const uint32_t i = tid + j * kCbThreads;
+                if (i < nodes) {
+                    dep[i] = nd[j];
+                    par[i] = na[j];
+                }
+            }
+            __syncthreads();
+            if (!any) break;
+        }
+    }
+
+    phase(3);
+    // (5) canonical order: stable counting sort by length over ascending symbols ---------
+    if (tid < 65) {
+        s_count[tid] = 0;
+        s_base[tid] = 0;
+    }
+    __syncthreads();
+    unsigned long long bits_part = 0;
+    uint32_t maxl = 0;
+    bool too_deep = false;
+    for (uint32_t p = tid; p < k; p += kCbThreads) {
+        const unsigned long long kk = key[p];
+        uint32_t l = dep[kk & 0xFFFF];
+        if (l > 64) {
+            too_deep = true;
+            l = 64;
+        }
+        atomicAdd(&s_count[l], 1u);
+        bits_part += (kk >> 16) * l;
+        maxl = max(maxl, l);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bits_part += __shfl_xor_sync(0xffffffffu, bits_part, o);
+    maxl = __reduce_max_sync(0xffffffffu, maxl);
+    if ((tid & 31) == 0) {
+        atomicAdd(&s_total_bits, bits_part);
+        atomicMax(&s_max_len, maxl);
+    }
+    if (too_deep) atomicOr(&s_flags, kFlagDepth64);
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long code = 0;
+        uint32_t prev = 0, idx = 0;
+        for (int l = 1; l <= 64; ++l) {
+            s_first_index[l] = idx;
+            if (s_count[l]) {
+                code <<= (l - prev);
+                s_first_code[l] = code;
+                code += s_count[l];
+                prev = l;
+                idx += s_count[l];
+            } else {
+                s_first_code[l] = 0;
+            }
+        }
+        s_first_code[0] = 0;
+        s_first_index[0] = 0;
+        if (s_max_len > 56) s_flags |= kFlagLenTooLong;
+    }
+    __syncthreads();
+    const unsigned lanemask_lt = (1u << lane) - 1;
+    for (uint32_t base = 0; base < k; base += kCbThreads) {
+        const uint32_t i = base + tid;
+        const bool valid = i < k;
+        const uint32_t l = valid ? min((uint32_t)dep[i], 64u) : 0xFFu;
+        const unsigned same = __match_any_sync(0xffffffffu, l);
+        const uint32_t rank_w = __popc(same & lanemask_lt);
+        for (int j = lane; j < 65; j += 32) s_wcnt[warp][j] = 0;
+        __syncwarp();
+        if (valid && rank_w == 0) s_wcnt[warp][l] = __popc(same);
+        __syncthreads();
+        if (tid < 65) {
+            uint32_t run = s_base[tid];
+            for (int w = 0; w < kCbWarps; ++w) {
+                const uint32_t c = s_wcnt[w][tid];
+                s_wcnt[w][tid] = run;
+                run += c;
+            }
+            s_base[tid] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t rank = s_wcnt[warp][l] + rank_w;
+            const uint32_t pos = s_first_index[l] + rank;
+            const uint32_t sym = leaf_sym[i];
+            book_sym[pos] = sym;
+            book_len[pos] = (uint8_t)l;
+            const unsigned long long code = s_first_code[l] + rank;
+            enc[sym] = (code << 8) | l;
+        }
+        __syncthreads();
+    }
+    phase(4);
+    // (6) decode tables ----------------------------------------------------------------
+    write_tables(s_count, s_first_code, s_first_index, book_sym, canon, lut);
+    __syncthreads();
+    phase(5);
+    if (tid == 0) {
+        atomicAdd(&g_cbstats[7], 1ull);
+        info->book_size = k;
+        info->total_bits = s_total_bits;
+        info->n_escapes = s_esc;
+        info->max_len = s_max_len;
+        info->flags = s_flags;
+        info->slow = 0;
+    }
+}
+
+// Slow K4 (books larger than kFastLeaves): global-memory scratch. Runs only when the fast
+// kernel flagged info->slow; also cleans the histogram bins and the touched bitmap.
+__global__ void __launch_bounds__(kCbThreads, 1) k_codebook_slow(
+    unsigned long long* __restrict__ hist, uint32_t* __restrict__ touched, uint32_t alphabet,
+    uint64_t max_leaves, void* scratch, uint32_t* __restrict__ book_sym,
+    uint8_t* __restrict__ book_len, unsigned long long* __restrict__ enc,
+    CanonTables* __restrict__ canon, uint32_t* __restrict__ lut, BookInfo* __restrict__ info) {
+    if (!info->slow) return;
     extern __shared__ unsigned long long dyn[];  // radix table / internal FIFO
     __shared__ uint32_t scan_tmp[kCbWarps + 1];
     __shared__ unsigned long long s_first_code[65];
@@ -155,6 +596,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook(
     for (uint64_t base = 0; base < alphabet; base += kCbThreads) {
         const uint64_t s = base + tid;
         const unsigned long long f = s < alphabet ? hist[s] : 0ull;
+        if (f) hist[s] = 0;  // self-cleaning histogram
         uint32_t tot;
         const uint32_t pos = block_scan_u32(f != 0, scan_tmp, &tot);
         if (f != 0 && k + pos < max_leaves) {
@@ -163,6 +605,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook(
         }
         k += tot;
     }
+    for (uint32_t w = tid; w < (alphabet + 31) / 32; w += kCbThreads) touched[w] = 0;
     if (tid == 0) {
         s_flags = 0;
         s_total_bits = 0;
@@ -176,6 +619,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook(
             info->n_escapes = alphabet ? hist[0] : 0;
             info->max_len = 0;
             info->flags = k > max_leaves ? kFlagBookTooBig : 0;
+            info->slow = 0;
         }
         return;
     }
@@ -473,32 +917,15 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook(
         __syncthreads();
     }
     // (6) decode tables ----------------------------------------------------------------
-    if (tid < 65) {
-        canon->first_code[tid] = s_first_code[tid];
-        canon->first_index[tid] = s_first_index[tid];
-        canon->count[tid] = s_count[tid];
-    }
     __syncthreads();
-    __threadfence_block();
-    for (uint32_t v = tid; v < kLutSize; v += kCbThreads) {
-        uint32_t e = 0;
-        for (int l = 1; l <= kLutBits; ++l) {
-            if (!s_count[l]) continue;
-            const unsigned long long c = v >> (kLutBits - l);
-            if (c >= s_first_code[l] && c - s_first_code[l] < s_count[l]) {
-                // symbol of canonical entry first_index + (c - first_code)
-                e = (book_sym[s_first_index[l] + (uint32_t)(c - s_first_code[l])] << 5) | l;
-                break;
-            }
-        }
-        lut[v] = e;
-    }
+    write_tables(s_count, s_first_code, s_first_index, book_sym, canon, lut);
     if (tid == 0) {
         info->book_size = k;
         info->total_bits = s_total_bits;
         info->n_escapes = S.leaf_sym[0] == 0 ? S.leaf_freq[0] : 0;
         info->max_len = s_max_len;
         info->flags = s_flags | (k > kMaxBook ? kFlagBookTooBig : 0);
+        info->slow = 0;
     }
 }
 
@@ -535,23 +962,7 @@ __global__ void __launch_bounds__(1024) k_build_tables(const uint32_t* __restric
         s_first_index[0] = 0;
     }
     __syncthreads();
-    if (tid < 65) {
-        canon->first_code[tid] = s_first_code[tid];
-        canon->first_index[tid] = s_first_index[tid];
-        canon->count[tid] = s_count[tid];
-    }
-    for (uint32_t v = tid; v < kLutSize; v += blockDim.x) {
-        uint32_t e = 0;
-        for (int l = 1; l <= kLutBits; ++l) {
-            if (!s_count[l]) continue;
-            const unsigned long long c = v >> (kLutBits - l);
-            if (c >= s_first_code[l] && c - s_first_code[l] < s_count[l]) {
-                e = (book_sym[s_first_index[l] + (uint32_t)(c - s_first_code[l])] << 5) | l;
-                break;
-            }
-        }
-        lut[v] = e;
-    }
+    write_tables(s_count, s_first_code, s_first_index, book_sym, canon, lut);
     (void)flags;
 }
 
@@ -577,7 +988,9 @@ __device__ __forceinline__ void smem_put_bits(uint32_t* w, uint64_t p, unsigned 
     }
 }
 
+template <typename SymT>
 __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
+    const SymT* __restrict__ symp = static_cast<const SymT*>(a.sym);
     extern __shared__ uint32_t stage[];
     __shared__ uint32_t s_tile;
     __shared__ unsigned long long s_prefix_bits, s_prefix_esc;
@@ -597,7 +1010,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     for (int i = 0; i < kEncPer; ++i) {
         const uint64_t g = my0 + i;
         if (g < a.n) {
-            const uint32_t sy = a.sym[g];
+            const uint32_t sy = symp[g];
             my_bits += (uint32_t)(__ldg(a.enc + sy) & 0xFF);
             if (sy == 0) {
                 ++my_esc;
@@ -721,11 +1134,11 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     for (int i = 0; i < kEncPer; ++i) {
         const uint64_t g = my0 + i;
         if (g >= a.n) break;
-        const unsigned long long e = __ldg(a.enc + a.sym[g]);
+        const unsigned long long e = __ldg(a.enc + (uint32_t)symp[g]);
         const uint32_t len = (uint32_t)(e & 0xFF);
         if (g == next_side) {
             a.side_bitoff[g / a.interval] = gbit;
-            a.side_outl[g / a.interval] = (uint32_t)gesc;
+            if (a.side_outl) a.side_outl[g / a.interval] = (uint32_t)gesc;
             next_side += a.interval;
         }
         smem_put_bits(stage, off, e >> 8, len);
@@ -755,20 +1168,33 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
 
 }  // namespace
 
-cudaError_t launch_histogram(const uint32_t* sym, uint64_t n, uint32_t alphabet,
-                             uint32_t center, unsigned long long* hist, int sms, cudaStream_t s,
-                             uint64_t* launches) {
-    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * alphabet, s);
-    if (e != cudaSuccess) return e;
-    uint32_t win_lo = center > kHistWindow / 2 ? center - kHistWindow / 2 : 0;
-    uint32_t win_n = alphabet - win_lo < (uint32_t)kHistWindow ? alphabet - win_lo : kHistWindow;
+cudaError_t launch_histogram(const void* sym, int sym16, uint64_t n, uint32_t alphabet,
+                             uint32_t center, unsigned long long* hist, uint32_t* touched,
+                             int sms, cudaStream_t s, uint64_t* launches) {
+    const uint32_t win_lo = center > kHistWindow / 2 ? ((center - kHistWindow / 2) & ~31u) : 0u;
+    const uint32_t win_n =
+        alphabet - win_lo < (uint32_t)kHistWindow ? alphabet - win_lo : (uint32_t)kHistWindow;
     uint64_t blocks = (n / 4 + 511) / 512;
     const uint64_t cap = (uint64_t)sms * 4;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) blocks = 1;
-    k_histogram<<<(unsigned)blocks, 512, 0, s>>>(sym, n, alphabet, win_lo, win_n, hist);
+    if (sym16)
+        k_histogram<uint16_t><<<(unsigned)blocks, 512, 0, s>>>(
+            static_cast<const uint16_t*>(sym), n, alphabet, win_lo, win_n, center, hist, touched);
+    else
+        k_histogram<uint32_t><<<(unsigned)blocks, 512, 0, s>>>(
+            static_cast<const uint32_t*>(sym), n, alphabet, win_lo, win_n, center, hist, touched);
     ++*launches;
     return cudaGetLastError();
+}
+
+cudaError_t codebook_stats(unsigned long long* out, bool reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_cbstats, sizeof(g_cbstats));
+    if (e == cudaSuccess && reset) {
+        unsigned long long z[8] = {0};
+        e = cudaMemcpyToSymbol(g_cbstats, z, sizeof(z));
+    }
+    return e;
 }
 
 size_t codebook_scratch_bytes(uint64_t k) {
@@ -776,21 +1202,33 @@ size_t codebook_scratch_bytes(uint64_t k) {
            4096;
 }
 
-cudaError_t launch_codebook(const unsigned long long* hist, uint32_t alphabet, uint64_t max_leaves,
-                            void* scratch, uint32_t* book_sym, uint8_t* book_len,
-                            unsigned long long* enc, CanonTables* canon, uint32_t* lut,
-                            BookInfo* info, cudaStream_t s, uint64_t* launches) {
-    const size_t smem = kSmemQueue * sizeof(unsigned long long);  // 128 KiB (>= radix table)
+cudaError_t launch_codebook(unsigned long long* hist, uint32_t* touched, uint32_t alphabet,
+                            uint64_t max_leaves, void* scratch, uint32_t* book_sym,
+                            uint8_t* book_len, unsigned long long* enc, CanonTables* canon,
+                            uint32_t* lut, BookInfo* info, cudaStream_t s, uint64_t* launches) {
+    const size_t smem_slow = kSmemQueue * sizeof(unsigned long long);  // 128 KiB (>= radix table)
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_codebook_slow,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem_slow);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_codebook_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kFastSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_codebook<<<1, kCbThreads, smem, s>>>(hist, alphabet, max_leaves, scratch, book_sym, book_len,
-                                           enc, canon, lut, info);
+    // the leaf symbols of the fast path live at the start of the slow path's scratch
+    k_codebook_fast<<<1, kCbThreads, kFastSmem, s>>>(hist, touched, alphabet,
+                                                     static_cast<uint32_t*>(scratch), book_sym,
+                                                     book_len, enc, canon, lut, info);
     ++*launches;
+    if (max_leaves > (uint64_t)kFastLeaves) {
+        k_codebook_slow<<<1, kCbThreads, smem_slow, s>>>(hist, touched, alphabet, max_leaves,
+                                                         scratch, book_sym, book_len, enc, canon,
+                                                         lut, info);
+        ++*launches;
+    }
     return cudaGetLastError();
 }
 
@@ -812,11 +1250,18 @@ cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t
     const size_t smem = ((size_t)kEncTile * (a.max_len ? a.max_len : 1) / 32 + 8) * 4;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
-        e = cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k_encode<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k_encode<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    k_encode<<<(unsigned)tiles, kEncThreads, smem, s>>>(a);
+    if (a.sym16)
+        k_encode<uint16_t><<<(unsigned)tiles, kEncThreads, smem, s>>>(a);
+    else
+        k_encode<uint32_t><<<(unsigned)tiles, kEncThreads, smem, s>>>(a);
     ++*launches;
     return cudaGetLastError();
 }

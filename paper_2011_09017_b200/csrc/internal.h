@@ -33,6 +33,9 @@ cudaError_t launch_stats(const float* x, uint64_t n, uint32_t* bitmap,
                          unsigned long long* d_nnz, unsigned int* d_flags, double* d_sumabs,
                          int sms, cudaStream_t s, uint64_t* launches);
 
+cudaError_t launch_widen_u16(const uint16_t* a, uint32_t* b, uint64_t n, int sms, cudaStream_t s,
+                             uint64_t* launches);
+
 // ---- quant.cu ----
 struct QuantArgs {
     const float* x;
@@ -40,7 +43,8 @@ struct QuantArgs {
     double eb, step;
     uint32_t radius;
     uint32_t predictor;
-    uint32_t* sym;            // n symbols out
+    uint32_t* sym;            // n symbols out (u32), or
+    uint16_t* sym16;          // n symbols out (u16; PrevValue with quant_radius <= 32768)
     float* side_state;        // chain state before every `interval`-th element (PrevValue)
     uint64_t interval;        // sidecar interval (power of two for PrevValue, plane size for Lorenzo2d)
     float* row_scratch;       // planes*cols floats (Lorenzo2d only)
@@ -55,18 +59,22 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
                               uint64_t* launches);
 
 // ---- huffman.cu ----
-cudaError_t launch_histogram(const uint32_t* sym, uint64_t n, uint32_t alphabet,
-                             uint32_t center, unsigned long long* hist, int sms, cudaStream_t s,
-                             uint64_t* launches);
+// hist (u64 x alphabet) and touched (1 bit per bin) must be zero on entry; the codebook
+// kernels leave them zero again (self-cleaning).
+cudaError_t launch_histogram(const void* sym, int sym16, uint64_t n, uint32_t alphabet,
+                             uint32_t center, unsigned long long* hist, uint32_t* touched,
+                             int sms, cudaStream_t s, uint64_t* launches);
 // Workspace needed by launch_codebook for an alphabet of `alphabet` symbols and at most
 // `max_leaves` distinct symbols.
 size_t codebook_scratch_bytes(uint64_t max_leaves);
-cudaError_t launch_codebook(const unsigned long long* hist, uint32_t alphabet, uint64_t max_leaves,
-                            void* scratch, uint32_t* book_sym, uint8_t* book_len,
-                            unsigned long long* enc, CanonTables* canon, uint32_t* lut,
-                            BookInfo* info, cudaStream_t s, uint64_t* launches);
+cudaError_t codebook_stats(unsigned long long* out, bool reset);
+cudaError_t launch_codebook(unsigned long long* hist, uint32_t* touched, uint32_t alphabet,
+                            uint64_t max_leaves, void* scratch, uint32_t* book_sym,
+                            uint8_t* book_len, unsigned long long* enc, CanonTables* canon,
+                            uint32_t* lut, BookInfo* info, cudaStream_t s, uint64_t* launches);
 struct EncodeArgs {
-    const uint32_t* sym;
+    const void* sym;                 // u16 (sym16) or u32 symbols
+    int sym16;
     uint64_t n;
     const unsigned long long* enc;   // dense symbol -> (code << 8 | len)
     const float* x;                  // for outlier values (nullptr: no outlier output)
@@ -111,6 +119,7 @@ struct DecodeArgs {
     float* row_scratch;              // Lorenzo2d
 };
 cudaError_t launch_decode(const DecodeArgs& a, int sms, cudaStream_t s, uint64_t* launches);
+cudaError_t decode_stats(unsigned long long* out, bool reset);
 
 // Sequential GPU decode of a whole stream (foreign blobs / generic Huffman decode):
 // records sidecar bit offsets + outlier prefixes every `interval` symbols, optional

@@ -13,39 +13,88 @@ namespace acz_b200 {
 
 namespace {
 
-// PrevValue (ref src/codec.cpp:41): pred = at == 0 ? 0 : recon[at-1].
-__global__ void __launch_bounds__(128) k_quant_prev_serial(const float* __restrict__ x,
-                                                           PlaneGeom g, double eb, double step,
-                                                           uint32_t radius,
-                                                           uint32_t* __restrict__ sym,
-                                                           float* __restrict__ side_state,
-                                                           uint64_t interval,
-                                                           unsigned int* flags) {
-    const uint64_t plane = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (plane >= g.planes) return;
+// PrevValue (ref src/codec.cpp:41): pred = at == 0 ? 0 : recon[at-1]. One thread per plane,
+// one warp per 32 consecutive planes. The planes are streamed through shared memory in
+// tiles of 32 elements per plane: a warp load covers 32 consecutive elements of ONE plane
+// (coalesced cp.async, double-buffered), each lane then walks its own plane's row of the
+// tile (conflict-free, padded stride), and the symbols leave through a transposed tile with
+// coalesced stores. The chain itself (about 90 cycles of dependent FP64 latency per element)
+// is the reference recurrence, exact.
+constexpr int kQW = 4;    // warps per CTA
+constexpr int kQT = 32;   // tile width (elements per plane)
+
+// x tiles, double-buffered; a lane overwrites the x slot it has just consumed with the
+// symbol (as a u32), so the same tile is then read back transposed for the stores.
+struct SerialSmem {
+    uint32_t xs[kQW][2][32][kQT + 1];
+};
+
+template <typename SymT>
+__global__ void __launch_bounds__(kQW * 32) k_quant_prev_serial(const float* __restrict__ x,
+                                                                PlaneGeom g, QParams qp,
+                                                                SymT* __restrict__ sym,
+                                                                float* __restrict__ side_state,
+                                                                uint64_t interval,
+                                                                unsigned int* flags) {
+    __shared__ SerialSmem S;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t plane0 = ((uint64_t)blockIdx.x * kQW + w) * 32;
+    if (plane0 >= g.planes) return;
+    const int np = (int)min((uint64_t)32, g.planes - plane0);
     const uint64_t P = g.plane_size;
-    const uint64_t base = plane * P;
-    const double radius_d = (double)radius;
-    const long long R = radius;
-    float r = 0.0f;
-    bool bad = false;
-    uint64_t to_side = base % interval;  // elements since the last sidecar point
-    to_side = to_side == 0 ? 0 : interval - to_side;
-    for (uint64_t i = 0; i < P; ++i) {
-        const uint64_t flat = base + i;
-        const float xf = __ldg(x + flat);
-        bad |= !isfinite(xf);
-        const double pred = i == 0 ? 0.0 : (double)r;
-        if (to_side == 0) {
-            side_state[flat / interval] = i == 0 ? 0.0f : r;
-            to_side = interval;
+    const uint64_t ntiles = (P + kQT - 1) / kQT;
+    const float* xw = x + plane0 * P;
+    SymT* sw = sym + plane0 * P;
+    auto issue = [&](uint64_t t) {
+        const uint64_t j0 = t * kQT;
+        const int cnt = (int)min((uint64_t)kQT, P - j0);
+        if (lane < cnt) {
+            const float* src = xw + j0 + lane;
+            uint32_t* dst = &S.xs[w][t & 1][0][lane];
+            for (int p = 0; p < np; ++p, src += P, dst += kQT + 1) cp_async4(dst, src);
         }
-        --to_side;
-        float v;
-        sym[flat] = quant_step(xf, pred, step, eb, radius_d, R, &v);
-        r = v;
+        cp_async_commit();
+    };
+    const bool active = lane < np;
+    const uint64_t base = (plane0 + lane) * P;  // my plane's flat offset
+    uint64_t next_side = ((base + interval - 1) / interval) * interval - base;  // plane-relative
+    double r = 0.0;
+    bool bad = false;
+    issue(0);
+    for (uint64_t t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) {
+            issue(t + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const uint64_t j0 = t * kQT;
+        const int cnt = (int)min((uint64_t)kQT, P - j0);
+        if (active) {
+            uint32_t* xr = S.xs[w][t & 1][lane];
+            // sidecar point inside this tile (interval >= 32: at most one)
+            const int js = next_side - j0 < (uint64_t)cnt ? (int)(next_side - j0) : -1;
+            if (js >= 0) next_side += interval;
+#pragma unroll 4
+            for (int j = 0; j < cnt; ++j) {
+                const float xf = __uint_as_float(xr[j]);
+                bad |= !isfinite(xf);
+                if (j == js) side_state[(base + j0 + j) / interval] = (float)r;
+                double v;
+                xr[j] = qstep((double)xf, xf, r, qp, &v);  // r == 0 at the plane start
+                r = v;
+            }
+        }
+        __syncwarp();
+        if (lane < cnt) {
+            SymT* dst = sw + j0 + lane;
+            const uint32_t* src = &S.xs[w][t & 1][0][lane];
+            for (int p = 0; p < np; ++p, dst += P, src += kQT + 1) *dst = (SymT)*src;
+        }
+        __syncwarp();
     }
-    if (bad) atomicOr(flags, kFlagNonFinite);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, kFlagNonFinite);
 }
 
 // Lorenzo2d (ref src/codec.cpp:42-47): pred = (left + top) - topleft in double, neighbours
@@ -89,12 +138,19 @@ __global__ void __launch_bounds__(128) k_quant_lorenzo_serial(const float* __res
 
 cudaError_t launch_quant(const QuantArgs& a, int sms, cudaStream_t s, uint64_t* launches) {
     (void)sms;
-    const unsigned threads = 128;
-    const uint64_t blocks = (a.g.planes + threads - 1) / threads;
     if (a.predictor == ACZ_PRED_PREV) {
-        k_quant_prev_serial<<<(unsigned)blocks, threads, 0, s>>>(
-            a.x, a.g, a.eb, a.step, a.radius, a.sym, a.side_state, a.interval, a.flags);
+        const uint64_t warps = (a.g.planes + 31) / 32;
+        const uint64_t blocks = (warps + kQW - 1) / kQW;
+        const QParams qp = make_qparams(a.eb, a.radius);
+        if (a.sym16)
+            k_quant_prev_serial<uint16_t><<<(unsigned)blocks, kQW * 32, 0, s>>>(
+                a.x, a.g, qp, a.sym16, a.side_state, a.interval, a.flags);
+        else
+            k_quant_prev_serial<uint32_t><<<(unsigned)blocks, kQW * 32, 0, s>>>(
+                a.x, a.g, qp, a.sym, a.side_state, a.interval, a.flags);
     } else {
+        const unsigned threads = 128;
+        const uint64_t blocks = (a.g.planes + threads - 1) / threads;
         k_quant_lorenzo_serial<<<(unsigned)blocks, threads, 0, s>>>(
             a.x, a.g, a.eb, a.step, a.radius, a.sym, a.row_scratch, a.flags);
     }

@@ -41,6 +41,9 @@ constexpr int kCapW = (kCap + 31) / 32;
 // Walk statistics (debug; read with acz_gpu_debug_counters): batches, state changes,
 // exact-mode steps, rebases, phase-A elements, walk visits.
 __device__ unsigned long long g_qstats[8];
+// per-phase SM cycles summed over segments (debug): geometry+phase A, look-back wait,
+// walk, exit+store
+__device__ unsigned long long g_qclk[4];
 
 struct SP {
     double eb, step, inv_step, radius_d, Tmax;
@@ -274,7 +277,7 @@ __device__ __forceinline__ uint64_t seg_bound_w(const float* xp, uint64_t j, con
 
 template <typename SymT>
 __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, SP p, const int* dB,
-                                                   uint32_t* __restrict__ sym_out,
+                                                   SymT* __restrict__ sym_out,
                                                    float* __restrict__ side_state,
                                                    unsigned int* __restrict__ status,
                                                    float* __restrict__ exits,
@@ -299,6 +302,14 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     const uint64_t sidx = plane * p.nseg + j;  // status/exit slot
     const float* xp = x + plane * p.P;
     const uint64_t plane_flat0 = plane * p.P;
+    long long tck = clock64();
+    auto tphase = [&](int slot) {
+        if (lane == 0) {
+            const long long t = clock64();
+            atomicAdd(&g_qclk[slot], (unsigned long long)(t - tck));
+            tck = t;
+        }
+    };
 
     // ---- segment geometry -------------------------------------------------------
     const uint64_t b0 = seg_bound_w(xp, j, p);         // first range start
@@ -382,6 +393,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     // ---- phase A: speculate all ranges (lattice origin 0: plane-start lattice) ----
     phase_a(S, xp, seg0, 0, 0.0, false, 0.0f, p, plane_flat0, flags);
 
+    tphase(0);
     // ---- entry state from the predecessor segment (decoupled look-back) ----------
     float tin = 0.0f;
     if (j > 0) {
@@ -400,6 +412,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         }
         tin = __shfl_sync(0xffffffffu, tin, 0);
     }
+    tphase(1);
     // offset of range 0
     double D = (j == 0) ? 0.0 : __dsub_rn((double)tin, (double)S.guess[0]);
     if (j > 0 && (fabs(D) > p.Tmax || gran(D) < p.B - 23)) {
@@ -598,6 +611,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             pos = __shfl_sync(0xffffffffu, vp, hl) + 1;
         }
     }
+    tphase(2);
     // ---- exit state ----------------------------------------------------------------
     float texit;
     if (exact_mode) {
@@ -620,8 +634,9 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         atomicExch(status + sidx, 1u);
     }
     // ---- symbols out (coalesced) ----------------------------------------------------
-    uint32_t* so = sym_out + plane_flat0 + seg0;
-    for (int i = lane; i < len; i += kW) so[i] = (uint32_t)S.sym[i];
+    SymT* so = sym_out + plane_flat0 + seg0;
+    for (int i = lane; i < len; i += kW) so[i] = S.sym[i];
+    tphase(3);
 }
 
 }  // namespace
@@ -652,8 +667,8 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     if (e != cudaSuccess) return e;
     k_anchor_binade<<<1, 256, 0, s>>>(a.x, a.g.n, dB);
     ++*launches;
-    if (a.radius <= 32768)
-        k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym, a.side_state,
+    if (a.sym16)
+        k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym16, a.side_state,
                                                               status, exits, ticket, a.flags, total);
     else
         k_quant_spec<uint32_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym, a.side_state,
@@ -664,9 +679,11 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
 
 cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
     cudaError_t e = cudaMemcpyFromSymbol(out, g_qstats, sizeof(g_qstats));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 8, g_qclk, sizeof(g_qclk));
     if (e == cudaSuccess && reset) {
         unsigned long long z[8] = {0};
         e = cudaMemcpyToSymbol(g_qstats, z, sizeof(z));
+        if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_qclk, z, sizeof(g_qclk));
     }
     return e;
 }

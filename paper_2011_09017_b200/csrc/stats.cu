@@ -72,7 +72,20 @@ __global__ void __launch_bounds__(256) k_stats(const float* __restrict__ x, uint
     }
 }
 
+__global__ void k_widen_u16(const uint16_t* __restrict__ a, uint32_t* __restrict__ b, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        b[i] = a[i];
+}
+
 }  // namespace
+
+cudaError_t launch_widen_u16(const uint16_t* a, uint32_t* b, uint64_t n, int sms, cudaStream_t s,
+                             uint64_t* launches) {
+    k_widen_u16<<<(unsigned)(sms * 8), 256, 0, s>>>(a, b, n);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_stats(const float* x, uint64_t n, uint32_t* bitmap,
                          unsigned long long* d_nnz, unsigned int* d_flags, double* d_sumabs,
