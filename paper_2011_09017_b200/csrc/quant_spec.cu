@@ -37,6 +37,8 @@ constexpr int kSeg = kW * kL;
 constexpr int kExt = 2 * kL;
 constexpr int kCap = kSeg + kExt;
 constexpr int kCapW = (kCap + 31) / 32;
+constexpr int kWin = kSeg + kExt + 1;  // staged x window: [j*kSeg - 1, (j+1)*kSeg + kExt)
+constexpr int kLev = 3;                // fine offset levels (binades below the anchor grid)
 
 // Walk statistics (debug; read with acz_gpu_debug_counters): batches, state changes,
 // exact-mode steps, rebases, phase-A elements, walk visits.
@@ -48,6 +50,7 @@ __device__ unsigned long long g_qclk[4];
 struct SP {
     double eb, step, inv_step, radius_d, Tmax;
     long long R;
+    int exact_div;
     float anchor_min;
     int B;  // anchor binade exponent
     uint64_t P, nseg, interval, planes;
@@ -68,7 +71,7 @@ __device__ __forceinline__ XS xstep(float xf, double pred, const SP& p) {
     r.t = __dmul_rn(d, p.inv_step);
     r.q = round(r.t);
     // round(RN64(d/step)) == round(t) unless t is within a few ulps of a half-integer
-    if (0.5 - fabs(r.t - r.q) <= fabs(r.t) * 0x1p-44 + 0x1p-60) {
+    if (p.exact_div || 0.5 - fabs(r.t - r.q) <= fabs(r.t) * 0x1p-44 + 0x1p-60) {
         r.t = __ddiv_rn(d, p.step);
         r.q = round(r.t);
     }
@@ -113,10 +116,16 @@ __device__ __forceinline__ float lattice_guess(double lam, float xa, const SP& p
 
 template <typename SymT>
 struct Smem {
+    float xs[kWin];       // staged input window (plane index j*kSeg - 1 + i)
     float s[kCap];
     SymT sym[kCap];
     uint32_t abits[kSeg / 32];  // anchor bitmap of the segment's nominal span
     uint32_t cand[kCapW];
+    // lvl[L-1]: outputs whose grid is coarser than an offset L binades below the anchor
+    // grid (exponent > B - L); visited only while the walk carries such a fine offset
+    uint32_t lvl[kLev][kCapW];
+    uint32_t rsb[kCapW];  // range-start bitmap (segment-relative)
+    uint8_t rsp[kCapW];   // number of range starts before each word
     int rstart[kW + 1];   // segment-relative range starts (sorted), rstart[nr] = len
     float guess[kW];      // speculative entry state of each range
     float send[kW];       // speculative exit (state after the last element)
@@ -125,78 +134,130 @@ struct Smem {
     int forced[kW];       // range start is not an anchor-aligned guess
 };
 
-// Speculative chain over range k (phase A) from its guess; writes s, sym, candidate bits.
+// Phase A, pass 1: the speculative chain over range k from its guess (one lane per range):
+// the reference step only (symbols + chain states), the tightest dependent chain.
 template <typename SymT>
-__device__ void spec_range(Smem<SymT>& S, const float* xp, uint64_t seg0, int k, const SP& p,
-                           uint64_t plane_flat0, unsigned* flags) {
+__device__ void spec_range(Smem<SymT>& S, int xoff, uint64_t seg0, int k, const SP& p,
+                           const QParams& qp, unsigned* flags) {
     const int b = S.rstart[k], e = S.rstart[k + 1];
-    float r = S.guess[k];
-    bool collapsed = false;
-    double ycol = 0.0;
+    double r = (double)S.guess[k];
     bool bad = false;
+#pragma unroll 4
     for (int i = b; i < e; ++i) {
-        const uint64_t pi = seg0 + (uint64_t)i;  // plane index
-        const float xf = __ldg(xp + pi);
+        const float xf = S.xs[xoff + i];
         bad |= !isfinite(xf);
-        const double pred = pi == 0 ? 0.0 : (double)r;
-        const XS o = xstep(xf, pred, p);
-        bool c = (i == b);
-        if (o.sym == 0) {
-            c = true;
-            collapsed = false;
-        } else {
-            const double dm = (0.5 - fabs(o.t - o.q)) * p.step;
-            const double am = p.eb - fabs((double)xf - (double)o.out);
-            if (fmin(dm, am) <= 2.0 * p.Tmax) c = true;
-            if (fabs(o.q) >= p.radius_d - 1.0) c = true;
-            if (o.q == 0.0 && collapsed) {
-                // identity inside a collapsed run
-            } else if (fabs((double)o.out) < p.eb) {
-                collapsed = true;
-                ycol = o.pre;
-                // the lazy collapse formula RN32(pre + D) needs pre == prev + q*step exactly
-                if (__dsub_rn(o.pre, pred) != __dmul_rn(o.q, p.step)) c = true;
-            } else {
-                const int ex = fexp((double)o.out);
-                if (ex > p.B) c = true;
-                const double a = fabs((double)o.out), lo = pow2(ex);
-                if (a - lo <= 2.0 * p.Tmax || 2.0 * lo - a <= 2.0 * p.Tmax) c = true;
-                // distance of the pre-value to the nearest rounding midpoint of its grid
-                const double half = pow2(fexp(o.pre) - 24);
-                const double fr = half - fabs(o.pre - (double)o.out);
-                if (fr == 0.0) c = true;  // exact RNE tie
-                if (collapsed) {
-                    // re-expansion certificate for any |D| <= Tmax
-                    const double dmax = pow2(fexp(2.0 * fmax(fabs(ycol), 2.0 * p.Tmax)) - 22);
-                    if (!(fr > dmax + fabs(o.pre) * 0x1p-50)) c = true;
-                }
-                collapsed = false;
-            }
-        }
-        if (((plane_flat0 + pi) & (p.interval - 1)) == 0) c = true;  // sidecar point
-        S.s[i] = o.out;
-        S.sym[i] = (SymT)o.sym;
-        if (c) atomicOr(&S.cand[i >> 5], 1u << (i & 31));
-        r = o.out;
+        const double pred = (seg0 + (uint64_t)i == 0) ? 0.0 : r;
+        double v;
+        S.sym[i] = (SymT)qstep((double)xf, xf, pred, qp, &v);
+        S.s[i] = (float)v;
+        r = v;
     }
-    S.send[k] = r;
+    S.send[k] = (float)r;
     atomicAdd(&g_qstats[4], (unsigned long long)(e - b));
     if (bad) atomicOr(flags, kFlagNonFinite);
 }
 
+// Phase A, pass 2 (warp-cooperative, load-balanced over elements, no loop-carried state):
+// candidate classification of positions [i0, len) from x, the speculative states and
+// symbols. An element is a candidate when translating its pre-state by any offset D with
+// |D| <= Tmax on the anchor grid might not translate its output: range starts, escapes,
+// fragile decision/acceptance margins (<= 2 Tmax), |q| near the radius, outputs above the
+// anchor binade or within 2 Tmax of a binade edge, exact RNE ties, collapse starts whose
+// pre-value is not exactly prev + q*step, re-expansions without a certificate, sidecar
+// points. lvl[L-1] marks outputs with exponent > B - L (fine offsets, see levelD).
+template <typename SymT>
+__device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len, const SP& p,
+                         uint64_t plane_flat0) {
+    const int lane = threadIdx.x;
+    const double M52 = 6755399441055744.0;
+    auto range_of = [&](int q) {
+        const int w = q >> 5;
+        return (int)S.rsp[w] + __popc(S.rsb[w] & (0xFFFFFFFFu >> (31 - (q & 31)))) - 1;
+    };
+    auto tiny_acc = [&](int c) { return S.sym[c] != 0 && fabs((double)S.s[c]) < p.eb; };
+    auto pred_of = [&](int c, int kc) -> double {
+        if (seg0 + (uint64_t)c == 0) return 0.0;
+        return (c == S.rstart[kc]) ? (double)S.guess[kc] : (double)S.s[c - 1];
+    };
+    for (int w = i0 >> 5; w * 32 < len; ++w) {
+        const int i = w * 32 + lane;
+        const bool valid = i >= i0 && i < len;
+        bool c = false;
+        int lvlex = -100000;
+        if (valid) {
+            const int k = range_of(i);
+            const int b = S.rstart[k];
+            const float xf = S.xs[xoff + i];
+            const float out = S.s[i];
+            const uint32_t sy = (uint32_t)S.sym[i];
+            const double pred = pred_of(i, k);
+            c = (i == b);
+            if (sy == 0) {
+                c = true;
+            } else {
+                const double orig = (double)xf;
+                const double d = __dsub_rn(orig, pred);
+                double t = __dmul_rn(d, p.inv_step);
+                double q = __dsub_rn(__dadd_rn(t, M52), M52);
+                if (p.exact_div || 0.5 - fabs(t - q) <= fabs(t) * 0x1p-44 + 0x1p-60) {
+                    t = __ddiv_rn(d, p.step);
+                    q = round(t);
+                }
+                const double pre = __dadd_rn(pred, __dmul_rn(q, p.step));
+                const double dm = (0.5 - fabs(t - q)) * p.step;
+                const double am = p.eb - fabs(orig - (double)out);
+                if (fmin(dm, am) <= 2.0 * p.Tmax) c = true;
+                if (fabs(q) >= p.radius_d - 1.0) c = true;
+                const bool coll_before = i > b && tiny_acc(i - 1);
+                if (q == 0.0 && coll_before) {
+                    // identity inside a collapsed run
+                } else if (fabs((double)out) < p.eb) {
+                    if (out != 0.0f) lvlex = fexp((double)out);
+                    // the lazy collapse formula RN32(pre + D) needs pre == prev + q*step exactly
+                    if (__dsub_rn(pre, pred) != __dmul_rn(q, p.step)) c = true;
+                } else {
+                    const int ex = fexp((double)out);
+                    lvlex = ex;
+                    if (ex > p.B) c = true;
+                    const double a = fabs((double)out), lo = pow2(ex);
+                    if (a - lo <= 2.0 * p.Tmax || 2.0 * lo - a <= 2.0 * p.Tmax) c = true;
+                    // distance of the pre-value to the nearest rounding midpoint of its grid
+                    const double half = pow2(fexp(pre) - 24);
+                    const double fr = half - fabs(pre - (double)out);
+                    if (fr == 0.0) c = true;  // exact RNE tie
+                    if (coll_before) {
+                        // re-expansion certificate for any |D| <= Tmax; ycol = pre-value of
+                        // the run's last non-identity element
+                        int cc = i - 1;
+                        while (cc > b && S.sym[cc] == (SymT)p.R && tiny_acc(cc - 1)) --cc;
+                        const double ycol = __dadd_rn(pred_of(cc, k),
+                                                      __dmul_rn((double)((long long)S.sym[cc] - p.R), p.step));
+                        const double dmax = pow2(fexp(2.0 * fmax(fabs(ycol), 2.0 * p.Tmax)) - 22);
+                        if (!(fr > dmax + fabs(pre) * 0x1p-50)) c = true;
+                    }
+                }
+            }
+            if (((plane_flat0 + seg0 + (uint64_t)i) & (p.interval - 1)) == 0) c = true;  // sidecar
+        }
+        const unsigned cb = __ballot_sync(0xffffffffu, c);
+        unsigned lb[kLev];
+#pragma unroll
+        for (int L = 1; L <= kLev; ++L) lb[L - 1] = __ballot_sync(0xffffffffu, lvlex > p.B - L);
+        if (lane == 0) {
+            const uint32_t keep = (w == (i0 >> 5) && (i0 & 31)) ? ((1u << (i0 & 31)) - 1u) : 0u;
+            S.cand[w] = (S.cand[w] & keep) | cb;
+#pragma unroll
+            for (int L = 0; L < kLev; ++L) S.lvl[L][w] = (S.lvl[L][w] & keep) | lb[L];
+        }
+    }
+}
+
 // Phase A for ranges k0.. with lattice origin lam (all lanes participate).
 template <typename SymT>
-__device__ void phase_a(Smem<SymT>& S, const float* xp, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
-                        float k0_entry, const SP& p, uint64_t plane_flat0, unsigned* flags) {
+__device__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
+                        float k0_entry, const SP& p, const QParams& qp, uint64_t plane_flat0,
+                        unsigned* flags, int len) {
     const int lane = threadIdx.x;
-    // clear candidate bits of the affected span
-    const int b0 = S.rstart[k0];
-    for (int w = (b0 >> 5) + lane; w < kCapW; w += kW) {
-        uint32_t keep = 0;
-        if (w == (b0 >> 5)) keep = (b0 & 31) ? ((1u << (b0 & 31)) - 1) : 0u;
-        S.cand[w] &= keep;
-    }
-    __syncwarp();
     for (int k = k0 + lane; k < S.nr; k += kW) {
         const int st = S.rstart[k];
         if (k == k0 && lam_exact_k0) {
@@ -204,10 +265,12 @@ __device__ void phase_a(Smem<SymT>& S, const float* xp, uint64_t seg0, int k0, d
         } else if (seg0 + (uint64_t)st == 0) {
             S.guess[k] = 0.0f;
         } else {
-            S.guess[k] = lattice_guess(lam, __ldg(xp + seg0 + st - 1), p);
+            S.guess[k] = lattice_guess(lam, S.xs[xoff + st - 1], p);
         }
-        spec_range(S, xp, seg0, k, p, plane_flat0, flags);
+        spec_range(S, xoff, seg0, k, p, qp, flags);
     }
+    __syncwarp();
+    classify(S, xoff, seg0, S.rstart[k0], len, p, plane_flat0);
     __syncwarp();
     // prefix C[k] = sum_{j<=k, j>0} (send[j-1] - guess[j])
     if (lane == 0) {
@@ -221,20 +284,26 @@ __device__ void phase_a(Smem<SymT>& S, const float* xp, uint64_t seg0, int k0, d
 }
 
 // Top frequent binade of a tensor from a strided sample: the largest e with
-// #(|x| >= 2^e) >= max(1, nonzero/32). Writes B to *out (one CTA).
-__global__ void __launch_bounds__(256) k_anchor_binade(const float* __restrict__ x, uint64_t n,
-                                                      int* out) {
+// #(|x| >= 2^e) >= max(1, nonzero/32). Writes B to *out (one CTA; every thread issues its
+// 16 sample loads before using any, so the kernel costs ~one memory round trip).
+__global__ void __launch_bounds__(1024) k_anchor_binade(const float* __restrict__ x, uint64_t n,
+                                                       int* out) {
     __shared__ unsigned cnt[300];
     for (int i = threadIdx.x; i < 300; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    const uint64_t samples = n < 65536 ? n : 65536;
+    constexpr int kPer = 16;
+    const uint64_t samples = n < 1024ull * kPer ? n : 1024ull * kPer;
     const uint64_t stride = n / samples;
-    for (uint64_t s = threadIdx.x; s < samples; s += blockDim.x) {
-        const float v = fabsf(__ldg(x + s * stride));
-        if (v > 0.0f && isfinite(v)) {
-            int e = ((__float_as_int(v) >> 23) & 0xFF) - 127;
-            atomicAdd(&cnt[e + 150], 1u);
-        }
+    float v[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const uint64_t s = threadIdx.x + (uint64_t)k * 1024;
+        v[k] = s < samples ? __ldg(x + s * stride) : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const float a = fabsf(v[k]);
+        if (a > 0.0f && isfinite(a)) atomicAdd(&cnt[((__float_as_int(a) >> 23) & 0xFF) - 127 + 150], 1u);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -254,11 +323,13 @@ __global__ void __launch_bounds__(256) k_anchor_binade(const float* __restrict__
     }
 }
 
-// Warp-cooperative: first anchor in [b, e) (plane coordinates), or e if none.
-__device__ __forceinline__ uint64_t first_anchor(const float* xp, uint64_t b, uint64_t e, float amin) {
+// Warp-cooperative: first anchor in [b, e) (plane coordinates), or e if none. xs holds the
+// staged window starting at plane index xbase.
+__device__ __forceinline__ uint64_t first_anchor(const float* xs, int64_t xbase, uint64_t b,
+                                                 uint64_t e, float amin) {
     for (uint64_t base = b; base < e; base += 32) {
         const uint64_t i = base + threadIdx.x;
-        const bool a = i < e && is_anchor(__ldg(xp + i), amin);
+        const bool a = i < e && is_anchor(xs[(int64_t)i - xbase], amin);
         const unsigned m = __ballot_sync(0xffffffffu, a);
         if (m) return base + __ffs(m) - 1;
     }
@@ -266,12 +337,13 @@ __device__ __forceinline__ uint64_t first_anchor(const float* xp, uint64_t b, ui
 }
 
 // First range start of segment j (warp-cooperative version of seg_bound).
-__device__ __forceinline__ uint64_t seg_bound_w(const float* xp, uint64_t j, const SP& p) {
+__device__ __forceinline__ uint64_t seg_bound_w(const float* xs, int64_t xbase, uint64_t j,
+                                                const SP& p) {
     if (j == 0) return 0;
     const uint64_t b = j * kSeg;
     if (b >= p.P) return p.P;
     const uint64_t e = min(p.P, b + kExt);
-    const uint64_t a = first_anchor(xp, b, e, p.anchor_min);
+    const uint64_t a = first_anchor(xs, xbase, b, e, p.anchor_min);
     return a < e ? a + 1 : e;
 }
 
@@ -292,6 +364,13 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         p.anchor_min = ldexpf(1.0f, B) * (1.0f + 1.0f / 64.0f);
         p.Tmax = fmin(ldexp(1.0, B - 23) * 32.0, p.eb / 8.0);
     }
+    QParams qp;
+    qp.eb = p.eb;
+    qp.step = p.step;
+    qp.inv_step = p.inv_step;
+    qp.radius_d = p.radius_d;
+    qp.R = p.R;
+    qp.exact_div = p.exact_div;
     if (lane == 0) s_tk = atomicAdd(ticket, 1u);
     __syncwarp();
     const unsigned long long seg_id = s_tk;
@@ -311,9 +390,21 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         }
     };
 
+    // ---- stage the input window [j*kSeg - 1, (j+1)*kSeg + kExt) into shared memory ----
+    const int64_t xbase = (int64_t)(j * kSeg) - 1;
+    for (int i = lane; i < kWin; i += kW) {
+        const int64_t pi = xbase + i;
+        if (pi >= 0 && pi < (int64_t)p.P) cp_async4(&S.xs[i], xp + pi);
+        else S.xs[i] = 0.0f;
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+
     // ---- segment geometry -------------------------------------------------------
-    const uint64_t b0 = seg_bound_w(xp, j, p);         // first range start
-    const uint64_t b1 = seg_bound_w(xp, j + 1, p);     // next segment's first start
+    const uint64_t b0 = seg_bound_w(S.xs, xbase, j, p);      // first range start
+    const uint64_t b1 = seg_bound_w(S.xs, xbase, j + 1, p);  // next segment's first start
+    const int xoff = (int)((int64_t)b0 - xbase);            // xs index of segment position 0
     const uint64_t seg0 = b0;
     const int len = (int)(b1 - b0);
     if (len <= 0) {
@@ -345,7 +436,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         const uint64_t nb = j * kSeg;
         for (int w = 0; w < kSeg / 32; ++w) {
             const uint64_t i = nb + (uint64_t)w * 32 + lane;
-            const bool a = i < p.P && is_anchor(__ldg(xp + i), p.anchor_min);
+            const bool a = i < p.P && is_anchor(S.xs[(int64_t)i - xbase], p.anchor_min);
             const unsigned m = __ballot_sync(0xffffffffu, a);
             if (lane == 0) S.abits[w] = m;
         }
@@ -382,16 +473,32 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         // the segment's first range starts at a forced (non-anchor) boundary?
         bool forced = false;
         if (j > 0) {
-            const float xa = __ldg(xp + b0 - 1);
+            const float xa = S.xs[xoff - 1];
             forced = !is_anchor(xa, p.anchor_min);
         }
         S.forced[0] = forced ? 1 : 0;
     }
-    for (int w = lane; w < kCapW; w += kW) S.cand[w] = 0;
+    for (int w = lane; w < kCapW; w += kW) {
+        S.cand[w] = 0;
+        S.rsb[w] = 0;
+#pragma unroll
+        for (int L = 0; L < kLev; ++L) S.lvl[L][w] = 0;
+    }
+    __syncwarp();
+    // range-start bitmap + per-word prefix: range_of() in O(1)
+    if (my_start >= 0) atomicOr(&S.rsb[my_start >> 5], 1u << (my_start & 31));
+    __syncwarp();
+    if (lane == 0) {
+        int run = 0;
+        for (int w = 0; w < kCapW; ++w) {
+            S.rsp[w] = (uint8_t)run;
+            run += __popc(S.rsb[w]);
+        }
+    }
     __syncwarp();
 
     // ---- phase A: speculate all ranges (lattice origin 0: plane-start lattice) ----
-    phase_a(S, xp, seg0, 0, 0.0, false, 0.0f, p, plane_flat0, flags);
+    phase_a(S, xoff, seg0, 0, 0.0, false, 0.0f, p, qp, plane_flat0, flags, len);
 
     tphase(0);
     // ---- entry state from the predecessor segment (decoupled look-back) ----------
@@ -413,12 +520,24 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         tin = __shfl_sync(0xffffffffu, tin, 0);
     }
     tphase(1);
+    // Offset levels: an offset D (true - speculative) whose granularity is L binades finer
+    // than the anchor grid (L <= kLev) keeps the translation exact everywhere except at the
+    // static candidates and at outputs with exponent > B - L (bitmap lvl[L-1]); coarser or
+    // larger offsets are not representable (-1): exact stepping or re-speculation.
+    auto levelD = [&](double d) -> int {
+        if (d == 0.0) return 0;
+        if (!(fabs(d) <= p.Tmax)) return -1;
+        const int L = (p.B - 23) - gran(d);
+        return L <= 0 ? 0 : (L <= kLev ? L : -1);
+    };
     // offset of range 0
     double D = (j == 0) ? 0.0 : __dsub_rn((double)tin, (double)S.guess[0]);
-    if (j > 0 && (fabs(D) > p.Tmax || gran(D) < p.B - 23)) {
+    int lev = levelD(D);
+    if (j > 0 && lev < 0) {
         // lattice differs (escape upstream) or guess too far: re-speculate from tin
-        phase_a(S, xp, seg0, 0, (double)tin, true, tin, p, plane_flat0, flags);
+        phase_a(S, xoff, seg0, 0, (double)tin, true, tin, p, qp, plane_flat0, flags, len);
         D = 0.0;
+        lev = 0;
     }
     int rcur = 0;          // range the offset D refers to
     bool exact_mode = false;  // EXACT: the true state T is tracked explicitly
@@ -426,13 +545,9 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     int pos = 0;           // next position to consider
     __shared__ int s_vis[kW];
 
-    auto range_of = [&](int q) {
-        int k = 0;
-        while (k + 1 < S.nr && S.rstart[k + 1] <= q) ++k;
-        return k;
-    };
-    auto okD = [&](double d) {
-        return d == 0.0 || (fabs(d) <= p.Tmax && gran(d) >= p.B - 23);
+    auto range_of = [&](int q) {  // number of range starts <= q, minus one
+        const int w = q >> 5;
+        return (int)S.rsp[w] + __popc(S.rsb[w] & (0xFFFFFFFFu >> (31 - (q & 31)))) - 1;
     };
     // spec pre-value of element c of range kc: RN64(prev + q*step)
     auto spec_pre = [&](int c, int kc) -> double {
@@ -449,11 +564,14 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             if (pos == S.rstart[k] && pos > 0) {
                 // exact entry T at a range start: resume translation (rebase if needed)
                 const double Dk = __dsub_rn((double)T, (double)S.guess[k]);
-                if (!okD(Dk)) {
-                    phase_a(S, xp, seg0, k, (double)T, true, T, p, plane_flat0, flags);
+                const int lk = levelD(Dk);
+                if (lk < 0) {
+                    phase_a(S, xoff, seg0, k, (double)T, true, T, p, qp, plane_flat0, flags, len);
                     D = 0.0;
+                    lev = 0;
                 } else {
                     D = Dk;
+                    lev = lk;
                 }
                 rcur = k;
                 exact_mode = false;
@@ -461,7 +579,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             }
             const uint64_t pi = seg0 + (uint64_t)pos;
             const float tprev = T;
-            const XS ex = xstep(__ldg(xp + pi), pi == 0 ? 0.0 : (double)tprev, p);
+            const XS ex = xstep(S.xs[xoff + pos], pi == 0 ? 0.0 : (double)tprev, p);
             if (lane == 0) {
                 S.sym[pos] = (SymT)ex.sym;
                 const uint64_t flat = plane_flat0 + pi;
@@ -472,8 +590,10 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             const float ss = S.s[pos];
             if (fabs((double)T) >= p.eb && fabs((double)ss) >= p.eb) {
                 const double Dn = __dsub_rn((double)T, (double)ss);
-                if (okD(Dn)) {
+                const int ln = levelD(Dn);
+                if (ln >= 0) {
                     D = Dn;
+                    lev = ln;
                     rcur = k;
                     exact_mode = false;
                 }
@@ -484,7 +604,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
         // ---- TRANSLATE: gather the next 32 candidate positions -----------------------
         {
             const int w = (pos >> 5) + lane;
-            uint32_t bits = (w < kCapW) ? S.cand[w] : 0u;
+            uint32_t bits = (w < kCapW) ? (S.cand[w] | (lev ? S.lvl[lev - 1][w] : 0u)) : 0u;
             if (lane == 0) bits &= ~((1u << (pos & 31)) - 1u);
             const int c = __popc(bits);
             int incl = c;
@@ -523,7 +643,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             kv = range_of(vp);
             Dp = __dadd_rn(D, __dsub_rn(S.C[kv], S.C[rcur]));
             const uint64_t pi = seg0 + (uint64_t)vp;
-            if (vp == S.rstart[kv] && kv > 0 && !okD(Dp)) {
+            if (vp == S.rstart[kv] && kv > 0 && levelD(Dp) < 0) {
                 ok = false;
                 rebase = true;
                 tprev = __double2float_rn(__dadd_rn((double)S.guess[kv], Dp));
@@ -540,7 +660,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
                 } else {
                     tprev = __double2float_rn(__dadd_rn((double)S.s[vp - 1], Dp));
                 }
-                ex = xstep(__ldg(xp + pi), pi == 0 ? 0.0 : (double)tprev, p);
+                ex = xstep(S.xs[xoff + vp], pi == 0 ? 0.0 : (double)tprev, p);
                 const uint32_t ssym = (uint32_t)S.sym[vp];
                 const float ss = S.s[vp];
                 if (ex.sym != ssym) {
@@ -580,8 +700,9 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
                 if (lane == 0) atomicAdd(&g_qstats[3], 1ull);
                 // lattice changed at range start fk: re-speculate ranges >= fk from the
                 // exact entry state and re-evaluate from fvp
-                phase_a(S, xp, seg0, fk, (double)ftp, true, ftp, p, plane_flat0, flags);
+                phase_a(S, xoff, seg0, fk, (double)ftp, true, ftp, p, qp, plane_flat0, flags, len);
                 D = 0.0;
+                lev = 0;
                 rcur = fk;
                 pos = fvp;
                 continue;
@@ -597,8 +718,10 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             const float fss = S.s[fvp];
             rcur = fk;
             const double Dn = __dsub_rn((double)fout, (double)fss);
-            if (fabs((double)fout) >= p.eb && fabs((double)fss) >= p.eb && okD(Dn)) {
+            const int ln = levelD(Dn);
+            if (fabs((double)fout) >= p.eb && fabs((double)fss) >= p.eb && ln >= 0) {
                 D = Dn;
+                lev = ln;
             } else {
                 exact_mode = true;
                 T = fout;
@@ -657,6 +780,7 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     p.interval = a.interval;
     p.planes = a.g.planes;
     p.inv_step = 1.0 / a.step;
+    p.exact_div = make_qparams(a.eb, a.radius).exact_div;
     const unsigned long long total = (unsigned long long)a.g.planes * p.nseg;
     char* sc = static_cast<char*>(scratch);
     int* dB = reinterpret_cast<int*>(sc);
@@ -665,7 +789,7 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     float* exits = reinterpret_cast<float*>(sc + 256 + ((4 * total + 255) & ~255ull));
     cudaError_t e = cudaMemsetAsync(sc, 0, 256 + ((4 * total + 255) & ~255ull), s);
     if (e != cudaSuccess) return e;
-    k_anchor_binade<<<1, 256, 0, s>>>(a.x, a.g.n, dB);
+    k_anchor_binade<<<1, 1024, 0, s>>>(a.x, a.g.n, dB);
     ++*launches;
     if (a.sym16)
         k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym16, a.side_state,
