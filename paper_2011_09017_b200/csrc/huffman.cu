@@ -17,6 +17,8 @@
 //                     bit concatenation in shared memory, coalesced word stores (boundary
 //                     words by atomicOr). Also writes the outlier list and the decode
 //                     sidecar (bit offset / outlier prefix every `interval` symbols).
+#include <type_traits>
+
 #include "internal.h"
 
 namespace acz_b200 {
@@ -219,7 +221,8 @@ constexpr int kFastLeaves = 8192;
 // compaction, sort, rounds, depths, canonical, tables (SM cycles), round count, calls
 __device__ unsigned long long g_cbstats[8];
 constexpr size_t kFastSmem = kFastLeaves * 8 /*keys*/ + kFastLeaves * 8 /*ifreq*/ +
-                             2 * kFastLeaves * 2 /*parent*/ + 2 * kFastLeaves /*depth*/;
+                             2 * kFastLeaves * 2 /*parent*/ + 2 * kFastLeaves /*depth*/ +
+                             kFastLeaves * 4 /*leaf symbols*/;
 
 __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
     unsigned long long* __restrict__ hist, uint32_t* __restrict__ touched, uint32_t alphabet,
@@ -248,15 +251,27 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
         }
     };
 
+    uint32_t* lsym = reinterpret_cast<uint32_t*>(dep + 2 * kFastLeaves);  // [kFastLeaves]
     // (1) compaction -------------------------------------------------------------------
-    // warp wp owns bitmap words [wp*per, (wp+1)*per); lane b of a word loads bin b
-    // (coalesced, independent loads); positions = block prefix of set bits.
+    // The touched bitmap is staged into shared memory and every touched bin is fetched
+    // with an asynchronous 8-byte copy straight into its compacted slot: the whole gather
+    // costs about two memory round trips. Warp wp owns bitmap words [wp*per, (wp+1)*per);
+    // positions = block prefix of set bits (ascending symbol order).
     const int lane = tid & 31, warp = tid >> 5;
     const uint32_t nwords = (alphabet + 31) / 32;
+    const bool staged = nwords <= 2 * kFastLeaves;  // fits the ifreq region (64 KiB)
+    uint32_t* s_bm = reinterpret_cast<uint32_t*>(ifreq);
+    if (staged) {
+        for (uint32_t w = tid; w < nwords; w += kCbThreads) cp_async4(s_bm + w, touched + w);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+    const uint32_t* bm = staged ? s_bm : touched;
     const uint32_t per = (nwords + kCbWarps - 1) / kCbWarps;
     const uint32_t w0 = min(nwords, warp * per), w1 = min(nwords, w0 + per);
     uint32_t mine = 0;
-    for (uint32_t w = w0 + lane; w < w1; w += 32) mine += __popc(touched[w]);
+    for (uint32_t w = w0 + lane; w < w1; w += 32) mine += __popc(bm[w]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     if (tid == 0) {
@@ -273,30 +288,34 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
         return;
     }
     const unsigned lt = (1u << lane) - 1u;
-#pragma unroll 4
     for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t m = touched[w];
+        const uint32_t m = bm[w];
         if ((m >> lane) & 1u) {
             const uint32_t p = pos + __popc(m & lt);
             const uint32_t sy = w * 32 + lane;
-            const unsigned long long f = hist[sy];
-            leaf_sym[p] = sy;
-            key[p] = (f << 16) | p;
-            if (sy == 0) s_esc = f;
+            cp_async8(&key[p], &hist[sy]);
+            lsym[p] = sy;
         }
         pos += __popc(m);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
-    // self-cleaning: zero the consumed bins and the bitmap (no longer read)
+    for (uint32_t p = tid; p < kFastLeaves; p += kCbThreads) {
+        if (p < k) {
+            const unsigned long long f = key[p];
+            if (lsym[p] == 0) s_esc = f;
+            key[p] = (f << 16) | p;
+        } else {
+            key[p] = ~0ull;  // padding sorts last
+        }
+    }
+    // self-cleaning: zero the consumed bins and the bitmap (the copies above have landed)
     for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t m = touched[w];
+        const uint32_t m = bm[w];
         if ((m >> lane) & 1u) hist[w * 32 + lane] = 0;
     }
-    __syncwarp();
     for (uint32_t w = w0 + lane; w < w1; w += 32) touched[w] = 0;
-    uint32_t p2 = 2;
-    while (p2 < k) p2 <<= 1;
-    for (uint32_t i = k + tid; i < p2; i += kCbThreads) key[i] = ~0ull;
     __syncthreads();
     phase(0);
     if (k == 0) {
@@ -311,20 +330,25 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
         return;
     }
 
-    // (2) bitonic sort of the keys -------------------------------------------------------
-    for (uint32_t size = 2; size <= p2; size <<= 1) {
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = tid; i < p2 / 2; i += kCbThreads) {
-                const uint32_t lo = 2 * i - (i & (stride - 1));
-                const uint32_t hi = lo + stride;
-                const bool asc = (lo & size) == 0;
-                const unsigned long long a = key[lo], b = key[hi];
-                if ((a > b) == asc) {
-                    key[lo] = b;
-                    key[hi] = a;
+    // (2) bitonic sort of the keys in shared memory (p2 = next power of two >= k; a
+    // register/shuffle hybrid measured slower on B200 for 64-bit keys)
+    {
+        uint32_t p2 = 2;
+        while (p2 < k) p2 <<= 1;
+        for (uint32_t size = 2; size <= p2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = tid; i < p2 / 2; i += kCbThreads) {
+                    const uint32_t lo = 2 * i - (i & (stride - 1));
+                    const uint32_t hi = lo + stride;
+                    const bool asc = (lo & size) == 0;
+                    const unsigned long long a = key[lo], b = key[hi];
+                    if ((a > b) == asc) {
+                        key[lo] = b;
+                        key[hi] = a;
+                    }
                 }
+                __syncthreads();
             }
-            __syncthreads();
         }
     }
 
@@ -525,6 +549,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
     }
     __syncthreads();
     const unsigned lanemask_lt = (1u << lane) - 1;
+    uint32_t* s_book = reinterpret_cast<uint32_t*>(key);  // keys are dead from here on
     for (uint32_t base = 0; base < k; base += kCbThreads) {
         const uint32_t i = base + tid;
         const bool valid = i < k;
@@ -548,8 +573,9 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
         if (valid) {
             const uint32_t rank = s_wcnt[warp][l] + rank_w;
             const uint32_t pos = s_first_index[l] + rank;
-            const uint32_t sym = leaf_sym[i];
+            const uint32_t sym = lsym[i];
             book_sym[pos] = sym;
+            s_book[pos] = sym;
             book_len[pos] = (uint8_t)l;
             const unsigned long long code = s_first_code[l] + rank;
             enc[sym] = (code << 8) | l;
@@ -558,7 +584,7 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
     }
     phase(4);
     // (6) decode tables ----------------------------------------------------------------
-    write_tables(s_count, s_first_code, s_first_index, book_sym, canon, lut);
+    write_tables(s_count, s_first_code, s_first_index, s_book, canon, lut);
     __syncthreads();
     phase(5);
     if (tid == 0) {
@@ -967,108 +993,140 @@ __global__ void __launch_bounds__(1024) k_build_tables(const uint32_t* __restric
 }
 
 // --------------------------------------------------------------------------- K5 ----
-__device__ __forceinline__ void smem_put_bits(uint32_t* w, uint64_t p, unsigned long long code,
-                                              uint32_t len) {
-    // MSB-first: stream bit p is bit (31 - p%32) of word p/32.
-    const uint32_t o = (uint32_t)(p & 31);
-    const uint64_t wi = p >> 5;
-    if (o + len <= 64) {
-        const unsigned long long v = code << (64 - o - len);
-        const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
-        if (hi) atomicOr(&w[wi], hi);
-        if (lo) atomicOr(&w[wi + 1], lo);
-    } else {
-        const uint32_t l2 = o + len - 64;  // bits spilling into the third word
-        const unsigned long long v = code >> l2;  // first 64 - o bits
-        const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
-        if (hi) atomicOr(&w[wi], hi);
-        if (lo) atomicOr(&w[wi + 1], lo);
-        const uint32_t tail = (uint32_t)(code & ((1ull << l2) - 1)) << (32 - l2);
-        if (tail) atomicOr(&w[wi + 2], tail);
+// Block-wide exclusive scan of two u32 per thread (kEncThreads threads). Returns the
+// exclusive prefixes; *ta / *tb receive the block totals.
+__device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t* ea, uint32_t* eb,
+                                            uint32_t* ta, uint32_t* tb, uint32_t* sa,
+                                            uint32_t* sb) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int W = kEncThreads / 32;
+    uint32_t ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t xa = __shfl_up_sync(0xffffffffu, ia, o);
+        const uint32_t xb = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) {
+            ia += xa;
+            ib += xb;
+        }
     }
+    if (lane == 31) {
+        sa[warp] = ia;
+        sb[warp] = ib;
+    }
+    __syncthreads();
+    uint32_t pa = 0, pb = 0, qa = 0, qb = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        const uint32_t va = sa[w], vb = sb[w];
+        if (w < warp) {
+            pa += va;
+            pb += vb;
+        }
+        qa += va;
+        qb += vb;
+    }
+    *ea = pa + ia - a;
+    *eb = pb + ib - b;
+    *ta = qa;
+    *tb = qb;
+    __syncthreads();
 }
 
+// K5 encode (ref src/huffman.cpp:127-131 + BitWriter :88-103), persistent reduce-then-scan:
+// CTA c owns a contiguous span of 2048-symbol tiles. Phase 1 sums its span's code lengths
+// and escapes; one decoupled look-back across CTAs (warp 0) gives the span's global bit
+// offset and outlier index. Phase 2 re-reads the (L2-resident) symbols tile by tile, keeps
+// the 8 codes of each thread in registers, packs them MSB-first with a 64-bit accumulator
+// into a shared stage (plain stores for words a thread owns entirely, OR for shared
+// boundary words), and stores the stage with coalesced word writes (tile-boundary words
+// OR-ed). It also writes the outlier list and the decode sidecar bit offsets.
 template <typename SymT>
 __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     const SymT* __restrict__ symp = static_cast<const SymT*>(a.sym);
     extern __shared__ uint32_t stage[];
-    __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_prefix_bits, s_prefix_esc;
-    __shared__ uint32_t s_warp_bits[kEncThreads / 32], s_warp_esc[kEncThreads / 32];
-    __shared__ uint32_t s_tile_total;
+    __shared__ uint32_t s_a[kEncThreads / 32], s_b[kEncThreads / 32];
+    __shared__ unsigned long long s_red_bits[kEncThreads / 32], s_red_esc[kEncThreads / 32];
+    __shared__ unsigned long long s_base_bits, s_base_esc;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(a.ticket, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint64_t t0 = (uint64_t)tile * kEncTile;
-    if (t0 >= a.n) return;
-    const uint64_t my0 = t0 + (uint64_t)tid * kEncPer;
-
-    // pass 1: code lengths and escapes of my 16 symbols
-    uint32_t my_bits = 0, my_esc = 0, escmask = 0;
+    const uint64_t tiles = (a.n + kEncTile - 1) / kEncTile;
+    const uint64_t span = (tiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t tb = (uint64_t)blockIdx.x * span, te = min(tiles, tb + span);
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(symp) & 15) == 0;
+    auto load8 = [&](uint64_t my0, uint32_t* sy) {
+        if (vec_ok && my0 + kEncPer <= a.n) {
+            if (sizeof(SymT) == 2) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(symp + my0));
+                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int i = 0; i < kEncPer; ++i) {
-        const uint64_t g = my0 + i;
-        if (g < a.n) {
-            const uint32_t sy = symp[g];
-            my_bits += (uint32_t)(__ldg(a.enc + sy) & 0xFF);
-            if (sy == 0) {
-                ++my_esc;
-                escmask |= 1u << i;
+                for (int k = 0; k < 4; ++k) {
+                    sy[2 * k] = w4[k] & 0xFFFFu;
+                    sy[2 * k + 1] = w4[k] >> 16;
+                }
+            } else {
+                const uint4* v4 = reinterpret_cast<const uint4*>(symp + my0);
+                const uint4 v0 = __ldg(v4), v1 = __ldg(v4 + 1);
+                sy[0] = v0.x; sy[1] = v0.y; sy[2] = v0.z; sy[3] = v0.w;
+                sy[4] = v1.x; sy[5] = v1.y; sy[6] = v1.z; sy[7] = v1.w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kEncPer; ++i) sy[i] = my0 + i < a.n ? (uint32_t)symp[my0 + i] : 0u;
+        }
+    };
+
+    // ---- phase 1: span totals ----------------------------------------------------------
+    unsigned long long tb_bits = 0, tb_esc = 0;
+    for (uint64_t t = tb; t < te; ++t) {
+        const uint64_t my0 = t * kEncTile + (uint64_t)tid * kEncPer;
+        uint32_t sy[kEncPer];
+        load8(my0, sy);
+        uint32_t bsum = 0, esum = 0;
+#pragma unroll
+        for (int i = 0; i < kEncPer; ++i) {
+            if (my0 + i < a.n) {
+                bsum += (uint32_t)(__ldg(a.enc + sy[i]) & 0xFF);
+                esum += sy[i] == 0;
             }
         }
+        tb_bits += bsum;
+        tb_esc += esum;
     }
-    // CTA exclusive scan of (bits, escapes)
-    uint32_t ib = my_bits, ie = my_esc;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t tb = __shfl_up_sync(0xffffffffu, ib, o);
-        const uint32_t te = __shfl_up_sync(0xffffffffu, ie, o);
-        if (lane >= o) {
-            ib += tb;
-            ie += te;
-        }
+    for (int o = 16; o > 0; o >>= 1) {
+        tb_bits += __shfl_xor_sync(0xffffffffu, tb_bits, o);
+        tb_esc += __shfl_xor_sync(0xffffffffu, tb_esc, o);
     }
-    if (lane == 31) {
-        s_warp_bits[warp] = ib;
-        s_warp_esc[warp] = ie;
+    if (lane == 0) {
+        s_red_bits[warp] = tb_bits;
+        s_red_esc[warp] = tb_esc;
     }
     __syncthreads();
     if (warp == 0) {
-        uint32_t wb = lane < kEncThreads / 32 ? s_warp_bits[lane] : 0;
-        uint32_t we = lane < kEncThreads / 32 ? s_warp_esc[lane] : 0;
-        uint32_t xb = wb, xe = we;
+        unsigned long long rb = lane < kEncThreads / 32 ? s_red_bits[lane] : 0ull;
+        unsigned long long re = lane < kEncThreads / 32 ? s_red_esc[lane] : 0ull;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t tb = __shfl_up_sync(0xffffffffu, xb, o);
-            const uint32_t te = __shfl_up_sync(0xffffffffu, xe, o);
-            if (lane >= o) {
-                xb += tb;
-                xe += te;
-            }
+        for (int o = 16; o > 0; o >>= 1) {
+            rb += __shfl_xor_sync(0xffffffffu, rb, o);
+            re += __shfl_xor_sync(0xffffffffu, re, o);
         }
-        if (lane < kEncThreads / 32) {
-            s_warp_bits[lane] = xb - wb;
-            s_warp_esc[lane] = xe - we;
-        }
-        const uint32_t rb = __shfl_sync(0xffffffffu, xb, kEncThreads / 32 - 1);
-        const uint32_t re = __shfl_sync(0xffffffffu, xe, kEncThreads / 32 - 1);
-        // decoupled look-back, 32 predecessors per probe
+        // decoupled look-back over the CTAs, 32 predecessors per probe
+        const uint32_t c = blockIdx.x;
         TileStatus* st = a.status;
         volatile TileStatus* vst = st;
         unsigned long long pb = 0, pe = 0;
         if (lane == 0) {
-            st[tile].agg_bits = rb;
-            st[tile].agg_esc = re;
-            if (tile == 0) {
-                st[tile].incl_bits = rb;
-                st[tile].incl_esc = re;
+            st[c].agg_bits = rb;
+            st[c].agg_esc = re;
+            if (c == 0) {
+                st[c].incl_bits = rb;
+                st[c].incl_esc = re;
             }
             __threadfence();
-            atomicExch(&st[tile].flag, tile == 0 ? 2u : 1u);
+            atomicExch(&st[c].flag, c == 0 ? 2u : 1u);
         }
-        if (tile > 0) {
-            int64_t base = (int64_t)tile - 1;
+        if (c > 0) {
+            int64_t base = (int64_t)c - 1;
             for (;;) {
                 const int64_t j = base - lane;
                 unsigned f = 2;
@@ -1104,65 +1162,120 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
                 base -= 32;
             }
             if (lane == 0) {
-                st[tile].incl_bits = pb + rb;
-                st[tile].incl_esc = pe + re;
+                st[c].incl_bits = pb + rb;
+                st[c].incl_esc = pe + re;
                 __threadfence();
-                atomicExch(&st[tile].flag, 2u);
+                atomicExch(&st[c].flag, 2u);
             }
         }
         if (lane == 0) {
-            s_prefix_bits = pb;
-            s_prefix_esc = pe;
-            s_tile_total = rb;
+            s_base_bits = pb;
+            s_base_esc = pe;
         }
     }
     __syncthreads();
-    const unsigned long long tile_bit0 = s_prefix_bits;
-    const unsigned long long tile_esc0 = s_prefix_esc;
-    const uint32_t total = s_tile_total;
-    const uint32_t s0 = (uint32_t)(tile_bit0 & 31);
-    const uint32_t nw = (s0 + total + 31) / 32;
-    for (uint32_t i = tid; i < nw + 3; i += kEncThreads) stage[i] = 0;
-    __syncthreads();
-    const uint32_t excl_bits = s_warp_bits[warp] + (ib - my_bits);
-    uint64_t off = (uint64_t)s0 + excl_bits;
-    unsigned long long gbit = tile_bit0 + excl_bits;
-    unsigned long long gesc = tile_esc0 + s_warp_esc[warp] + (ie - my_esc);
-    uint64_t next_side = a.side_bitoff ? ((my0 + a.interval - 1) / a.interval) * a.interval : ~0ull;
-    // pass 2: write codes (re-fetched from the L1-resident table)
-#pragma unroll 4
-    for (int i = 0; i < kEncPer; ++i) {
-        const uint64_t g = my0 + i;
-        if (g >= a.n) break;
-        const unsigned long long e = __ldg(a.enc + (uint32_t)symp[g]);
-        const uint32_t len = (uint32_t)(e & 0xFF);
-        if (g == next_side) {
-            a.side_bitoff[g / a.interval] = gbit;
-            if (a.side_outl) a.side_outl[g / a.interval] = (uint32_t)gesc;
-            next_side += a.interval;
-        }
-        smem_put_bits(stage, off, e >> 8, len);
-        if ((escmask >> i) & 1u) {
-            if (a.x) {
-                a.out_index[gesc] = g;
-                a.out_value[gesc] = a.x[g];
+
+    // ---- phase 2: write ---------------------------------------------------------------
+    unsigned long long run_bits = s_base_bits, run_esc = s_base_esc;
+    for (uint64_t t = tb; t < te; ++t) {
+        const uint64_t my0 = t * kEncTile + (uint64_t)tid * kEncPer;
+        uint32_t sy[kEncPer];
+        load8(my0, sy);
+        unsigned long long code[kEncPer];
+        uint32_t my_bits = 0, my_esc = 0, escmask = 0;
+#pragma unroll
+        for (int i = 0; i < kEncPer; ++i) {
+            code[i] = my0 + i < a.n ? __ldg(a.enc + sy[i]) : 0ull;
+            my_bits += (uint32_t)(code[i] & 0xFF);
+            if (my0 + i < a.n && sy[i] == 0) {
+                ++my_esc;
+                escmask |= 1u << i;
             }
-            ++gesc;
         }
-        off += len;
-        gbit += len;
-    }
-    __syncthreads();
-    const uint64_t gw0 = tile_bit0 >> 5;
-    for (uint32_t i = tid; i < nw; i += kEncThreads) {
-        const uint64_t gw = gw0 + i;
-        if (gw >= a.nwords) break;
-        const uint32_t v = bswap32(stage[i]);
-        if (i == 0 || i == nw - 1) {
-            if (v) atomicOr(&a.words[gw], v);
-        } else {
-            a.words[gw] = v;
+        uint32_t ex_bits, ex_esc, tot_bits, tot_esc;
+        block_scan2(my_bits, my_esc, &ex_bits, &ex_esc, &tot_bits, &tot_esc, s_a, s_b);
+        const uint32_t s0 = (uint32_t)(run_bits & 31);
+        const uint32_t nw = (s0 + tot_bits + 31) / 32;
+        for (uint32_t i = tid; i < nw + 2; i += kEncThreads) stage[i] = 0;
+        __syncthreads();
+        const uint32_t off = s0 + ex_bits;
+        unsigned long long gbit = run_bits + ex_bits;
+        unsigned long long gesc = run_esc + ex_esc;
+        // PrevValue sidecar intervals are powers of two: mask arithmetic (a 64-bit divide is
+        // ~100 instructions); Lorenzo2d uses the plane size and divides
+        const bool ipow2 = (a.interval & (a.interval - 1)) == 0;
+        const uint64_t imask = a.interval - 1;
+        const int ishift = __ffsll((long long)a.interval) - 1;
+        uint64_t next_side = !a.side_bitoff ? ~0ull
+                             : ipow2 ? ((my0 + imask) & ~imask)
+                                     : ((my0 + a.interval - 1) / a.interval) * a.interval;
+        unsigned long long acc = 0;
+        int nacc = (int)(off & 31);
+        uint32_t wi = off >> 5;
+        bool first = true;
+        auto emit = [&]() {
+            const uint32_t word = (uint32_t)(acc >> 32);
+            if (first) {
+                if (word) atomicOr(&stage[wi], word);
+                first = false;
+            } else {
+                stage[wi] = word;
+            }
+            ++wi;
+            acc <<= 32;
+            nacc -= 32;
+        };
+        auto append = [&](unsigned long long c, int len) {  // len <= 32
+            acc |= c << (64 - nacc - len);
+            nacc += len;
+            if (nacc >= 32) emit();
+        };
+#pragma unroll
+        for (int i = 0; i < kEncPer; ++i) {
+            const uint64_t g = my0 + i;
+            if (g >= a.n) break;
+            const int len = (int)(code[i] & 0xFF);
+            const unsigned long long c = code[i] >> 8;
+            if (g == next_side) {
+                const uint64_t si = ipow2 ? (g >> ishift) : g / a.interval;
+                a.side_bitoff[si] = gbit;
+                if (a.side_outl) a.side_outl[si] = (uint32_t)gesc;
+                next_side += a.interval;
+            }
+            if (len > 32) {
+                append(c >> 32, len - 32);
+                append(c & 0xFFFFFFFFull, 32);
+            } else {
+                append(c, len);
+            }
+            if ((escmask >> i) & 1u) {
+                if (a.x) {
+                    a.out_index[gesc] = g;
+                    a.out_value[gesc] = a.x[g];
+                }
+                ++gesc;
+            }
+            gbit += len;
         }
+        if (nacc > 0) {
+            const uint32_t word = (uint32_t)(acc >> 32);
+            if (word) atomicOr(&stage[wi], word);
+        }
+        __syncthreads();
+        const uint64_t gw0 = run_bits >> 5;
+        for (uint32_t i = tid; i < nw; i += kEncThreads) {
+            const uint64_t gw = gw0 + i;
+            if (gw >= a.nwords) break;
+            const uint32_t v = bswap32(stage[i]);
+            if (i == 0 || i == nw - 1) {
+                if (v) atomicOr(&a.words[gw], v);
+            } else {
+                a.words[gw] = v;
+            }
+        }
+        run_bits += tot_bits;
+        run_esc += tot_esc;
+        __syncthreads();
     }
 }
 
@@ -1241,11 +1354,11 @@ cudaError_t launch_build_tables(const uint32_t* book_sym, const uint8_t* book_le
 }
 
 cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t* launches) {
-    (void)sms;
     const uint64_t tiles = (a.n + kEncTile - 1) / kEncTile;
-    cudaError_t e = cudaMemsetAsync(a.status, 0, sizeof(TileStatus) * tiles, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned int), s);
+    uint64_t grid = (uint64_t)sms * 3;  // persistent: 3 CTAs of 256 threads per SM
+    if (grid > tiles) grid = tiles;
+    if (grid == 0) grid = 1;
+    cudaError_t e = cudaMemsetAsync(a.status, 0, sizeof(TileStatus) * grid, s);
     if (e != cudaSuccess) return e;
     const size_t smem = ((size_t)kEncTile * (a.max_len ? a.max_len : 1) / 32 + 8) * 4;
     static size_t attr = 0;
@@ -1259,9 +1372,9 @@ cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t
         attr = smem;
     }
     if (a.sym16)
-        k_encode<uint16_t><<<(unsigned)tiles, kEncThreads, smem, s>>>(a);
+        k_encode<uint16_t><<<(unsigned)grid, kEncThreads, smem, s>>>(a);
     else
-        k_encode<uint32_t><<<(unsigned)tiles, kEncThreads, smem, s>>>(a);
+        k_encode<uint32_t><<<(unsigned)grid, kEncThreads, smem, s>>>(a);
     ++*launches;
     return cudaGetLastError();
 }

@@ -86,11 +86,11 @@ struct EncodeArgs {
     uint32_t* side_outl;
     uint64_t interval;
     uint32_t max_len;
-    TileStatus* status;              // ceil(n / kEncTile) entries, zeroed by the launcher
+    TileStatus* status;              // one entry per encode CTA (<= ceil(n / kEncTile)), zeroed by the launcher
     unsigned int* ticket;            // zeroed by the launcher
 };
 constexpr int kEncThreads = 256;
-constexpr int kEncPer = 16;
+constexpr int kEncPer = 8;
 constexpr int kEncTile = kEncThreads * kEncPer;
 cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t* launches);
 
