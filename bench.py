@@ -140,15 +140,10 @@ def run_ours(args, rank, world, local_rank):
     params = acz.CodecParams(args.eb)
 
     def step():
-        cbytes = 0
-        blobs = []
-        for x in tensors:
-            c = acz.compress(x, params, stream=stream, ctx=ctx)
-            cbytes += c.compressed_bytes
-            blobs.append(c)
-        for c, o in zip(blobs, outs):
-            acz.decompress(c, zero_filter=True, out=o, stream=stream)
-        return cbytes, blobs
+        # the whole activation set through the batched entry points (one call each way)
+        blobs = acz.compress_many(tensors, params, stream=stream, ctx=ctx)
+        acz.decompress_many(blobs, zero_filter=True, outs=outs, stream=stream)
+        return sum(c.compressed_bytes for c in blobs), blobs
 
     for _ in range(args.warmup):
         step()

@@ -26,6 +26,10 @@
  *                                include/acz/huffman.hpp:26, src/huffman.cpp:107-135
  *   acz_gpu_huffman_decode    <- std::vector<uint32_t> huffman_decode(...)
  *                                include/acz/huffman.hpp:30-32, src/huffman.cpp:137-189
+ *   acz_gpu_compress_batch / acz_gpu_decompress_batch
+ *                             <- compress/decompress of every stashed activation of a step
+ *                                (Controller::wrap_forward / unwrap_backward, src/controller.cpp
+ *                                :194-249, called once per conv layer)
  *   acz_gpu_compress_host / acz_gpu_decompress_host
  *                             <- compress/decompress on host tensors (the reference's own
  *                                calling convention, host buffers in and out)
@@ -109,6 +113,21 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
  * (ref src/codec.cpp:162-164). Stream-ordered, no host synchronisation. */
 int acz_gpu_decompress(acz_gpu_ctx* ctx, const acz_gpu_blob* blob, int zero_filter, float* d_out,
                        void* stream);
+/* Batched compress of `count` tensors (the controller's per-step activation set, ref
+ * Controller::wrap_forward src/controller.cpp:194-230 applied to every conv input). Tensor i
+ * has rank ranks[i] and extents shapes[sum(ranks[<i]) ..]. Each tensor gets its own
+ * workspace and one of the context's internal streams (forked from / joined back into
+ * `stream`), so the tensors' kernels overlap; there is one host wait per tensor for its
+ * codebook size. out[i] receives tensor i's blob or NULL; status[i] (optional) its status
+ * (the reference degrades a failing layer to pass-through). Returns the first failure. */
+int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const* d_in,
+                           const uint64_t* shapes, const uint32_t* ranks, double eb,
+                           uint32_t quant_radius, uint32_t predictor, void* stream,
+                           acz_gpu_blob** out, int* status);
+/* Batched decompress (ref Controller::unwrap_backward src/controller.cpp:234-249 for every
+ * handle of a step), stream-ordered on `stream` through the internal streams. */
+int acz_gpu_decompress_batch(acz_gpu_ctx* ctx, uint32_t count, const acz_gpu_blob* const* blobs,
+                             int zero_filter, float* const* d_out, void* stream);
 int acz_gpu_blob_info(const acz_gpu_blob* blob, acz_gpu_blob_info_t* info);
 int acz_gpu_blob_free(acz_gpu_blob* blob);
 

@@ -335,6 +335,56 @@ def decompress(c: CompressedTensor, zero_filter: bool = False, out=None, stream=
     return out
 
 
+def compress_many(tensors: Sequence, p: CodecParams = CodecParams(), stream=None,
+                  ctx: Optional[Context] = None, errors: str = "raise") -> List[Optional[CompressedTensor]]:
+    """Batched :func:`compress` of a whole activation set (one call per training step, as
+    Controller::wrap_forward does per conv layer, ref src/controller.cpp:194-230). The
+    tensors' kernels overlap on the context's internal streams. errors="raise" raises the
+    first failure; errors="none" returns None for failing tensors (the reference controller
+    degrades such layers to pass-through, src/controller.cpp:216-220)."""
+    ts = [_require_cuda_f32(t) for t in tensors]
+    if not ts:
+        return []
+    ctx = ctx or default_context(ts[0].device.index)
+    k = len(ts)
+    ptrs = (C.c_void_p * k)(*[t.data_ptr() for t in ts])
+    ranks = (C.c_uint32 * k)(*[t.dim() for t in ts])
+    flat = [int(e) for t in ts for e in t.shape]
+    shapes = (C.c_uint64 * max(1, len(flat)))(*flat)
+    outs = (C.c_void_p * k)()
+    status = (C.c_int * k)()
+    rc = _native.load().acz_gpu_compress_batch(ctx.handle, k, ptrs, shapes, ranks, float(p.eb),
+                                               int(p.quant_radius), int(p.predictor),
+                                               _stream_handle(stream), outs, status)
+    res = [CompressedTensor(C.c_void_p(outs[i]), ctx) if outs[i] else None for i in range(k)]
+    if rc and errors == "raise":
+        _check(rc, ctx)
+    return res
+
+
+def decompress_many(blobs: Sequence[CompressedTensor], zero_filter: bool = False, outs=None,
+                    stream=None):
+    """Batched :func:`decompress` (ref Controller::unwrap_backward, src/controller.cpp:234-249)."""
+    import torch
+    if not blobs:
+        return []
+    ctx = blobs[0]._ctx
+    if outs is None:
+        outs = [torch.empty(c.shape, dtype=torch.float32, device=f"cuda:{ctx.device}")
+                for c in blobs]
+    outs = [_require_cuda_f32(o, "out") for o in outs]
+    for c, o in zip(blobs, outs):
+        if o.numel() != c.element_count():
+            raise ShapeError("output size mismatch")
+    k = len(blobs)
+    hs = (C.c_void_p * k)(*[c._h.value for c in blobs])
+    ps = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    rc = _native.load().acz_gpu_decompress_batch(ctx.handle, k, hs, int(bool(zero_filter)), ps,
+                                                 _stream_handle(stream))
+    _check(rc, ctx)
+    return outs
+
+
 def compression_ratio(c: CompressedTensor) -> float:
     """ref src/codec.cpp:173-175"""
     return c.uncompressed_bytes / c.compressed_bytes

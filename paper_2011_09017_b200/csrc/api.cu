@@ -20,13 +20,22 @@
 using namespace acz_b200;
 
 // ------------------------------------------------------------------------- structs --
-struct acz_gpu_ctx {
-    int device = 0;
-    int sms = 148;
-    std::string err;
-    uint64_t launches = 0;
-    cudaStream_t own = nullptr;  // stream used by the host-buffer entry points
-    // workspace (grown on demand)
+// Device block read back once per compress (codebook results + error flags).
+struct SmallBlock {
+    BookInfo info;
+    unsigned int flags;
+    unsigned int ticket;
+    unsigned long long nnz;
+    double sumabs;
+    unsigned int maxsym;
+    unsigned int pad;
+    CanonTables canon;
+    uint32_t lut[kLutSize];
+};
+
+// Per-tensor workspace. A batched compress uses one slot per tensor so the tensors'
+// kernels can run concurrently on the context's internal streams.
+struct Slot {
     void* ws_sym = nullptr;
     size_t ws_sym_cap = 0;
     void* ws_hist = nullptr;  // u64 bins x alphabet + touched bitmap; kept zero between calls
@@ -40,32 +49,33 @@ struct acz_gpu_ctx {
     size_t ws_status_cap = 0;
     void* ws_row = nullptr;
     size_t ws_row_cap = 0;
-    void* ws_io = nullptr;  // host-API staging (input / output floats)
-    size_t ws_io_cap = 0;
-    void* ws_aux = nullptr;  // sequential-decode scratch (symbols, plane prefixes)
-    size_t ws_aux_cap = 0;
     void* ws_book = nullptr;  // codebook output (sym u32 + len u8) before the blob exists
     size_t ws_book_cap = 0;
     void* ws_side = nullptr;  // sidecar chain states produced by K2
     size_t ws_side_cap = 0;
     void* ws_qs = nullptr;  // speculative quantiser scratch (look-back status, anchors)
     size_t ws_qs_cap = 0;
-    // small fixed device block
-    struct Small {
-        BookInfo info;
-        unsigned int flags;
-        unsigned int ticket;
-        unsigned long long nnz;
-        double sumabs;
-        unsigned int maxsym;
-        unsigned int pad;
-        CanonTables canon;
-        uint32_t lut[kLutSize];
-    };
-    Small* d_small = nullptr;
-    Small* h_small = nullptr;  // pinned mirror
+    SmallBlock* d_small = nullptr;
+    SmallBlock* h_small = nullptr;  // pinned mirror
+    cudaEvent_t ev_book = nullptr;  // recorded after the codebook read-back
     uint64_t last_n = 0;
     bool last_sym16 = false;
+};
+
+struct acz_gpu_ctx {
+    int device = 0;
+    int sms = 148;
+    std::string err;
+    uint64_t launches = 0;
+    cudaStream_t own = nullptr;  // stream used by the host-buffer entry points
+    std::vector<Slot*> slots;    // slot 0 serves the single-tensor entry points
+    std::vector<cudaStream_t> pool;     // internal streams of the batched entry points
+    std::vector<cudaEvent_t> pool_ev;   // one per pool stream (join)
+    cudaEvent_t ev_fork = nullptr;
+    void* ws_io = nullptr;  // host-API staging (input / output floats)
+    size_t ws_io_cap = 0;
+    void* ws_aux = nullptr;  // sequential-decode scratch (symbols, plane prefixes)
+    size_t ws_aux_cap = 0;
     // profiling: events recorded around every launch when enabled
     bool prof = false;
     struct Pending {
@@ -277,32 +287,51 @@ uint64_t blob_binding(const acz_gpu_blob_info_t& in) {
     return h;
 }
 
-int ensure_small(acz_gpu_ctx* ctx) {
-    if (ctx->d_small) return ACZ_OK;
-    CK(cudaMalloc(&ctx->d_small, sizeof(acz_gpu_ctx::Small)));
-    CK(cudaMallocHost(&ctx->h_small, sizeof(acz_gpu_ctx::Small)));
+int ensure_small(acz_gpu_ctx* ctx, Slot* sl) {
+    if (sl->d_small) return ACZ_OK;
+    CK(cudaMalloc(&sl->d_small, sizeof(SmallBlock)));
+    CK(cudaMallocHost(&sl->h_small, sizeof(SmallBlock)));
+    CK(cudaEventCreateWithFlags(&sl->ev_book, cudaEventDisableTiming));
     return ACZ_OK;
+}
+
+// Slot i (created on first use).
+Slot* get_slot(acz_gpu_ctx* ctx, size_t i) {
+    while (ctx->slots.size() <= i) ctx->slots.push_back(new (std::nothrow) Slot());
+    return ctx->slots[i];
+}
+
+void free_slot(Slot* sl) {
+    if (!sl) return;
+    for (void* p : {sl->ws_sym, sl->ws_hist, sl->ws_enc, sl->ws_cb, sl->ws_status, sl->ws_row,
+                    sl->ws_book, sl->ws_side, sl->ws_qs})
+        if (p) cudaFree(p);
+    if (sl->d_small) cudaFree(sl->d_small);
+    if (sl->h_small) cudaFreeHost(sl->h_small);
+    if (sl->ev_book) cudaEventDestroy(sl->ev_book);
+    delete sl;
 }
 
 // Runs the fused stats pass and returns non-finite / nnz / sum|x|.
 int run_stats(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, uint32_t* d_bitmap,
               cudaStream_t s, unsigned* flags, uint64_t* nnz, double* sumabs) {
-    int rc = ensure_small(ctx);
+    Slot* sl = get_slot(ctx, 0);
+    int rc = ensure_small(ctx, sl);
     if (rc) return rc;
-    CK(cudaMemsetAsync(&ctx->d_small->flags, 0, sizeof(unsigned), s));
-    CK(cudaMemsetAsync(&ctx->d_small->nnz, 0, sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(&ctx->d_small->sumabs, 0, sizeof(double), s));
+    CK(cudaMemsetAsync(&sl->d_small->flags, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(&sl->d_small->nnz, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(&sl->d_small->sumabs, 0, sizeof(double), s));
     {
         KTimer kt(ctx, ACZ_K_STATS, s);
-        CK(launch_stats(d_in, n, d_bitmap, &ctx->d_small->nnz, &ctx->d_small->flags,
-                        &ctx->d_small->sumabs, ctx->sms, s, &ctx->launches));
+        CK(launch_stats(d_in, n, d_bitmap, &sl->d_small->nnz, &sl->d_small->flags,
+                        &sl->d_small->sumabs, ctx->sms, s, &ctx->launches));
     }
-    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, offsetof(acz_gpu_ctx::Small, canon),
+    CK(cudaMemcpyAsync(sl->h_small, sl->d_small, offsetof(SmallBlock, canon),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (flags) *flags = ctx->h_small->flags;
-    if (nnz) *nnz = ctx->h_small->nnz;
-    if (sumabs) *sumabs = ctx->h_small->sumabs;
+    if (flags) *flags = sl->h_small->flags;
+    if (nnz) *nnz = sl->h_small->nnz;
+    if (sumabs) *sumabs = sl->h_small->sumabs;
     return ACZ_OK;
 }
 
@@ -345,8 +374,9 @@ int acz_gpu_ctx_create(int device, acz_gpu_ctx** out) {
         delete ctx;
         return ACZ_ERR_CUDA;
     }
-    if (ensure_small(ctx) != ACZ_OK) {
-        delete ctx;
+    if (ensure_small(ctx, get_slot(ctx, 0)) != ACZ_OK ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+        acz_gpu_ctx_destroy(ctx);
         return ACZ_ERR_CUDA;
     }
     *out = ctx;
@@ -356,11 +386,12 @@ int acz_gpu_ctx_create(int device, acz_gpu_ctx** out) {
 int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
     if (!ctx) return ACZ_ERR_INVALID;
     cudaDeviceSynchronize();
-    for (void* p : {ctx->ws_sym, ctx->ws_hist, ctx->ws_enc, ctx->ws_cb, ctx->ws_status,
-                    ctx->ws_row, ctx->ws_io, ctx->ws_aux, ctx->ws_book, ctx->ws_side, ctx->ws_qs})
+    for (void* p : {ctx->ws_io, ctx->ws_aux})
         if (p) cudaFree(p);
-    if (ctx->d_small) cudaFree(ctx->d_small);
-    if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    for (Slot* sl : ctx->slots) free_slot(sl);
+    for (auto st : ctx->pool) cudaStreamDestroy(st);
+    for (auto e : ctx->pool_ev) cudaEventDestroy(e);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     for (auto& p : ctx->pending) {
         cudaEventDestroy(p.a);
@@ -382,9 +413,10 @@ namespace {
 
 // Blob-side finalisation shared by compress and the generic Huffman encoder: after the
 // codebook sync, allocates the blob, copies the tables and runs K5.
-int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const void* d_sym, int sym16, uint64_t n,
-                  const float* d_x, uint64_t interval, bool with_outl, cudaStream_t s) {
-    const BookInfo& bi = ctx->h_small->info;
+int finish_encode(acz_gpu_ctx* ctx, Slot* sl, acz_gpu_blob* b, const void* d_sym, int sym16,
+                  uint64_t n, const float* d_x, uint64_t interval, bool with_outl,
+                  cudaStream_t s) {
+    const BookInfo& bi = sl->h_small->info;
     const uint64_t nwords = (bi.total_bits + 31) / 32;
     const uint64_t nout = d_x ? bi.n_escapes : 0;
     const uint64_t nchunks = interval ? (n + interval - 1) / interval : 0;
@@ -394,22 +426,22 @@ int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const void* d_sym, int sym1
     b->nchunks = nchunks;
     b->max_len = bi.max_len;
     CK(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 32), s));
-    const uint32_t* wb_sym = static_cast<const uint32_t*>(ctx->ws_book);
+    const uint32_t* wb_sym = static_cast<const uint32_t*>(sl->ws_book);
     const uint8_t* wb_len =
-        reinterpret_cast<const uint8_t*>(wb_sym + std::max<uint64_t>(ctx->ws_book_cap / 5, 1));
+        reinterpret_cast<const uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
     CK(cudaMemcpyAsync(b->book_sym, wb_sym, 4ull * bi.book_size, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(b->book_len, wb_len, bi.book_size, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(b->lut, ctx->d_small->lut, 4ull * kLutSize, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(b->canon, &ctx->d_small->canon, sizeof(CanonTables),
+    CK(cudaMemcpyAsync(b->lut, sl->d_small->lut, 4ull * kLutSize, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(b->canon, &sl->d_small->canon, sizeof(CanonTables),
                        cudaMemcpyDeviceToDevice, s));
     if (nchunks && d_x)
-        CK(cudaMemcpyAsync(b->side_state, ctx->ws_side, 4ull * nchunks, cudaMemcpyDeviceToDevice,
+        CK(cudaMemcpyAsync(b->side_state, sl->ws_side, 4ull * nchunks, cudaMemcpyDeviceToDevice,
                            s));
     EncodeArgs ea;
     ea.sym = d_sym;
     ea.sym16 = sym16;
     ea.n = n;
-    ea.enc = static_cast<const unsigned long long*>(ctx->ws_enc);
+    ea.enc = static_cast<const unsigned long long*>(sl->ws_enc);
     ea.x = d_x;
     ea.words = b->words;
     ea.nwords = nwords;
@@ -419,8 +451,8 @@ int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const void* d_sym, int sym1
     ea.side_outl = b->side_outl;
     ea.interval = interval ? interval : 1;
     ea.max_len = bi.max_len;
-    ea.status = static_cast<TileStatus*>(ctx->ws_status);
-    ea.ticket = &ctx->d_small->ticket;
+    ea.status = static_cast<TileStatus*>(sl->ws_status);
+    ea.ticket = &sl->d_small->ticket;
     {
         KTimer kt(ctx, ACZ_K_ENCODE, s);
         CK(launch_encode(ea, ctx->sms, s, &ctx->launches));
@@ -428,160 +460,54 @@ int finish_encode(acz_gpu_ctx* ctx, acz_gpu_blob* b, const void* d_sym, int sym1
     return ACZ_OK;
 }
 
-// Histogram + codebook + the single synchronisation. Leaves BookInfo in h_small.
-int build_book(acz_gpu_ctx* ctx, const void* d_sym, int sym16, uint64_t n, uint32_t alphabet,
-               uint32_t center, cudaStream_t s) {
+// Histogram + codebook + the BookInfo read-back, recorded on sl->ev_book (the caller waits
+// for it before sizing the blob: the single host synchronisation of a compress).
+int build_book(acz_gpu_ctx* ctx, Slot* sl, const void* d_sym, int sym16, uint64_t n,
+               uint32_t alphabet, uint32_t center, cudaStream_t s) {
     const uint64_t max_leaves = std::min<uint64_t>(alphabet, n);
     const size_t hist_bytes = 8ull * alphabet + 4ull * ((alphabet + 31) / 32);
-    if (hist_bytes > ctx->ws_hist_cap) ctx->hist_clean = false;
-    CK(grow(&ctx->ws_hist, &ctx->ws_hist_cap, hist_bytes));
-    if (!ctx->hist_clean) {
-        CK(cudaMemsetAsync(ctx->ws_hist, 0, ctx->ws_hist_cap, s));
-        ctx->hist_clean = true;
+    if (hist_bytes > sl->ws_hist_cap) sl->hist_clean = false;
+    CK(grow(&sl->ws_hist, &sl->ws_hist_cap, hist_bytes));
+    if (!sl->hist_clean) {
+        CK(cudaMemsetAsync(sl->ws_hist, 0, sl->ws_hist_cap, s));
+        sl->hist_clean = true;
     }
-    unsigned long long* hist = static_cast<unsigned long long*>(ctx->ws_hist);
+    unsigned long long* hist = static_cast<unsigned long long*>(sl->ws_hist);
     uint32_t* touched = reinterpret_cast<uint32_t*>(hist + alphabet);
-    CK(grow(&ctx->ws_enc, &ctx->ws_enc_cap, 8ull * alphabet));
-    CK(grow(&ctx->ws_cb, &ctx->ws_cb_cap, codebook_scratch_bytes(max_leaves)));
-    CK(grow(&ctx->ws_book, &ctx->ws_book_cap, 5ull * max_leaves + 64));
+    CK(grow(&sl->ws_enc, &sl->ws_enc_cap, 8ull * alphabet));
+    CK(grow(&sl->ws_cb, &sl->ws_cb_cap, codebook_scratch_bytes(max_leaves)));
+    CK(grow(&sl->ws_book, &sl->ws_book_cap, 5ull * max_leaves + 64));
     const uint64_t tiles = (n + kEncTile - 1) / kEncTile;
-    CK(grow(&ctx->ws_status, &ctx->ws_status_cap, sizeof(TileStatus) * tiles));
+    CK(grow(&sl->ws_status, &sl->ws_status_cap, sizeof(TileStatus) * tiles));
     {
     KTimer kt(ctx, ACZ_K_HIST, s);
-    ctx->hist_clean = false;  // until the codebook kernels have consumed the bins
+    sl->hist_clean = false;  // until the codebook kernels have consumed the bins
     CK(launch_histogram(d_sym, sym16, n, alphabet, center, hist, touched, ctx->sms, s,
                         &ctx->launches));
     }
-    uint32_t* wb_sym = static_cast<uint32_t*>(ctx->ws_book);
-    uint8_t* wb_len = reinterpret_cast<uint8_t*>(wb_sym + std::max<uint64_t>(ctx->ws_book_cap / 5, 1));
+    uint32_t* wb_sym = static_cast<uint32_t*>(sl->ws_book);
+    uint8_t* wb_len = reinterpret_cast<uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
     {
     KTimer kt(ctx, ACZ_K_BOOK, s);
-    CK(launch_codebook(hist, touched, alphabet, max_leaves, ctx->ws_cb, wb_sym, wb_len,
-                       static_cast<unsigned long long*>(ctx->ws_enc), &ctx->d_small->canon,
-                       ctx->d_small->lut, &ctx->d_small->info, s, &ctx->launches));
+    CK(launch_codebook(hist, touched, alphabet, max_leaves, sl->ws_cb, wb_sym, wb_len,
+                       static_cast<unsigned long long*>(sl->ws_enc), &sl->d_small->canon,
+                       sl->d_small->lut, &sl->d_small->info, s, &ctx->launches));
     }
-    ctx->hist_clean = true;
-    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, offsetof(acz_gpu_ctx::Small, canon),
+    sl->hist_clean = true;
+    CK(cudaMemcpyAsync(sl->h_small, sl->d_small, offsetof(SmallBlock, canon),
                        cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    CK(cudaEventRecord(sl->ev_book, s));
     return ACZ_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape, uint32_t rank,
-                     double eb, uint32_t quant_radius, uint32_t predictor, void* stream,
-                     acz_gpu_blob** out) {
-    if (!ctx || !out) return ACZ_ERR_INVALID;
-    *out = nullptr;
-    ctx->err.clear();
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    uint64_t n = 0;
-    int rc = validate_shape(ctx, shape, rank, &n);
-    if (rc) return rc;
-    if (n && !d_in) return fail(ctx, ACZ_ERR_INVALID, "null input");
-    if (predictor > 1) return fail(ctx, ACZ_ERR_PARAM, "unknown predictor");
-    if (!params_ok(eb, quant_radius)) {
-        // The reference builds the Tensor (finiteness check) before compress validates.
-        if (n) {
-            unsigned fl = 0;
-            rc = run_stats(ctx, d_in, n, nullptr, s, &fl, nullptr, nullptr);
-            if (rc) return rc;
-            if (fl & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
-        }
-        return fail(ctx, ACZ_ERR_PARAM, param_msg(eb));
-    }
-    if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "compress: empty tensor");
-    const PlaneGeom g = plane_geom(shape, rank);
-    const uint32_t alphabet = 2u * quant_radius;
-    const uint64_t interval = predictor == ACZ_PRED_PREV ? sidecar_interval_default() : g.plane_size;
-    const uint64_t nchunks = (n + interval - 1) / interval;
-
-    CK(grow(&ctx->ws_sym, &ctx->ws_sym_cap, 4ull * n));
-    CK(grow(&ctx->ws_side, &ctx->ws_side_cap, 4ull * nchunks));
-    if (predictor == ACZ_PRED_LORENZO2D)
-        CK(grow(&ctx->ws_row, &ctx->ws_row_cap, 4ull * g.planes * g.cols));
-    ctx->last_n = n;
-
-    acz_gpu_ctx::Small* sm = ctx->d_small;
-    CK(cudaMemsetAsync(&sm->flags, 0, sizeof(unsigned), s));
-    QuantArgs qa;
-    qa.x = d_in;
-    qa.g = g;
-    qa.eb = eb;
-    qa.step = 2.0 * eb;
-    qa.radius = quant_radius;
-    qa.predictor = predictor;
-    const int sym16 = (predictor == ACZ_PRED_PREV && quant_radius <= 32768) ? 1 : 0;
-    ctx->last_sym16 = sym16 != 0;
-    qa.sym = sym16 ? nullptr : static_cast<uint32_t*>(ctx->ws_sym);
-    qa.sym16 = sym16 ? static_cast<uint16_t*>(ctx->ws_sym) : nullptr;
-    qa.side_state = static_cast<float*>(ctx->ws_side);
-    qa.interval = interval;
-    qa.row_scratch = static_cast<float*>(ctx->ws_row);
-    qa.flags = &sm->flags;
-    {
-        KTimer kt(ctx, ACZ_K_QUANT, s);
-        if (quant_spec_applicable(predictor, g.plane_size) && !std::getenv("ACZ_SERIAL_QUANT")) {
-            CK(grow(&ctx->ws_qs, &ctx->ws_qs_cap, quant_spec_scratch_bytes(g.planes, g.plane_size)));
-            CK(launch_quant_spec(qa, ctx->ws_qs, s, &ctx->launches));
-        } else {
-            CK(launch_quant(qa, ctx->sms, s, &ctx->launches));
-        }
-    }
-    rc = build_book(ctx, ctx->ws_sym, sym16, n, alphabet, quant_radius, s);
-    if (rc) return rc;
-    const BookInfo bi = ctx->h_small->info;
-    const unsigned flags = ctx->h_small->flags | bi.flags;
-    // precedence follows the reference: Tensor ctor (DomainError), huffman_encode
-    // (DecodeError), then the codebook limit in compress (FormatError).
-    if (flags & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
-    if (flags & kFlagInternal) return fail(ctx, ACZ_ERR_CUDA, "internal: look-back timeout");
-    if (flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
-    if (bi.book_size > kMaxBook)
-        return fail(ctx, ACZ_ERR_FORMAT, "codebook exceeds the 65535-entry limit of the blob format");
-    if (flags & kFlagLenTooLong) return fail(ctx, ACZ_ERR_FORMAT, "code length > 56 bits unsupported");
-
-    acz_gpu_blob* b = new (std::nothrow) acz_gpu_blob();
-    if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
-    rc = finish_encode(ctx, b, ctx->ws_sym, sym16, n, d_in, interval,
-                       predictor == ACZ_PRED_LORENZO2D, s);
-    if (rc) {
-        if (b->arena) cudaFreeAsync(b->arena, s);
-        delete b;
-        return rc;
-    }
-    acz_gpu_blob_info_t& in = b->info;
-    in.rank = rank;
-    for (uint32_t i = 0; i < rank; ++i) in.shape[i] = shape[i];
-    in.eb = eb;
-    in.quant_radius = quant_radius;
-    in.predictor = predictor;
-    in.element_count = n;
-    in.codebook_size = bi.book_size;
-    in.bit_length = bi.total_bits;
-    in.outlier_count = bi.n_escapes;
-    in.uncompressed_bytes = 4ull * n;
-    in.compressed_bytes = acz1_size(rank, bi.book_size, bi.total_bits, bi.n_escapes);
-    in.device_bytes = b->arena_bytes;
-    in.sidecar_bytes = sidecar_bytes(b->nchunks, b->side_outl != nullptr);
-    in.max_code_length = bi.max_len;
-    *out = b;
-    return ACZ_OK;
-}
-
-int acz_gpu_decompress(acz_gpu_ctx* ctx, const acz_gpu_blob* b, int zero_filter, float* d_out,
-                       void* stream) {
-    if (!ctx || !b || !d_out) return ACZ_ERR_INVALID;
-    ctx->err.clear();
+int decompress_on(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, int zero_filter,
+                  float* d_out, cudaStream_t s) {
+    if (!b || !d_out || !sl) return ACZ_ERR_INVALID;
     if (b->invalid) return fail(ctx, b->invalid, b->invalid_msg);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     const acz_gpu_blob_info_t& in = b->info;
     const PlaneGeom g = plane_geom(in.shape, in.rank);
     if (in.predictor == ACZ_PRED_LORENZO2D)
-        CK(grow(&ctx->ws_row, &ctx->ws_row_cap, 4ull * g.planes * g.cols));
+        CK(grow(&sl->ws_row, &sl->ws_row_cap, 4ull * g.planes * g.cols));
     DecodeArgs a;
     a.words = b->words;
     a.nwords = b->nwords;
@@ -605,12 +531,264 @@ int acz_gpu_decompress(acz_gpu_ctx* ctx, const acz_gpu_blob* b, int zero_filter,
     a.predictor = in.predictor;
     a.zero_filter = zero_filter;
     a.out = d_out;
-    a.row_scratch = static_cast<float*>(ctx->ws_row);
+    a.row_scratch = static_cast<float*>(sl->ws_row);
     {
         KTimer kt(ctx, ACZ_K_DECODE, s);
         CK(launch_decode(a, ctx->sms, s, &ctx->launches));
     }
     return ACZ_OK;
+}
+
+
+// State of a compress between its asynchronous first half (quantiser, histogram, codebook)
+// and its second half (blob sizing after the BookInfo read-back, encode).
+struct Plan {
+    uint64_t n = 0;
+    PlaneGeom g{};
+    uint32_t rank = 0;
+    uint64_t shape[ACZ_MAX_RANK] = {0};
+    double eb = 0;
+    uint32_t radius = 0, predictor = 0;
+    uint64_t interval = 0;
+    int sym16 = 0;
+    const float* d_in = nullptr;
+};
+
+int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t* shape,
+                   uint32_t rank, double eb, uint32_t quant_radius, uint32_t predictor,
+                   cudaStream_t s, Plan* pl) {
+    uint64_t n = 0;
+    int rc = validate_shape(ctx, shape, rank, &n);
+    if (rc) return rc;
+    if (n && !d_in) return fail(ctx, ACZ_ERR_INVALID, "null input");
+    if (predictor > 1) return fail(ctx, ACZ_ERR_PARAM, "unknown predictor");
+    if (!params_ok(eb, quant_radius)) {
+        // The reference builds the Tensor (finiteness check) before compress validates.
+        if (n) {
+            unsigned fl = 0;
+            rc = run_stats(ctx, d_in, n, nullptr, s, &fl, nullptr, nullptr);
+            if (rc) return rc;
+            if (fl & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
+        }
+        return fail(ctx, ACZ_ERR_PARAM, param_msg(eb));
+    }
+    if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "compress: empty tensor");
+    rc = ensure_small(ctx, sl);
+    if (rc) return rc;
+    const PlaneGeom g = plane_geom(shape, rank);
+    const uint32_t alphabet = 2u * quant_radius;
+    const uint64_t interval = predictor == ACZ_PRED_PREV ? sidecar_interval_default() : g.plane_size;
+    const uint64_t nchunks = (n + interval - 1) / interval;
+
+    CK(grow(&sl->ws_sym, &sl->ws_sym_cap, 4ull * n));
+    CK(grow(&sl->ws_side, &sl->ws_side_cap, 4ull * nchunks));
+    if (predictor == ACZ_PRED_LORENZO2D)
+        CK(grow(&sl->ws_row, &sl->ws_row_cap, 4ull * g.planes * g.cols));
+    sl->last_n = n;
+
+    SmallBlock* sm = sl->d_small;
+    CK(cudaMemsetAsync(&sm->flags, 0, sizeof(unsigned), s));
+    QuantArgs qa;
+    qa.x = d_in;
+    qa.g = g;
+    qa.eb = eb;
+    qa.step = 2.0 * eb;
+    qa.radius = quant_radius;
+    qa.predictor = predictor;
+    const int sym16 = (predictor == ACZ_PRED_PREV && quant_radius <= 32768) ? 1 : 0;
+    sl->last_sym16 = sym16 != 0;
+    qa.sym = sym16 ? nullptr : static_cast<uint32_t*>(sl->ws_sym);
+    qa.sym16 = sym16 ? static_cast<uint16_t*>(sl->ws_sym) : nullptr;
+    qa.side_state = static_cast<float*>(sl->ws_side);
+    qa.interval = interval;
+    qa.row_scratch = static_cast<float*>(sl->ws_row);
+    qa.flags = &sm->flags;
+    {
+        KTimer kt(ctx, ACZ_K_QUANT, s);
+        if (quant_spec_applicable(predictor, g.plane_size) && !std::getenv("ACZ_SERIAL_QUANT")) {
+            CK(grow(&sl->ws_qs, &sl->ws_qs_cap, quant_spec_scratch_bytes(g.planes, g.plane_size)));
+            CK(launch_quant_spec(qa, sl->ws_qs, s, &ctx->launches));
+        } else {
+            CK(launch_quant(qa, ctx->sms, s, &ctx->launches));
+        }
+    }
+    rc = build_book(ctx, sl, sl->ws_sym, sym16, n, alphabet, quant_radius, s);
+    if (rc) return rc;
+    pl->n = n;
+    pl->g = g;
+    pl->rank = rank;
+    for (uint32_t i = 0; i < rank; ++i) pl->shape[i] = shape[i];
+    pl->eb = eb;
+    pl->radius = quant_radius;
+    pl->predictor = predictor;
+    pl->interval = interval;
+    pl->sym16 = sym16;
+    pl->d_in = d_in;
+    return ACZ_OK;
+}
+
+int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz_gpu_blob** out) {
+    CK(cudaEventSynchronize(sl->ev_book));
+    const BookInfo bi = sl->h_small->info;
+    const unsigned flags = sl->h_small->flags | bi.flags;
+    // precedence follows the reference: Tensor ctor (DomainError), huffman_encode
+    // (DecodeError), then the codebook limit in compress (FormatError).
+    if (flags & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
+    if (flags & kFlagInternal) return fail(ctx, ACZ_ERR_CUDA, "internal: look-back timeout");
+    if (flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
+    if (bi.book_size > kMaxBook)
+        return fail(ctx, ACZ_ERR_FORMAT, "codebook exceeds the 65535-entry limit of the blob format");
+    if (flags & kFlagLenTooLong) return fail(ctx, ACZ_ERR_FORMAT, "code length > 56 bits unsupported");
+
+    acz_gpu_blob* b = new (std::nothrow) acz_gpu_blob();
+    if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
+    int rc = finish_encode(ctx, sl, b, sl->ws_sym, pl.sym16, pl.n, pl.d_in, pl.interval,
+                           pl.predictor == ACZ_PRED_LORENZO2D, s);
+    if (rc) {
+        if (b->arena) cudaFreeAsync(b->arena, s);
+        delete b;
+        return rc;
+    }
+    acz_gpu_blob_info_t& in = b->info;
+    in.rank = pl.rank;
+    for (uint32_t i = 0; i < pl.rank; ++i) in.shape[i] = pl.shape[i];
+    in.eb = pl.eb;
+    in.quant_radius = pl.radius;
+    in.predictor = pl.predictor;
+    in.element_count = pl.n;
+    in.codebook_size = bi.book_size;
+    in.bit_length = bi.total_bits;
+    in.outlier_count = bi.n_escapes;
+    in.uncompressed_bytes = 4ull * pl.n;
+    in.compressed_bytes = acz1_size(pl.rank, bi.book_size, bi.total_bits, bi.n_escapes);
+    in.device_bytes = b->arena_bytes;
+    in.sidecar_bytes = sidecar_bytes(b->nchunks, b->side_outl != nullptr);
+    in.max_code_length = bi.max_len;
+    *out = b;
+    return ACZ_OK;
+}
+
+// Internal streams for the batched entry points: fork from the caller's stream.
+int pool_fork(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
+    while (ctx->pool.size() < k) {
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev = nullptr;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        ctx->pool.push_back(st);
+        ctx->pool_ev.push_back(ev);
+    }
+    CK(cudaEventRecord(ctx->ev_fork, user));
+    for (size_t i = 0; i < k; ++i) CK(cudaStreamWaitEvent(ctx->pool[i], ctx->ev_fork, 0));
+    return ACZ_OK;
+}
+
+// Join: the caller's stream waits for the first k internal streams.
+int pool_join(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
+    for (size_t i = 0; i < k; ++i) {
+        CK(cudaEventRecord(ctx->pool_ev[i], ctx->pool[i]));
+        CK(cudaStreamWaitEvent(user, ctx->pool_ev[i], 0));
+    }
+    return ACZ_OK;
+}
+
+constexpr size_t kPoolStreams = 8;
+
+}  // namespace
+
+extern "C" {
+
+int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape, uint32_t rank,
+                     double eb, uint32_t quant_radius, uint32_t predictor, void* stream,
+                     acz_gpu_blob** out) {
+    if (!ctx || !out) return ACZ_ERR_INVALID;
+    *out = nullptr;
+    ctx->err.clear();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Slot* sl = get_slot(ctx, 0);
+    Plan pl;
+    int rc = compress_begin(ctx, sl, d_in, shape, rank, eb, quant_radius, predictor, s, &pl);
+    if (rc) return rc;
+    return compress_end(ctx, sl, pl, s, out);
+}
+
+int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const* d_in,
+                           const uint64_t* shapes, const uint32_t* ranks, double eb,
+                           uint32_t quant_radius, uint32_t predictor, void* stream,
+                           acz_gpu_blob** out, int* status) {
+    if (!ctx || !out || (count && (!d_in || !shapes || !ranks))) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    for (uint32_t i = 0; i < count; ++i) {
+        out[i] = nullptr;
+        if (status) status[i] = ACZ_OK;
+    }
+    if (count == 0) return ACZ_OK;
+    const size_t k = std::min<size_t>(count, kPoolStreams);
+    int rc = pool_fork(ctx, k, user);
+    if (rc) return rc;
+    std::vector<Plan> plans(count);
+    std::vector<int> st(count, ACZ_OK);
+    std::vector<size_t> off(count);
+    size_t o = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        off[i] = o;
+        o += ranks[i];
+    }
+    // first halves: every tensor's quantiser/histogram/codebook, round-robin over streams
+    for (uint32_t i = 0; i < count; ++i) {
+        Slot* sl = get_slot(ctx, i);
+        if (!sl) {
+            st[i] = ACZ_ERR_NOMEM;
+            continue;
+        }
+        st[i] = compress_begin(ctx, sl, d_in[i], shapes + off[i], ranks[i], eb, quant_radius,
+                               predictor, ctx->pool[i % k], &plans[i]);
+    }
+    // second halves in order: each waits only for its own codebook read-back
+    int first_err = ACZ_OK;
+    std::string first_msg;
+    for (uint32_t i = 0; i < count; ++i) {
+        if (st[i] == ACZ_OK)
+            st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], ctx->pool[i % k], &out[i]);
+        if (st[i] != ACZ_OK && first_err == ACZ_OK) {
+            first_err = st[i];
+            first_msg = ctx->err;
+        }
+        if (status) status[i] = st[i];
+    }
+    rc = pool_join(ctx, k, user);
+    if (rc) return rc;
+    if (first_err) ctx->err = first_msg;
+    return first_err;
+}
+
+int acz_gpu_decompress_batch(acz_gpu_ctx* ctx, uint32_t count, const acz_gpu_blob* const* blobs,
+                             int zero_filter, float* const* d_out, void* stream) {
+    if (!ctx || (count && (!blobs || !d_out))) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    if (count == 0) return ACZ_OK;
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    const size_t k = std::min<size_t>(count, kPoolStreams);
+    int rc = pool_fork(ctx, k, user);
+    if (rc) return rc;
+    int first_err = ACZ_OK;
+    for (uint32_t i = 0; i < count; ++i) {
+        rc = decompress_on(ctx, get_slot(ctx, i), blobs[i], zero_filter, d_out[i],
+                           ctx->pool[i % k]);
+        if (rc && first_err == ACZ_OK) first_err = rc;
+    }
+    rc = pool_join(ctx, k, user);
+    if (rc) return rc;
+    return first_err;
+}
+
+int acz_gpu_decompress(acz_gpu_ctx* ctx, const acz_gpu_blob* b, int zero_filter, float* d_out,
+                       void* stream) {
+    if (!ctx || !b || !d_out) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    return decompress_on(ctx, get_slot(ctx, 0), b, zero_filter, d_out,
+                         static_cast<cudaStream_t>(stream));
 }
 
 int acz_gpu_blob_info(const acz_gpu_blob* b, acz_gpu_blob_info_t* info) {
@@ -722,6 +900,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
                            const uint8_t* sidecar, uint64_t sidecar_size, void* stream,
                            acz_gpu_blob** out) {
     if (!ctx || !out || (!src && size)) return ACZ_ERR_INVALID;
+    Slot* sl = get_slot(ctx, 0);
     *out = nullptr;
     ctx->err.clear();
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -906,7 +1085,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
     CKB(grow(&ctx->ws_aux, &ctx->ws_aux_cap, aux));
     unsigned long long* plane_outl = static_cast<unsigned long long*>(ctx->ws_aux);
     uint32_t* syms = prev ? reinterpret_cast<uint32_t*>(plane_outl + g.planes + 1) : nullptr;
-    CKB(cudaMemsetAsync(&ctx->d_small->flags, 0, sizeof(unsigned), s));
+    CKB(cudaMemsetAsync(&sl->d_small->flags, 0, sizeof(unsigned), s));
     ScanArgs sa;
     sa.words = b->words;
     sa.nwords = nwords;
@@ -923,15 +1102,15 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
     sa.sym_out = syms;
     sa.plane_outl = plane_outl;
     sa.plane_size = g.plane_size;
-    sa.flags = &ctx->d_small->flags;
+    sa.flags = &sl->d_small->flags;
     {
         KTimer kt(ctx, ACZ_K_SCAN, s);
         CKB(launch_scan_decode(sa, s, &ctx->launches));
     }
-    CKB(cudaMemcpyAsync(&ctx->h_small->flags, &ctx->d_small->flags, sizeof(unsigned),
+    CKB(cudaMemcpyAsync(&sl->h_small->flags, &sl->d_small->flags, sizeof(unsigned),
                         cudaMemcpyDeviceToHost, s));
     CKB(cudaStreamSynchronize(s));
-    const unsigned fl = ctx->h_small->flags;
+    const unsigned fl = sl->h_small->flags;
     if (fl) {
         b->invalid = (fl & (kDecTruncated | kDecNoMatch)) ? ACZ_ERR_DECODE : ACZ_ERR_FORMAT;
         b->invalid_msg = (fl & kDecTruncated)        ? "truncated bitstream"
@@ -1073,6 +1252,7 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
                            uint64_t* bit_length, void* stream) {
     if (!ctx || !book_size || !bit_length) return ACZ_ERR_INVALID;
     ctx->err.clear();
+    Slot* sl = get_slot(ctx, 0);
     *book_size = 0;
     *bit_length = 0;
     if (n == 0) return ACZ_OK;  // ref src/huffman.cpp:108
@@ -1092,15 +1272,16 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
     }
     if (maxsym >= (1u << 26)) return fail(ctx, ACZ_ERR_PARAM, "symbol alphabet beyond 2^26 unsupported");
     const uint32_t alphabet = maxsym + 1;
-    int rc = build_book(ctx, d_symbols, 0, n, alphabet, 0, s);
+    int rc = build_book(ctx, sl, d_symbols, 0, n, alphabet, 0, s);
     if (rc) return rc;
-    const BookInfo bi = ctx->h_small->info;
+    CK(cudaEventSynchronize(sl->ev_book));
+    const BookInfo bi = sl->h_small->info;
     if (bi.flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
     if (bi.flags & kFlagLenTooLong) return fail(ctx, ACZ_ERR_FORMAT, "code length > 56 bits unsupported");
     if (bi.book_size > book_cap) return fail(ctx, ACZ_ERR_INVALID, "book capacity too small");
     if ((bi.total_bits + 7) / 8 > bits_cap) return fail(ctx, ACZ_ERR_INVALID, "bits capacity too small");
     acz_gpu_blob tmpb;
-    rc = finish_encode(ctx, &tmpb, d_symbols, 0, n, nullptr, 0, false, s);
+    rc = finish_encode(ctx, sl, &tmpb, d_symbols, 0, n, nullptr, 0, false, s);
     if (rc) {
         if (tmpb.arena) cudaFreeAsync(tmpb.arena, s);
         return rc;
@@ -1120,6 +1301,7 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
                            uint64_t count, uint32_t* d_out, void* stream) {
     if (!ctx) return ACZ_ERR_INVALID;
     ctx->err.clear();
+    Slot* sl = get_slot(ctx, 0);
     if (count == 0) return ACZ_OK;  // ref src/huffman.cpp:140
     if (book_size == 0) return fail(ctx, ACZ_ERR_DECODE, "empty codebook");
     for (uint32_t i = 1; i < book_size; ++i)
@@ -1142,7 +1324,7 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
     CK(cudaMemcpyAsync(tmpb.book_len, book_len, book_size, cudaMemcpyHostToDevice, s));
     CK(launch_build_tables(tmpb.book_sym, tmpb.book_len, book_size, tmpb.canon, tmpb.lut, nullptr,
                            s, &ctx->launches));
-    CK(cudaMemsetAsync(&ctx->d_small->flags, 0, sizeof(unsigned), s));
+    CK(cudaMemsetAsync(&sl->d_small->flags, 0, sizeof(unsigned), s));
     ScanArgs sa{};
     sa.words = tmpb.words;
     sa.nwords = nwords;
@@ -1159,13 +1341,13 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
     sa.sym_out = d_out;
     sa.plane_outl = nullptr;
     sa.plane_size = count;
-    sa.flags = &ctx->d_small->flags;
+    sa.flags = &sl->d_small->flags;
     CK(launch_scan_decode(sa, s, &ctx->launches));
-    CK(cudaMemcpyAsync(&ctx->h_small->flags, &ctx->d_small->flags, sizeof(unsigned),
+    CK(cudaMemcpyAsync(&sl->h_small->flags, &sl->d_small->flags, sizeof(unsigned),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaFreeAsync(tmpb.arena, s));
     CK(cudaStreamSynchronize(s));
-    const unsigned fl = ctx->h_small->flags;
+    const unsigned fl = sl->h_small->flags;
     if (fl & kDecTruncated) return fail(ctx, ACZ_ERR_DECODE, "truncated bitstream");
     if (fl & kDecNoMatch) return fail(ctx, ACZ_ERR_DECODE, "no codeword matches bitstream");
     return ACZ_OK;
@@ -1228,12 +1410,13 @@ int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int rese
 
 int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, void* stream) {
     if (!ctx || !d_out) return ACZ_ERR_INVALID;
-    if (n != ctx->last_n || !ctx->ws_sym) return fail(ctx, ACZ_ERR_SHAPE, "no symbols of that size");
-    if (ctx->last_sym16)
-        CK(launch_widen_u16(static_cast<const uint16_t*>(ctx->ws_sym), d_out, n, ctx->sms,
+    Slot* sl = get_slot(ctx, 0);
+    if (n != sl->last_n || !sl->ws_sym) return fail(ctx, ACZ_ERR_SHAPE, "no symbols of that size");
+    if (sl->last_sym16)
+        CK(launch_widen_u16(static_cast<const uint16_t*>(sl->ws_sym), d_out, n, ctx->sms,
                             static_cast<cudaStream_t>(stream), &ctx->launches));
     else
-        CK(cudaMemcpyAsync(d_out, ctx->ws_sym, 4ull * n, cudaMemcpyDeviceToDevice,
+        CK(cudaMemcpyAsync(d_out, sl->ws_sym, 4ull * n, cudaMemcpyDeviceToDevice,
                            static_cast<cudaStream_t>(stream)));
     return ACZ_OK;
 }
