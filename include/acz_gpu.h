@@ -183,6 +183,21 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
                            uint32_t book_size, const uint8_t* bits, uint64_t bit_length,
                            uint64_t count, uint32_t* d_out, void* stream);
 
+/* ---- device memory helpers for host layers that link only this library ---- */
+/* Stream-ordered allocation from the device's memory pool / release. */
+int acz_gpu_malloc(acz_gpu_ctx* ctx, uint64_t bytes, void* stream, void** d_ptr);
+int acz_gpu_free(acz_gpu_ctx* ctx, void* d_ptr, void* stream);
+#define ACZ_COPY_H2D 1
+#define ACZ_COPY_D2H 2
+#define ACZ_COPY_D2D 3
+int acz_gpu_memcpy(acz_gpu_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind,
+                   void* stream);
+int acz_gpu_stream_sync(acz_gpu_ctx* ctx, void* stream);
+/* In-place ReLU recompute x = x > 0 ? x : 0 (ref nn::recompute_relu,
+ * include/acz/nn/layers.hpp:152-157; the controller's relu-recompute zero restoration,
+ * src/controller.cpp:210-213,244). */
+int acz_gpu_relu(acz_gpu_ctx* ctx, float* d_x, uint64_t n, void* stream);
+
 /* ---- profiling ---- */
 /* Kernel classes timed by acz_gpu_profile_* (CUDA events on the launching stream). */
 #define ACZ_K_STATS 0     /* K1 zero bitmap / sparsity                     */
@@ -207,7 +222,8 @@ int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, vo
  * out[8..15]: codebook phase cycles (compaction, sort, rounds, depths, canonical, tables),
  * round count, calls; when n >= 20, out[16..19]: speculative-quantiser cycles summed over
  * segments (phase A, look-back wait, walk, output); when n >= 24, out[20..23]: decoder
- * cycles summed over warps (table prologue, stream staging, symbol loop) and warp count. */
+ * cycles summed over warps (table prologue, stream staging, symbol loop) and warp count;
+ * when n >= 26, out[24..25]: speculative-quantiser walk cycles in exact steps / batches. */
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset);
 /* Number of CUDA kernel launches issued by this context since creation. */
 uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx);

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "acz/codec.hpp"
+#include "acz/controller.hpp"
 #include "acz/error.hpp"
 #include "acz/huffman.hpp"
 #include "acz/tensor.hpp"
@@ -190,6 +191,50 @@ int ref_roundtrip_sharded(const float* x, const std::uint64_t* shape, int rank, 
         for (auto b : bytes) tot += b;
         *total_blob_bytes = tot;
         *seconds = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+// The UNMODIFIED reference controller (src/controller.cpp) on one layer: config knobs,
+// collection at iteration 0 with host activation/loss/momentum, then `wraps` forward
+// passes at iteration 1 (compress-or-pass-through + unwrap); returns the layer stats, the
+// window's bound and sigma, and the ledger CSV after finalize() (malloc'd).
+int ref_controller_run(std::int64_t W, double sigma_fraction, double coefficient_a,
+                       double eb_min, double eb_max, const float* act, const std::uint64_t* shape,
+                       int rank, const float* loss, std::uint64_t nloss, const float* mom,
+                       std::uint64_t nmom, std::uint64_t batch, int wraps, double* stats_out,
+                       char** csv, char* err, int errcap) {
+    return guarded(err, errcap, [&] {
+        acz::ControllerConfig cfg;
+        cfg.collect_interval = W;
+        cfg.sigma_fraction = sigma_fraction;
+        cfg.coefficient_a = coefficient_a;
+        cfg.eb_min = eb_min;
+        cfg.eb_max = eb_max;
+        acz::Controller c(cfg, 1);
+        const std::size_t n = volume(shape, rank);
+        acz::Tensor ta(to_shape(shape, rank), std::vector<float>(act, act + n));
+        acz::Tensor tl({static_cast<std::size_t>(nloss)}, std::vector<float>(loss, loss + nloss));
+        acz::Tensor tm({static_cast<std::size_t>(nmom)}, std::vector<float>(mom, mom + nmom));
+        c.begin_iteration(0);
+        acz::LayerStats st = c.collect_stats(0, ta, tl, tm, static_cast<std::size_t>(batch));
+        stats_out[0] = st.l_bar;
+        stats_out[1] = st.r;
+        stats_out[2] = st.m_avg;
+        stats_out[3] = st.degenerate ? 1.0 : 0.0;
+        c.begin_iteration(1);
+        stats_out[4] = c.layer_eb(0);
+        stats_out[5] = c.layer_active(0) ? 1.0 : 0.0;
+        for (int i = 0; i < wraps; ++i) {
+            acz::Tensor copy = ta;
+            acz::ActivationHandle h = c.wrap_forward(0, std::move(copy), true);
+            stats_out[6] = static_cast<double>(h.held_bytes);
+            acz::Tensor back = c.unwrap_backward(h);
+            (void)back;
+        }
+        c.finalize();
+        const std::string s = c.ledger().to_csv();
+        *csv = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(*csv, s.c_str(), s.size() + 1);
     });
 }
 

@@ -40,6 +40,11 @@ SIGNATURES = [
     ("acz_gpu_compress", C.c_int, [_vp, _vp, _u64p, C.c_uint32, C.c_double, C.c_uint32,
                                    C.c_uint32, _vp, C.POINTER(_vp)]),
     ("acz_gpu_decompress", C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
+    ("acz_gpu_malloc", C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_vp)]),
+    ("acz_gpu_free", C.c_int, [_vp, _vp, _vp]),
+    ("acz_gpu_memcpy", C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_int, _vp]),
+    ("acz_gpu_stream_sync", C.c_int, [_vp, _vp]),
+    ("acz_gpu_relu", C.c_int, [_vp, _vp, C.c_uint64, _vp]),
     ("acz_gpu_compress_batch", C.c_int, [_vp, C.c_uint32, C.POINTER(_vp), _u64p, _u32p,
                                          C.c_double, C.c_uint32, C.c_uint32, _vp,
                                          C.POINTER(_vp), C.POINTER(C.c_int)]),

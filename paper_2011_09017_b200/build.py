@@ -22,7 +22,8 @@ HEADERS = ["common.cuh", "internal.h"]
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+EXTRA = os.environ.get("ACZ_NVCC_EXTRA", "").split()
+FLAGS = EXTRA + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xptxas", "-warn-spills", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 
@@ -63,6 +64,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     return LIB
+
+
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_host.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "test_host")
+
+
+def build_cpp_test(force: bool = False) -> str:
+    """Builds the C++ host-layer test (cpp/acz_b200.hpp over libacz_gpu.so) with g++."""
+    hdr = os.path.join(HERE, "cpp", "acz_b200.hpp")
+    if (not force and os.path.exists(CPP_TEST_BIN)
+            and all(os.path.getmtime(CPP_TEST_BIN) > os.path.getmtime(d)
+                    for d in (CPP_TEST_SRC, hdr, LIB))):
+        return CPP_TEST_BIN
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
+           f"-I{os.path.join(HERE, 'cpp')}", CPP_TEST_SRC, "-o", CPP_TEST_BIN, f"-L{LIBDIR}",
+           "-lacz_gpu", "-Wl,-rpath,$ORIGIN/../../paper_2011_09017_b200/lib"]
+    subprocess.run(cmd, check=True)
+    return CPP_TEST_BIN
 
 
 if __name__ == "__main__":

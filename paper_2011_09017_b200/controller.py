@@ -1,0 +1,354 @@
+"""Adaptive error-bound controller for PyTorch training (host side, ref
+proj/core/include/acz/controller.hpp:14-155, src/controller.cpp:14-253), mirroring the C++
+controller of cpp/acz_b200.hpp.
+
+Four phases (section 4): every W iterations collect L_bar (mean |loss gradient|),
+R (nonzero ratio of the activation) and M_avg (mean |momentum|) per layer; derive
+sigma = sigma_fraction * M_avg; invert the estimator into eb = sigma / (a * L_bar *
+sqrt(N * R)) clamped to [eb_min, eb_max]; compress every stashed activation of the layer
+with that bound until the next collection (the collection iteration itself and degenerate
+windows pass through).
+
+Multi-GPU: data-parallel ranks compress their own activations with no
+collective on the data path. The statistics become global with ONE all-reduce of 7 doubles
+per layer every W iterations (sums of |loss|, loss count, nonzeros, activation count,
+|momentum|, momentum count, batch) -- :class:`DistributedStats`. The batch-size scheme of
+BASELINE config 5 (not implemented by the reference) is
+:func:`suggest_batch`.
+"""
+from __future__ import annotations
+
+import math
+import sys
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+from . import codec as _codec
+
+ZERO_FILTER = "codec-filter"
+RELU_RECOMPUTE = "relu-recompute"
+
+
+@dataclass
+class ControllerConfig:
+    collect_interval: int = 1000     # W
+    sigma_fraction: float = 0.01
+    coefficient_a: float = 0.32
+    eb_min: float = 1e-8
+    eb_max: float = 1e-1
+    zero_restoration: str = ZERO_FILTER
+    predictor: int = 0
+    quant_radius: int = 32768
+
+    def validate(self) -> None:
+        """ref src/controller.cpp:14-21"""
+        if self.collect_interval < 1:
+            raise _codec.ParamError("collect_interval (W) must be >= 1")
+        if not self.sigma_fraction > 0.0:
+            raise _codec.ParamError("sigma_fraction must be positive")
+        if not self.coefficient_a > 0.0:
+            raise _codec.ParamError("coefficient_a must be positive")
+        if not (self.eb_min > 0.0 and self.eb_min <= self.eb_max):
+            raise _codec.ParamError("error-bound clamps must satisfy 0 < eb_min <= eb_max")
+        if self.zero_restoration not in (ZERO_FILTER, RELU_RECOMPUTE):
+            raise _codec.ParamError("zero_restoration must be codec-filter or relu-recompute")
+        _codec.CodecParams(self.eb_min, self.quant_radius, self.predictor).validate()
+
+
+@dataclass
+class LayerStats:
+    layer_id: int = -1
+    l_bar: float = 0.0
+    r: float = 0.0
+    m_avg: float = 0.0
+    batch: int = 0
+    collected_at: int = -1
+    degenerate: bool = False
+
+
+@dataclass
+class LedgerRecord:
+    iteration: int
+    layer_id: int
+    eb: float
+    predicted_sigma: float
+    l_bar: float
+    r: float
+    m_avg: float
+    ratio: float
+    fallback: bool
+
+
+class CompressionLedger:
+    def __init__(self):
+        self.records: List[LedgerRecord] = []
+
+    def append(self, r: LedgerRecord) -> None:
+        self.records.append(r)
+
+    def to_csv(self) -> str:
+        """ref src/controller.cpp:67-76 (same header, %.17g formatting)."""
+        out = ["iteration,layer,eb,predicted_sigma,L_bar,R,M_avg,ratio,fallback_flag\n"]
+        for r in self.records:
+            out.append("%d,%d,%.17g,%.17g,%.17g,%.17g,%.17g,%.17g,%d\n" % (
+                r.iteration, r.layer_id, r.eb, r.predicted_sigma, r.l_bar, r.r, r.m_avg, r.ratio,
+                1 if r.fallback else 0))
+        return "".join(out)
+
+
+@dataclass
+class ActivationHandle:
+    """Exactly one of raw / blob is engaged (ref include/acz/controller.hpp:65-78)."""
+    raw: object = None
+    blob: Optional[_codec.CompressedTensor] = None
+    apply_relu: bool = False
+    zero_filter: bool = False
+    layer_id: int = -1
+    held_bytes: int = 0
+    achieved_ratio: float = 1.0
+
+
+@dataclass
+class _Window:
+    stats: LayerStats = field(default_factory=LayerStats)
+    eb: float = 0.0
+    sigma: float = 0.0
+    fallback: bool = True
+    open: bool = False
+    bytes_in: int = 0
+    bytes_stored: int = 0
+
+
+def local_stat_sums(activation, loss, momentum, batch: int) -> List[float]:
+    """The 7 per-layer sums of one rank: sum|loss|, #loss, #nonzero(act), #act, sum|mom|,
+    #mom, batch. CUDA tensors go through the codec's GPU statistics kernels (K1); CPU tensors
+    (tests, CPU ranks) are summed in double by torch."""
+    import torch
+    if activation.is_cuda:
+        nz = int(_codec.zero_bitmap(activation)[1])
+        la = _codec.mean_abs(loss) * loss.numel()
+        ma = _codec.mean_abs(momentum) * momentum.numel()
+    else:
+        nz = int(torch.count_nonzero(activation).item())
+        la = float(loss.detach().double().abs().sum().item())
+        ma = float(momentum.detach().double().abs().sum().item())
+    return [la, float(loss.numel()), float(nz), float(activation.numel()), ma,
+            float(momentum.numel()), float(batch)]
+
+
+class DistributedStats:
+    """Sum-reduces the 7 statistics sums over the data-parallel group (torch.distributed;
+    NCCL on GPUs, gloo on CPU): the only collective of the compressor."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def __call__(self, sums: List[float]) -> List[float]:
+        import torch
+        import torch.distributed as dist
+        if not (dist.is_available() and dist.is_initialized()):
+            return sums
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor(sums, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return [float(v) for v in t.cpu().tolist()]
+
+
+class Controller:
+    """ref src/controller.cpp:94-253 over torch CUDA activations."""
+
+    def __init__(self, cfg: ControllerConfig, num_layers: int,
+                 reducer: Optional[Callable[[List[float]], List[float]]] = None,
+                 ctx: Optional[_codec.Context] = None):
+        cfg.validate()
+        if num_layers < 0:
+            raise _codec.ParamError("controller needs a non-negative layer count")
+        self.cfg = cfg
+        self.reducer = reducer
+        self.ctx = ctx
+        self.windows = [_Window() for _ in range(num_layers)]
+        self.ledger = CompressionLedger()
+        self.iteration = 0
+        self.current_bytes = 0
+        self.peak_bytes = 0
+        self.total_in = 0
+        self.total_stored = 0
+
+    # ---- phases 1-3 ----------------------------------------------------------------
+    def begin_iteration(self, iteration: int) -> None:
+        if iteration < 0:
+            raise _codec.ParamError("iteration must be >= 0")
+        self.iteration = iteration
+
+    def collecting(self) -> bool:
+        return self.iteration % self.cfg.collect_interval == 0
+
+    def collect_stats(self, layer: int, activation, loss, momentum, batch: int) -> LayerStats:
+        """ref src/controller.cpp:124-152 (global over ranks when a reducer is set)."""
+        return self.collect_stats_from_sums(layer, local_stat_sums(activation, loss, momentum,
+                                                                   batch))
+
+    def collect_stats_from_sums(self, layer: int, sums: List[float]) -> LayerStats:
+        if not 0 <= layer < len(self.windows):
+            raise _codec.ParamError("collect_stats: unknown layer id")
+        if not self.collecting():
+            raise _codec.ParamError("collect_stats invoked outside a collection iteration")
+        if self.reducer is not None:
+            sums = self.reducer(list(sums))
+        st = LayerStats(layer_id=layer,
+                        l_bar=sums[0] / sums[1] if sums[1] > 0 else 0.0,
+                        r=sums[2] / sums[3] if sums[3] > 0 else 0.0,
+                        m_avg=sums[4] / sums[5] if sums[5] > 0 else 0.0,
+                        batch=int(sums[6]), collected_at=self.iteration)
+        st.degenerate = st.l_bar == 0.0 or st.m_avg == 0.0 or st.r == 0.0
+        self._close_window(layer)
+        w = _Window(stats=st, open=True)
+        if not st.degenerate:
+            w.sigma = self.target_sigma(st, self.cfg)
+            w.eb = self.compute_error_bound(st, w.sigma, self.cfg)
+            w.fallback = False
+        self.windows[layer] = w
+        return st
+
+    @staticmethod
+    def target_sigma(st: LayerStats, cfg: ControllerConfig) -> float:
+        if not st.m_avg > 0.0:
+            raise _codec.ParamError("target_sigma: degenerate M_avg")
+        return cfg.sigma_fraction * st.m_avg
+
+    @staticmethod
+    def compute_error_bound(st: LayerStats, sigma: float, cfg: ControllerConfig) -> float:
+        if not sigma > 0.0:
+            raise _codec.ParamError("compute_error_bound: sigma must be positive")
+        if not (st.l_bar > 0.0 and st.r > 0.0):
+            raise _codec.ParamError("compute_error_bound: degenerate stats")
+        eb = sigma / (cfg.coefficient_a * st.l_bar * math.sqrt(float(st.batch) * st.r))
+        return min(max(eb, cfg.eb_min), cfg.eb_max)
+
+    def layer_active(self, layer: int) -> bool:
+        if not 0 <= layer < len(self.windows):
+            return False
+        w = self.windows[layer]
+        return w.open and not w.fallback and self.iteration > w.stats.collected_at
+
+    def layer_eb(self, layer: int) -> float:
+        return self.windows[layer].eb if self.layer_active(layer) else 0.0
+
+    # ---- phase 4 -----------------------------------------------------------------------
+    def wrap_forward(self, layer: int, activation, is_post_relu: bool) -> ActivationHandle:
+        """ref src/controller.cpp:194-232: compress on the GPU or pass through; codec
+        failures degrade to pass-through with a warning."""
+        if not 0 <= layer < len(self.windows):
+            raise _codec.ParamError("wrap_forward: unknown layer id")
+        in_bytes = activation.numel() * 4
+        h = ActivationHandle(layer_id=layer)
+        if not self.layer_active(layer):
+            h.raw, h.held_bytes = activation, in_bytes
+        else:
+            w = self.windows[layer]
+            try:
+                c = _codec.compress(activation, _codec.CodecParams(w.eb, self.cfg.quant_radius,
+                                                                   self.cfg.predictor),
+                                    ctx=self.ctx)
+                h.blob, h.held_bytes = c, c.compressed_bytes
+                h.achieved_ratio = _codec.compression_ratio(c)
+                if self.cfg.zero_restoration == RELU_RECOMPUTE and is_post_relu:
+                    h.apply_relu = True
+                else:
+                    h.zero_filter = True
+            except _codec.Error as e:
+                print(f"warning: compression failed for layer {layer} ({e}); passing through",
+                      file=sys.stderr)
+                h.raw, h.held_bytes = activation, in_bytes
+        w = self.windows[layer]
+        if w.open:
+            w.bytes_in += in_bytes
+            w.bytes_stored += h.held_bytes
+        self.total_in += in_bytes
+        self.total_stored += h.held_bytes
+        self.current_bytes += h.held_bytes
+        self.peak_bytes = max(self.peak_bytes, self.current_bytes)
+        return h
+
+    def unwrap_backward(self, h: ActivationHandle):
+        """ref src/controller.cpp:234-249"""
+        if h.raw is not None:
+            t, h.raw = h.raw, None
+        elif h.blob is not None:
+            t = _codec.decompress(h.blob, zero_filter=h.zero_filter)
+            if h.apply_relu:
+                t.clamp_(min=0.0)  # nn::recompute_relu (layers.hpp:152-157)
+            h.blob = None
+        else:
+            raise _codec.ParamError("unwrap_backward: handle already consumed")
+        self.current_bytes -= h.held_bytes
+        h.held_bytes = 0
+        return t
+
+    def finalize(self) -> None:
+        for i in range(len(self.windows)):
+            self._close_window(i)
+
+    def _close_window(self, layer: int) -> None:
+        """ref src/controller.cpp:98-122"""
+        w = self.windows[layer]
+        if not w.open:
+            return
+        self.ledger.append(LedgerRecord(
+            iteration=w.stats.collected_at, layer_id=layer, eb=0.0 if w.fallback else w.eb,
+            predicted_sigma=0.0 if w.fallback else w.sigma, l_bar=w.stats.l_bar, r=w.stats.r,
+            m_avg=w.stats.m_avg,
+            ratio=1.0 if w.bytes_stored == 0 else w.bytes_in / w.bytes_stored,
+            fallback=w.fallback))
+        w.open = False
+
+
+def suggest_batch(batch: int, peak_stash_bytes: int, budget_bytes: int, granularity: int = 8,
+                  max_batch: int = 1 << 20) -> int:
+    """Batch-size scheme (BASELINE config 5): the largest batch whose
+    stashed activation bytes fit the budget, from the stash measured at `batch`."""
+    if batch <= 0 or peak_stash_bytes <= 0:
+        return batch
+    b = int(budget_bytes / (peak_stash_bytes / batch))
+    b = (b // granularity) * granularity
+    return max(granularity, min(b, max_batch))
+
+
+class SavedActivationHooks:
+    """torch.autograd.graph.saved_tensors_hooks that route every fp32 CUDA tensor autograd
+    saves (conv inputs, post-ReLU activations) through the controller: layer ids are the
+    save order within an iteration (call :meth:`new_iteration` each step)."""
+
+    def __init__(self, controller: Controller, min_numel: int = 1 << 14):
+        self.ctl = controller
+        self.min_numel = min_numel
+        self.next_layer = 0
+
+    def new_iteration(self, iteration: int) -> None:
+        self.ctl.begin_iteration(iteration)
+        self.next_layer = 0
+
+    def pack(self, t):
+        import torch
+        if not (t.is_cuda and t.dtype == torch.float32 and t.numel() >= self.min_numel
+                and t.is_contiguous() and self.next_layer < len(self.ctl.windows)):
+            return ("raw", t)
+        layer = self.next_layer
+        self.next_layer += 1
+        post_relu = bool(t.min().item() >= 0) if self.ctl.cfg.zero_restoration == RELU_RECOMPUTE else False
+        return ("acz", self.ctl.wrap_forward(layer, t.detach(), post_relu))
+
+    def unpack(self, packed):
+        kind, v = packed
+        if kind == "raw":
+            return v
+        return self.ctl.unwrap_backward(v)
+
+    def __enter__(self):
+        import torch
+        self._cm = torch.autograd.graph.saved_tensors_hooks(self.pack, self.unpack)
+        self._cm.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        return self._cm.__exit__(*exc)

@@ -1353,6 +1353,46 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
     return ACZ_OK;
 }
 
+// ------------------------------------------------------------------ memory helpers --
+int acz_gpu_malloc(acz_gpu_ctx* ctx, uint64_t bytes, void* stream, void** d_ptr) {
+    if (!ctx || !d_ptr) return ACZ_ERR_INVALID;
+    *d_ptr = nullptr;
+    if (bytes == 0) return ACZ_OK;
+    cudaError_t e = cudaMallocAsync(d_ptr, bytes, static_cast<cudaStream_t>(stream));
+    if (e == cudaErrorMemoryAllocation) return fail(ctx, ACZ_ERR_NOMEM, "device allocation failed");
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaMallocAsync");
+    return ACZ_OK;
+}
+
+int acz_gpu_free(acz_gpu_ctx* ctx, void* d_ptr, void* stream) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    if (d_ptr) CK(cudaFreeAsync(d_ptr, static_cast<cudaStream_t>(stream)));
+    return ACZ_OK;
+}
+
+int acz_gpu_memcpy(acz_gpu_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind,
+                   void* stream) {
+    if (!ctx || (bytes && (!dst || !src))) return ACZ_ERR_INVALID;
+    const cudaMemcpyKind k = kind == ACZ_COPY_H2D   ? cudaMemcpyHostToDevice
+                             : kind == ACZ_COPY_D2H ? cudaMemcpyDeviceToHost
+                             : kind == ACZ_COPY_D2D ? cudaMemcpyDeviceToDevice
+                                                    : cudaMemcpyDefault;
+    if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, k, static_cast<cudaStream_t>(stream)));
+    return ACZ_OK;
+}
+
+int acz_gpu_stream_sync(acz_gpu_ctx* ctx, void* stream) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return ACZ_OK;
+}
+
+int acz_gpu_relu(acz_gpu_ctx* ctx, float* d_x, uint64_t n, void* stream) {
+    if (!ctx || (n && !d_x)) return ACZ_ERR_INVALID;
+    if (n) CK(launch_relu(d_x, n, ctx->sms, static_cast<cudaStream_t>(stream), &ctx->launches));
+    return ACZ_OK;
+}
+
 // ----------------------------------------------------------------------- profiling --
 int acz_gpu_profile_enable(acz_gpu_ctx* ctx, int on) {
     if (!ctx) return ACZ_ERR_INVALID;
@@ -1390,7 +1430,7 @@ int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches) {
 // --------------------------------------------------------------------------- debug --
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset) {
     if (!ctx || !out || n < 8) return ACZ_ERR_INVALID;
-    unsigned long long v[12];
+    unsigned long long v[16];
     CK(quant_spec_stats(v, reset != 0));
     for (int i = 0; i < 8; ++i) out[i] = v[i];
     if (n >= 16) {
@@ -1405,6 +1445,8 @@ int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int rese
         CK(decode_stats(d, reset != 0));
         for (int i = 0; i < 4; ++i) out[20 + i] = d[i];
     }
+    if (n >= 26)
+        for (int i = 0; i < 2; ++i) out[24 + i] = v[12 + i];
     return ACZ_OK;
 }
 

@@ -33,6 +33,7 @@ cudaError_t launch_stats(const float* x, uint64_t n, uint32_t* bitmap,
                          unsigned long long* d_nnz, unsigned int* d_flags, double* d_sumabs,
                          int sms, cudaStream_t s, uint64_t* launches);
 
+cudaError_t launch_relu(float* x, uint64_t n, int sms, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_widen_u16(const uint16_t* a, uint32_t* b, uint64_t n, int sms, cudaStream_t s,
                              uint64_t* launches);
 

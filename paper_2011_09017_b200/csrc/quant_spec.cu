@@ -25,6 +25,8 @@
 //   re-speculates the remaining ranges from the exact state ("rebase").
 // Segments of one plane chain their exact exit states through a decoupled look-back in
 // ticket order (deadlock-free).
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace acz_b200 {
@@ -32,7 +34,10 @@ namespace acz_b200 {
 namespace {
 
 constexpr int kW = 32;
-constexpr int kL = 64;
+#ifndef ACZ_SPEC_L
+#define ACZ_SPEC_L 64
+#endif
+constexpr int kL = ACZ_SPEC_L;  // lane window (elements); a segment is 32 lane windows
 constexpr int kSeg = kW * kL;
 constexpr int kExt = 2 * kL;
 constexpr int kCap = kSeg + kExt;
@@ -45,7 +50,7 @@ constexpr int kLev = 3;                // fine offset levels (binades below the 
 __device__ unsigned long long g_qstats[8];
 // per-phase SM cycles summed over segments (debug): geometry+phase A, look-back wait,
 // walk, exit+store
-__device__ unsigned long long g_qclk[4];
+__device__ unsigned long long g_qclk[8];  // + [4] exact-step cycles, [5] batch cycles
 
 struct SP {
     double eb, step, inv_step, radius_d, Tmax;
@@ -287,7 +292,7 @@ __device__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int k0, double l
 // #(|x| >= 2^e) >= max(1, nonzero/32). Writes B to *out (one CTA; every thread issues its
 // 16 sample loads before using any, so the kernel costs ~one memory round trip).
 __global__ void __launch_bounds__(1024) k_anchor_binade(const float* __restrict__ x, uint64_t n,
-                                                       int* out) {
+                                                       unsigned qdiv, int* out) {
     __shared__ unsigned cnt[300];
     for (int i = threadIdx.x; i < 300; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(1024) k_anchor_binade(const float* __restrict_
     if (threadIdx.x == 0) {
         unsigned tot = 0;
         for (int i = 0; i < 300; ++i) tot += cnt[i];
-        const unsigned need = tot / 32 > 0 ? tot / 32 : 1;
+        const unsigned need = tot / qdiv > 0 ? tot / qdiv : 1;
         unsigned acc = 0;
         int B = -126;
         for (int i = 299; i >= 0; --i) {
@@ -557,7 +562,15 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     };
     auto is_coll = [&](int c) { return S.sym[c] != 0 && fabs((double)S.s[c]) < p.eb; };
 
+    long long tw = clock64();
+    int wmode = -1;  // 0 exact, 1 batch
     while (pos < len) {
+        {
+            const long long t = clock64();
+            if (lane == 0 && wmode >= 0) atomicAdd(&g_qclk[4 + wmode], (unsigned long long)(t - tw));
+            tw = t;
+            wmode = exact_mode ? 0 : 1;
+        }
         if (exact_mode) {
             if (lane == 0) atomicAdd(&g_qstats[2], 1ull);
             const int k = range_of(pos);
@@ -789,7 +802,12 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     float* exits = reinterpret_cast<float*>(sc + 256 + ((4 * total + 255) & ~255ull));
     cudaError_t e = cudaMemsetAsync(sc, 0, 256 + ((4 * total + 255) & ~255ull), s);
     if (e != cudaSuccess) return e;
-    k_anchor_binade<<<1, 1024, 0, s>>>(a.x, a.g.n, dB);
+    static const unsigned qdiv = [] {
+        const char* e = std::getenv("ACZ_ANCHOR_Q");
+        const unsigned v = e ? (unsigned)std::strtoul(e, nullptr, 10) : 0u;
+        return v >= 2 ? v : 32u;
+    }();
+    k_anchor_binade<<<1, 1024, 0, s>>>(a.x, a.g.n, qdiv, dB);
     ++*launches;
     if (a.sym16)
         k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym16, a.side_state,
@@ -803,7 +821,7 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
 
 cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
     cudaError_t e = cudaMemcpyFromSymbol(out, g_qstats, sizeof(g_qstats));
-    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 8, g_qclk, sizeof(g_qclk));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 8, g_qclk, sizeof(g_qclk));  // 8 values
     if (e == cudaSuccess && reset) {
         unsigned long long z[8] = {0};
         e = cudaMemcpyToSymbol(g_qstats, z, sizeof(z));

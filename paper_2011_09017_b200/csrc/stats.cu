@@ -78,7 +78,21 @@ __global__ void k_widen_u16(const uint16_t* __restrict__ a, uint32_t* __restrict
         b[i] = a[i];
 }
 
+__global__ void k_relu(float* __restrict__ x, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = x[i];
+        x[i] = v > 0.0f ? v : 0.0f;  // ref include/acz/nn/layers.hpp:134-157 (NaN -> 0)
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_relu(float* x, uint64_t n, int sms, cudaStream_t s, uint64_t* launches) {
+    k_relu<<<(unsigned)(sms * 8), 256, 0, s>>>(x, n);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_widen_u16(const uint16_t* a, uint32_t* b, uint64_t n, int sms, cudaStream_t s,
                              uint64_t* launches) {

@@ -48,3 +48,11 @@ def test_no_oracle_in_product_path():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace(
                     "oracle/", ""), f
+
+
+def test_cpp_host_layer_builds():
+    """The C++ host layer (reference signatures over the C-ABI) compiles and links."""
+    from paper_2011_09017_b200 import build as B
+    B.build()
+    exe = B.build_cpp_test()
+    assert os.path.exists(exe)
