@@ -452,6 +452,67 @@ def decompress_host(blob: bytes, n: int, zero_filter: bool = False,
     return out
 
 
+def compress_host_many(hosts: Sequence, p: CodecParams = CodecParams(), blob_bufs=None,
+                       side_bufs=None, ctx: Optional[Context] = None, stream=None):
+    """Batched host-buffer compress: host fp32 tensors in (page-locked torch tensors copy at
+    full PCIe speed), ACZ1 bytes + decode sidecars out. The H2D copies, the batched kernels
+    and the D2H copies are stream-ordered; blob_bufs / side_bufs (optional, page-locked
+    torch uint8 tensors) receive the bytes. Returns [(blob view, sidecar view)] as numpy
+    uint8 arrays."""
+    import torch
+    ctx = ctx or default_context()
+    dev = torch.device("cuda", ctx.device)
+    s = stream or torch.cuda.current_stream(dev)
+    with torch.cuda.stream(s):
+        ds = [torch.as_tensor(h).to(dev, non_blocking=True) for h in hosts]
+        blobs = compress_many(ds, p, stream=s, ctx=ctx)
+    lib = _native.load()
+    out = []
+    for i, c in enumerate(blobs):
+        nb, ns = c.compressed_bytes, c.sidecar_bytes
+        bb = blob_bufs[i] if blob_bufs is not None else torch.empty(nb, dtype=torch.uint8,
+                                                                     pin_memory=True)
+        sb = side_bufs[i] if side_bufs is not None else torch.empty(ns, dtype=torch.uint8,
+                                                                     pin_memory=True)
+        if bb.numel() < nb or sb.numel() < ns:
+            raise ValueError("host buffer too small")
+        _check(lib.acz_gpu_blob_to_host(ctx.handle, c._h, C.c_void_p(bb.data_ptr()), nb, None,
+                                        _stream_handle(s)), ctx)
+        _check(lib.acz_gpu_sidecar_to_host(ctx.handle, c._h, C.c_void_p(sb.data_ptr()), ns, None,
+                                           _stream_handle(s)), ctx)
+        out.append((bb[:nb].numpy(), sb[:ns].numpy()))
+    return out
+
+
+def decompress_host_many(blobs, zero_filter: bool = False, outs=None,
+                         ctx: Optional[Context] = None, stream=None):
+    """Batched host-buffer decompress: [(ACZ1 bytes, sidecar or None)] (numpy uint8 views of
+    page-locked memory copy at full PCIe speed) in, host fp32 tensors out (outs: optional
+    page-locked torch tensors). Parses + validates like ref blob_from_bytes."""
+    import torch
+    ctx = ctx or default_context()
+    dev = torch.device("cuda", ctx.device)
+    s = stream or torch.cuda.current_stream(dev)
+    lib = _native.load()
+    cts = []
+    for blob, side in blobs:
+        blob = np.ascontiguousarray(blob, dtype=np.uint8)
+        h = C.c_void_p()
+        sp = C.c_void_p(side.ctypes.data) if side is not None and len(side) else None
+        _check(lib.acz_gpu_blob_from_host(ctx.handle, C.c_void_p(blob.ctypes.data), blob.size, sp,
+                                          len(side) if sp is not None else 0, _stream_handle(s),
+                                          C.byref(h)), ctx)
+        cts.append(CompressedTensor(h, ctx))
+    with torch.cuda.stream(s):
+        douts = decompress_many(cts, zero_filter=zero_filter, stream=s)
+        if outs is None:
+            outs = [torch.empty(o.shape, dtype=torch.float32, pin_memory=True) for o in douts]
+        for o, d in zip(outs, douts):
+            o.view(d.shape).copy_(d, non_blocking=True)
+    s.synchronize()
+    return outs
+
+
 # --------------------------------------------------------------------- statistics ----
 def zero_bitmap(t, stream=None, ctx: Optional[Context] = None):
     """Fused zero-bitmap + sparsity pass: returns (int32 CUDA tensor of ceil(n/32)
