@@ -745,10 +745,13 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
         st[i] = compress_begin(ctx, sl, d_in[i], shapes + off[i], ranks[i], eb, quant_radius,
                                predictor, ctx->pool[i % k], &plans[i]);
     }
-    // second halves in order: each waits only for its own codebook read-back
+    // second halves in completion order: a tensor's encode is launched as soon as its own
+    // codebook read-back has landed, so short tensors do not queue behind a long quantiser
     int first_err = ACZ_OK;
     std::string first_msg;
-    for (uint32_t i = 0; i < count; ++i) {
+    std::vector<char> done(count, 0);
+    uint32_t remaining = count;
+    auto finish = [&](uint32_t i) {
         if (st[i] == ACZ_OK)
             st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], ctx->pool[i % k], &out[i]);
         if (st[i] != ACZ_OK && first_err == ACZ_OK) {
@@ -756,6 +759,26 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
             first_msg = ctx->err;
         }
         if (status) status[i] = st[i];
+        done[i] = 1;
+        --remaining;
+    };
+    while (remaining) {
+        bool progressed = false;
+        for (uint32_t i = 0; i < count; ++i) {
+            if (done[i]) continue;
+            if (st[i] != ACZ_OK || cudaEventQuery(get_slot(ctx, i)->ev_book) != cudaErrorNotReady) {
+                finish(i);
+                progressed = true;
+            }
+        }
+        if (!progressed) {
+            // nothing ready yet: block on the first pending tensor
+            for (uint32_t i = 0; i < count; ++i)
+                if (!done[i]) {
+                    finish(i);
+                    break;
+                }
+        }
     }
     rc = pool_join(ctx, k, user);
     if (rc) return rc;
