@@ -189,10 +189,21 @@ def run_ours(args, rank, world, local_rank):
     kms = (C.c_double * 7)()
     kn = (C.c_uint64 * 7)()
     lib.acz_gpu_profile_read(ctx.handle, kms, kn)
-    lib.acz_gpu_profile_enable(ctx.handle, 0)
     kclass = ["stats", "quant", "histogram", "codebook", "encode", "decode", "scan"]
     kern = {kclass[i]: {"ms_per_step": kms[i] / prof_steps, "launches_per_step": kn[i] / prof_steps}
             for i in range(7) if kn[i]}
+    # per-tensor, per-class times (tensors one at a time, so every launch is timed alone):
+    # the dominant single kernel of the step for the roofline
+    per_tensor = []
+    for nm, x, o in zip(names, tensors, outs):
+        lib.acz_gpu_profile_enable(ctx.handle, 1)
+        c = acz.compress(x, params, stream=stream, ctx=ctx)
+        acz.decompress(c, zero_filter=True, out=o, stream=stream)
+        torch.cuda.synchronize()
+        lib.acz_gpu_profile_read(ctx.handle, kms, kn)
+        per_tensor.append((nm, x.numel(), c.compressed_bytes,
+                           {kclass[i]: kms[i] for i in range(7) if kn[i]}))
+    lib.acz_gpu_profile_enable(ctx.handle, 0)
 
     # per-tensor detail (one extra pass, not timed)
     detail = []
@@ -207,7 +218,7 @@ def run_ours(args, rank, world, local_rank):
 
     res = dict(value=value, ms_per_step=ms_max / args.steps, n=n_total, cbytes=cbytes,
                B_step=8 * n_total + 2 * cbytes, launches=launches, clocks=clk, kernels=kern,
-               detail=detail, ratio=ratios_in / ratios_out, batch=batch)
+               detail=detail, ratio=ratios_in / ratios_out, batch=batch, per_tensor=per_tensor)
 
     # ---- e2e through the public host-buffer API (page-locked host memory in and out) ----
     if not args.no_e2e and rank == 0:
@@ -324,14 +335,23 @@ def main():
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         peak, kind = load_peaks()
-        # dominant kernel roofline: algorithmic bytes per launch / average launch time
-        kern = res["kernels"]
-        dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
-        n, C = res["n"], res["cbytes"]
-        alg = {"quant": 4 * n, "histogram": 4 * n, "encode": 4 * n + C, "decode": C + 4 * n,
-               "codebook": 0, "stats": 4 * n, "scan": C}
-        dms = kern[dom]["ms_per_step"]
-        achieved = alg.get(dom, 0) / (dms * 1e-3) / 1e9 if dms > 0 else 0.0
+        # roofline of the dominant single kernel launch of the step: algorithmic bytes of
+        # that launch (quantiser reads 4n, histogram reads the symbols, encode
+        # writes C, decode reads C and writes 4n) / its event-timed duration
+        alg_of = {"quant": lambda n, C: 4 * n, "histogram": lambda n, C: 2 * n,
+                  "encode": lambda n, C: 2 * n + C, "decode": lambda n, C: C + 4 * n,
+                  "codebook": lambda n, C: 0, "stats": lambda n, C: 4 * n}
+        best = max(((nm, n_t, C_t, cls, ms) for nm, n_t, C_t, d in res["per_tensor"]
+                    for cls, ms in d.items()), key=lambda r: r[4])
+        dnm, dn, dC, dom, dms = best
+        dalg = alg_of.get(dom, lambda n, C: 0)(dn, dC)
+        achieved = dalg / (dms * 1e-3) / 1e9 if dms > 0 else 0.0
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01", "v3", "traffic.json")) as f:
+                traffic = json.load(f)["dram_bytes_per_launch"]
+        except Exception:  # noqa: BLE001
+            traffic = None
         line = {
             "metric": "compress+decompress GB/s per B200 at eb=1e-3 (% of HBM peak); compression ratio",
             "value": res["value"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -344,10 +364,11 @@ def main():
                        "basis": "B = 8n + 2C algorithmic bytes per round trip"},
             "pct_hbm": res["value"] / world / peak,
             "compression_ratio": res["ratio"],
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                         "peak_kind": kind,
-                         "algorithmic_bytes_per_step": alg.get(dom, 0),
+            "roofline": {"bound": "hbm", "kernel": f"{dom} ({dnm})", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_kind": kind,
+                         "algorithmic_bytes_per_launch": dalg, "launch_ms": dms,
+                         "traffic_source": "profiles/r01/v3/traffic.json (ncu --set full)",
                          "roundtrip_frac": res["value"] / world / peak},
             "kernels": kern,
             "gpu_launches": res["launches"],
