@@ -124,6 +124,16 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
                            const uint64_t* shapes, const uint32_t* ranks, double eb,
                            uint32_t quant_radius, uint32_t predictor, void* stream,
                            acz_gpu_blob** out, int* status);
+/* Batched compress of host tensors (page-locked buffers upload at full PCIe speed): each
+ * tensor's upload and kernels run on its own internal stream, so compression of tensor i
+ * overlaps the upload of tensor i+1; the ACZ1 bytes (and, when sidecar[i] is non-NULL, the
+ * decode sidecar) are written to the caller's buffers. Synchronous on return. */
+int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const* h_in,
+                                const uint64_t* shapes, const uint32_t* ranks, double eb,
+                                uint32_t quant_radius, uint32_t predictor, uint8_t* const* acz1,
+                                const uint64_t* acz1_cap, uint64_t* acz1_size,
+                                uint8_t* const* sidecar, const uint64_t* sidecar_cap,
+                                uint64_t* sidecar_size, int* status);
 /* Batched decompress (ref Controller::unwrap_backward src/controller.cpp:234-249 for every
  * handle of a step), stream-ordered on `stream` through the internal streams. */
 int acz_gpu_decompress_batch(acz_gpu_ctx* ctx, uint32_t count, const acz_gpu_blob* const* blobs,

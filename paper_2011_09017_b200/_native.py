@@ -48,6 +48,10 @@ SIGNATURES = [
     ("acz_gpu_compress_batch", C.c_int, [_vp, C.c_uint32, C.POINTER(_vp), _u64p, _u32p,
                                          C.c_double, C.c_uint32, C.c_uint32, _vp,
                                          C.POINTER(_vp), C.POINTER(C.c_int)]),
+    ("acz_gpu_compress_host_batch", C.c_int, [_vp, C.c_uint32, C.POINTER(_vp), _u64p, _u32p,
+                                              C.c_double, C.c_uint32, C.c_uint32, C.POINTER(_vp),
+                                              _u64p, _u64p, C.POINTER(_vp), _u64p, _u64p,
+                                              C.POINTER(C.c_int)]),
     ("acz_gpu_decompress_batch", C.c_int, [_vp, C.c_uint32, C.POINTER(_vp), C.c_int,
                                            C.POINTER(_vp), _vp]),
     ("acz_gpu_blob_info", C.c_int, [_vp, C.POINTER(BlobInfo)]),

@@ -454,63 +454,82 @@ def decompress_host(blob: bytes, n: int, zero_filter: bool = False,
 
 def compress_host_many(hosts: Sequence, p: CodecParams = CodecParams(), blob_bufs=None,
                        side_bufs=None, ctx: Optional[Context] = None, stream=None):
-    """Batched host-buffer compress: host fp32 tensors in (page-locked torch tensors copy at
-    full PCIe speed), ACZ1 bytes + decode sidecars out. The H2D copies, the batched kernels
-    and the D2H copies are stream-ordered; blob_bufs / side_bufs (optional, page-locked
-    torch uint8 tensors) receive the bytes. Returns [(blob view, sidecar view)] as numpy
-    uint8 arrays."""
+    """Host-buffer compress of a whole activation set (acz_gpu_compress_host_batch): host
+    fp32 tensors in (page-locked torch tensors upload at full PCIe speed), ACZ1 bytes +
+    decode sidecars out. Each tensor's upload and kernels run on its own stream, so the
+    compression of tensor i overlaps the upload of tensor i+1. blob_bufs / side_bufs
+    (optional page-locked torch uint8 tensors; default: allocated at 5 B / element) receive
+    the bytes. Returns [(ACZ1 view, sidecar view)] as numpy uint8 arrays."""
     import torch
     ctx = ctx or default_context()
-    dev = torch.device("cuda", ctx.device)
-    s = stream or torch.cuda.current_stream(dev)
-    with torch.cuda.stream(s):
-        ds = [torch.as_tensor(h).to(dev, non_blocking=True) for h in hosts]
-        blobs = compress_many(ds, p, stream=s, ctx=ctx)
-    lib = _native.load()
-    out = []
-    for i, c in enumerate(blobs):
-        nb, ns = c.compressed_bytes, c.sidecar_bytes
-        bb = blob_bufs[i] if blob_bufs is not None else torch.empty(nb, dtype=torch.uint8,
-                                                                     pin_memory=True)
-        sb = side_bufs[i] if side_bufs is not None else torch.empty(ns, dtype=torch.uint8,
-                                                                     pin_memory=True)
-        if bb.numel() < nb or sb.numel() < ns:
-            raise ValueError("host buffer too small")
-        _check(lib.acz_gpu_blob_to_host(ctx.handle, c._h, C.c_void_p(bb.data_ptr()), nb, None,
-                                        _stream_handle(s)), ctx)
-        _check(lib.acz_gpu_sidecar_to_host(ctx.handle, c._h, C.c_void_p(sb.data_ptr()), ns, None,
-                                           _stream_handle(s)), ctx)
-        out.append((bb[:nb].numpy(), sb[:ns].numpy()))
-    return out
+    if stream is not None:
+        stream.synchronize()
+    hs = [torch.as_tensor(h) for h in hosts]
+    k = len(hs)
+    if k == 0:
+        return []
+    for h in hs:
+        if h.dtype != torch.float32 or not h.is_contiguous() or h.is_cuda:
+            raise ValueError("host tensors must be contiguous fp32 CPU tensors")
+    if blob_bufs is None:
+        blob_bufs = [torch.empty(5 * h.numel() + (1 << 20), dtype=torch.uint8, pin_memory=True)
+                     for h in hs]
+    if side_bufs is None:
+        side_bufs = [torch.empty(h.numel() // 8 + (1 << 20), dtype=torch.uint8, pin_memory=True)
+                     for h in hs]
+    ptrs = (C.c_void_p * k)(*[h.data_ptr() for h in hs])
+    ranks = (C.c_uint32 * k)(*[h.dim() for h in hs])
+    flat = [int(e) for h in hs for e in h.shape]
+    shapes = (C.c_uint64 * max(1, len(flat)))(*flat)
+    bp = (C.c_void_p * k)(*[b.data_ptr() for b in blob_bufs])
+    bc = (C.c_uint64 * k)(*[b.numel() for b in blob_bufs])
+    bs = (C.c_uint64 * k)()
+    sp = (C.c_void_p * k)(*[b.data_ptr() for b in side_bufs])
+    sc = (C.c_uint64 * k)(*[b.numel() for b in side_bufs])
+    ss = (C.c_uint64 * k)()
+    st = (C.c_int * k)()
+    rc = _native.load().acz_gpu_compress_host_batch(ctx.handle, k, ptrs, shapes, ranks,
+                                                    float(p.eb), int(p.quant_radius),
+                                                    int(p.predictor), bp, bc, bs, sp, sc, ss, st)
+    _check(rc, ctx)
+    return [(blob_bufs[i][:bs[i]].numpy(), side_bufs[i][:ss[i]].numpy()) for i in range(k)]
 
 
 def decompress_host_many(blobs, zero_filter: bool = False, outs=None,
                          ctx: Optional[Context] = None, stream=None):
-    """Batched host-buffer decompress: [(ACZ1 bytes, sidecar or None)] (numpy uint8 views of
-    page-locked memory copy at full PCIe speed) in, host fp32 tensors out (outs: optional
-    page-locked torch tensors). Parses + validates like ref blob_from_bytes."""
+    """Host-buffer decompress of a whole activation set: [(ACZ1 bytes, sidecar or None)]
+    (numpy uint8 views of page-locked memory copy at full PCIe speed) in, host fp32 tensors
+    out (outs: optional page-locked torch tensors). Parses + validates like ref
+    blob_from_bytes. Pipelined across tensors: tensor i's reconstruction is copied back to
+    the host on a copy stream while tensor i+1 is uploaded and decoded."""
     import torch
     ctx = ctx or default_context()
     dev = torch.device("cuda", ctx.device)
     s = stream or torch.cuda.current_stream(dev)
+    cin = torch.cuda.Stream(dev)   # uploads (blob_from_host waits for its own copies only)
+    cout = torch.cuda.Stream(dev)  # downloads: overlap the next tensor's upload (full duplex)
+    cin.wait_stream(s)
     lib = _native.load()
-    cts = []
-    for blob, side in blobs:
+    res = []
+    for i, (blob, side) in enumerate(blobs):
         blob = np.ascontiguousarray(blob, dtype=np.uint8)
         h = C.c_void_p()
         sp = C.c_void_p(side.ctypes.data) if side is not None and len(side) else None
         _check(lib.acz_gpu_blob_from_host(ctx.handle, C.c_void_p(blob.ctypes.data), blob.size, sp,
-                                          len(side) if sp is not None else 0, _stream_handle(s),
+                                          len(side) if sp is not None else 0, _stream_handle(cin),
                                           C.byref(h)), ctx)
-        cts.append(CompressedTensor(h, ctx))
-    with torch.cuda.stream(s):
-        douts = decompress_many(cts, zero_filter=zero_filter, stream=s)
-        if outs is None:
-            outs = [torch.empty(o.shape, dtype=torch.float32, pin_memory=True) for o in douts]
-        for o, d in zip(outs, douts):
+        s.wait_stream(cin)  # the blob's device copy is complete (blob_from_host synchronised)
+        c = CompressedTensor(h, ctx)
+        d = decompress(c, zero_filter=zero_filter, stream=s)
+        o = outs[i] if outs is not None else torch.empty(tuple(c.shape), dtype=torch.float32,
+                                                         pin_memory=True)
+        cout.wait_stream(s)
+        d.record_stream(cout)
+        with torch.cuda.stream(cout):
             o.view(d.shape).copy_(d, non_blocking=True)
-    s.synchronize()
-    return outs
+        res.append(o)
+    cout.synchronize()
+    return res
 
 
 # --------------------------------------------------------------------- statistics ----

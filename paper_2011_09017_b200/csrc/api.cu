@@ -55,6 +55,8 @@ struct Slot {
     size_t ws_side_cap = 0;
     void* ws_qs = nullptr;  // speculative quantiser scratch (look-back status, anchors)
     size_t ws_qs_cap = 0;
+    void* ws_in = nullptr;  // device copy of a host input (host-buffer batched compress)
+    size_t ws_in_cap = 0;
     SmallBlock* d_small = nullptr;
     SmallBlock* h_small = nullptr;  // pinned mirror
     cudaEvent_t ev_book = nullptr;  // recorded after the codebook read-back
@@ -304,7 +306,7 @@ Slot* get_slot(acz_gpu_ctx* ctx, size_t i) {
 void free_slot(Slot* sl) {
     if (!sl) return;
     for (void* p : {sl->ws_sym, sl->ws_hist, sl->ws_enc, sl->ws_cb, sl->ws_status, sl->ws_row,
-                    sl->ws_book, sl->ws_side, sl->ws_qs})
+                    sl->ws_book, sl->ws_side, sl->ws_qs, sl->ws_in})
         if (p) cudaFree(p);
     if (sl->d_small) cudaFree(sl->d_small);
     if (sl->h_small) cudaFreeHost(sl->h_small);
@@ -781,6 +783,94 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
         }
     }
     rc = pool_join(ctx, k, user);
+    if (rc) return rc;
+    if (first_err) ctx->err = first_msg;
+    return first_err;
+}
+
+int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const* h_in,
+                                const uint64_t* shapes, const uint32_t* ranks, double eb,
+                                uint32_t quant_radius, uint32_t predictor, uint8_t* const* acz1,
+                                const uint64_t* acz1_cap, uint64_t* acz1_size,
+                                uint8_t* const* sidecar, const uint64_t* sidecar_cap,
+                                uint64_t* sidecar_size, int* status) {
+    if (!ctx || (count && (!h_in || !shapes || !ranks || !acz1 || !acz1_cap || !acz1_size)))
+        return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    if (count == 0) return ACZ_OK;
+    const size_t k = std::min<size_t>(count, kPoolStreams);
+    int rc = pool_fork(ctx, k, ctx->own);
+    if (rc) return rc;
+    std::vector<Plan> plans(count);
+    std::vector<int> st(count, ACZ_OK);
+    size_t o = 0;
+    // upload + first half per tensor on its own stream: tensor i's quantiser starts as soon as
+    // its own input has landed, while later inputs are still crossing PCIe
+    for (uint32_t i = 0; i < count; ++i) {
+        const uint64_t* shp = shapes + o;
+        o += ranks[i];
+        Slot* sl = get_slot(ctx, i);
+        cudaStream_t s = ctx->pool[i % k];
+        uint64_t n = 0;
+        st[i] = sl ? validate_shape(ctx, shp, ranks[i], &n) : ACZ_ERR_NOMEM;
+        if (st[i] == ACZ_OK && n) {
+            cudaError_t e = grow(&sl->ws_in, &sl->ws_in_cap, 4ull * n);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(sl->ws_in, h_in[i], 4ull * n,
+                                                      cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) st[i] = cuda_fail(ctx, e, "host input upload");
+        }
+        if (st[i] == ACZ_OK)
+            st[i] = compress_begin(ctx, sl, static_cast<const float*>(sl->ws_in), shp, ranks[i],
+                                   eb, quant_radius, predictor, s, &plans[i]);
+    }
+    // second halves in completion order, then the bytes back to the host
+    int first_err = ACZ_OK;
+    std::string first_msg;
+    std::vector<char> done(count, 0);
+    uint32_t remaining = count;
+    auto finish = [&](uint32_t i) {
+        cudaStream_t s = ctx->pool[i % k];
+        acz_gpu_blob* b = nullptr;
+        if (st[i] == ACZ_OK) st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], s, &b);
+        if (st[i] == ACZ_OK) {
+            if (acz1_cap[i] < b->info.compressed_bytes)
+                st[i] = fail(ctx, ACZ_ERR_INVALID, "ACZ1 destination too small");
+            else
+                st[i] = acz_gpu_blob_to_host(ctx, b, acz1[i], acz1_cap[i], &acz1_size[i], s);
+        }
+        if (st[i] == ACZ_OK && sidecar && sidecar[i]) {
+            if (!sidecar_cap || sidecar_cap[i] < b->info.sidecar_bytes)
+                st[i] = fail(ctx, ACZ_ERR_INVALID, "sidecar destination too small");
+            else
+                st[i] = acz_gpu_sidecar_to_host(ctx, b, sidecar[i], sidecar_cap[i],
+                                                sidecar_size ? &sidecar_size[i] : nullptr, s);
+        }
+        if (b) acz_gpu_blob_free(b);
+        if (st[i] != ACZ_OK && first_err == ACZ_OK) {
+            first_err = st[i];
+            first_msg = ctx->err;
+        }
+        if (status) status[i] = st[i];
+        done[i] = 1;
+        --remaining;
+    };
+    while (remaining) {
+        bool progressed = false;
+        for (uint32_t i = 0; i < count; ++i) {
+            if (done[i]) continue;
+            if (st[i] != ACZ_OK || cudaEventQuery(get_slot(ctx, i)->ev_book) != cudaErrorNotReady) {
+                finish(i);
+                progressed = true;
+            }
+        }
+        if (!progressed)
+            for (uint32_t i = 0; i < count; ++i)
+                if (!done[i]) {
+                    finish(i);
+                    break;
+                }
+    }
+    rc = pool_join(ctx, k, ctx->own);
     if (rc) return rc;
     if (first_err) ctx->err = first_msg;
     return first_err;

@@ -1,0 +1,19 @@
+"""Raw H2D / D2H bandwidth with page-locked buffers (ceiling of the e2e path)."""
+import torch, time
+n = 256 << 20
+h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+d = torch.empty(n, dtype=torch.uint8, device="cuda")
+for name, f in [("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))]:
+    f(); torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(10): f()
+    torch.cuda.synchronize()
+    print(name, "%.1f GB/s" % (10 * n / (time.perf_counter() - t) / 1e9))
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True); d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+torch.cuda.synchronize(); t = time.perf_counter()
+for _ in range(10):
+    with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize()
+print("bidirectional %.1f GB/s total" % (20 * n / (time.perf_counter() - t) / 1e9))
