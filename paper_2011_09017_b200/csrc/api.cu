@@ -1558,7 +1558,9 @@ int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int rese
         CK(decode_stats(d, reset != 0));
         for (int i = 0; i < 4; ++i) out[20 + i] = d[i];
     }
-    if (n >= 26)
+    if (n >= 28)
+        for (int i = 0; i < 4; ++i) out[24 + i] = v[12 + i];
+    else if (n >= 26)
         for (int i = 0; i < 2; ++i) out[24 + i] = v[12 + i];
     return ACZ_OK;
 }
