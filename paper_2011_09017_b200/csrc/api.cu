@@ -607,7 +607,7 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     qa.flags = &sm->flags;
     {
         KTimer kt(ctx, ACZ_K_QUANT, s);
-        if (quant_spec_applicable(predictor, g.plane_size) && !std::getenv("ACZ_SERIAL_QUANT")) {
+        if (quant_spec_applicable(predictor, g.plane_size, g.planes, ctx->sms)) {
             CK(grow(&sl->ws_qs, &sl->ws_qs_cap, quant_spec_scratch_bytes(g.planes, g.plane_size)));
             CK(launch_quant_spec(qa, sl->ws_qs, s, &ctx->launches));
         } else {

@@ -835,8 +835,20 @@ size_t quant_spec_scratch_bytes(uint64_t planes, uint64_t plane_size) {
     return 256 + 2 * ((4 * total + 255) & ~255ull);
 }
 
-bool quant_spec_applicable(uint32_t predictor, uint64_t plane_size) {
-    return predictor == ACZ_PRED_PREV && plane_size > 1024;
+// Speculative (K2b) vs thread-per-plane (K2a) quantiser, by a cost model calibrated on B200
+// (profiles/r01/v3): K2a is latency-bound at ~330 cycles per element step while there are few
+// planes per SM, else throughput-bound at ~1.2 SM-cycles per element; K2b costs ~25 SM-cycles
+// per element. K2b therefore wins only when planes are long AND few (e.g. 768 planes of 227^2:
+// AlexNet conv1), K2a for many planes (56^2 / 224^2 activation maps at training batch sizes).
+// ACZ_SPEC_QUANT=1 / ACZ_SERIAL_QUANT=1 force either.
+bool quant_spec_applicable(uint32_t predictor, uint64_t plane_size, uint64_t planes, int sms) {
+    if (predictor != ACZ_PRED_PREV || plane_size <= 1024) return false;
+    if (std::getenv("ACZ_SERIAL_QUANT")) return false;
+    if (std::getenv("ACZ_SPEC_QUANT")) return true;
+    const double n = (double)plane_size * (double)planes;
+    const double t_serial = fmax((double)plane_size * 330.0, n * 1.2 / sms);
+    const double t_spec = n * 25.0 / sms;
+    return t_spec < t_serial;
 }
 
 }  // namespace acz_b200

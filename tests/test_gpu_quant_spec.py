@@ -11,6 +11,15 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(scope="module", autouse=True)
+def force_spec():
+    # these cases exercise the speculative kernel itself, whatever the cost model would pick
+    import os
+    os.environ["ACZ_SPEC_QUANT"] = "1"
+    yield
+    del os.environ["ACZ_SPEC_QUANT"]
+
+
 @pytest.fixture(scope="module")
 def acz(gpu_lib):
     import torch
