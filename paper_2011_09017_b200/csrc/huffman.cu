@@ -1053,21 +1053,24 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     const uint64_t span = (tiles + gridDim.x - 1) / gridDim.x;
     const uint64_t tb = (uint64_t)blockIdx.x * span, te = min(tiles, tb + span);
     const bool vec_ok = (reinterpret_cast<uintptr_t>(symp) & 15) == 0;
-    auto load8 = [&](uint64_t my0, uint32_t* sy) {
+    // kEncPer consecutive symbols of one thread (128-bit loads when aligned and complete)
+    auto load_syms = [&](uint64_t my0, uint32_t* sy) {
         if (vec_ok && my0 + kEncPer <= a.n) {
-            if (sizeof(SymT) == 2) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(symp + my0));
+            const uint4* v4 = reinterpret_cast<const uint4*>(symp + my0);
+            constexpr int per16 = 16 / (int)sizeof(SymT);
+#pragma unroll
+            for (int q = 0; q < kEncPer / per16; ++q) {
+                const uint4 v = __ldg(v4 + q);
                 const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    sy[2 * k] = w4[k] & 0xFFFFu;
-                    sy[2 * k + 1] = w4[k] >> 16;
+                    if (sizeof(SymT) == 2) {
+                        sy[q * 8 + 2 * k] = w4[k] & 0xFFFFu;
+                        sy[q * 8 + 2 * k + 1] = w4[k] >> 16;
+                    } else {
+                        sy[q * 4 + k] = w4[k];
+                    }
                 }
-            } else {
-                const uint4* v4 = reinterpret_cast<const uint4*>(symp + my0);
-                const uint4 v0 = __ldg(v4), v1 = __ldg(v4 + 1);
-                sy[0] = v0.x; sy[1] = v0.y; sy[2] = v0.z; sy[3] = v0.w;
-                sy[4] = v1.x; sy[5] = v1.y; sy[6] = v1.z; sy[7] = v1.w;
             }
         } else {
 #pragma unroll
@@ -1080,7 +1083,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     for (uint64_t t = tb; t < te; ++t) {
         const uint64_t my0 = t * kEncTile + (uint64_t)tid * kEncPer;
         uint32_t sy[kEncPer];
-        load8(my0, sy);
+        load_syms(my0, sy);
         uint32_t bsum = 0, esum = 0;
 #pragma unroll
         for (int i = 0; i < kEncPer; ++i) {
@@ -1180,7 +1183,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     for (uint64_t t = tb; t < te; ++t) {
         const uint64_t my0 = t * kEncTile + (uint64_t)tid * kEncPer;
         uint32_t sy[kEncPer];
-        load8(my0, sy);
+        load_syms(my0, sy);
         unsigned long long code[kEncPer];
         uint32_t my_bits = 0, my_esc = 0, escmask = 0;
 #pragma unroll
