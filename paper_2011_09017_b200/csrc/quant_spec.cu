@@ -120,8 +120,7 @@ __device__ __forceinline__ float lattice_guess(double lam, float xa, const SP& p
 }
 
 template <typename SymT>
-struct Smem {
-    float xs[kWin];       // staged input window (plane index j*kSeg - 1 + i)
+struct alignas(16) Smem {
     float s[kCap];
     SymT sym[kCap];
     uint32_t abits[kSeg / 32];  // anchor bitmap of the segment's nominal span
@@ -137,6 +136,17 @@ struct Smem {
     double C[kW];         // prefix of (send[k-1] - guess[k])
     int nr;
     int forced[kW];       // range start is not an anchor-aligned guess
+    // staged input window (plane index j*kSeg - 1 + i); LAST: everything before it is the
+    // segment state the decoupled phase-A kernel persists for the walk kernel
+    float xs[kWin];
+};
+
+// Per-segment header of the decoupled path (phase-A kernel -> walk kernel).
+struct SegHdr {
+    int64_t xbase;
+    uint64_t seg0;
+    int len, xoff;
+    int pad[2];
 };
 
 // Phase A, pass 1: the speculative chain over range k from its guess (one lane per range):
@@ -352,38 +362,37 @@ __device__ __forceinline__ uint64_t seg_bound_w(const float* xs, int64_t xbase, 
     return a < e ? a + 1 : e;
 }
 
-template <typename SymT>
-__global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, SP p, const int* dB,
-                                                   SymT* __restrict__ sym_out,
-                                                   float* __restrict__ side_state,
-                                                   unsigned int* __restrict__ status,
-                                                   float* __restrict__ exits,
-                                                   unsigned int* ticket, unsigned int* flags,
-                                                   unsigned long long total_segs) {
-    __shared__ Smem<SymT> S;
-    __shared__ unsigned s_tk;
-    const int lane = threadIdx.x;
-    {
-        const int B = *dB;
-        p.B = B;
-        p.anchor_min = ldexpf(1.0f, B) * (1.0f + 1.0f / 64.0f);
-        p.Tmax = fmin(ldexp(1.0, B - 23) * 32.0, p.eb / 8.0);
-    }
-    QParams qp;
+// Derived parameters (anchor binade B from k_anchor_binade).
+__device__ __forceinline__ void spec_params(SP& p, QParams& qp, const int* dB) {
+    const int B = *dB;
+    p.B = B;
+    p.anchor_min = ldexpf(1.0f, B) * (1.0f + 1.0f / 64.0f);
+    p.Tmax = fmin(ldexp(1.0, B - 23) * 32.0, p.eb / 8.0);
     qp.eb = p.eb;
     qp.step = p.step;
     qp.inv_step = p.inv_step;
     qp.radius_d = p.radius_d;
     qp.R = p.R;
     qp.exact_div = p.exact_div;
-    if (lane == 0) s_tk = atomicAdd(ticket, 1u);
-    __syncwarp();
-    const unsigned long long seg_id = s_tk;
-    if (seg_id >= total_segs) return;
-    // segment-major order: all planes' segment j before any segment j+1, so a segment's
-    // predecessor (same plane, j-1) always holds an earlier ticket and is usually done
-    const uint64_t j = seg_id / p.planes, plane = seg_id % p.planes;
-    const uint64_t sidx = plane * p.nseg + j;  // status/exit slot
+}
+
+constexpr int kFused = 0;  // one kernel, segments chained by a decoupled look-back
+constexpr int kFront = 1;  // phase A only; the segment state is persisted to `store`
+constexpr int kBack = 2;   // walk only, from the persisted state and the given entry state
+
+// One segment (plane, j) of the speculative quantiser. Returns the exit state (kBack).
+template <typename SymT, int MODE>
+__device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const SP& p,
+                              const QParams& qp, uint64_t plane, uint64_t j,
+                              SymT* __restrict__ sym_out, float* __restrict__ side_state,
+                              unsigned int* __restrict__ status, float* __restrict__ exits,
+                              unsigned int* flags, unsigned char* store, float tin_given) {
+    const int lane = threadIdx.x;
+    const uint64_t sidx = plane * p.nseg + j;  // status/exit/store slot
+    constexpr size_t kState = offsetof(Smem<SymT>, xs);
+    constexpr size_t kStore = ((kState + 15) / 16) * 16 + sizeof(SegHdr);
+    SegHdr* hdr = store ? reinterpret_cast<SegHdr*>(store + sidx * kStore + ((kState + 15) / 16) * 16)
+                        : nullptr;
     const float* xp = x + plane * p.P;
     const uint64_t plane_flat0 = plane * p.P;
     long long tck = clock64();
@@ -407,12 +416,28 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     __syncwarp();
 
     // ---- segment geometry -------------------------------------------------------
-    const uint64_t b0 = seg_bound_w(S.xs, xbase, j, p);      // first range start
-    const uint64_t b1 = seg_bound_w(S.xs, xbase, j + 1, p);  // next segment's first start
-    const int xoff = (int)((int64_t)b0 - xbase);            // xs index of segment position 0
+    uint64_t b0, b1;
+    if (MODE == kBack) {
+        b0 = hdr->seg0;
+        b1 = b0 + (uint64_t)max(0, hdr->len);
+        if (hdr->len <= 0) return tin_given;  // empty segment: state passes through
+    } else {
+        b0 = seg_bound_w(S.xs, xbase, j, p);      // first range start
+        b1 = seg_bound_w(S.xs, xbase, j + 1, p);  // next segment's first start
+    }
+    const int xoff = (int)((int64_t)b0 - xbase);  // xs index of segment position 0
     const uint64_t seg0 = b0;
     const int len = (int)(b1 - b0);
-    if (len <= 0) {
+    if (MODE == kFront && len <= 0) {
+        if (lane == 0) {
+            hdr->xbase = xbase;
+            hdr->seg0 = b0;
+            hdr->len = 0;
+            hdr->xoff = xoff;
+        }
+        return 0.0f;
+    }
+    if (MODE == kFused && len <= 0) {
         // empty segment (plane too short for this index): pass the state through
         if (lane == 0) {
             float tin = 0.0f;
@@ -433,8 +458,19 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             __threadfence();
             atomicExch(status + sidx, 1u);
         }
-        return;
+        return 0.0f;
     }
+    if (MODE == kBack) {
+        // restore the persisted segment state (everything before xs)
+        const uint4* src = reinterpret_cast<const uint4*>(store + sidx * kStore);
+        uint4* dst = reinterpret_cast<uint4*>(&S);
+        for (int i = lane; i < (int)(kState / 16); i += kW) dst[i] = __ldcs(src + i);
+        if (lane < (int)((kState % 16) / 4)) {
+            const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src + kState / 16);
+            reinterpret_cast<uint32_t*>(dst + kState / 16)[lane] = s32[lane];
+        }
+        __syncwarp();
+    } else {
     // lane windows: lane l > 0 starts after the first anchor in
     // [max(j*Seg + l*L, b0), j*Seg + (l+1)*L) if that start lies before b1
     {
@@ -504,11 +540,28 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
 
     // ---- phase A: speculate all ranges (lattice origin 0: plane-start lattice) ----
     phase_a(S, xoff, seg0, 0, 0.0, false, 0.0f, p, qp, plane_flat0, flags, len);
+    }  // !kBack
 
     tphase(0);
-    // ---- entry state from the predecessor segment (decoupled look-back) ----------
-    float tin = 0.0f;
-    if (j > 0) {
+    if (MODE == kFront) {
+        // persist the segment state for the walk kernel (coalesced 16-byte stores)
+        const uint4* src = reinterpret_cast<const uint4*>(&S);
+        uint4* dst = reinterpret_cast<uint4*>(store + sidx * kStore);
+        for (int i = lane; i < (int)(kState / 16); i += kW) __stcs(dst + i, src[i]);
+        if (lane < (int)((kState % 16) / 4))
+            reinterpret_cast<uint32_t*>(dst + kState / 16)[lane] =
+                reinterpret_cast<const uint32_t*>(src + kState / 16)[lane];
+        if (lane == 0) {
+            hdr->xbase = xbase;
+            hdr->seg0 = seg0;
+            hdr->len = len;
+            hdr->xoff = xoff;
+        }
+        return 0.0f;
+    }
+    // ---- entry state from the predecessor segment ----------------------------------
+    float tin = tin_given;
+    if (MODE == kFused && j > 0) {
         if (lane == 0) {
             volatile unsigned* vf = status + sidx - 1;
             unsigned long long spins = 0;
@@ -764,7 +817,7 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
             texit = __double2float_rn(__dadd_rn((double)S.s[last], Dl));
         }
     }
-    if (lane == 0) {
+    if (MODE == kFused && lane == 0) {
         exits[sidx] = texit;
         __threadfence();
         atomicExch(status + sidx, 1u);
@@ -773,9 +826,76 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     SymT* so = sym_out + plane_flat0 + seg0;
     for (int i = lane; i < len; i += kW) so[i] = S.sym[i];
     tphase(3);
+    return texit;
+}
+
+template <typename SymT>
+__global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, SP p, const int* dB,
+                                                   SymT* __restrict__ sym_out,
+                                                   float* __restrict__ side_state,
+                                                   unsigned int* __restrict__ status,
+                                                   float* __restrict__ exits,
+                                                   unsigned int* ticket, unsigned int* flags,
+                                                   unsigned long long total_segs) {
+    __shared__ Smem<SymT> S;
+    __shared__ unsigned s_tk;
+    QParams qp;
+    spec_params(p, qp, dB);
+    if (threadIdx.x == 0) s_tk = atomicAdd(ticket, 1u);
+    __syncwarp();
+    const unsigned long long seg_id = s_tk;
+    if (seg_id >= total_segs) return;
+    // segment-major order: all planes' segment j before any segment j+1, so a segment's
+    // predecessor (same plane, j-1) always holds an earlier ticket and is usually done
+    spec_segment<SymT, kFused>(S, x, p, qp, seg_id % p.planes, seg_id / p.planes, sym_out,
+                               side_state, status, exits, flags, nullptr, 0.0f);
+}
+
+// Decoupled path, kernel A: phase A of every segment (no waiting), state persisted.
+template <typename SymT>
+__global__ void __launch_bounds__(kW) k_quant_spec_front(const float* __restrict__ x, SP p,
+                                                         const int* dB, unsigned int* flags,
+                                                         unsigned char* store,
+                                                         unsigned long long total_segs) {
+    __shared__ Smem<SymT> S;
+    QParams qp;
+    spec_params(p, qp, dB);
+    const unsigned long long seg_id = blockIdx.x;
+    if (seg_id >= total_segs) return;
+    spec_segment<SymT, kFront>(S, x, p, qp, seg_id % p.planes, seg_id / p.planes, nullptr,
+                               nullptr, nullptr, nullptr, flags, store, 0.0f);
+}
+
+// Decoupled path, kernel B: one warp per plane walks its segments in order.
+template <typename SymT>
+__global__ void __launch_bounds__(kW) k_quant_spec_back(const float* __restrict__ x, SP p,
+                                                        const int* dB, SymT* __restrict__ sym_out,
+                                                        float* __restrict__ side_state,
+                                                        unsigned int* flags,
+                                                        unsigned char* store) {
+    __shared__ Smem<SymT> S;
+    QParams qp;
+    spec_params(p, qp, dB);
+    const uint64_t plane = blockIdx.x;
+    if (plane >= p.planes) return;
+    float t = 0.0f;
+    for (uint64_t j = 0; j < p.nseg; ++j) {
+        t = spec_segment<SymT, kBack>(S, x, p, qp, plane, j, sym_out, side_state, nullptr,
+                                      nullptr, flags, store, t);
+        __syncwarp();
+    }
 }
 
 }  // namespace
+
+// Scratch layout: [B | ticket | status (u32/segment) | exits (f32/segment) | segment states]
+size_t spec_store_stride() {
+    constexpr size_t st = offsetof(Smem<uint32_t>, xs);  // the larger of the two symbol types
+    return ((st + 15) / 16) * 16 + sizeof(SegHdr);
+}
+size_t spec_store_offset(uint64_t total) {
+    return ((256 + 2 * ((4 * total + 255) & ~255ull)) + 255) & ~size_t(255);
+}
 
 // Host launcher. `scratch` must hold quant_spec_scratch_bytes(planes, plane_size).
 cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
@@ -809,13 +929,34 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     }();
     k_anchor_binade<<<1, 1024, 0, s>>>(a.x, a.g.n, qdiv, dB);
     ++*launches;
-    if (a.sym16)
-        k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym16, a.side_state,
-                                                              status, exits, ticket, a.flags, total);
-    else
-        k_quant_spec<uint32_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.sym, a.side_state,
-                                                              status, exits, ticket, a.flags, total);
-    ++*launches;
+    // Fused kernel by default. The decoupled pair (ACZ_SPEC_DECOUPLED=1) is bit-identical;
+    // measured slower on B200 (AlexNet conv1: 2.59 vs 2.36 ms): phase A costs the same and an
+    // isolated walk batch still takes ~3.3k cycles, so the per-plane walk chain dominates.
+    if (!std::getenv("ACZ_SPEC_DECOUPLED")) {
+        if (a.sym16)
+            k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(
+                a.x, p, dB, a.sym16, a.side_state, status, exits, ticket, a.flags, total);
+        else
+            k_quant_spec<uint32_t><<<(unsigned)total, kW, 0, s>>>(
+                a.x, p, dB, a.sym, a.side_state, status, exits, ticket, a.flags, total);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    // decoupled: phase A of every segment (throughput), then one warp per plane walks its
+    // segments in order (the only sequential part), from the persisted segment states
+    unsigned char* store = reinterpret_cast<unsigned char*>(sc) + spec_store_offset(total);
+    if (a.sym16) {
+        k_quant_spec_front<uint16_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.flags, store,
+                                                                    total);
+        k_quant_spec_back<uint16_t><<<(unsigned)a.g.planes, kW, 0, s>>>(
+            a.x, p, dB, a.sym16, a.side_state, a.flags, store);
+    } else {
+        k_quant_spec_front<uint32_t><<<(unsigned)total, kW, 0, s>>>(a.x, p, dB, a.flags, store,
+                                                                    total);
+        k_quant_spec_back<uint32_t><<<(unsigned)a.g.planes, kW, 0, s>>>(
+            a.x, p, dB, a.sym, a.side_state, a.flags, store);
+    }
+    *launches += 2;
     return cudaGetLastError();
 }
 
@@ -832,7 +973,7 @@ cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
 
 size_t quant_spec_scratch_bytes(uint64_t planes, uint64_t plane_size) {
     const uint64_t total = planes * ((plane_size + kSeg - 1) / kSeg);
-    return 256 + 2 * ((4 * total + 255) & ~255ull);
+    return spec_store_offset(total) + total * spec_store_stride();
 }
 
 // Speculative (K2b) vs thread-per-plane (K2a) quantiser, by a cost model calibrated on B200

@@ -125,3 +125,10 @@ def test_quant_spec_random_fuzz(acz, oracle):
             x[rng.random(x.shape) < 0.3] = 0
         eb = float(rng.choice([1e-4, 5e-4, 1e-3, 2e-3, 1e-2]))
         _run(acz, oracle, x.reshape(planes, 1, P), eb)
+
+
+@pytest.mark.parametrize("case", ["dense_227", "relu_227", "eb1e-4", "radius4", "huge_outliers"])
+def test_quant_spec_decoupled_path(acz, oracle, case, monkeypatch):
+    """The decoupled phase-A / walk kernel pair (opt-in) is bit-identical to the oracle."""
+    monkeypatch.setenv("ACZ_SPEC_DECOUPLED", "1")
+    test_quant_spec_cases(acz, oracle, case)
