@@ -184,7 +184,6 @@ template <typename SymT>
 __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len, const SP& p,
                          uint64_t plane_flat0) {
     const int lane = threadIdx.x;
-    const double M52 = 6755399441055744.0;
     auto range_of = [&](int q) {
         const int w = q >> 5;
         return (int)S.rsp[w] + __popc(S.rsb[w] & (0xFFFFFFFFu >> (31 - (q & 31)))) - 1;
@@ -194,36 +193,38 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
         if (seg0 + (uint64_t)c == 0) return 0.0;
         return (c == S.rstart[kc]) ? (double)S.guess[kc] : (double)S.s[c - 1];
     };
+    // sidecar points of this segment: i == sc_off (mod interval), in 32-bit arithmetic
+    const uint64_t ph = (p.interval - ((plane_flat0 + seg0) & (p.interval - 1))) & (p.interval - 1);
+    const uint32_t sc_off = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
+    const uint32_t sc_mask = p.interval > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)(p.interval - 1);
     for (int w = i0 >> 5; w * 32 < len; ++w) {
         const int i = w * 32 + lane;
         const bool valid = i >= i0 && i < len;
         bool c = false;
         int lvlex = -100000;
         if (valid) {
-            const int k = range_of(i);
-            const int b = S.rstart[k];
+            // range starts are rare (one per range): only they need the range index
+            const bool start = (S.rsb[w] >> (i & 31)) & 1u;
             const float xf = S.xs[xoff + i];
             const float out = S.s[i];
             const uint32_t sy = (uint32_t)S.sym[i];
-            const double pred = pred_of(i, k);
-            c = (i == b);
+            c = start;
             if (sy == 0) {
                 c = true;
             } else {
+                const double pred = start ? ((seg0 == 0 && i == 0) ? 0.0 : (double)S.guess[range_of(i)])
+                                          : (double)S.s[i - 1];
                 const double orig = (double)xf;
                 const double d = __dsub_rn(orig, pred);
-                double t = __dmul_rn(d, p.inv_step);
-                double q = __dsub_rn(__dadd_rn(t, M52), M52);
-                if (p.exact_div || 0.5 - fabs(t - q) <= fabs(t) * 0x1p-44 + 0x1p-60) {
-                    t = __ddiv_rn(d, p.step);
-                    q = round(t);
-                }
+                // the chain already fixed q exactly (pass 1, same prefix): q = sym - R
+                const double q = (double)((int)sy - (int)p.R);
+                const double t = __dmul_rn(d, p.inv_step);
                 const double pre = __dadd_rn(pred, __dmul_rn(q, p.step));
                 const double dm = (0.5 - fabs(t - q)) * p.step;
                 const double am = p.eb - fabs(orig - (double)out);
                 if (fmin(dm, am) <= 2.0 * p.Tmax) c = true;
                 if (fabs(q) >= p.radius_d - 1.0) c = true;
-                const bool coll_before = i > b && tiny_acc(i - 1);
+                const bool coll_before = !start && tiny_acc(i - 1);
                 if (q == 0.0 && coll_before) {
                     // identity inside a collapsed run
                 } else if (fabs((double)out) < p.eb) {
@@ -243,6 +244,8 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
                     if (coll_before) {
                         // re-expansion certificate for any |D| <= Tmax; ycol = pre-value of
                         // the run's last non-identity element
+                        const int k = range_of(i);
+                        const int b = S.rstart[k];
                         int cc = i - 1;
                         while (cc > b && S.sym[cc] == (SymT)p.R && tiny_acc(cc - 1)) --cc;
                         const double ycol = __dadd_rn(pred_of(cc, k),
@@ -252,7 +255,7 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
                     }
                 }
             }
-            if (((plane_flat0 + seg0 + (uint64_t)i) & (p.interval - 1)) == 0) c = true;  // sidecar
+            if ((((uint32_t)i - sc_off) & sc_mask) == 0) c = true;  // sidecar point
         }
         const unsigned cb = __ballot_sync(0xffffffffu, c);
         unsigned lb[kLev];

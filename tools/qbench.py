@@ -22,6 +22,7 @@ for nm in which:
     p = acz.CodecParams(1e-3)
     for _ in range(2):
         blob = acz.compress(x, p)
+        acz.decompress(blob, True)
     v = (C.c_uint64 * 28)()
     lib.acz_gpu_debug_counters(ctx.handle, v, 28, 1)
     lib.acz_gpu_profile_enable(ctx.handle, 1)
