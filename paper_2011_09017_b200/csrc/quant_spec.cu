@@ -270,11 +270,16 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
     }
 }
 
-// Phase A for ranges k0.. with lattice origin lam (all lanes participate).
+// Phase A for ranges k0.. with lattice origin lam (all lanes participate). Out of line: the
+// kernel calls it from four places and one copy keeps the kernel inside the instruction
+// cache. The parameters are copied to registers on entry (the stack copies the call ABI
+// makes could alias the shared-memory stores of the chain and would be reloaded per step).
 template <typename SymT>
-__device__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
-                        float k0_entry, const SP& p, const QParams& qp, uint64_t plane_flat0,
+__device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
+                        float k0_entry, const SP& p_in, const QParams& qp_in, uint64_t plane_flat0,
                         unsigned* flags, int len) {
+    const SP p = p_in;
+    const QParams qp = qp_in;
     const int lane = threadIdx.x;
     for (int k = k0 + lane; k < S.nr; k += kW) {
         const int st = S.rstart[k];
