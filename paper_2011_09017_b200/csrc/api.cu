@@ -57,9 +57,13 @@ struct Slot {
     size_t ws_qs_cap = 0;
     void* ws_in = nullptr;  // device copy of a host input (host-buffer batched compress)
     size_t ws_in_cap = 0;
+    void* ws_pack = nullptr;  // ACZ1 codebook + outliers serialised on the device
+    size_t ws_pack_cap = 0;
     SmallBlock* d_small = nullptr;
     SmallBlock* h_small = nullptr;  // pinned mirror
+    void* h_small_dev = nullptr;    // its device-side (mapped) address
     cudaEvent_t ev_book = nullptr;  // recorded after the codebook read-back
+    cudaEvent_t ev_up = nullptr;    // host-input upload complete (serialises batch uploads)
     uint64_t last_n = 0;
     bool last_sym16 = false;
 };
@@ -292,8 +296,10 @@ uint64_t blob_binding(const acz_gpu_blob_info_t& in) {
 int ensure_small(acz_gpu_ctx* ctx, Slot* sl) {
     if (sl->d_small) return ACZ_OK;
     CK(cudaMalloc(&sl->d_small, sizeof(SmallBlock)));
-    CK(cudaMallocHost(&sl->h_small, sizeof(SmallBlock)));
+    CK(cudaHostAlloc(&sl->h_small, sizeof(SmallBlock), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&sl->h_small_dev, sl->h_small, 0));
     CK(cudaEventCreateWithFlags(&sl->ev_book, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sl->ev_up, cudaEventDisableTiming));
     return ACZ_OK;
 }
 
@@ -306,11 +312,12 @@ Slot* get_slot(acz_gpu_ctx* ctx, size_t i) {
 void free_slot(Slot* sl) {
     if (!sl) return;
     for (void* p : {sl->ws_sym, sl->ws_hist, sl->ws_enc, sl->ws_cb, sl->ws_status, sl->ws_row,
-                    sl->ws_book, sl->ws_side, sl->ws_qs, sl->ws_in})
+                    sl->ws_book, sl->ws_side, sl->ws_qs, sl->ws_in, sl->ws_pack})
         if (p) cudaFree(p);
     if (sl->d_small) cudaFree(sl->d_small);
     if (sl->h_small) cudaFreeHost(sl->h_small);
     if (sl->ev_book) cudaEventDestroy(sl->ev_book);
+    if (sl->ev_up) cudaEventDestroy(sl->ev_up);
     delete sl;
 }
 
@@ -431,14 +438,19 @@ int finish_encode(acz_gpu_ctx* ctx, Slot* sl, acz_gpu_blob* b, const void* d_sym
     const uint32_t* wb_sym = static_cast<const uint32_t*>(sl->ws_book);
     const uint8_t* wb_len =
         reinterpret_cast<const uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
-    CK(cudaMemcpyAsync(b->book_sym, wb_sym, 4ull * bi.book_size, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(b->book_len, wb_len, bi.book_size, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(b->lut, sl->d_small->lut, 4ull * kLutSize, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(b->canon, &sl->d_small->canon, sizeof(CanonTables),
-                       cudaMemcpyDeviceToDevice, s));
-    if (nchunks && d_x)
-        CK(cudaMemcpyAsync(b->side_state, sl->ws_side, 4ull * nchunks, cudaMemcpyDeviceToDevice,
-                           s));
+    CopyRegions cr{};
+    auto add = [&](const void* src, void* dst, uint64_t bytes) {
+        cr.src[cr.n] = src;
+        cr.dst[cr.n] = dst;
+        cr.bytes[cr.n] = bytes;
+        ++cr.n;
+    };
+    add(wb_sym, b->book_sym, 4ull * bi.book_size);
+    add(wb_len, b->book_len, bi.book_size);
+    add(sl->d_small->lut, b->lut, 4ull * kLutSize);
+    add(&sl->d_small->canon, b->canon, sizeof(CanonTables));
+    if (nchunks && d_x) add(sl->ws_side, b->side_state, 4ull * nchunks);
+    CK(launch_copy_regions(cr, ctx->sms, s, &ctx->launches));
     EncodeArgs ea;
     ea.sym = d_sym;
     ea.sym16 = sym16;
@@ -496,8 +508,14 @@ int build_book(acz_gpu_ctx* ctx, Slot* sl, const void* d_sym, int sym16, uint64_
                        sl->d_small->lut, &sl->d_small->info, s, &ctx->launches));
     }
     sl->hist_clean = true;
-    CK(cudaMemcpyAsync(sl->h_small, sl->d_small, offsetof(SmallBlock, canon),
-                       cudaMemcpyDeviceToHost, s));
+    // BookInfo + flags straight into the mapped pinned mirror (no copy-engine queueing)
+    CopyRegions cr{};
+    cr.src[0] = sl->d_small;
+    cr.dst[0] = sl->h_small_dev;
+    cr.bytes[0] = offsetof(SmallBlock, canon);
+    cr.n = 1;
+    cr.to_host = 1;
+    CK(launch_copy_regions(cr, ctx->sms, s, &ctx->launches));
     CK(cudaEventRecord(sl->ev_book, s));
     return ACZ_OK;
 }
@@ -670,6 +688,81 @@ int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz
     return ACZ_OK;
 }
 
+// ACZ1 bytes of a blob into host memory dst (ref src/codec.cpp:177-199 blob_to_bytes): the
+// header is written here, the codebook and outliers are serialised on the device into the
+// slot's pack buffer, and every device part goes out as an async copy on s. The caller
+// synchronises s before reading dst (the batch entry point once, at the end).
+int blob_to_host_enqueue(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, uint8_t* dst,
+                         uint64_t cap, cudaStream_t s) {
+    const acz_gpu_blob_info_t& in = b->info;
+    if (cap < in.compressed_bytes) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
+    if (!sl) return fail(ctx, ACZ_ERR_NOMEM, "slot");
+    const uint32_t k = in.codebook_size;
+    const uint64_t nout = in.outlier_count;
+    uint8_t* p = dst;
+    auto put = [&](uint64_t v, int bytes) {
+        for (int i = 0; i < bytes; ++i) *p++ = (uint8_t)(v >> (8 * i));
+    };
+    std::memcpy(p, "ACZ1", 4);
+    p += 4;
+    put(1, 1);
+    put(in.predictor, 1);
+    put(in.rank, 1);
+    for (uint32_t i = 0; i < in.rank; ++i) put(in.shape[i], 8);
+    uint64_t ebits;
+    std::memcpy(&ebits, &in.eb, 8);
+    put(ebits, 8);
+    put(in.quant_radius, 4);
+    put(nout, 4);
+    put(k, 2);
+    uint8_t* book_at = p;
+    p += 5ull * k;
+    put(in.bit_length, 8);
+    const uint64_t nbytes = (in.bit_length + 7) / 8;
+    CK(cudaMemcpyAsync(p, b->words, nbytes, cudaMemcpyDeviceToHost, s));
+    p += nbytes;
+    uint8_t* outl_at = p;
+    p += 12ull * nout;
+    if ((uint64_t)(p - dst) != in.compressed_bytes)
+        return fail(ctx, ACZ_ERR_FORMAT, "internal: ACZ1 size mismatch");
+    if (k || nout) {
+        const size_t need = 5ull * k + 12ull * nout;
+        CK(grow(&sl->ws_pack, &sl->ws_pack_cap, need));
+        uint8_t* pk = static_cast<uint8_t*>(sl->ws_pack);
+        CK(launch_pack_acz1(b->book_sym, b->book_len, k, b->out_index, b->out_value, nout, pk,
+                            pk + 5ull * k, ctx->sms, s, &ctx->launches));
+        if (k) CK(cudaMemcpyAsync(book_at, pk, 5ull * k, cudaMemcpyDeviceToHost, s));
+        if (nout) CK(cudaMemcpyAsync(outl_at, pk + 5ull * k, 12ull * nout, cudaMemcpyDeviceToHost, s));
+    }
+    return ACZ_OK;
+}
+
+// Decode sidecar ("ACZS" v2) into host memory dst, async on s (see blob_to_host_enqueue).
+int sidecar_to_host_enqueue(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
+                            cudaStream_t s) {
+    const bool has_outl = b->side_outl != nullptr;
+    const uint64_t need = sidecar_bytes(b->nchunks, has_outl);
+    if (cap < need) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
+    uint8_t* p = dst;
+    std::memcpy(p, "ACZS", 4);
+    p += 4;
+    const uint32_t ver = 2;
+    std::memcpy(p, &ver, 4);
+    p += 4;
+    const uint64_t hdr[6] = {b->info.element_count, b->info.bit_length, b->interval, b->nchunks,
+                             blob_binding(b->info), has_outl ? 1ull : 0ull};
+    std::memcpy(p, hdr, sizeof(hdr));
+    p += sizeof(hdr);
+    CK(cudaMemcpyAsync(p, b->side_bitoff, 8ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+    p += 8ull * b->nchunks;
+    if (has_outl) {
+        CK(cudaMemcpyAsync(p, b->side_outl, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+        p += 4ull * b->nchunks;
+    }
+    CK(cudaMemcpyAsync(p, b->side_state, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+    return ACZ_OK;
+}
+
 // Internal streams for the batched entry points: fork from the caller's stream.
 int pool_fork(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
     while (ctx->pool.size() < k) {
@@ -803,24 +896,39 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
     if (rc) return rc;
     std::vector<Plan> plans(count);
     std::vector<int> st(count, ACZ_OK);
-    size_t o = 0;
-    // upload + first half per tensor on its own stream: tensor i's quantiser starts as soon as
-    // its own input has landed, while later inputs are still crossing PCIe
-    for (uint32_t i = 0; i < count; ++i) {
-        const uint64_t* shp = shapes + o;
-        o += ranks[i];
+    std::vector<const uint64_t*> shp(count);
+    std::vector<uint64_t> nel(count, 0);
+    for (uint32_t i = 0, o = 0; i < count; o += ranks[i], ++i) {
+        shp[i] = shapes + o;
+        st[i] = validate_shape(ctx, shp[i], ranks[i], &nel[i]);
+    }
+    // Uploads go one at a time, largest tensor first (an event chain across the pool
+    // streams): concurrent copies would share PCIe and all land together at the end, while
+    // in sequence the big tensor's kernels run under the remaining uploads and the tail after
+    // the last upload is the smallest tensor's work. Each tensor's kernels start on its own
+    // stream as soon as its own input has landed.
+    std::vector<uint32_t> order(count);
+    for (uint32_t i = 0; i < count; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint32_t a, uint32_t b) { return nel[a] > nel[b]; });
+    cudaEvent_t prev_up = nullptr;
+    for (uint32_t i : order) {
         Slot* sl = get_slot(ctx, i);
         cudaStream_t s = ctx->pool[i % k];
-        uint64_t n = 0;
-        st[i] = sl ? validate_shape(ctx, shp, ranks[i], &n) : ACZ_ERR_NOMEM;
+        const uint64_t n = nel[i];
+        if (!sl) st[i] = ACZ_ERR_NOMEM;
+        if (st[i] == ACZ_OK) st[i] = ensure_small(ctx, sl);
         if (st[i] == ACZ_OK && n) {
             cudaError_t e = grow(&sl->ws_in, &sl->ws_in_cap, 4ull * n);
+            if (e == cudaSuccess && prev_up) e = cudaStreamWaitEvent(s, prev_up, 0);
             if (e == cudaSuccess) e = cudaMemcpyAsync(sl->ws_in, h_in[i], 4ull * n,
                                                       cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaEventRecord(sl->ev_up, s);
             if (e != cudaSuccess) st[i] = cuda_fail(ctx, e, "host input upload");
+            else prev_up = sl->ev_up;
         }
         if (st[i] == ACZ_OK)
-            st[i] = compress_begin(ctx, sl, static_cast<const float*>(sl->ws_in), shp, ranks[i],
+            st[i] = compress_begin(ctx, sl, static_cast<const float*>(sl->ws_in), shp[i], ranks[i],
                                    eb, quant_radius, predictor, s, &plans[i]);
     }
     // second halves in completion order, then the bytes back to the host
@@ -836,16 +944,17 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
             if (acz1_cap[i] < b->info.compressed_bytes)
                 st[i] = fail(ctx, ACZ_ERR_INVALID, "ACZ1 destination too small");
             else
-                st[i] = acz_gpu_blob_to_host(ctx, b, acz1[i], acz1_cap[i], &acz1_size[i], s);
+                st[i] = blob_to_host_enqueue(ctx, get_slot(ctx, i), b, acz1[i], acz1_cap[i], s);
+            if (st[i] == ACZ_OK) acz1_size[i] = b->info.compressed_bytes;
         }
         if (st[i] == ACZ_OK && sidecar && sidecar[i]) {
             if (!sidecar_cap || sidecar_cap[i] < b->info.sidecar_bytes)
                 st[i] = fail(ctx, ACZ_ERR_INVALID, "sidecar destination too small");
             else
-                st[i] = acz_gpu_sidecar_to_host(ctx, b, sidecar[i], sidecar_cap[i],
-                                                sidecar_size ? &sidecar_size[i] : nullptr, s);
+                st[i] = sidecar_to_host_enqueue(ctx, b, sidecar[i], sidecar_cap[i], s);
+            if (st[i] == ACZ_OK && sidecar_size) sidecar_size[i] = b->info.sidecar_bytes;
         }
-        if (b) acz_gpu_blob_free(b);
+        if (b) acz_gpu_blob_free(b);  // stream-ordered: the copies above complete first
         if (st[i] != ACZ_OK && first_err == ACZ_OK) {
             first_err = st[i];
             first_msg = ctx->err;
@@ -863,8 +972,8 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
                 progressed = true;
             }
         }
-        if (!progressed)
-            for (uint32_t i = 0; i < count; ++i)
+        if (!progressed)  // block on the tensor expected next: the earliest upload pending
+            for (uint32_t i : order)
                 if (!done[i]) {
                     finish(i);
                     break;
@@ -872,6 +981,7 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
     }
     rc = pool_join(ctx, k, ctx->own);
     if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->own));  // every ACZ1 / sidecar byte is in host memory
     if (first_err) ctx->err = first_msg;
     return first_err;
 }
@@ -922,90 +1032,22 @@ int acz_gpu_blob_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, 
                          uint64_t* written, void* stream) {
     if (!ctx || !b || !dst) return ACZ_ERR_INVALID;
     ctx->err.clear();
-    const acz_gpu_blob_info_t& in = b->info;
-    if (cap < in.compressed_bytes) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const uint32_t k = in.codebook_size;
-    const uint64_t nout = in.outlier_count;
-    std::vector<uint32_t> bsym(k);
-    std::vector<uint8_t> blen(k);
-    std::vector<unsigned long long> oidx(nout);
-    std::vector<float> oval(nout);
-    // header: ref src/codec.cpp:179-191
-    uint8_t* p = dst;
-    auto put = [&](uint64_t v, int bytes) {
-        for (int i = 0; i < bytes; ++i) *p++ = (uint8_t)(v >> (8 * i));
-    };
-    std::memcpy(p, "ACZ1", 4);
-    p += 4;
-    put(1, 1);
-    put(in.predictor, 1);
-    put(in.rank, 1);
-    for (uint32_t i = 0; i < in.rank; ++i) put(in.shape[i], 8);
-    uint64_t ebits;
-    std::memcpy(&ebits, &in.eb, 8);
-    put(ebits, 8);
-    put(in.quant_radius, 4);
-    put(nout, 4);
-    put(k, 2);
-    uint8_t* book_at = p;
-    p += 5ull * k;
-    put(in.bit_length, 8);
-    const uint64_t nbytes = (in.bit_length + 7) / 8;
-    CK(cudaMemcpyAsync(p, b->words, nbytes, cudaMemcpyDeviceToHost, s));
-    p += nbytes;
-    if (k) {
-        CK(cudaMemcpyAsync(bsym.data(), b->book_sym, 4ull * k, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(blen.data(), b->book_len, k, cudaMemcpyDeviceToHost, s));
-    }
-    if (nout) {
-        CK(cudaMemcpyAsync(oidx.data(), b->out_index, 8ull * nout, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(oval.data(), b->out_value, 4ull * nout, cudaMemcpyDeviceToHost, s));
-    }
+    const int rc = blob_to_host_enqueue(ctx, get_slot(ctx, 0), b, dst, cap, s);
+    if (rc) return rc;
     CK(cudaStreamSynchronize(s));
-    uint8_t* q = book_at;
-    for (uint32_t i = 0; i < k; ++i) {
-        for (int j = 0; j < 4; ++j) *q++ = (uint8_t)(bsym[i] >> (8 * j));
-        *q++ = blen[i];
-    }
-    for (uint64_t i = 0; i < nout; ++i) {
-        put(oidx[i], 8);
-        uint32_t vb;
-        std::memcpy(&vb, &oval[i], 4);
-        put(vb, 4);
-    }
-    if ((uint64_t)(p - dst) != in.compressed_bytes)
-        return fail(ctx, ACZ_ERR_FORMAT, "internal: ACZ1 size mismatch");
-    if (written) *written = in.compressed_bytes;
+    if (written) *written = b->info.compressed_bytes;
     return ACZ_OK;
 }
 
 int acz_gpu_sidecar_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
                             uint64_t* written, void* stream) {
     if (!ctx || !b || !dst) return ACZ_ERR_INVALID;
-    const bool has_outl = b->side_outl != nullptr;
-    const uint64_t need = sidecar_bytes(b->nchunks, has_outl);
-    if (cap < need) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    uint8_t* p = dst;
-    std::memcpy(p, "ACZS", 4);
-    p += 4;
-    const uint32_t ver = 2;
-    std::memcpy(p, &ver, 4);
-    p += 4;
-    const uint64_t hdr[6] = {b->info.element_count, b->info.bit_length, b->interval, b->nchunks,
-                             blob_binding(b->info), has_outl ? 1ull : 0ull};
-    std::memcpy(p, hdr, sizeof(hdr));
-    p += sizeof(hdr);
-    CK(cudaMemcpyAsync(p, b->side_bitoff, 8ull * b->nchunks, cudaMemcpyDeviceToHost, s));
-    p += 8ull * b->nchunks;
-    if (has_outl) {
-        CK(cudaMemcpyAsync(p, b->side_outl, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
-        p += 4ull * b->nchunks;
-    }
-    CK(cudaMemcpyAsync(p, b->side_state, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
+    const int rc = sidecar_to_host_enqueue(ctx, b, dst, cap, s);
+    if (rc) return rc;
     CK(cudaStreamSynchronize(s));
-    if (written) *written = need;
+    if (written) *written = sidecar_bytes(b->nchunks, b->side_outl != nullptr);
     return ACZ_OK;
 }
 

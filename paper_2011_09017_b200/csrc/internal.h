@@ -34,6 +34,19 @@ cudaError_t launch_stats(const float* x, uint64_t n, uint32_t* bitmap,
                          int sms, cudaStream_t s, uint64_t* launches);
 
 cudaError_t launch_relu(float* x, uint64_t n, int sms, cudaStream_t s, uint64_t* launches);
+struct CopyRegions {
+    const void* src[8];
+    void* dst[8];
+    uint64_t bytes[8];
+    int n;
+    int to_host;  // a destination is mapped host memory
+};
+cudaError_t launch_copy_regions(const CopyRegions& r, int sms, cudaStream_t s,
+                                uint64_t* launches);
+cudaError_t launch_pack_acz1(const uint32_t* bsym, const uint8_t* blen, uint32_t k,
+                             const unsigned long long* oidx, const float* oval, uint64_t nout,
+                             uint8_t* book_out, uint8_t* outl_out, int sms, cudaStream_t s,
+                             uint64_t* launches);
 cudaError_t launch_widen_u16(const uint16_t* a, uint32_t* b, uint64_t n, int sms, cudaStream_t s,
                              uint64_t* launches);
 

@@ -50,7 +50,7 @@ constexpr int kLev = 3;                // fine offset levels (binades below the 
 __device__ unsigned long long g_qstats[8];
 // per-phase SM cycles summed over segments (debug): geometry+phase A, look-back wait,
 // walk, exit+store
-__device__ unsigned long long g_qclk[8];  // + [4] exact-step cycles, [5] batch cycles
+__device__ unsigned long long g_qclk[8];  // + [4] exact-step, [5] batch, [6] pass-1, [7] classify cycles
 
 struct SP {
     double eb, step, inv_step, radius_d, Tmax;
@@ -188,7 +188,6 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
         const int w = q >> 5;
         return (int)S.rsp[w] + __popc(S.rsb[w] & (0xFFFFFFFFu >> (31 - (q & 31)))) - 1;
     };
-    auto tiny_acc = [&](int c) { return S.sym[c] != 0 && fabs((double)S.s[c]) < p.eb; };
     auto pred_of = [&](int c, int kc) -> double {
         if (seg0 + (uint64_t)c == 0) return 0.0;
         return (c == S.rstart[kc]) ? (double)S.guess[kc] : (double)S.s[c - 1];
@@ -197,23 +196,45 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
     const uint64_t ph = (p.interval - ((plane_flat0 + seg0) & (p.interval - 1))) & (p.interval - 1);
     const uint32_t sc_off = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
     const uint32_t sc_mask = p.interval > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)(p.interval - 1);
+    // Carried across the 32-position words: the previous position's output and "tiny
+    // accepted" flag, and the last position that is not an identity continuation of a
+    // collapsed run (id[c]: sym[c] == R and position c-1 tiny accepted). The re-expansion
+    // certificate needs, for position i, the last c in [b, i-1] with c == b or !id[c]; a
+    // ballot over the word finds it in O(1) instead of walking the run back.
+    float carry_out = 0.0f;
+    bool carry_tiny = false;
+    int carry_nid = -1;
     for (int w = i0 >> 5; w * 32 < len; ++w) {
         const int i = w * 32 + lane;
         const bool valid = i >= i0 && i < len;
+        const float out = valid ? S.s[i] : 0.0f;
+        const uint32_t sy = valid ? (uint32_t)S.sym[i] : 0u;
+        const bool tiny = sy != 0 && fabs((double)out) < p.eb;
+        float prev_out = __shfl_up_sync(0xffffffffu, out, 1);
+        bool prev_tiny = __shfl_up_sync(0xffffffffu, (int)tiny, 1) != 0;
+        if (lane == 0) {
+            prev_out = carry_out;
+            prev_tiny = carry_tiny;
+        }
+        const bool id = valid && sy == (uint32_t)p.R && prev_tiny;
+        const unsigned nid = __ballot_sync(0xffffffffu, !id);
+        const unsigned nid_below = nid & ((1u << lane) - 1u);
+        const int last_nid = nid_below ? (w << 5) + 31 - __clz(nid_below) : carry_nid;
+        carry_out = __shfl_sync(0xffffffffu, out, 31);
+        carry_tiny = __shfl_sync(0xffffffffu, (int)tiny, 31) != 0;
+        carry_nid = (w << 5) + 31 - __clz(nid);  // nid != 0: invalid tail lanes count as !id
         bool c = false;
         int lvlex = -100000;
         if (valid) {
             // range starts are rare (one per range): only they need the range index
             const bool start = (S.rsb[w] >> (i & 31)) & 1u;
             const float xf = S.xs[xoff + i];
-            const float out = S.s[i];
-            const uint32_t sy = (uint32_t)S.sym[i];
             c = start;
             if (sy == 0) {
                 c = true;
             } else {
                 const double pred = start ? ((seg0 == 0 && i == 0) ? 0.0 : (double)S.guess[range_of(i)])
-                                          : (double)S.s[i - 1];
+                                          : (double)prev_out;
                 const double orig = (double)xf;
                 const double d = __dsub_rn(orig, pred);
                 // the chain already fixed q exactly (pass 1, same prefix): q = sym - R
@@ -224,7 +245,7 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
                 const double am = p.eb - fabs(orig - (double)out);
                 if (fmin(dm, am) <= 2.0 * p.Tmax) c = true;
                 if (fabs(q) >= p.radius_d - 1.0) c = true;
-                const bool coll_before = !start && tiny_acc(i - 1);
+                const bool coll_before = !start && prev_tiny;
                 if (q == 0.0 && coll_before) {
                     // identity inside a collapsed run
                 } else if (fabs((double)out) < p.eb) {
@@ -245,9 +266,7 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
                         // re-expansion certificate for any |D| <= Tmax; ycol = pre-value of
                         // the run's last non-identity element
                         const int k = range_of(i);
-                        const int b = S.rstart[k];
-                        int cc = i - 1;
-                        while (cc > b && S.sym[cc] == (SymT)p.R && tiny_acc(cc - 1)) --cc;
+                        const int cc = max(last_nid, (int)S.rstart[k]);
                         const double ycol = __dadd_rn(pred_of(cc, k),
                                                       __dmul_rn((double)((long long)S.sym[cc] - p.R), p.step));
                         const double dmax = pow2(fexp(2.0 * fmax(fabs(ycol), 2.0 * p.Tmax)) - 22);
@@ -281,6 +300,7 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int
     const SP p = p_in;
     const QParams qp = qp_in;
     const int lane = threadIdx.x;
+    const long long t0 = clock64();
     for (int k = k0 + lane; k < S.nr; k += kW) {
         const int st = S.rstart[k];
         if (k == k0 && lam_exact_k0) {
@@ -293,8 +313,13 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int
         spec_range(S, xoff, seg0, k, p, qp, flags);
     }
     __syncwarp();
+    const long long t1 = clock64();
     classify(S, xoff, seg0, S.rstart[k0], len, p, plane_flat0);
     __syncwarp();
+    if (lane == 0) {
+        atomicAdd(&g_qclk[6], (unsigned long long)(t1 - t0));
+        atomicAdd(&g_qclk[7], (unsigned long long)(clock64() - t1));
+    }
     // prefix C[k] = sum_{j<=k, j>0} (send[j-1] - guess[j])
     if (lane == 0) {
         double acc = 0.0;

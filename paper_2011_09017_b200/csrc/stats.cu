@@ -86,7 +86,81 @@ __global__ void k_relu(float* __restrict__ x, uint64_t n) {
     }
 }
 
+// ACZ1 serialisation of the codebook (u32 symbol, u8 length: 5 bytes per entry) and the
+// outlier list (u64 index, f32 value: 12 bytes), little-endian (ref src/codec.cpp:179-199),
+// packed on the device so the blob goes to the host as plain async copies.
+__global__ void k_pack_acz1(const uint32_t* __restrict__ bsym, const uint8_t* __restrict__ blen,
+                            uint32_t k, const unsigned long long* __restrict__ oidx,
+                            const float* __restrict__ oval, uint64_t nout,
+                            uint8_t* __restrict__ book_out, uint8_t* __restrict__ outl_out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += stride) {
+        const uint32_t v = bsym[i];
+        uint8_t* q = book_out + 5 * i;
+        q[0] = (uint8_t)v;
+        q[1] = (uint8_t)(v >> 8);
+        q[2] = (uint8_t)(v >> 16);
+        q[3] = (uint8_t)(v >> 24);
+        q[4] = blen[i];
+    }
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nout; i += stride) {
+        const unsigned long long a = oidx[i];
+        const uint32_t b = __float_as_uint(oval[i]);
+        uint8_t* q = outl_out + 12 * i;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = (uint8_t)(a >> (8 * j));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[8 + j] = (uint8_t)(b >> (8 * j));
+    }
+}
+
+// Several small copies in one launch, executed by SMs instead of a copy engine: a copy engine
+// queues them behind multi-megabyte host transfers of other streams, which would stall this
+// stream's next kernel (or, for the BookInfo read-back into mapped host memory, the host).
+__global__ void k_copy_regions(CopyRegions r) {
+    for (int k = 0; k < r.n; ++k) {
+        const char* src = static_cast<const char*>(r.src[k]);
+        char* dst = static_cast<char*>(r.dst[k]);
+        const uint64_t bytes = r.bytes[k];
+        const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        if ((((uintptr_t)src | (uintptr_t)dst | bytes) & 3) == 0) {
+            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+            for (uint64_t i = t; i < bytes / 4; i += stride) d4[i] = s4[i];
+        } else {
+            for (uint64_t i = t; i < bytes; i += stride) dst[i] = src[i];
+        }
+    }
+    if (r.to_host) __threadfence_system();  // mapped host destination
+}
+
 }  // namespace
+
+cudaError_t launch_copy_regions(const CopyRegions& r, int sms, cudaStream_t s,
+                                uint64_t* launches) {
+    uint64_t most = 0;
+    for (int k = 0; k < r.n; ++k) most = r.bytes[k] > most ? r.bytes[k] : most;
+    if (most == 0) return cudaSuccess;
+    const uint64_t want = (most / 4 + 255) / 256;
+    const unsigned grid = (unsigned)(want < (uint64_t)sms ? (want ? want : 1) : (uint64_t)sms);
+    k_copy_regions<<<grid, 256, 0, s>>>(r);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_acz1(const uint32_t* bsym, const uint8_t* blen, uint32_t k,
+                             const unsigned long long* oidx, const float* oval, uint64_t nout,
+                             uint8_t* book_out, uint8_t* outl_out, int sms, cudaStream_t s,
+                             uint64_t* launches) {
+    const uint64_t m = k > nout ? k : nout;
+    if (m == 0) return cudaSuccess;
+    const uint64_t want = (m + 255) / 256;
+    const unsigned grid = (unsigned)(want < (uint64_t)sms * 4 ? want : (uint64_t)sms * 4);
+    k_pack_acz1<<<grid, 256, 0, s>>>(bsym, blen, k, oidx, oval, nout, book_out, outl_out);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_relu(float* x, uint64_t n, int sms, cudaStream_t s, uint64_t* launches) {
     k_relu<<<(unsigned)(sms * 8), 256, 0, s>>>(x, n);

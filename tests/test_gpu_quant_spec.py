@@ -52,7 +52,8 @@ def _smooth(rng, shape, scale=3.0):
 CASES = ["dense_227", "relu_227", "smooth_relu_224", "relu_3136", "dense_3136",
          "eb1e-4", "eb3e-4", "eb1e-2", "eb3e-2", "radius4", "radius64", "wide_x100",
          "tiny_x1e-3", "zeros_plane", "const_plane", "sparse_spikes", "huge_outliers",
-         "rank1_long", "neg_relu", "mixed_scale", "near_eb_values", "quantized_grid"]
+         "rank1_long", "neg_relu", "mixed_scale", "near_eb_values", "quantized_grid",
+         "tiny_runs"]
 
 
 @pytest.mark.parametrize("case", CASES)
@@ -107,6 +108,19 @@ def test_quant_spec_cases(acz, oracle, case):
     elif case == "quantized_grid":
         # values exactly on the quantisation lattice and on round binary fractions (ties)
         x = rng.integers(-2000, 2000, (2, 2, 128, 128)) * 2e-3 + rng.choice([0, 0.25, 0.5], (2, 2, 128, 128))
+    elif case == "tiny_runs":
+        # long runs of sub-eb values (collapsed chain) re-expanding into normal values
+        n = 4 * 60_000
+        x = np.empty(n)
+        pos = 0
+        while pos < n:
+            L = int(rng.integers(1, 400))
+            if rng.random() < 0.5:
+                x[pos:pos + L] = rng.uniform(-9e-4, 9e-4, min(L, n - pos))
+            else:
+                x[pos:pos + L] = rng.standard_normal(min(L, n - pos)) * 0.3
+            pos += L
+        x = x.reshape(4, 1, 60_000)
     _run(acz, oracle, x, eb, radius)
 
 
