@@ -13,6 +13,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -763,31 +764,52 @@ int sidecar_to_host_enqueue(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* ds
     return ACZ_OK;
 }
 
-// Internal streams for the batched entry points: fork from the caller's stream.
+constexpr size_t kPoolStreams = 8;
+
+// Internal streams for the batched entry points, forked from the caller's stream: pool[i]
+// (i < kPoolStreams) run at the device's highest priority, pool[kPoolStreams + i] at the
+// lowest. A tensor whose quantiser is the long speculative kernel (thousands of one-warp
+// CTAs) goes to a low-priority stream, so the CTA scheduler slots the other tensors' short
+// kernels in as its CTAs retire instead of queueing them behind the whole grid.
 int pool_fork(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
-    while (ctx->pool.size() < k) {
-        cudaStream_t st = nullptr;
-        cudaEvent_t ev = nullptr;
-        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        ctx->pool.push_back(st);
-        ctx->pool_ev.push_back(ev);
+    if (ctx->pool.empty()) {
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        for (size_t i = 0; i < 2 * kPoolStreams; ++i) {
+            cudaStream_t st = nullptr;
+            cudaEvent_t ev = nullptr;
+            CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking,
+                                            i < kPoolStreams ? greatest : least));
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            ctx->pool.push_back(st);
+            ctx->pool_ev.push_back(ev);
+        }
     }
     CK(cudaEventRecord(ctx->ev_fork, user));
-    for (size_t i = 0; i < k; ++i) CK(cudaStreamWaitEvent(ctx->pool[i], ctx->ev_fork, 0));
-    return ACZ_OK;
-}
-
-// Join: the caller's stream waits for the first k internal streams.
-int pool_join(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
     for (size_t i = 0; i < k; ++i) {
-        CK(cudaEventRecord(ctx->pool_ev[i], ctx->pool[i]));
-        CK(cudaStreamWaitEvent(user, ctx->pool_ev[i], 0));
+        CK(cudaStreamWaitEvent(ctx->pool[i], ctx->ev_fork, 0));
+        CK(cudaStreamWaitEvent(ctx->pool[kPoolStreams + i], ctx->ev_fork, 0));
     }
     return ACZ_OK;
 }
 
-constexpr size_t kPoolStreams = 8;
+// Join: the caller's stream waits for the first k internal streams of both priorities.
+int pool_join(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
+    for (size_t i = 0; i < k; ++i)
+        for (size_t j : {i, kPoolStreams + i}) {
+            CK(cudaEventRecord(ctx->pool_ev[j], ctx->pool[j]));
+            CK(cudaStreamWaitEvent(user, ctx->pool_ev[j], 0));
+        }
+    return ACZ_OK;
+}
+
+// Stream of tensor i of a batch (see pool_fork).
+cudaStream_t tensor_stream(acz_gpu_ctx* ctx, uint32_t i, size_t k, const uint64_t* shape,
+                           uint32_t rank, uint32_t predictor) {
+    const PlaneGeom g = plane_geom(shape, rank);
+    const bool bulk = g.n && quant_spec_applicable(predictor, g.plane_size, g.planes, ctx->sms);
+    return ctx->pool[(bulk ? kPoolStreams : 0) + i % k];
+}
 
 }  // namespace
 
@@ -825,10 +847,12 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
     std::vector<Plan> plans(count);
     std::vector<int> st(count, ACZ_OK);
     std::vector<size_t> off(count);
+    std::vector<cudaStream_t> ts(count);
     size_t o = 0;
     for (uint32_t i = 0; i < count; ++i) {
         off[i] = o;
         o += ranks[i];
+        ts[i] = tensor_stream(ctx, i, k, shapes + off[i], ranks[i], predictor);
     }
     // first halves: every tensor's quantiser/histogram/codebook, round-robin over streams
     for (uint32_t i = 0; i < count; ++i) {
@@ -838,7 +862,7 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
             continue;
         }
         st[i] = compress_begin(ctx, sl, d_in[i], shapes + off[i], ranks[i], eb, quant_radius,
-                               predictor, ctx->pool[i % k], &plans[i]);
+                               predictor, ts[i], &plans[i]);
     }
     // second halves in completion order: a tensor's encode is launched as soon as its own
     // codebook read-back has landed, so short tensors do not queue behind a long quantiser
@@ -848,7 +872,7 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
     uint32_t remaining = count;
     auto finish = [&](uint32_t i) {
         if (st[i] == ACZ_OK)
-            st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], ctx->pool[i % k], &out[i]);
+            st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], ts[i], &out[i]);
         if (st[i] != ACZ_OK && first_err == ACZ_OK) {
             first_err = st[i];
             first_msg = ctx->err;
@@ -866,14 +890,9 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
                 progressed = true;
             }
         }
-        if (!progressed) {
-            // nothing ready yet: block on the first pending tensor
-            for (uint32_t i = 0; i < count; ++i)
-                if (!done[i]) {
-                    finish(i);
-                    break;
-                }
-        }
+        // nothing ready: poll again (blocking on one tensor would hold back the others, whose
+        // completion order depends on the stream priorities and the scheduler)
+        if (!progressed) std::this_thread::yield();
     }
     rc = pool_join(ctx, k, user);
     if (rc) return rc;
@@ -898,9 +917,12 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
     std::vector<int> st(count, ACZ_OK);
     std::vector<const uint64_t*> shp(count);
     std::vector<uint64_t> nel(count, 0);
+    std::vector<cudaStream_t> ts(count);
     for (uint32_t i = 0, o = 0; i < count; o += ranks[i], ++i) {
         shp[i] = shapes + o;
         st[i] = validate_shape(ctx, shp[i], ranks[i], &nel[i]);
+        ts[i] = st[i] == ACZ_OK ? tensor_stream(ctx, i, k, shp[i], ranks[i], predictor)
+                                : ctx->pool[i % k];
     }
     // Uploads go one at a time, largest tensor first (an event chain across the pool
     // streams): concurrent copies would share PCIe and all land together at the end, while
@@ -914,7 +936,7 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
     cudaEvent_t prev_up = nullptr;
     for (uint32_t i : order) {
         Slot* sl = get_slot(ctx, i);
-        cudaStream_t s = ctx->pool[i % k];
+        cudaStream_t s = ts[i];
         const uint64_t n = nel[i];
         if (!sl) st[i] = ACZ_ERR_NOMEM;
         if (st[i] == ACZ_OK) st[i] = ensure_small(ctx, sl);
@@ -937,7 +959,7 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
     std::vector<char> done(count, 0);
     uint32_t remaining = count;
     auto finish = [&](uint32_t i) {
-        cudaStream_t s = ctx->pool[i % k];
+        cudaStream_t s = ts[i];
         acz_gpu_blob* b = nullptr;
         if (st[i] == ACZ_OK) st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], s, &b);
         if (st[i] == ACZ_OK) {
@@ -972,12 +994,7 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
                 progressed = true;
             }
         }
-        if (!progressed)  // block on the tensor expected next: the earliest upload pending
-            for (uint32_t i : order)
-                if (!done[i]) {
-                    finish(i);
-                    break;
-                }
+        if (!progressed) std::this_thread::yield();  // see acz_gpu_compress_batch
     }
     rc = pool_join(ctx, k, ctx->own);
     if (rc) return rc;
