@@ -44,6 +44,7 @@ struct Slot {
     bool hist_clean = false;
     void* ws_enc = nullptr;
     size_t ws_enc_cap = 0;
+    uint32_t enc_alphabet = 0;
     void* ws_cb = nullptr;
     size_t ws_cb_cap = 0;
     void* ws_status = nullptr;
@@ -435,7 +436,7 @@ int finish_encode(acz_gpu_ctx* ctx, Slot* sl, acz_gpu_blob* b, const void* d_sym
     b->interval = interval;
     b->nchunks = nchunks;
     b->max_len = bi.max_len;
-    CK(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 32), s));
+    // the encoder writes every word of the stream and zeroes the padding (no memset)
     const uint32_t* wb_sym = static_cast<const uint32_t*>(sl->ws_book);
     const uint8_t* wb_len =
         reinterpret_cast<const uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
@@ -457,6 +458,7 @@ int finish_encode(acz_gpu_ctx* ctx, Slot* sl, acz_gpu_blob* b, const void* d_sym
     ea.sym16 = sym16;
     ea.n = n;
     ea.enc = static_cast<const unsigned long long*>(sl->ws_enc);
+    ea.enc32 = reinterpret_cast<const uint32_t*>(ea.enc + sl->enc_alphabet);
     ea.x = d_x;
     ea.words = b->words;
     ea.nwords = nwords;
@@ -489,11 +491,11 @@ int build_book(acz_gpu_ctx* ctx, Slot* sl, const void* d_sym, int sym16, uint64_
     }
     unsigned long long* hist = static_cast<unsigned long long*>(sl->ws_hist);
     uint32_t* touched = reinterpret_cast<uint32_t*>(hist + alphabet);
-    CK(grow(&sl->ws_enc, &sl->ws_enc_cap, 8ull * alphabet));
+    CK(grow(&sl->ws_enc, &sl->ws_enc_cap, 12ull * alphabet));  // u64 table + u32 compact table
+    sl->enc_alphabet = alphabet;
     CK(grow(&sl->ws_cb, &sl->ws_cb_cap, codebook_scratch_bytes(max_leaves)));
     CK(grow(&sl->ws_book, &sl->ws_book_cap, 5ull * max_leaves + 64));
-    const uint64_t tiles = (n + kEncTile - 1) / kEncTile;
-    CK(grow(&sl->ws_status, &sl->ws_status_cap, sizeof(TileStatus) * tiles));
+    CK(grow(&sl->ws_status, &sl->ws_status_cap, encode_scratch_bytes(n, ctx->sms)));
     {
     KTimer kt(ctx, ACZ_K_HIST, s);
     sl->hist_clean = false;  // until the codebook kernels have consumed the bins

@@ -17,6 +17,7 @@
 //                     bit concatenation in shared memory, coalesced word stores (boundary
 //                     words by atomicOr). Also writes the outlier list and the decode
 //                     sidecar (bit offset / outlier prefix every `interval` symbols).
+#include <algorithm>
 #include <type_traits>
 
 #include "internal.h"
@@ -579,6 +580,9 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
             book_len[pos] = (uint8_t)l;
             const unsigned long long code = s_first_code[l] + rank;
             enc[sym] = (code << 8) | l;
+            // compact form for books with codes <= 27 bits: code | len << 27
+            reinterpret_cast<uint32_t*>(enc + alphabet)[sym] =
+                l <= 27 ? (uint32_t)code | ((uint32_t)l << 27) : 0u;
         }
         __syncthreads();
     }
@@ -939,6 +943,9 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_slow(
             book_len[pos] = (uint8_t)l;
             const unsigned long long code = s_first_code[l] + rank;
             enc[sym] = (code << 8) | l;
+            // compact form for books with codes <= 27 bits: code | len << 27
+            reinterpret_cast<uint32_t*>(enc + alphabet)[sym] =
+                l <= 27 ? (uint32_t)code | ((uint32_t)l << 27) : 0u;
         }
         __syncthreads();
     }
@@ -995,11 +1002,12 @@ __global__ void __launch_bounds__(1024) k_build_tables(const uint32_t* __restric
 // --------------------------------------------------------------------------- K5 ----
 // Block-wide exclusive scan of two u32 per thread (kEncThreads threads). Returns the
 // exclusive prefixes; *ta / *tb receive the block totals.
+template <int NT>
 __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t* ea, uint32_t* eb,
                                             uint32_t* ta, uint32_t* tb, uint32_t* sa,
                                             uint32_t* sb) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int W = kEncThreads / 32;
+    constexpr int W = NT / 32;
     uint32_t ia = a, ib = b;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1033,87 +1041,121 @@ __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t* ea
     __syncthreads();
 }
 
-// K5 encode (ref src/huffman.cpp:127-131 + BitWriter :88-103), persistent reduce-then-scan:
-// CTA c owns a contiguous span of 2048-symbol tiles. Phase 1 sums its span's code lengths
-// and escapes; one decoupled look-back across CTAs (warp 0) gives the span's global bit
-// offset and outlier index. Phase 2 re-reads the (L2-resident) symbols tile by tile, keeps
-// the 8 codes of each thread in registers, packs them MSB-first with a 64-bit accumulator
-// into a shared stage (plain stores for words a thread owns entirely, OR for shared
-// boundary words), and stores the stage with coalesced word writes (tile-boundary words
-// OR-ed). It also writes the outlier list and the decode sidecar bit offsets.
-template <typename SymT>
-__global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
-    const SymT* __restrict__ symp = static_cast<const SymT*>(a.sym);
-    extern __shared__ uint32_t stage[];
-    __shared__ uint32_t s_a[kEncThreads / 32], s_b[kEncThreads / 32];
-    __shared__ unsigned long long s_red_bits[kEncThreads / 32], s_red_esc[kEncThreads / 32];
-    __shared__ unsigned long long s_base_bits, s_base_esc;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t tiles = (a.n + kEncTile - 1) / kEncTile;
-    const uint64_t span = (tiles + gridDim.x - 1) / gridDim.x;
-    const uint64_t tb = (uint64_t)blockIdx.x * span, te = min(tiles, tb + span);
-    const bool vec_ok = (reinterpret_cast<uintptr_t>(symp) & 15) == 0;
-    // kEncPer consecutive symbols of one thread (128-bit loads when aligned and complete)
-    auto load_syms = [&](uint64_t my0, uint32_t* sy) {
-        if (vec_ok && my0 + kEncPer <= a.n) {
-            const uint4* v4 = reinterpret_cast<const uint4*>(symp + my0);
-            constexpr int per16 = 16 / (int)sizeof(SymT);
+// K5 encode (ref src/huffman.cpp:127-131 + BitWriter :88-103), two kernels over 256-symbol
+// chunks (one warp, 8 symbols per lane):
+//  K5a k_encode_count (persistent, CTA c owns a contiguous span of chunks): per-chunk bit and
+//      escape counts, one decoupled look-back across CTAs for the span's global offsets, a
+//      CTA scan turning the span's counts into absolute per-chunk offsets, and zeroing of the
+//      words two chunks share (so no memset of the bitstream is needed).
+//  K5b k_encode_write (one warp per chunk, no CTA-wide synchronisation): codes in registers,
+//      warp scan of the lengths, MSB-first packing with a 64-bit accumulator into a per-warp
+//      shared stage (OR only where two lanes share a word), coalesced word stores (the two
+//      chunk-boundary words OR-ed), the outlier list and the decode sidecar.
+constexpr int kChunk = 32 * kEncPer;  // symbols per chunk
+
+// kLast: the second (last) read of the symbols, streamed (evict-first); the counting pass
+// keeps them in L2 for it.
+template <typename SymT, bool kLast>
+__device__ __forceinline__ void load_chunk_syms(const SymT* __restrict__ symp, uint64_t n,
+                                                uint64_t my0, bool vec_ok, uint32_t* sy) {
+    if (vec_ok && my0 + kEncPer <= n) {
+        const uint4* v4 = reinterpret_cast<const uint4*>(symp + my0);
+        constexpr int per16 = 16 / (int)sizeof(SymT);
 #pragma unroll
-            for (int q = 0; q < kEncPer / per16; ++q) {
-                const uint4 v = __ldg(v4 + q);
-                const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+        for (int q = 0; q < kEncPer / per16; ++q) {
+            const uint4 v = kLast ? __ldcs(v4 + q) : __ldg(v4 + q);
+            const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (sizeof(SymT) == 2) {
-                        sy[q * 8 + 2 * k] = w4[k] & 0xFFFFu;
-                        sy[q * 8 + 2 * k + 1] = w4[k] >> 16;
-                    } else {
-                        sy[q * 4 + k] = w4[k];
-                    }
+            for (int k = 0; k < 4; ++k) {
+                if (sizeof(SymT) == 2) {
+                    sy[q * 8 + 2 * k] = w4[k] & 0xFFFFu;
+                    sy[q * 8 + 2 * k + 1] = w4[k] >> 16;
+                } else {
+                    sy[q * 4 + k] = w4[k];
                 }
             }
-        } else {
-#pragma unroll
-            for (int i = 0; i < kEncPer; ++i) sy[i] = my0 + i < a.n ? (uint32_t)symp[my0 + i] : 0u;
         }
-    };
+    } else {
+#pragma unroll
+        for (int i = 0; i < kEncPer; ++i) sy[i] = my0 + i < n ? (uint32_t)symp[my0 + i] : 0u;
+    }
+}
 
-    // ---- phase 1: span totals ----------------------------------------------------------
-    unsigned long long tb_bits = 0, tb_esc = 0;
-    for (uint64_t t = tb; t < te; ++t) {
-        const uint64_t my0 = t * kEncTile + (uint64_t)tid * kEncPer;
-        uint32_t sy[kEncPer];
-        load_syms(my0, sy);
-        uint32_t bsum = 0, esum = 0;
+constexpr int kCountThreads = 1024;  // one counting CTA per SM: a short look-back chain
+
+// code length of symbol v: the compact table when every code is <= 27 bits
+template <bool kCompact>
+__device__ __forceinline__ uint32_t code_len(const EncodeArgs& a, uint32_t v) {
+    return kCompact ? __ldg(a.enc32 + v) >> 27 : (uint32_t)(__ldg(a.enc + v) & 0xFF);
+}
+
+template <typename SymT, bool kCompact>
+__global__ void __launch_bounds__(kCountThreads) k_encode_count(EncodeArgs a) {
+    const SymT* __restrict__ symp = static_cast<const SymT*>(a.sym);
+    __shared__ uint32_t s_a[kCountThreads / 32], s_b[kCountThreads / 32];
+    __shared__ unsigned long long s_red_bits[kCountThreads / 32], s_red_esc[kCountThreads / 32];
+    __shared__ unsigned long long s_base_bits, s_base_esc;
+    constexpr int W = kCountThreads / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t chunks = (a.n + kChunk - 1) / kChunk;
+    const uint64_t span = (chunks + gridDim.x - 1) / gridDim.x;
+    const uint64_t cb = (uint64_t)blockIdx.x * span, ce = min(chunks, cb + span);
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(symp) & 15) == 0;
+    unsigned long long* coff = a.chunk_off;
+
+    // ---- per-chunk counts (two chunks in flight per warp) -----------------------------
+    unsigned long long wb = 0, we = 0;
+    for (uint64_t c = cb + warp; c < ce; c += 2 * W) {
+        const uint64_t c2 = c + W;
+        uint32_t sy[kEncPer], sy2[kEncPer];
+        load_chunk_syms<SymT, false>(symp, a.n, c * kChunk + (uint64_t)lane * kEncPer, vec_ok, sy);
+        if (c2 < ce)
+            load_chunk_syms<SymT, false>(symp, a.n, c2 * kChunk + (uint64_t)lane * kEncPer, vec_ok, sy2);
+        uint32_t b1 = 0, e1 = 0, b2 = 0, e2 = 0;
 #pragma unroll
         for (int i = 0; i < kEncPer; ++i) {
-            if (my0 + i < a.n) {
-                bsum += (uint32_t)(__ldg(a.enc + sy[i]) & 0xFF);
-                esum += sy[i] == 0;
+            if (c * kChunk + (uint64_t)lane * kEncPer + i < a.n) {
+                b1 += code_len<kCompact>(a, sy[i]);
+                e1 += sy[i] == 0;
+            }
+            if (c2 < ce && c2 * kChunk + (uint64_t)lane * kEncPer + i < a.n) {
+                b2 += code_len<kCompact>(a, sy2[i]);
+                e2 += sy2[i] == 0;
             }
         }
-        tb_bits += bsum;
-        tb_esc += esum;
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        tb_bits += __shfl_xor_sync(0xffffffffu, tb_bits, o);
-        tb_esc += __shfl_xor_sync(0xffffffffu, tb_esc, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            b1 += __shfl_xor_sync(0xffffffffu, b1, o);
+            e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+            b2 += __shfl_xor_sync(0xffffffffu, b2, o);
+            e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        }
+        if (lane == 0) {
+            coff[2 * c] = b1;
+            coff[2 * c + 1] = e1;
+            if (c2 < ce) {
+                coff[2 * c2] = b2;
+                coff[2 * c2 + 1] = e2;
+            }
+        }
+        wb += b1 + (c2 < ce ? b2 : 0u);
+        we += e1 + (c2 < ce ? e2 : 0u);
     }
     if (lane == 0) {
-        s_red_bits[warp] = tb_bits;
-        s_red_esc[warp] = tb_esc;
+        s_red_bits[warp] = wb;
+        s_red_esc[warp] = we;
     }
     __syncthreads();
+
+    // ---- span offsets: decoupled look-back over the CTAs (warp 0) ----------------------
     if (warp == 0) {
-        unsigned long long rb = lane < kEncThreads / 32 ? s_red_bits[lane] : 0ull;
-        unsigned long long re = lane < kEncThreads / 32 ? s_red_esc[lane] : 0ull;
+        unsigned long long rb = lane < W ? s_red_bits[lane] : 0ull;
+        unsigned long long re = lane < W ? s_red_esc[lane] : 0ull;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             rb += __shfl_xor_sync(0xffffffffu, rb, o);
             re += __shfl_xor_sync(0xffffffffu, re, o);
         }
-        // decoupled look-back over the CTAs, 32 predecessors per probe
         const uint32_t c = blockIdx.x;
         TileStatus* st = a.status;
         volatile TileStatus* vst = st;
@@ -1178,49 +1220,129 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
     }
     __syncthreads();
 
-    // ---- phase 2: write ---------------------------------------------------------------
-    unsigned long long run_bits = s_base_bits, run_esc = s_base_esc;
-    for (uint64_t t = tb; t < te; ++t) {
-        const uint64_t my0 = t * kEncTile + (uint64_t)tid * kEncPer;
+    // ---- absolute chunk offsets (CTA scan of the span's counts) ------------------------
+    unsigned long long run_b = s_base_bits, run_e = s_base_esc;
+    for (uint64_t c0 = cb; c0 < ce; c0 += kCountThreads) {
+        const uint64_t c = c0 + tid;
+        const uint32_t vb = c < ce ? (uint32_t)coff[2 * c] : 0u;
+        const uint32_t ve = c < ce ? (uint32_t)coff[2 * c + 1] : 0u;
+        uint32_t xb, xe, tb, te;
+        block_scan2<kCountThreads>(vb, ve, &xb, &xe, &tb, &te, s_a, s_b);
+        if (c < ce) {
+            const unsigned long long off = run_b + xb;
+            coff[2 * c] = off;
+            coff[2 * c + 1] = run_e + xe;
+            // a word shared with the previous chunk: zeroed here, OR-ed by both writers
+            if ((off & 31) && c > 0) a.words[off >> 5] = 0u;
+        }
+        run_b += tb;
+        run_e += te;
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+        // the stream's last partial word and the decoder's read-ahead padding
+        const unsigned long long total = run_b;
+        const uint64_t w0 = total >> 5;
+        for (uint64_t w = w0 + tid; w < a.nwords + 32; w += kCountThreads) a.words[w] = 0u;
+    }
+}
+
+// kMode 0: every code <= 27 bits (compact u32 table); 1: <= 32 bits; 2: longer codes
+// (appended in two pieces).
+template <typename SymT, int kMode>
+__global__ void __launch_bounds__(kEncThreads) k_encode_write(EncodeArgs a, uint32_t stage_words) {
+    const SymT* __restrict__ symp = static_cast<const SymT*>(a.sym);
+    extern __shared__ uint32_t stage_all[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* stage = stage_all + warp * stage_words;
+    const uint64_t chunks = (a.n + kChunk - 1) / kChunk;
+    const bool vec_ok = (reinterpret_cast<uintptr_t>(symp) & 15) == 0;
+    // PrevValue sidecar intervals are powers of two >= kEncPer: at most one sidecar point per
+    // lane, at its first symbol; other intervals (Lorenzo2d: the plane size) take the general
+    // per-symbol path
+    const bool ipow2 = (a.interval & (a.interval - 1)) == 0;
+    const bool side_fast = ipow2 && a.interval >= (uint64_t)kEncPer;
+    const uint64_t imask = a.interval - 1;
+    const int ishift = __ffsll((long long)a.interval) - 1;
+    for (uint64_t c = blockIdx.x * (uint64_t)(kEncThreads / 32) + warp; c < chunks;
+         c += (uint64_t)gridDim.x * (kEncThreads / 32)) {
+        const uint64_t my0 = c * kChunk + (uint64_t)lane * kEncPer;
+        const int cnt = my0 >= a.n ? 0 : (a.n - my0 >= (uint64_t)kEncPer ? kEncPer : (int)(a.n - my0));
         uint32_t sy[kEncPer];
-        load_syms(my0, sy);
-        unsigned long long code[kEncPer];
-        uint32_t my_bits = 0, my_esc = 0, escmask = 0;
+        load_chunk_syms<SymT, true>(symp, a.n, my0, vec_ok, sy);
+        const unsigned long long cbit = a.chunk_off[2 * c];
+        const unsigned long long cesc = a.chunk_off[2 * c + 1];
+        unsigned long long code[kEncPer];  // (code << 8) | len
+        uint32_t my_bits = 0, escmask = 0;
 #pragma unroll
         for (int i = 0; i < kEncPer; ++i) {
-            code[i] = my0 + i < a.n ? __ldg(a.enc + sy[i]) : 0ull;
+            if (kMode == 0) {
+                const uint32_t e = i < cnt ? __ldg(a.enc32 + sy[i]) : 0u;
+                code[i] = ((unsigned long long)(e & 0x7FFFFFFu) << 8) | (e >> 27);
+            } else {
+                code[i] = i < cnt ? __ldg(a.enc + sy[i]) : 0ull;
+            }
             my_bits += (uint32_t)(code[i] & 0xFF);
-            if (my0 + i < a.n && sy[i] == 0) {
-                ++my_esc;
-                escmask |= 1u << i;
+            if (i < cnt && sy[i] == 0) escmask |= 1u << i;
+        }
+        const uint32_t my_esc = __popc(escmask);
+        uint32_t ib = my_bits, ie = my_esc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t xb = __shfl_up_sync(0xffffffffu, ib, o);
+            const uint32_t xe = __shfl_up_sync(0xffffffffu, ie, o);
+            if (lane >= o) {
+                ib += xb;
+                ie += xe;
             }
         }
-        uint32_t ex_bits, ex_esc, tot_bits, tot_esc;
-        block_scan2(my_bits, my_esc, &ex_bits, &ex_esc, &tot_bits, &tot_esc, s_a, s_b);
-        const uint32_t s0 = (uint32_t)(run_bits & 31);
-        const uint32_t nw = (s0 + tot_bits + 31) / 32;
-        for (uint32_t i = tid; i < nw + 2; i += kEncThreads) stage[i] = 0;
-        __syncthreads();
+        const uint32_t tot = __shfl_sync(0xffffffffu, ib, 31);
+        const uint32_t ex_bits = ib - my_bits, ex_esc = ie - my_esc;
+        const uint32_t s0 = (uint32_t)(cbit & 31);
+        const uint32_t nw = (s0 + tot + 31) / 32;
+        for (uint32_t i = lane; i < nw + 1; i += 32) stage[i] = 0;
+        __syncwarp();
+        // sidecar points and outliers (rare per symbol)
+        if (a.side_bitoff && cnt) {
+            if (side_fast) {
+                if ((my0 & imask) == 0) {
+                    const uint64_t si = my0 >> ishift;
+                    a.side_bitoff[si] = cbit + ex_bits;
+                    if (a.side_outl) a.side_outl[si] = (uint32_t)(cesc + ex_esc);
+                }
+            } else {
+                uint32_t lb = 0, le = 0;
+                for (int i = 0; i < cnt; ++i) {
+                    const uint64_t g = my0 + i;
+                    if ((ipow2 ? (g & imask) : g % a.interval) == 0) {
+                        const uint64_t si = ipow2 ? (g >> ishift) : g / a.interval;
+                        a.side_bitoff[si] = cbit + ex_bits + lb;
+                        if (a.side_outl) a.side_outl[si] = (uint32_t)(cesc + ex_esc + le);
+                    }
+                    lb += (uint32_t)(code[i] & 0xFF);
+                    le += (escmask >> i) & 1u;
+                }
+            }
+        }
+        if (escmask && a.x) {
+            unsigned long long gesc = cesc + ex_esc;
+            for (uint32_t m = escmask; m; m &= m - 1) {
+                const int i = __ffs(m) - 1;
+                a.out_index[gesc] = my0 + i;
+                a.out_value[gesc] = a.x[my0 + i];
+                ++gesc;
+            }
+        }
+        // MSB-first packing: 64-bit accumulator, whole words stored, the lane's first word
+        // (shared with the previous lane) and its trailing partial word OR-ed
         const uint32_t off = s0 + ex_bits;
-        unsigned long long gbit = run_bits + ex_bits;
-        unsigned long long gesc = run_esc + ex_esc;
-        // PrevValue sidecar intervals are powers of two: mask arithmetic (a 64-bit divide is
-        // ~100 instructions); Lorenzo2d uses the plane size and divides
-        const bool ipow2 = (a.interval & (a.interval - 1)) == 0;
-        const uint64_t imask = a.interval - 1;
-        const int ishift = __ffsll((long long)a.interval) - 1;
-        uint64_t next_side = !a.side_bitoff ? ~0ull
-                             : ipow2 ? ((my0 + imask) & ~imask)
-                                     : ((my0 + a.interval - 1) / a.interval) * a.interval;
         unsigned long long acc = 0;
         int nacc = (int)(off & 31);
         uint32_t wi = off >> 5;
-        bool first = true;
+        const uint32_t w_first = wi;
         auto emit = [&]() {
             const uint32_t word = (uint32_t)(acc >> 32);
-            if (first) {
+            if (wi == w_first) {
                 if (word) atomicOr(&stage[wi], word);
-                first = false;
             } else {
                 stage[wi] = word;
             }
@@ -1228,57 +1350,39 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(EncodeArgs a) {
             acc <<= 32;
             nacc -= 32;
         };
-        auto append = [&](unsigned long long c, int len) {  // len <= 32
-            acc |= c << (64 - nacc - len);
-            nacc += len;
-            if (nacc >= 32) emit();
-        };
 #pragma unroll
         for (int i = 0; i < kEncPer; ++i) {
-            const uint64_t g = my0 + i;
-            if (g >= a.n) break;
             const int len = (int)(code[i] & 0xFF);
-            const unsigned long long c = code[i] >> 8;
-            if (g == next_side) {
-                const uint64_t si = ipow2 ? (g >> ishift) : g / a.interval;
-                a.side_bitoff[si] = gbit;
-                if (a.side_outl) a.side_outl[si] = (uint32_t)gesc;
-                next_side += a.interval;
-            }
-            if (len > 32) {
-                append(c >> 32, len - 32);
-                append(c & 0xFFFFFFFFull, 32);
+            if (kMode == 2 && len > 32) {
+                const unsigned long long cv = code[i] >> 8;
+                acc |= (cv >> 32) << (64 - nacc - (len - 32));
+                nacc += len - 32;
+                if (nacc >= 32) emit();
+                acc |= (cv & 0xFFFFFFFFull) << (32 - nacc);
+                nacc += 32;
+                emit();
             } else {
-                append(c, len);
+                acc |= (code[i] >> 8) << (64 - nacc - len);
+                nacc += len;
+                if (nacc >= 32) emit();
             }
-            if ((escmask >> i) & 1u) {
-                if (a.x) {
-                    a.out_index[gesc] = g;
-                    a.out_value[gesc] = a.x[g];
-                }
-                ++gesc;
-            }
-            gbit += len;
         }
         if (nacc > 0) {
             const uint32_t word = (uint32_t)(acc >> 32);
             if (word) atomicOr(&stage[wi], word);
         }
-        __syncthreads();
-        const uint64_t gw0 = run_bits >> 5;
-        for (uint32_t i = tid; i < nw; i += kEncThreads) {
+        __syncwarp();
+        const uint64_t gw0 = cbit >> 5;
+        for (uint32_t i = lane; i < nw; i += 32) {
             const uint64_t gw = gw0 + i;
-            if (gw >= a.nwords) break;
             const uint32_t v = bswap32(stage[i]);
-            if (i == 0 || i == nw - 1) {
+            if ((i == 0 && s0) || (i == nw - 1 && ((s0 + tot) & 31))) {
                 if (v) atomicOr(&a.words[gw], v);
             } else {
                 a.words[gw] = v;
             }
         }
-        run_bits += tot_bits;
-        run_esc += tot_esc;
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -1356,28 +1460,58 @@ cudaError_t launch_build_tables(const uint32_t* book_sym, const uint8_t* book_le
     return cudaGetLastError();
 }
 
-cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t* launches) {
-    const uint64_t tiles = (a.n + kEncTile - 1) / kEncTile;
-    uint64_t grid = (uint64_t)sms * 3;  // persistent: 3 CTAs of 256 threads per SM
-    if (grid > tiles) grid = tiles;
+size_t encode_scratch_bytes(uint64_t n, int sms) {
+    const uint64_t chunks = (n + kChunk - 1) / kChunk;
+    return align256(sizeof(TileStatus) * (uint64_t)sms) + 16 * chunks + 256;
+}
+
+cudaError_t launch_encode(const EncodeArgs& a0, int sms, cudaStream_t s, uint64_t* launches) {
+    EncodeArgs a = a0;
+    const uint64_t chunks = (a.n + kChunk - 1) / kChunk;
+    uint64_t grid = (uint64_t)sms;  // persistent counting pass: one 1024-thread CTA per SM
+    if (grid > chunks) grid = chunks;
     if (grid == 0) grid = 1;
     cudaError_t e = cudaMemsetAsync(a.status, 0, sizeof(TileStatus) * grid, s);
     if (e != cudaSuccess) return e;
-    const size_t smem = ((size_t)kEncTile * (a.max_len ? a.max_len : 1) / 32 + 8) * 4;
+    a.chunk_off = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(a.status) + align256(sizeof(TileStatus) * (uint64_t)sms));
+    const int mode = a.max_len <= 27 ? 0 : a.max_len <= 32 ? 1 : 2;
+    if (a.sym16) {
+        if (mode == 0) k_encode_count<uint16_t, true><<<(unsigned)grid, kCountThreads, 0, s>>>(a);
+        else k_encode_count<uint16_t, false><<<(unsigned)grid, kCountThreads, 0, s>>>(a);
+    } else {
+        if (mode == 0) k_encode_count<uint32_t, true><<<(unsigned)grid, kCountThreads, 0, s>>>(a);
+        else k_encode_count<uint32_t, false><<<(unsigned)grid, kCountThreads, 0, s>>>(a);
+    }
+    ++*launches;
+    const uint32_t stage_words = (uint32_t)((uint64_t)kChunk * (a.max_len ? a.max_len : 1) / 32 + 4);
+    const size_t smem = (size_t)stage_words * 4 * (kEncThreads / 32);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
-        e = cudaFuncSetAttribute(k_encode<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(k_encode<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        if (e != cudaSuccess) return e;
+        for (const void* f : {(const void*)k_encode_write<uint16_t, 0>,
+                              (const void*)k_encode_write<uint16_t, 1>,
+                              (const void*)k_encode_write<uint16_t, 2>,
+                              (const void*)k_encode_write<uint32_t, 0>,
+                              (const void*)k_encode_write<uint32_t, 1>,
+                              (const void*)k_encode_write<uint32_t, 2>}) {
+            e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
         attr = smem;
     }
-    if (a.sym16)
-        k_encode<uint16_t><<<(unsigned)grid, kEncThreads, smem, s>>>(a);
-    else
-        k_encode<uint32_t><<<(unsigned)grid, kEncThreads, smem, s>>>(a);
+    const uint64_t wgrid = std::min<uint64_t>((chunks + kEncThreads / 32 - 1) / (kEncThreads / 32),
+                                              (uint64_t)sms * 16);
+#define ACZ_ENC_WRITE(T, M) k_encode_write<T, M><<<(unsigned)wgrid, kEncThreads, smem, s>>>(a, stage_words)
+    if (a.sym16) {
+        if (mode == 0) ACZ_ENC_WRITE(uint16_t, 0);
+        else if (mode == 1) ACZ_ENC_WRITE(uint16_t, 1);
+        else ACZ_ENC_WRITE(uint16_t, 2);
+    } else {
+        if (mode == 0) ACZ_ENC_WRITE(uint32_t, 0);
+        else if (mode == 1) ACZ_ENC_WRITE(uint32_t, 1);
+        else ACZ_ENC_WRITE(uint32_t, 2);
+    }
+#undef ACZ_ENC_WRITE
     ++*launches;
     return cudaGetLastError();
 }

@@ -91,6 +91,7 @@ struct EncodeArgs {
     int sym16;
     uint64_t n;
     const unsigned long long* enc;   // dense symbol -> (code << 8 | len)
+    const uint32_t* enc32;           // dense symbol -> code | len << 27 (books with codes <= 27 bits)
     const float* x;                  // for outlier values (nullptr: no outlier output)
     uint32_t* words;                 // bitstream, big-endian bit order, stored byte-swapped
     uint64_t nwords;
@@ -100,12 +101,14 @@ struct EncodeArgs {
     uint32_t* side_outl;
     uint64_t interval;
     uint32_t max_len;
-    TileStatus* status;              // one entry per encode CTA (<= ceil(n / kEncTile)), zeroed by the launcher
-    unsigned int* ticket;            // zeroed by the launcher
+    TileStatus* status;              // encode_scratch_bytes(n, sms) of scratch (look-back + chunk offsets)
+    unsigned int* ticket;            // unused
+    unsigned long long* chunk_off;   // set by the launcher (inside the scratch)
 };
 constexpr int kEncThreads = 256;
 constexpr int kEncPer = 8;
 constexpr int kEncTile = kEncThreads * kEncPer;
+size_t encode_scratch_bytes(uint64_t n, int sms);
 cudaError_t launch_encode(const EncodeArgs& a, int sms, cudaStream_t s, uint64_t* launches);
 
 // ---- decode.cu ----
