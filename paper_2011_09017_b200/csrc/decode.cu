@@ -160,47 +160,61 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
     const uint32_t I = (uint32_t)a.interval;
     const uint32_t P32 = (uint32_t)min(a.g.plane_size, (uint64_t)0xFFFFFFFFu);
     const int R = (int)a.radius;
-    const double step = a.step, eb = a.eb;
-    const bool zf = a.zero_filter != 0;
+    const double step = a.step;
+    // q = sym - R as a double without an int->double conversion: hi:lo = 1.5*2^52 + sym
+    const double magic = 6755399441055744.0 + (double)R;
+    // zero filter |v| <= eb on a float v  <=>  |v| <= the largest float <= eb
+    float zthr = -1.0f;
+    if (a.zero_filter) {
+        zthr = __double2float_rd(a.eb);
+    }
     uint32_t oi = 0xFFFFFFFFu;  // outlier cursor, found at the first escape
     auto word = [&](PosT i) -> uint32_t {
         return bswap32(kStaged ? bits[i] : __ldg(bits + i));
     };
+    // one symbol: parse (LUT, long codes by canonical limits), reconstruct
+    // (ref src/codec.cpp:143-164; r is an exact float held in a double)
+    auto step_one = [&](uint32_t gidx, bool reset) -> float {
+        const PosT i = p >> 5;
+        const uint32_t o = (uint32_t)p & 31u;
+        const uint32_t w0 = word(i), w1 = word(i + 1);
+        const uint32_t top = __funnelshift_l(w1, w0, o);  // stream bits [p, p+32)
+        const uint32_t e = s_lut[top >> (32 - kLutBits)];
+        uint32_t len = e & 31, sym = e >> 5;
+        if (!len) {
+            // long code: canonical limit search on a 64-bit window
+            const uint32_t w2 = word(i + 2);
+            const unsigned long long win =
+                ((unsigned long long)top << 32) | __funnelshift_l(w2, w1, o);
+            len = kLutBits + 1;
+            while (len < 64 && (win >> (64 - len)) >= lim.lim[len]) ++len;
+            const unsigned long long c = win >> (64 - len);
+            const uint32_t idx = ct.first_index[len] + (uint32_t)(c - lim.nc[len]);
+            sym = lbook ? lbook[idx - lfirst] : __ldg(a.book_sym + idx);
+        }
+        p += len;
+        float v;
+        if (sym == 0) {
+            if (oi == 0xFFFFFFFFu)
+                oi = lower_bound_u64(a.out_index, (uint32_t)a.n_outliers, start + gidx);
+            v = __ldg(a.out_value + oi);
+            ++oi;
+        } else {
+            const double q = __dsub_rn(__hiloint2double(0x43380000, (int)sym), magic);
+            const double pred = reset ? 0.0 : r;
+            v = __double2float_rn(__dadd_rn(pred, __dmul_rn(q, step)));
+        }
+        r = (double)v;
+        return fabsf(v) <= zthr ? 0.0f : v;
+    };
     for (uint32_t t0 = 0; t0 < I; t0 += 32) {
         if (t0 < cnt) {
             const uint32_t m = min(32u, cnt - t0);
+            // (a per-lane fast path without the plane-start test diverges across the warp's
+            // lanes on small planes and measured slower)
+#pragma unroll 4
             for (uint32_t j = 0; j < m; ++j) {
-                const PosT i = p >> 5;
-                const uint32_t o = (uint32_t)p & 31u;
-                const uint32_t w0 = word(i), w1 = word(i + 1);
-                const uint32_t top = __funnelshift_l(w1, w0, o);  // stream bits [p, p+32)
-                const uint32_t e = s_lut[top >> (32 - kLutBits)];
-                uint32_t len = e & 31, sym = e >> 5;
-                if (!len) {
-                    // long code: canonical limit search on a 64-bit window
-                    const uint32_t w2 = word(i + 2);
-                    const unsigned long long win =
-                        ((unsigned long long)top << 32) | __funnelshift_l(w2, w1, o);
-                    len = kLutBits + 1;
-                    while (len < 64 && (win >> (64 - len)) >= lim.lim[len]) ++len;
-                    const unsigned long long c = win >> (64 - len);
-                    const uint32_t idx = ct.first_index[len] + (uint32_t)(c - lim.nc[len]);
-                    sym = lbook ? lbook[idx - lfirst] : __ldg(a.book_sym + idx);
-                }
-                p += len;
-                // reconstruct (ref src/codec.cpp:143-164); r is an exact float in a double
-                float v;
-                if (sym == 0) {
-                    if (oi == 0xFFFFFFFFu)
-                        oi = lower_bound_u64(a.out_index, (uint32_t)a.n_outliers, start + t0 + j);
-                    v = __ldg(a.out_value + oi);
-                    ++oi;
-                } else {
-                    const double pred = to_reset == 0 ? 0.0 : r;
-                    v = __double2float_rn(__dadd_rn(pred, __dmul_rn((double)((int)sym - R), step)));
-                }
-                r = (double)v;
-                tile[j] = (zf && fabs(r) <= eb) ? 0.0f : v;
+                tile[j] = step_one(t0 + j, to_reset == 0);
                 to_reset = to_reset + 1 == P32 ? 0u : to_reset + 1;
             }
         }
