@@ -196,40 +196,53 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
     const uint64_t ph = (p.interval - ((plane_flat0 + seg0) & (p.interval - 1))) & (p.interval - 1);
     const uint32_t sc_off = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
     const uint32_t sc_mask = p.interval > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)(p.interval - 1);
-    // Carried across the 32-position words: the previous position's output and "tiny
-    // accepted" flag, and the last position that is not an identity continuation of a
-    // collapsed run (id[c]: sym[c] == R and position c-1 tiny accepted). The re-expansion
-    // certificate needs, for position i, the last c in [b, i-1] with c == b or !id[c]; a
-    // ballot over the word finds it in O(1) instead of walking the run back.
-    float carry_out = 0.0f;
-    bool carry_tiny = false;
-    int carry_nid = -1;
-    for (int w = i0 >> 5; w * 32 < len; ++w) {
-        const int i = w * 32 + lane;
-        const bool valid = i >= i0 && i < len;
-        const float out = valid ? S.s[i] : 0.0f;
-        const uint32_t sy = valid ? (uint32_t)S.sym[i] : 0u;
-        const bool tiny = sy != 0 && fabs((double)out) < p.eb;
-        float prev_out = __shfl_up_sync(0xffffffffu, out, 1);
-        bool prev_tiny = __shfl_up_sync(0xffffffffu, (int)tiny, 1) != 0;
-        if (lane == 0) {
-            prev_out = carry_out;
-            prev_tiny = carry_tiny;
+    // Masks of positions >= i0 are rebuilt (OR-ed below); positions < i0 keep theirs.
+    for (int w = (i0 >> 5) + lane; w < kCapW; w += kW) {
+        const uint32_t keep = w == (i0 >> 5) ? ((1u << (i0 & 31)) - 1u) : 0u;
+        S.cand[w] &= keep;
+#pragma unroll
+        for (int L = 0; L < kLev; ++L) S.lvl[L][w] &= keep;
+    }
+    __syncwarp();
+    // Lane-sequential over a contiguous window of an odd number of positions (odd strides
+    // between the lanes' shared-memory accesses are bank-conflict free): no warp-synchronous
+    // step per element, so a lane's consecutive elements overlap. Carried in registers: the
+    // previous position's output and "tiny accepted" flag, and the last position that is not
+    // an identity continuation of a collapsed run (id[c]: sym[c] == R and position c-1 tiny
+    // accepted), which the re-expansion certificate needs.
+    const int wl = ((len - i0 + kW - 1) / kW) | 1;
+    const int b = i0 + lane * wl, e = min(len, b + wl);
+    if (b < e) {
+        float prev_out = 0.0f;
+        bool prev_tiny = false;
+        if (b > i0) {  // (position i0 is a range start: no carry needed)
+            prev_out = S.s[b - 1];
+            prev_tiny = S.sym[b - 1] != 0 && fabs((double)prev_out) < p.eb;
         }
-        const bool id = valid && sy == (uint32_t)p.R && prev_tiny;
-        const unsigned nid = __ballot_sync(0xffffffffu, !id);
-        const unsigned nid_below = nid & ((1u << lane) - 1u);
-        const int last_nid = nid_below ? (w << 5) + 31 - __clz(nid_below) : carry_nid;
-        carry_out = __shfl_sync(0xffffffffu, out, 31);
-        carry_tiny = __shfl_sync(0xffffffffu, (int)tiny, 31) != 0;
-        carry_nid = (w << 5) + 31 - __clz(nid);  // nid != 0: invalid tail lanes count as !id
-        bool c = false;
-        int lvlex = -100000;
-        if (valid) {
-            // range starts are rare (one per range): only they need the range index
-            const bool start = (S.rsb[w] >> (i & 31)) & 1u;
+        int last_nid = -1;  // -1: none seen in this window yet (then walk the run back)
+        int cur = b >> 5;
+        uint32_t cw = 0, lw[kLev] = {};
+        auto flush = [&]() {
+            if (cw) atomicOr(&S.cand[cur], cw);
+#pragma unroll
+            for (int L = 0; L < kLev; ++L)
+                if (lw[L]) atomicOr(&S.lvl[L][cur], lw[L]);
+            cw = 0;
+#pragma unroll
+            for (int L = 0; L < kLev; ++L) lw[L] = 0;
+        };
+        for (int i = b; i < e; ++i) {
+            if ((i >> 5) != cur) {
+                flush();
+                cur = i >> 5;
+            }
+            const bool start = (S.rsb[i >> 5] >> (i & 31)) & 1u;
             const float xf = S.xs[xoff + i];
-            c = start;
+            const float out = S.s[i];
+            const uint32_t sy = (uint32_t)S.sym[i];
+            const bool tiny = sy != 0 && fabs((double)out) < p.eb;
+            bool c = start;
+            int lvlex = -100000;
             if (sy == 0) {
                 c = true;
             } else {
@@ -266,7 +279,15 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
                         // re-expansion certificate for any |D| <= Tmax; ycol = pre-value of
                         // the run's last non-identity element
                         const int k = range_of(i);
-                        const int cc = max(last_nid, (int)S.rstart[k]);
+                        const int rb = S.rstart[k];
+                        int cc = last_nid;
+                        if (cc < 0) {
+                            cc = i - 1;
+                            while (cc > rb && S.sym[cc] == (SymT)p.R && S.sym[cc - 1] != 0 &&
+                                   fabs((double)S.s[cc - 1]) < p.eb)
+                                --cc;
+                        }
+                        cc = max(cc, rb);
                         const double ycol = __dadd_rn(pred_of(cc, k),
                                                       __dmul_rn((double)((long long)S.sym[cc] - p.R), p.step));
                         const double dmax = pow2(fexp(2.0 * fmax(fabs(ycol), 2.0 * p.Tmax)) - 22);
@@ -275,17 +296,16 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
                 }
             }
             if ((((uint32_t)i - sc_off) & sc_mask) == 0) c = true;  // sidecar point
-        }
-        const unsigned cb = __ballot_sync(0xffffffffu, c);
-        unsigned lb[kLev];
+            const uint32_t bit = 1u << (i & 31);
+            if (c) cw |= bit;
 #pragma unroll
-        for (int L = 1; L <= kLev; ++L) lb[L - 1] = __ballot_sync(0xffffffffu, lvlex > p.B - L);
-        if (lane == 0) {
-            const uint32_t keep = (w == (i0 >> 5) && (i0 & 31)) ? ((1u << (i0 & 31)) - 1u) : 0u;
-            S.cand[w] = (S.cand[w] & keep) | cb;
-#pragma unroll
-            for (int L = 0; L < kLev; ++L) S.lvl[L][w] = (S.lvl[L][w] & keep) | lb[L];
+            for (int L = 1; L <= kLev; ++L)
+                if (lvlex > p.B - L) lw[L - 1] |= bit;
+            if (!(sy == (uint32_t)p.R && prev_tiny)) last_nid = i;
+            prev_out = out;
+            prev_tiny = tiny;
         }
+        flush();
     }
 }
 
