@@ -213,12 +213,13 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
     const int wl = ((len - i0 + kW - 1) / kW) | 1;
     const int b = i0 + lane * wl, e = min(len, b + wl);
     if (b < e) {
-        float prev_out = 0.0f;
+        double prev_out = 0.0;
         bool prev_tiny = false;
         if (b > i0) {  // (position i0 is a range start: no carry needed)
-            prev_out = S.s[b - 1];
-            prev_tiny = S.sym[b - 1] != 0 && fabs((double)prev_out) < p.eb;
+            prev_out = (double)S.s[b - 1];
+            prev_tiny = S.sym[b - 1] != 0 && fabs(prev_out) < p.eb;
         }
+        const double qmagic = 6755399441055744.0 + (double)p.R;  // q = (1.5*2^52 + sym) - this
         int last_nid = -1;  // -1: none seen in this window yet (then walk the run back)
         int cur = b >> 5;
         uint32_t cw = 0, lw[kLev] = {};
@@ -238,42 +239,42 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
             }
             const bool start = (S.rsb[i >> 5] >> (i & 31)) & 1u;
             const float xf = S.xs[xoff + i];
-            const float out = S.s[i];
+            const double outd = (double)S.s[i];
             const uint32_t sy = (uint32_t)S.sym[i];
-            const bool tiny = sy != 0 && fabs((double)out) < p.eb;
+            const bool tiny = sy != 0 && fabs(outd) < p.eb;
             bool c = start;
             int lvlex = -100000;
             if (sy == 0) {
                 c = true;
             } else {
                 const double pred = start ? ((seg0 == 0 && i == 0) ? 0.0 : (double)S.guess[range_of(i)])
-                                          : (double)prev_out;
+                                          : prev_out;
                 const double orig = (double)xf;
                 const double d = __dsub_rn(orig, pred);
                 // the chain already fixed q exactly (pass 1, same prefix): q = sym - R
-                const double q = (double)((int)sy - (int)p.R);
+                const double q = __dsub_rn(__hiloint2double(0x43380000, (int)sy), qmagic);
                 const double t = __dmul_rn(d, p.inv_step);
                 const double pre = __dadd_rn(pred, __dmul_rn(q, p.step));
                 const double dm = (0.5 - fabs(t - q)) * p.step;
-                const double am = p.eb - fabs(orig - (double)out);
+                const double am = p.eb - fabs(orig - outd);
                 if (fmin(dm, am) <= 2.0 * p.Tmax) c = true;
                 if (fabs(q) >= p.radius_d - 1.0) c = true;
                 const bool coll_before = !start && prev_tiny;
                 if (q == 0.0 && coll_before) {
                     // identity inside a collapsed run
-                } else if (fabs((double)out) < p.eb) {
-                    if (out != 0.0f) lvlex = fexp((double)out);
+                } else if (fabs(outd) < p.eb) {
+                    if (outd != 0.0) lvlex = fexp(outd);
                     // the lazy collapse formula RN32(pre + D) needs pre == prev + q*step exactly
                     if (__dsub_rn(pre, pred) != __dmul_rn(q, p.step)) c = true;
                 } else {
-                    const int ex = fexp((double)out);
+                    const int ex = fexp(outd);
                     lvlex = ex;
                     if (ex > p.B) c = true;
-                    const double a = fabs((double)out), lo = pow2(ex);
+                    const double a = fabs(outd), lo = pow2(ex);
                     if (a - lo <= 2.0 * p.Tmax || 2.0 * lo - a <= 2.0 * p.Tmax) c = true;
                     // distance of the pre-value to the nearest rounding midpoint of its grid
                     const double half = pow2(fexp(pre) - 24);
-                    const double fr = half - fabs(pre - (double)out);
+                    const double fr = half - fabs(pre - outd);
                     if (fr == 0.0) c = true;  // exact RNE tie
                     if (coll_before) {
                         // re-expansion certificate for any |D| <= Tmax; ycol = pre-value of
@@ -302,7 +303,7 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
             for (int L = 1; L <= kLev; ++L)
                 if (lvlex > p.B - L) lw[L - 1] |= bit;
             if (!(sy == (uint32_t)p.R && prev_tiny)) last_nid = i;
-            prev_out = out;
+            prev_out = outd;
             prev_tiny = tiny;
         }
         flush();
