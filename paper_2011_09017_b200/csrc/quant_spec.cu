@@ -59,6 +59,7 @@ struct SP {
     float anchor_min;
     int B;  // anchor binade exponent
     uint64_t P, nseg, interval, planes;
+    int ishift;  // log2(interval): PrevValue sidecar intervals are powers of two
 };
 
 struct XS {
@@ -703,7 +704,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             if (lane == 0) {
                 S.sym[pos] = (SymT)ex.sym;
                 const uint64_t flat = plane_flat0 + pi;
-                if ((flat & (p.interval - 1)) == 0) side_state[flat / p.interval] = pi == 0 ? 0.0f : tprev;
+                if ((flat & (p.interval - 1)) == 0) side_state[flat >> p.ishift] = pi == 0 ? 0.0f : tprev;
             }
             __syncwarp();
             T = ex.out;
@@ -809,7 +810,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         }
         if (active && lane < f) {
             const uint64_t flat = plane_flat0 + seg0 + (uint64_t)vp;
-            if ((flat & (p.interval - 1)) == 0) side_state[flat / p.interval] = (seg0 + vp == 0) ? 0.0f : tprev;
+            if ((flat & (p.interval - 1)) == 0) side_state[flat >> p.ishift] = (seg0 + vp == 0) ? 0.0f : tprev;
         }
         if (f < 32) {
             const int fvp = __shfl_sync(0xffffffffu, vp, f);
@@ -832,7 +833,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             if (lane == f) {
                 S.sym[fvp] = (SymT)fsym;
                 const uint64_t flat = plane_flat0 + seg0 + (uint64_t)fvp;
-                if ((flat & (p.interval - 1)) == 0) side_state[flat / p.interval] = (seg0 + fvp == 0) ? 0.0f : ftp;
+                if ((flat & (p.interval - 1)) == 0) side_state[flat >> p.ishift] = (seg0 + fvp == 0) ? 0.0f : ftp;
             }
             __syncwarp();
             const float fss = S.s[fvp];
@@ -965,6 +966,7 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     p.P = a.g.plane_size;
     p.nseg = (p.P + kSeg - 1) / kSeg;
     p.interval = a.interval;
+    p.ishift = __builtin_ctzll(a.interval);
     p.planes = a.g.planes;
     p.inv_step = 1.0 / a.step;
     p.exact_div = make_qparams(a.eb, a.radius).exact_div;

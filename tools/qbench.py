@@ -45,4 +45,7 @@ for nm in which:
     print("   decode cycles/warp: prologue %.0f staging %.0f loop %.0f (warps %d)" % (v[20] / nw, v[21] / nw, v[22] / nw, v[23]))
     print("   walk cycles: per exact step %.0f, per batch %.0f" % (v[24] / max(1, v[2]), v[25] / max(1, v[0])))
     print("   phase A split (cycles/elem): pass1 %.1f classify %.1f" % (v[26] / n, v[27] / n))
+    nb = max(1, v[15])
+    print("   codebook cycles: compact %.0f sort %.0f tree %.0f depths %.0f canon %.0f tables %.0f (books %d)" % tuple(
+        [v[8 + i] / nb for i in range(6)] + [v[15]]))
     print("   spec cycles/elem (per segment-warp): phaseA %.1f wait %.1f walk %.1f out %.1f" % tuple(v[16 + i] / n for i in range(4)))
