@@ -331,25 +331,116 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
         return;
     }
 
-    // (2) bitonic sort of the keys in shared memory (p2 = next power of two >= k; a
-    // register/shuffle hybrid measured slower on B200 for 64-bit keys)
+    // (2) stable LSD radix sort of the keys by frequency, 4-bit digits (keys are
+    // freq << 16 | leaf with leaves in ascending symbol order, so a stable sort by frequency
+    // gives the (freq, leaf) order). Thread t owns keys [8t, 8t+8); the 16 bucket counters
+    // of a thread are packed as 16-bit fields in four u64 (sums <= 8192 never carry across
+    // fields) and block-scanned together. The ifreq region is the ping-pong buffer.
     {
-        uint32_t p2 = 2;
-        while (p2 < k) p2 <<= 1;
-        for (uint32_t size = 2; size <= p2; size <<= 1) {
-            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t i = tid; i < p2 / 2; i += kCbThreads) {
-                    const uint32_t lo = 2 * i - (i & (stride - 1));
-                    const uint32_t hi = lo + stride;
-                    const bool asc = (lo & size) == 0;
-                    const unsigned long long a = key[lo], b = key[hi];
-                    if ((a > b) == asc) {
-                        key[lo] = b;
-                        key[hi] = a;
-                    }
-                }
-                __syncthreads();
+        constexpr int PER = kFastLeaves / kCbThreads;
+        __shared__ unsigned long long s_wsum[kCbWarps][4];
+        __shared__ unsigned long long s_wtot[4];
+        __shared__ unsigned long long s_mx;
+        unsigned long long mx = 0;
+        for (uint32_t p = tid; p < k; p += kCbThreads) mx = max(mx, key[p] >> 16);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (tid == 0) s_mx = 0;
+        __syncthreads();
+        if (lane == 0) atomicMax(&s_mx, mx);
+        __syncthreads();
+        const int fbits = 64 - __clzll(s_mx | 1ull);
+        const int passes = (fbits + 3) / 4;
+        unsigned long long* src = key;
+        unsigned long long* dst = ifreq;
+        for (int ps = 0; ps < passes; ++ps) {
+            const int sh = 16 + 4 * ps;
+            unsigned long long kk[PER];
+            uint32_t dg[PER];
+            unsigned long long c[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const uint32_t idx = (uint32_t)tid * PER + j;
+                kk[j] = idx < k ? src[idx] : 0ull;
+                dg[j] = (uint32_t)(kk[j] >> sh) & 15u;
+                const unsigned long long inc = idx < k ? 1ull << (16 * (dg[j] & 3)) : 0ull;
+                const uint32_t q = dg[j] >> 2;
+                c[0] += q == 0 ? inc : 0ull;
+                c[1] += q == 1 ? inc : 0ull;
+                c[2] += q == 2 ? inc : 0ull;
+                c[3] += q == 3 ? inc : 0ull;
             }
+            // block exclusive scan of the packed counters (thread order == key order)
+            unsigned long long x[4] = {c[0], c[1], c[2], c[3]};
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned long long y = __shfl_up_sync(0xffffffffu, x[q], o);
+                    if (lane >= o) x[q] += y;
+                }
+            }
+            if (lane == 31)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s_wsum[warp][q] = x[q];
+            __syncthreads();
+            if (warp == 0) {  // exclusive scan of the 32 warp sums; row kCbWarps = totals
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned long long v = s_wsum[lane][q];
+                    unsigned long long incl = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    __syncwarp();
+                    s_wsum[lane][q] = incl - v;
+                    if (lane == 31) s_wtot[q] = incl;
+                }
+            }
+            __syncthreads();
+            unsigned long long wpre[4], tot[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                wpre[q] = s_wsum[warp][q];
+                tot[q] = s_wtot[q];
+            }
+            // bucket bases: exclusive scan of the 16 totals, packed the same way
+            unsigned long long base[4] = {0ull, 0ull, 0ull, 0ull};
+            {
+                unsigned long long run = 0;
+#pragma unroll
+                for (int d = 0; d < 16; ++d) {
+                    base[d >> 2] |= run << (16 * (d & 3));
+                    run += (tot[d >> 2] >> (16 * (d & 3))) & 0xFFFFull;
+                }
+            }
+            unsigned long long cur[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cur[q] = base[q] + wpre[q] + (x[q] - c[q]);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const uint32_t idx = (uint32_t)tid * PER + j;
+                if (idx < k) {
+                    const uint32_t q = dg[j] >> 2, f = 16 * (dg[j] & 3);
+                    const unsigned long long cq = q == 0 ? cur[0] : q == 1 ? cur[1] : q == 2 ? cur[2] : cur[3];
+                    dst[(cq >> f) & 0xFFFFull] = kk[j];
+                    const unsigned long long inc = 1ull << f;
+                    cur[0] += q == 0 ? inc : 0ull;
+                    cur[1] += q == 1 ? inc : 0ull;
+                    cur[2] += q == 2 ? inc : 0ull;
+                    cur[3] += q == 3 ? inc : 0ull;
+                }
+            }
+            __syncthreads();
+            unsigned long long* t = src;
+            src = dst;
+            dst = t;
+        }
+        if (src != key) {
+            for (uint32_t p = tid; p < k; p += kCbThreads) key[p] = src[p];
+            __syncthreads();
         }
     }
 
