@@ -253,9 +253,9 @@ def run_ours(args, rank, world, local_rank):
         dt = time.perf_counter() - t0
         res["e2e"] = {"value": (8 * n_total + 2 * cb) * args.e2e_steps / dt / 1e9, "unit": "GB/s",
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                      "path": "compress_host_many + decompress_host_many (acz_gpu_compress_batch / "
-                              "decompress_batch, blob_to_host / blob_from_host; page-locked host "
-                              "buffers, copies inside the timed region)"}
+                      "path": "compress_host_many + decompress_host_many (C-ABI "
+                              "acz_gpu_compress_host_batch / acz_gpu_decompress_host_batch; "
+                              "page-locked host buffers, copies inside the timed region)"}
         # bit-exactness spot check of the e2e path against the device path
         res["e2e"]["matches_device_path"] = bool(all(torch.equal(h.to(dev), o)
                                                      for h, o in zip(hout, outs)))

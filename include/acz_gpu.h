@@ -134,6 +134,16 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
                                 const uint64_t* acz1_cap, uint64_t* acz1_size,
                                 uint8_t* const* sidecar, const uint64_t* sidecar_cap,
                                 uint64_t* sidecar_size, int* status);
+/* Host-buffer batched decompress: count ACZ1 blobs (+ optional decode sidecars) in host
+ * memory -> fp32 host tensors (h_out[i] holds out_cap[i] elements). Same checks and errors as
+ * acz_gpu_blob_from_host + acz_gpu_decompress per blob (status[i]); the blobs are uploaded
+ * smallest first on one copy stream, each decode starts when its own upload has landed and
+ * each reconstruction is copied back on a second copy stream (page-locked buffers overlap
+ * the two PCIe directions). Synchronous on return; the first failure is returned. */
+int acz_gpu_decompress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const uint8_t* const* acz1,
+                                  const uint64_t* acz1_size, const uint8_t* const* sidecar,
+                                  const uint64_t* sidecar_size, int zero_filter,
+                                  float* const* h_out, const uint64_t* out_cap, int* status);
 /* Batched decompress (ref Controller::unwrap_backward src/controller.cpp:234-249 for every
  * handle of a step), stream-ordered on `stream` through the internal streams. */
 int acz_gpu_decompress_batch(acz_gpu_ctx* ctx, uint32_t count, const acz_gpu_blob* const* blobs,

@@ -52,6 +52,9 @@ SIGNATURES = [
                                               C.c_double, C.c_uint32, C.c_uint32, C.POINTER(_vp),
                                               _u64p, _u64p, C.POINTER(_vp), _u64p, _u64p,
                                               C.POINTER(C.c_int)]),
+    ("acz_gpu_decompress_host_batch", C.c_int, [_vp, C.c_uint32, C.POINTER(_vp), _u64p,
+                                                C.POINTER(_vp), _u64p, C.c_int, C.POINTER(_vp),
+                                                _u64p, C.POINTER(C.c_int)]),
     ("acz_gpu_decompress_batch", C.c_int, [_vp, C.c_uint32, C.POINTER(_vp), C.c_int,
                                            C.POINTER(_vp), _vp]),
     ("acz_gpu_blob_info", C.c_int, [_vp, C.POINTER(BlobInfo)]),

@@ -497,43 +497,51 @@ def compress_host_many(hosts: Sequence, p: CodecParams = CodecParams(), blob_buf
 
 def decompress_host_many(blobs, zero_filter: bool = False, outs=None,
                          ctx: Optional[Context] = None, stream=None):
-    """Host-buffer decompress of a whole activation set: [(ACZ1 bytes, sidecar or None)]
-    (numpy uint8 views of page-locked memory copy at full PCIe speed) in, host fp32 tensors
-    out (outs: optional page-locked torch tensors). Parses + validates like ref
-    blob_from_bytes. Pipelined across tensors: tensor i's reconstruction is copied back to
-    the host on a copy stream while tensor i+1 is uploaded and decoded."""
+    """Host-buffer decompress of a whole activation set (acz_gpu_decompress_host_batch):
+    [(ACZ1 bytes, sidecar or None)] (numpy uint8 arrays; page-locked memory copies at full
+    PCIe speed) in, host fp32 tensors out (outs: optional page-locked torch tensors,
+    default: allocated). Parses + validates like ref blob_from_bytes; uploads, decodes and
+    downloads overlap across tensors. Raises the first failure's exception."""
     import torch
     ctx = ctx or default_context()
-    dev = torch.device("cuda", ctx.device)
-    s = stream or torch.cuda.current_stream(dev)
-    cin = torch.cuda.Stream(dev)   # uploads (blob_from_host waits for its own copies only)
-    cout = torch.cuda.Stream(dev)  # downloads: overlap the next tensor's upload (full duplex)
-    cin.wait_stream(s)
-    lib = _native.load()
-    res = [None] * len(blobs)
-    # smallest blob first: the download stream (the bound: outputs are ~3x the blobs) starts
-    # after one short upload + decode and then stays fed while later blobs upload
-    order = sorted(range(len(blobs)), key=lambda j: len(blobs[j][0]))
-    for i in order:
-        blob, side = blobs[i]
-        blob = np.ascontiguousarray(blob, dtype=np.uint8)
-        h = C.c_void_p()
-        sp = C.c_void_p(side.ctypes.data) if side is not None and len(side) else None
-        _check(lib.acz_gpu_blob_from_host(ctx.handle, C.c_void_p(blob.ctypes.data), blob.size, sp,
-                                          len(side) if sp is not None else 0, _stream_handle(cin),
-                                          C.byref(h)), ctx)
-        s.wait_stream(cin)  # the blob's device copy is complete (blob_from_host synchronised)
-        c = CompressedTensor(h, ctx)
-        d = decompress(c, zero_filter=zero_filter, stream=s)
-        o = outs[i] if outs is not None else torch.empty(tuple(c.shape), dtype=torch.float32,
-                                                         pin_memory=True)
-        cout.wait_stream(s)
-        d.record_stream(cout)
-        with torch.cuda.stream(cout):
-            o.view(d.shape).copy_(d, non_blocking=True)
-        res[i] = o
-    cout.synchronize()
+    if stream is not None:
+        stream.synchronize()
+    k = len(blobs)
+    if k == 0:
+        return []
+    arrs = [np.ascontiguousarray(b, dtype=np.uint8) for b, _ in blobs]
+    sides = [None if sd is None or len(sd) == 0 else np.ascontiguousarray(sd, dtype=np.uint8)
+             for _, sd in blobs]
+    if outs is None:
+        outs = []
+        for a in arrs:
+            shape = _acz1_shape(a)
+            outs.append(torch.empty(shape, dtype=torch.float32, pin_memory=True))
+    ptrs = (C.c_void_p * k)(*[a.ctypes.data for a in arrs])
+    sizes = (C.c_uint64 * k)(*[a.size for a in arrs])
+    sp = (C.c_void_p * k)(*[sd.ctypes.data if sd is not None else None for sd in sides])
+    ss = (C.c_uint64 * k)(*[sd.size if sd is not None else 0 for sd in sides])
+    op = (C.c_void_p * k)(*[o.data_ptr() for o in outs])
+    oc = (C.c_uint64 * k)(*[o.numel() for o in outs])
+    st = (C.c_int * k)()
+    rc = _native.load().acz_gpu_decompress_host_batch(ctx.handle, k, ptrs, sizes, sp, ss,
+                                                      1 if zero_filter else 0, op, oc, st)
+    _check(rc, ctx)
+    res = []
+    for a, o in zip(arrs, outs):
+        res.append(o.view(_acz1_shape(a)) if o.numel() == int(np.prod(_acz1_shape(a))) else o)
     return res
+
+
+def _acz1_shape(a) -> tuple:
+    """Shape from an ACZ1 header (ref src/codec.cpp:179-191 layout); the full validation
+    happens in the native parser."""
+    if a.size < 7 or bytes(a[:4]) != b"ACZ1":
+        raise FormatError("bad blob magic at offset 0 (expected \"ACZ1\")")
+    rank = int(a[6])
+    if rank == 0 or a.size < 7 + 8 * rank:
+        raise FormatError("unexpected end of stream")
+    return tuple(int.from_bytes(bytes(a[7 + 8 * i:15 + 8 * i]), "little") for i in range(rank))
 
 
 # --------------------------------------------------------------------- statistics ----

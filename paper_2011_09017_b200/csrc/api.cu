@@ -66,6 +66,7 @@ struct Slot {
     void* h_small_dev = nullptr;    // its device-side (mapped) address
     cudaEvent_t ev_book = nullptr;  // recorded after the codebook read-back
     cudaEvent_t ev_up = nullptr;    // host-input upload complete (serialises batch uploads)
+    cudaEvent_t ev_dec = nullptr;   // host-batch decode complete (download may start)
     uint64_t last_n = 0;
     bool last_sym16 = false;
 };
@@ -76,6 +77,8 @@ struct acz_gpu_ctx {
     std::string err;
     uint64_t launches = 0;
     cudaStream_t own = nullptr;  // stream used by the host-buffer entry points
+    cudaStream_t io_up = nullptr, io_down = nullptr;  // copy streams of the host batches
+    cudaEvent_t io_ev = nullptr;
     std::vector<Slot*> slots;    // slot 0 serves the single-tensor entry points
     std::vector<cudaStream_t> pool;     // internal streams of the batched entry points
     std::vector<cudaEvent_t> pool_ev;   // one per pool stream (join)
@@ -302,6 +305,7 @@ int ensure_small(acz_gpu_ctx* ctx, Slot* sl) {
     CK(cudaHostGetDevicePointer(&sl->h_small_dev, sl->h_small, 0));
     CK(cudaEventCreateWithFlags(&sl->ev_book, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sl->ev_up, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sl->ev_dec, cudaEventDisableTiming));
     return ACZ_OK;
 }
 
@@ -320,6 +324,7 @@ void free_slot(Slot* sl) {
     if (sl->h_small) cudaFreeHost(sl->h_small);
     if (sl->ev_book) cudaEventDestroy(sl->ev_book);
     if (sl->ev_up) cudaEventDestroy(sl->ev_up);
+    if (sl->ev_dec) cudaEventDestroy(sl->ev_dec);
     delete sl;
 }
 
@@ -404,6 +409,9 @@ int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
     for (auto e : ctx->pool_ev) cudaEventDestroy(e);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->own) cudaStreamDestroy(ctx->own);
+    if (ctx->io_up) cudaStreamDestroy(ctx->io_up);
+    if (ctx->io_down) cudaStreamDestroy(ctx->io_down);
+    if (ctx->io_ev) cudaEventDestroy(ctx->io_ev);
     for (auto& p : ctx->pending) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
@@ -1070,14 +1078,22 @@ int acz_gpu_sidecar_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* ds
     return ACZ_OK;
 }
 
-int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
-                           const uint8_t* sidecar, uint64_t sidecar_size, void* stream,
-                           acz_gpu_blob** out) {
+// ACZ1 bytes (+ optional ACZS sidecar) in host memory -> device blob on stream s, with the
+// reference's blob_from_bytes checks on the host. The bitstream, the raw codebook/outlier
+// sections and the sidecar are copied straight from the caller's buffers (async when they
+// are page-locked); the codebook and outliers are de-interleaved on the device. async: do
+// not synchronise s when a valid sidecar was supplied (the caller keeps src/sidecar alive
+// and orders its own work after s).
+static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uint64_t size,
+                      const uint8_t* sidecar, uint64_t sidecar_size, cudaStream_t s,
+                      acz_gpu_blob** out, bool async) {
     if (!ctx || !out || (!src && size)) return ACZ_ERR_INVALID;
-    Slot* sl = get_slot(ctx, 0);
+    if (!sl) return fail(ctx, ACZ_ERR_NOMEM, "slot");
     *out = nullptr;
-    ctx->err.clear();
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    {
+        const int rc = ensure_small(ctx, sl);
+        if (rc) return rc;
+    }
     // ---- ref src/codec.cpp:201-262 (blob_from_bytes), same checks and order ----
     uint64_t pos = 0;
     bool trunc = false;
@@ -1128,6 +1144,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
     const uint64_t k = get(2);
     NEED();
     if (k == 0) return fail(ctx, ACZ_ERR_FORMAT, "empty codebook");
+    const uint64_t book_off = pos;
     std::vector<uint32_t> bsym(k);
     std::vector<uint8_t> blen(k);
     for (uint64_t i = 0; i < k; ++i) {
@@ -1140,6 +1157,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
     if (nbytes > size - pos) return fail(ctx, ACZ_ERR_FORMAT, "unexpected end of stream");
     const uint8_t* bits = src + pos;
     pos += nbytes;
+    const uint64_t outl_off = pos;
     std::vector<unsigned long long> oidx(nout);
     std::vector<float> oval(nout);
     for (uint64_t i = 0; i < nout; ++i) {
@@ -1223,13 +1241,19 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
         cudaError_t _e = (expr);                                                   \
         if (_e != cudaSuccess) return cleanup(cuda_fail(ctx, _e, #expr));          \
     } while (0)
-    CKB(cudaMemsetAsync(b->words, 0, 4ull * (nwords + 32), s));
+    // the bitstream's byte image == the words array; zero only the tail and the padding
+    CKB(cudaMemsetAsync(reinterpret_cast<uint8_t*>(b->words) + nbytes, 0,
+                        4ull * (nwords + 32) - nbytes, s));
     CKB(cudaMemcpyAsync(b->words, bits, nbytes, cudaMemcpyHostToDevice, s));
-    CKB(cudaMemcpyAsync(b->book_sym, bsym.data(), 4ull * k, cudaMemcpyHostToDevice, s));
-    CKB(cudaMemcpyAsync(b->book_len, blen.data(), k, cudaMemcpyHostToDevice, s));
-    if (nout) {
-        CKB(cudaMemcpyAsync(b->out_index, oidx.data(), 8ull * nout, cudaMemcpyHostToDevice, s));
-        CKB(cudaMemcpyAsync(b->out_value, oval.data(), 4ull * nout, cudaMemcpyHostToDevice, s));
+    {
+        const size_t raw = 5ull * k + 12ull * nout;
+        CKB(grow(&sl->ws_pack, &sl->ws_pack_cap, raw));
+        uint8_t* rp = static_cast<uint8_t*>(sl->ws_pack);
+        CKB(cudaMemcpyAsync(rp, src + book_off, 5ull * k, cudaMemcpyHostToDevice, s));
+        if (nout) CKB(cudaMemcpyAsync(rp + 5ull * k, src + outl_off, 12ull * nout,
+                                      cudaMemcpyHostToDevice, s));
+        CKB(launch_unpack_acz1(rp, (uint32_t)k, nout, b->book_sym, b->book_len, b->out_index,
+                               b->out_value, ctx->sms, s, &ctx->launches));
     }
     if (deferred) {
         CKB(cudaStreamSynchronize(s));
@@ -1249,7 +1273,7 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
             p += 4ull * side_chunks;
         }
         CKB(cudaMemcpyAsync(b->side_state, p, 4ull * side_chunks, cudaMemcpyHostToDevice, s));
-        CKB(cudaStreamSynchronize(s));  // host vectors go out of scope
+        if (!async) CKB(cudaStreamSynchronize(s));  // the caller may release src / sidecar
         *out = b;
         return ACZ_OK;
     }
@@ -1303,6 +1327,91 @@ int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
 #undef CKB
     *out = b;
     return ACZ_OK;
+}
+
+extern "C" int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
+                                      const uint8_t* sidecar, uint64_t sidecar_size, void* stream,
+                                      acz_gpu_blob** out) {
+    if (!ctx || !out || (!src && size)) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    return blob_from_host_on(ctx, get_slot(ctx, 0), src, size, sidecar, sidecar_size,
+                             static_cast<cudaStream_t>(stream), out, false);
+}
+
+int acz_gpu_decompress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const uint8_t* const* acz1,
+                                  const uint64_t* acz1_size, const uint8_t* const* sidecar,
+                                  const uint64_t* sidecar_size, int zero_filter,
+                                  float* const* h_out, const uint64_t* out_cap, int* status) {
+    if (!ctx || (count && (!acz1 || !acz1_size || !h_out || !out_cap))) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    if (count == 0) return ACZ_OK;
+    const size_t k = std::min<size_t>(count, kPoolStreams);
+    int rc = pool_fork(ctx, k, ctx->own);
+    if (rc) return rc;
+    if (!ctx->io_up) {
+        CK(cudaStreamCreateWithFlags(&ctx->io_up, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->io_down, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->io_ev, cudaEventDisableTiming));
+    }
+    CK(cudaStreamWaitEvent(ctx->io_up, ctx->ev_fork, 0));
+    CK(cudaStreamWaitEvent(ctx->io_down, ctx->ev_fork, 0));
+    // smallest blob first: the download stream (the bound: outputs are ~3x the blobs) starts
+    // after one short upload + decode and then stays fed while the larger blobs upload
+    std::vector<uint32_t> order(count);
+    for (uint32_t i = 0; i < count; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](uint32_t a, uint32_t b) { return acz1_size[a] < acz1_size[b]; });
+    int first_err = ACZ_OK;
+    std::string first_msg;
+    for (uint32_t i : order) {
+        Slot* sl = get_slot(ctx, i);
+        cudaStream_t s = ctx->pool[i % k];
+        acz_gpu_blob* b = nullptr;
+        int st = sl ? ACZ_OK : ACZ_ERR_NOMEM;
+        if (st == ACZ_OK)
+            st = blob_from_host_on(ctx, sl, acz1[i], acz1_size[i], sidecar ? sidecar[i] : nullptr,
+                                   sidecar && sidecar_size ? sidecar_size[i] : 0, ctx->io_up, &b,
+                                   true);
+        uint64_t n = 0;
+        if (st == ACZ_OK) {
+            n = b->info.element_count;
+            if (out_cap[i] < n) st = fail(ctx, ACZ_ERR_SHAPE, "output buffer too small for the blob");
+        }
+        if (st == ACZ_OK) {
+            cudaError_t e = cudaEventRecord(sl->ev_up, ctx->io_up);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(s, sl->ev_up, 0);
+            if (e == cudaSuccess) e = grow(&sl->ws_in, &sl->ws_in_cap, 4ull * n);
+            st = e == cudaSuccess ? ACZ_OK : cuda_fail(ctx, e, "host batch decompress");
+        }
+        if (st == ACZ_OK)
+            st = decompress_on(ctx, sl, b, zero_filter, static_cast<float*>(sl->ws_in), s);
+        if (st == ACZ_OK) {
+            cudaError_t e = cudaEventRecord(sl->ev_dec, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->io_down, sl->ev_dec, 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(h_out[i], sl->ws_in, 4ull * n, cudaMemcpyDeviceToHost,
+                                    ctx->io_down);
+            if (e != cudaSuccess) st = cuda_fail(ctx, e, "host batch download");
+        }
+        if (b) {
+            b->stream = s;  // freed after its decode (stream order on s)
+            acz_gpu_blob_free(b);
+        }
+        if (status) status[i] = st;
+        if (st != ACZ_OK && first_err == ACZ_OK) {
+            first_err = st;
+            first_msg = ctx->err;
+        }
+    }
+    rc = pool_join(ctx, k, ctx->own);
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->io_ev, ctx->io_up));
+    CK(cudaStreamWaitEvent(ctx->own, ctx->io_ev, 0));
+    CK(cudaEventRecord(ctx->io_ev, ctx->io_down));
+    CK(cudaStreamWaitEvent(ctx->own, ctx->io_ev, 0));
+    CK(cudaStreamSynchronize(ctx->own));
+    if (first_err) ctx->err = first_msg;
+    return first_err;
 }
 
 // ------------------------------------------------------------------- host buffers --

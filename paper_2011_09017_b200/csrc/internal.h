@@ -43,6 +43,9 @@ struct CopyRegions {
 };
 cudaError_t launch_copy_regions(const CopyRegions& r, int sms, cudaStream_t s,
                                 uint64_t* launches);
+cudaError_t launch_unpack_acz1(const uint8_t* raw, uint32_t k, uint64_t nout, uint32_t* bsym,
+                               uint8_t* blen, unsigned long long* oidx, float* oval, int sms,
+                               cudaStream_t s, uint64_t* launches);
 cudaError_t launch_pack_acz1(const uint32_t* bsym, const uint8_t* blen, uint32_t k,
                              const unsigned long long* oidx, const float* oval, uint64_t nout,
                              uint8_t* book_out, uint8_t* outl_out, int sms, cudaStream_t s,

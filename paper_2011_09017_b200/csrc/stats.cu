@@ -135,7 +135,45 @@ __global__ void k_copy_regions(CopyRegions r) {
     if (r.to_host) __threadfence_system();  // mapped host destination
 }
 
+// Inverse of k_pack_acz1: the raw ACZ1 codebook (5-byte entries) and outlier records
+// (12 bytes), uploaded as they lie in the host blob, into the blob's device arrays.
+__global__ void k_unpack_acz1(const uint8_t* __restrict__ raw, uint32_t k, uint64_t nout,
+                              uint32_t* __restrict__ bsym, uint8_t* __restrict__ blen,
+                              unsigned long long* __restrict__ oidx, float* __restrict__ oval) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += stride) {
+        const uint8_t* q = raw + 5 * i;
+        bsym[i] = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) |
+                  ((uint32_t)q[3] << 24);
+        blen[i] = q[4];
+    }
+    const uint8_t* ro = raw + 5ull * k;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nout; i += stride) {
+        const uint8_t* q = ro + 12 * i;
+        unsigned long long a = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a |= (unsigned long long)q[j] << (8 * j);
+        uint32_t b = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b |= (uint32_t)q[8 + j] << (8 * j);
+        oidx[i] = a;
+        oval[i] = __uint_as_float(b);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_unpack_acz1(const uint8_t* raw, uint32_t k, uint64_t nout, uint32_t* bsym,
+                               uint8_t* blen, unsigned long long* oidx, float* oval, int sms,
+                               cudaStream_t s, uint64_t* launches) {
+    const uint64_t m = k > nout ? k : nout;
+    if (m == 0) return cudaSuccess;
+    const uint64_t want = (m + 255) / 256;
+    const unsigned grid = (unsigned)(want < (uint64_t)sms * 4 ? want : (uint64_t)sms * 4);
+    k_unpack_acz1<<<grid, 256, 0, s>>>(raw, k, nout, bsym, blen, oidx, oval);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_copy_regions(const CopyRegions& r, int sms, cudaStream_t s,
                                 uint64_t* launches) {

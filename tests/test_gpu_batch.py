@@ -81,3 +81,23 @@ def test_host_batch_roundtrip(acz, oracle):
     outs2 = acz.decompress_host_many([(b, None) for b, _ in res], zero_filter=True)
     for o, o2 in zip(outs, outs2):
         assert torch.equal(o, o2)
+
+
+def test_host_batch_decompress_errors(acz, oracle):
+    import torch
+    rng = np.random.default_rng(15)
+    xs = _set(rng)[:3]
+    res = acz.compress_host_many([torch.from_numpy(x).pin_memory() for x in xs], acz.CodecParams(1e-3))
+    # a blob with trailing bytes among valid ones: the reference's FormatError, same message
+    bad = np.concatenate([res[1][0], np.zeros(3, np.uint8)])
+    outs = [torch.empty(x.shape, dtype=torch.float32).pin_memory() for x in xs]
+    with pytest.raises(acz.FormatError, match="trailing bytes after blob"):
+        acz.decompress_host_many([res[0], (bad, None), res[2]], True, outs=outs)
+    # the valid blobs of that batch were still decoded
+    assert outs[0].numpy().ravel().tobytes() == oracle.decompress(res[0][0].tobytes(), xs[0].size, True).tobytes()
+    assert outs[2].numpy().ravel().tobytes() == oracle.decompress(res[2][0].tobytes(), xs[2].size, True).tobytes()
+    with pytest.raises(acz.FormatError):
+        acz.decompress_host_many([(np.frombuffer(b"ACZX0000000", np.uint8), None)], True)
+    # output buffer too small
+    with pytest.raises(acz.ShapeError, match="output buffer too small"):
+        acz.decompress_host_many([res[0]], True, outs=[torch.empty(3).pin_memory()])
