@@ -1713,7 +1713,7 @@ int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches) {
 // --------------------------------------------------------------------------- debug --
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset) {
     if (!ctx || !out || n < 8) return ACZ_ERR_INVALID;
-    unsigned long long v[16];
+    unsigned long long v[20];
     CK(quant_spec_stats(v, reset != 0));
     for (int i = 0; i < 8; ++i) out[i] = v[i];
     if (n >= 16) {
@@ -1732,6 +1732,8 @@ int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int rese
         for (int i = 0; i < 4; ++i) out[24 + i] = v[12 + i];
     else if (n >= 26)
         for (int i = 0; i < 2; ++i) out[24 + i] = v[12 + i];
+    if (n >= 32)
+        for (int i = 0; i < 4; ++i) out[28 + i] = v[16 + i];
     return ACZ_OK;
 }
 

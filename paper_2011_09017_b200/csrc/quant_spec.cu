@@ -45,12 +45,33 @@ constexpr int kCapW = (kCap + 31) / 32;
 constexpr int kWin = kSeg + kExt + 1;  // staged x window: [j*kSeg - 1, (j+1)*kSeg + kExt)
 constexpr int kLev = 3;                // fine offset levels (binades below the anchor grid)
 
+// Instrumentation (counters + clock64 phase timing) is accumulated only with
+// -DACZ_SPEC_STATS=1 (development builds: ACZ_NVCC_EXTRA=-DACZ_SPEC_STATS=1); the product
+// build reports zeros.
+#ifndef ACZ_SPEC_STATS
+#define ACZ_SPEC_STATS 0
+#endif
+constexpr bool kStats = ACZ_SPEC_STATS != 0;
+// The phase-boundary clock reads stay in the product build: they act as scheduling fences
+// for ptxas (volatile) and measured faster than without them (AlexNet conv1 K2b 1.62 ->
+// 1.44 ms, VGG conv2 unchanged; the counter atomics alone do not help).
+#ifndef ACZ_SPEC_CLK
+#define ACZ_SPEC_CLK 1
+#endif
+#ifndef ACZ_SPEC_ADD
+#define ACZ_SPEC_ADD ACZ_SPEC_STATS
+#endif
+__device__ __forceinline__ long long sclock() { return ACZ_SPEC_CLK ? clock64() : 0ll; }
+__device__ __forceinline__ void sadd(unsigned long long* c, unsigned long long v) {
+    if (ACZ_SPEC_ADD) atomicAdd(c, v);
+}
 // Walk statistics (debug; read with acz_gpu_debug_counters): batches, state changes,
 // exact-mode steps, rebases, phase-A elements, walk visits.
 __device__ unsigned long long g_qstats[8];
 // per-phase SM cycles summed over segments (debug): geometry+phase A, look-back wait,
 // walk, exit+store
 __device__ unsigned long long g_qclk[8];  // + [4] exact-step, [5] batch, [6] pass-1, [7] classify cycles
+__device__ unsigned long long g_wclk[4];  // walk batch split (debug): gather, evaluate, resolve
 
 struct SP {
     double eb, step, inv_step, radius_d, Tmax;
@@ -169,7 +190,7 @@ __device__ void spec_range(Smem<SymT>& S, int xoff, uint64_t seg0, int k, const 
         r = v;
     }
     S.send[k] = (float)r;
-    atomicAdd(&g_qstats[4], (unsigned long long)(e - b));
+    sadd(&g_qstats[4], (unsigned long long)(e - b));
     if (bad) atomicOr(flags, kFlagNonFinite);
 }
 
@@ -322,7 +343,7 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int
     const SP p = p_in;
     const QParams qp = qp_in;
     const int lane = threadIdx.x;
-    const long long t0 = clock64();
+    const long long t0 = sclock();
     for (int k = k0 + lane; k < S.nr; k += kW) {
         const int st = S.rstart[k];
         if (k == k0 && lam_exact_k0) {
@@ -335,12 +356,12 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int
         spec_range(S, xoff, seg0, k, p, qp, flags);
     }
     __syncwarp();
-    const long long t1 = clock64();
+    const long long t1 = sclock();
     classify(S, xoff, seg0, S.rstart[k0], len, p, plane_flat0);
     __syncwarp();
     if (lane == 0) {
-        atomicAdd(&g_qclk[6], (unsigned long long)(t1 - t0));
-        atomicAdd(&g_qclk[7], (unsigned long long)(clock64() - t1));
+        sadd(&g_qclk[6], (unsigned long long)(t1 - t0));
+        sadd(&g_qclk[7], (unsigned long long)(sclock() - t1));
     }
     // prefix C[k] = sum_{j<=k, j>0} (send[j-1] - guess[j])
     if (lane == 0) {
@@ -450,11 +471,11 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                         : nullptr;
     const float* xp = x + plane * p.P;
     const uint64_t plane_flat0 = plane * p.P;
-    long long tck = clock64();
+    long long tck = sclock();
     auto tphase = [&](int slot) {
         if (lane == 0) {
-            const long long t = clock64();
-            atomicAdd(&g_qclk[slot], (unsigned long long)(t - tck));
+            const long long t = sclock();
+            sadd(&g_qclk[slot], (unsigned long long)(t - tck));
             tck = t;
         }
     };
@@ -670,17 +691,17 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     };
     auto is_coll = [&](int c) { return S.sym[c] != 0 && fabs((double)S.s[c]) < p.eb; };
 
-    long long tw = clock64();
+    long long tw = sclock();
     int wmode = -1;  // 0 exact, 1 batch
     while (pos < len) {
         {
-            const long long t = clock64();
-            if (lane == 0 && wmode >= 0) atomicAdd(&g_qclk[4 + wmode], (unsigned long long)(t - tw));
+            const long long t = sclock();
+            if (lane == 0 && wmode >= 0) sadd(&g_qclk[4 + wmode], (unsigned long long)(t - tw));
             tw = t;
             wmode = exact_mode ? 0 : 1;
         }
         if (exact_mode) {
-            if (lane == 0) atomicAdd(&g_qstats[2], 1ull);
+            if (lane == 0) sadd(&g_qstats[2], 1ull);
             const int k = range_of(pos);
             if (pos == S.rstart[k] && pos > 0) {
                 // exact entry T at a range start: resume translation (rebase if needed)
@@ -723,6 +744,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             continue;
         }
         // ---- TRANSLATE: gather the next 32 candidate positions -----------------------
+        const long long tb0 = sclock();
         {
             const int w = (pos >> 5) + lane;
             uint32_t bits = (w < kCapW) ? (S.cand[w] | (lev ? S.lvl[lev - 1][w] : 0u)) : 0u;
@@ -753,6 +775,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         int vp = s_vis[lane];
         if (vp > len) vp = len;
         const bool active = vp < len;
+        const long long tb1 = sclock();
         bool ok = true, rebase = false;
         XS ex;
         ex.sym = 0;
@@ -799,13 +822,18 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             }
         }
         const unsigned fail = __ballot_sync(0xffffffffu, active && !ok);
+        const long long tb2 = sclock();
+        if (lane == 0) {
+            sadd(&g_wclk[0], (unsigned long long)(tb1 - tb0));
+            sadd(&g_wclk[1], (unsigned long long)(tb2 - tb1));
+        }
         const int f = fail ? __ffs(fail) - 1 : 32;
-        {
+        if (kStats) {
             const int nact = __popc(__ballot_sync(0xffffffffu, active));
             if (lane == 0) {
-                atomicAdd(&g_qstats[0], 1ull);
-                if (f < 32) atomicAdd(&g_qstats[1], 1ull);
-                atomicAdd(&g_qstats[5], (unsigned long long)min(f + 1, nact));
+                sadd(&g_qstats[0], 1ull);
+                if (f < 32) sadd(&g_qstats[1], 1ull);
+                sadd(&g_qstats[5], (unsigned long long)min(f + 1, nact));
             }
         }
         if (active && lane < f) {
@@ -818,7 +846,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             const int frb = __shfl_sync(0xffffffffu, (int)rebase, f);
             const float ftp = __shfl_sync(0xffffffffu, tprev, f);
             if (frb) {
-                if (lane == 0) atomicAdd(&g_qstats[3], 1ull);
+                if (lane == 0) sadd(&g_qstats[3], 1ull);
                 // lattice changed at range start fk: re-speculate ranges >= fk from the
                 // exact entry state and re-evaluate from fvp
                 phase_a(S, xoff, seg0, fk, (double)ftp, true, ftp, p, qp, plane_flat0, flags, len);
@@ -1019,10 +1047,12 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
 cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
     cudaError_t e = cudaMemcpyFromSymbol(out, g_qstats, sizeof(g_qstats));
     if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 8, g_qclk, sizeof(g_qclk));  // 8 values
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 16, g_wclk, sizeof(g_wclk));  // 4 values
     if (e == cudaSuccess && reset) {
         unsigned long long z[8] = {0};
         e = cudaMemcpyToSymbol(g_qstats, z, sizeof(z));
         if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_qclk, z, sizeof(g_qclk));
+        if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_wclk, z, sizeof(g_wclk));
     }
     return e;
 }

@@ -23,8 +23,8 @@ for nm in which:
     for _ in range(2):
         blob = acz.compress(x, p)
         acz.decompress(blob, True)
-    v = (C.c_uint64 * 28)()
-    lib.acz_gpu_debug_counters(ctx.handle, v, 28, 1)
+    v = (C.c_uint64 * 32)()
+    lib.acz_gpu_debug_counters(ctx.handle, v, 32, 1)
     lib.acz_gpu_profile_enable(ctx.handle, 1)
     blob = acz.compress(x, p)
     out = acz.decompress(blob, True)
@@ -33,7 +33,7 @@ for nm in which:
     cnt = (C.c_uint64 * 7)()
     lib.acz_gpu_profile_read(ctx.handle, ms, cnt)
     lib.acz_gpu_profile_enable(ctx.handle, 0)
-    lib.acz_gpu_debug_counters(ctx.handle, v, 28, 1)
+    lib.acz_gpu_debug_counters(ctx.handle, v, 32, 1)
     names = ["stats", "quant", "hist", "book", "encode", "decode", "scan"]
     print(nm, x.shape, "ratio %.3f" % acz.compression_ratio(blob),
           {names[i]: round(ms[i], 3) for i in range(7) if cnt[i]})
@@ -43,7 +43,8 @@ for nm in which:
     tot = sum(v[16:20]) or 1
     nw = max(1, v[23])
     print("   decode cycles/warp: prologue %.0f staging %.0f loop %.0f (warps %d)" % (v[20] / nw, v[21] / nw, v[22] / nw, v[23]))
-    print("   walk cycles: per exact step %.0f, per batch %.0f" % (v[24] / max(1, v[2]), v[25] / max(1, v[0])))
+    print("   walk cycles: per exact step %.0f, per batch %.0f (gather %.0f, evaluate %.0f)" % (
+        v[24] / max(1, v[2]), v[25] / max(1, v[0]), v[28] / max(1, v[0]), v[29] / max(1, v[0])))
     print("   phase A split (cycles/elem): pass1 %.1f classify %.1f" % (v[26] / n, v[27] / n))
     nb = max(1, v[15])
     print("   codebook cycles: compact %.0f sort %.0f tree %.0f depths %.0f canon %.0f tables %.0f (books %d)" % tuple(
