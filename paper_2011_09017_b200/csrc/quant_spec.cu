@@ -667,6 +667,10 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     // offset of range 0
     double D = (j == 0) ? 0.0 : __dsub_rn((double)tin, (double)S.guess[0]);
     int lev = levelD(D);
+    if (j > 0 && lane == 0) {  // debug: entry offsets that are exactly zero / representable
+        if (D == 0.0) sadd(&g_qstats[6], 1ull);
+        if (lev >= 0) sadd(&g_qstats[7], 1ull);
+    }
     if (j > 0 && lev < 0) {
         // lattice differs (escape upstream) or guess too far: re-speculate from tin
         phase_a(S, xoff, seg0, 0, (double)tin, true, tin, p, qp, plane_flat0, flags, len);

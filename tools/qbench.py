@@ -46,6 +46,7 @@ for nm in which:
     print("   walk cycles: per exact step %.0f, per batch %.0f (gather %.0f, evaluate %.0f)" % (
         v[24] / max(1, v[2]), v[25] / max(1, v[0]), v[28] / max(1, v[0]), v[29] / max(1, v[0])))
     print("   phase A split (cycles/elem): pass1 %.1f classify %.1f" % (v[26] / n, v[27] / n))
+    print("   segment entry offsets: D == 0 in %d, representable in %d" % (v[6], v[7]))
     nb = max(1, v[15])
     print("   codebook cycles: compact %.0f sort %.0f tree %.0f depths %.0f canon %.0f tables %.0f (books %d)" % tuple(
         [v[8 + i] / nb for i in range(6)] + [v[15]]))
