@@ -52,8 +52,8 @@ constexpr int kLev = 3;                // fine offset levels (binades below the 
 #define ACZ_SPEC_STATS 0
 #endif
 constexpr bool kStats = ACZ_SPEC_STATS != 0;
-// The phase-boundary clock reads stay in the product build: they act as scheduling fences
-// for ptxas (volatile) and measured faster than without them (AlexNet conv1 K2b 1.62 ->
+// The segment phase-boundary clock reads stay in the product build: volatile, they fence
+// ptxas's scheduling and measured faster than without them (AlexNet conv1 K2b 1.62 ->
 // 1.44 ms, VGG conv2 unchanged; the counter atomics alone do not help).
 #ifndef ACZ_SPEC_CLK
 #define ACZ_SPEC_CLK 1
@@ -61,7 +61,19 @@ constexpr bool kStats = ACZ_SPEC_STATS != 0;
 #ifndef ACZ_SPEC_ADD
 #define ACZ_SPEC_ADD ACZ_SPEC_STATS
 #endif
-__device__ __forceinline__ long long sclock() { return ACZ_SPEC_CLK ? clock64() : 0ll; }
+#ifndef ACZ_SPEC_SYNC_PHASE
+#define ACZ_SPEC_SYNC_PHASE 0
+#endif
+// Clock sites: 1 phase A, 2 segment phase boundaries, 4 walk loop, 8 walk batch. Measured:
+// the segment-boundary reads alone give the whole gain (a __syncwarp there does not); the
+// stats build enables all of them.
+#ifndef ACZ_SPEC_CLK_MASK
+#define ACZ_SPEC_CLK_MASK (ACZ_SPEC_STATS ? 15 : 2)
+#endif
+template <int kSite>
+__device__ __forceinline__ long long sclock() {
+    return (ACZ_SPEC_CLK && (ACZ_SPEC_CLK_MASK & kSite)) ? clock64() : 0ll;
+}
 __device__ __forceinline__ void sadd(unsigned long long* c, unsigned long long v) {
     if (ACZ_SPEC_ADD) atomicAdd(c, v);
 }
@@ -343,7 +355,7 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int
     const SP p = p_in;
     const QParams qp = qp_in;
     const int lane = threadIdx.x;
-    const long long t0 = sclock();
+    const long long t0 = sclock<1>();
     for (int k = k0 + lane; k < S.nr; k += kW) {
         const int st = S.rstart[k];
         if (k == k0 && lam_exact_k0) {
@@ -356,12 +368,12 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int
         spec_range(S, xoff, seg0, k, p, qp, flags);
     }
     __syncwarp();
-    const long long t1 = sclock();
+    const long long t1 = sclock<1>();
     classify(S, xoff, seg0, S.rstart[k0], len, p, plane_flat0);
     __syncwarp();
     if (lane == 0) {
         sadd(&g_qclk[6], (unsigned long long)(t1 - t0));
-        sadd(&g_qclk[7], (unsigned long long)(sclock() - t1));
+        sadd(&g_qclk[7], (unsigned long long)(sclock<1>() - t1));
     }
     // prefix C[k] = sum_{j<=k, j>0} (send[j-1] - guess[j])
     if (lane == 0) {
@@ -471,10 +483,13 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                         : nullptr;
     const float* xp = x + plane * p.P;
     const uint64_t plane_flat0 = plane * p.P;
-    long long tck = sclock();
+    long long tck = sclock<2>();
     auto tphase = [&](int slot) {
+#if ACZ_SPEC_SYNC_PHASE
+        __syncwarp();
+#endif
         if (lane == 0) {
-            const long long t = sclock();
+            const long long t = sclock<2>();
             sadd(&g_qclk[slot], (unsigned long long)(t - tck));
             tck = t;
         }
@@ -695,11 +710,11 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     };
     auto is_coll = [&](int c) { return S.sym[c] != 0 && fabs((double)S.s[c]) < p.eb; };
 
-    long long tw = sclock();
+    long long tw = sclock<4>();
     int wmode = -1;  // 0 exact, 1 batch
     while (pos < len) {
         {
-            const long long t = sclock();
+            const long long t = sclock<4>();
             if (lane == 0 && wmode >= 0) sadd(&g_qclk[4 + wmode], (unsigned long long)(t - tw));
             tw = t;
             wmode = exact_mode ? 0 : 1;
@@ -748,7 +763,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             continue;
         }
         // ---- TRANSLATE: gather the next 32 candidate positions -----------------------
-        const long long tb0 = sclock();
+        const long long tb0 = sclock<8>();
         {
             const int w = (pos >> 5) + lane;
             uint32_t bits = (w < kCapW) ? (S.cand[w] | (lev ? S.lvl[lev - 1][w] : 0u)) : 0u;
@@ -779,7 +794,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         int vp = s_vis[lane];
         if (vp > len) vp = len;
         const bool active = vp < len;
-        const long long tb1 = sclock();
+        const long long tb1 = sclock<8>();
         bool ok = true, rebase = false;
         XS ex;
         ex.sym = 0;
@@ -826,7 +841,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             }
         }
         const unsigned fail = __ballot_sync(0xffffffffu, active && !ok);
-        const long long tb2 = sclock();
+        const long long tb2 = sclock<8>();
         if (lane == 0) {
             sadd(&g_wclk[0], (unsigned long long)(tb1 - tb0));
             sadd(&g_wclk[1], (unsigned long long)(tb2 - tb1));
