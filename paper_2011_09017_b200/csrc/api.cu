@@ -777,10 +777,11 @@ int sidecar_to_host_enqueue(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* ds
 constexpr size_t kPoolStreams = 8;
 
 // Internal streams for the batched entry points, forked from the caller's stream: pool[i]
-// (i < kPoolStreams) run at the device's highest priority, pool[kPoolStreams + i] at the
-// lowest. A tensor whose quantiser is the long speculative kernel (thousands of one-warp
-// CTAs) goes to a low-priority stream, so the CTA scheduler slots the other tensors' short
-// kernels in as its CTAs retire instead of queueing them behind the whole grid.
+// (i < kPoolStreams) run at the device's lowest priority, pool[kPoolStreams + i] at the
+// highest. A tensor whose quantiser is the long speculative kernel (the step's critical
+// path) goes to a high-priority stream: its CTAs keep the SMs, and the other tensors'
+// short kernels fill its tail and run alongside its histogram/codebook/encode (measured on
+// AlexNet: 2.61 vs 2.87 ms per step with the priorities the other way round).
 int pool_fork(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
     if (ctx->pool.empty()) {
         int least = 0, greatest = 0;
@@ -789,7 +790,7 @@ int pool_fork(acz_gpu_ctx* ctx, size_t k, cudaStream_t user) {
             cudaStream_t st = nullptr;
             cudaEvent_t ev = nullptr;
             CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking,
-                                            i < kPoolStreams ? greatest : least));
+                                            i < kPoolStreams ? least : greatest));
             CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             ctx->pool.push_back(st);
             ctx->pool_ev.push_back(ev);
