@@ -892,13 +892,22 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
         done[i] = 1;
         --remaining;
     };
+    // Poll in priority order (tensors on the high-priority stream first: their encode is on
+    // the critical path) and rescan from the top after every finish, so a critical tensor
+    // whose codebook lands while others are being finished waits for at most one of them.
+    std::vector<uint32_t> prio(count);
+    for (uint32_t i = 0; i < count; ++i) prio[i] = i;
+    std::stable_partition(prio.begin(), prio.end(), [&](uint32_t i) {
+        return ts[i] != ctx->pool[i % k];  // on a high-priority stream
+    });
     while (remaining) {
         bool progressed = false;
-        for (uint32_t i = 0; i < count; ++i) {
+        for (uint32_t i : prio) {
             if (done[i]) continue;
             if (st[i] != ACZ_OK || cudaEventQuery(get_slot(ctx, i)->ev_book) != cudaErrorNotReady) {
                 finish(i);
                 progressed = true;
+                break;
             }
         }
         // nothing ready: poll again (blocking on one tensor would hold back the others, whose
@@ -996,16 +1005,21 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
         done[i] = 1;
         --remaining;
     };
-    while (remaining) {
+    std::vector<uint32_t> prio(count);
+    for (uint32_t i = 0; i < count; ++i) prio[i] = i;
+    std::stable_partition(prio.begin(), prio.end(),
+                          [&](uint32_t i) { return ts[i] != ctx->pool[i % k]; });
+    while (remaining) {  // see acz_gpu_compress_batch
         bool progressed = false;
-        for (uint32_t i = 0; i < count; ++i) {
+        for (uint32_t i : prio) {
             if (done[i]) continue;
             if (st[i] != ACZ_OK || cudaEventQuery(get_slot(ctx, i)->ev_book) != cudaErrorNotReady) {
                 finish(i);
                 progressed = true;
+                break;
             }
         }
-        if (!progressed) std::this_thread::yield();  // see acz_gpu_compress_batch
+        if (!progressed) std::this_thread::yield();
     }
     rc = pool_join(ctx, k, ctx->own);
     if (rc) return rc;
