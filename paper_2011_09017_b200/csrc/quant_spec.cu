@@ -44,6 +44,16 @@ constexpr int kCap = kSeg + kExt;
 constexpr int kCapW = (kCap + 31) / 32;
 constexpr int kWin = kSeg + kExt + 1;  // staged x window: [j*kSeg - 1, (j+1)*kSeg + kExt)
 constexpr int kLev = 3;                // fine offset levels (binades below the anchor grid)
+// ACZ_SPEC_XS_GLOBAL=1: read the input through L1/L2 instead of staging the segment's window
+// in shared memory (8.7 KB less per segment: more resident segments per SM).
+#ifndef ACZ_SPEC_XS_GLOBAL
+#define ACZ_SPEC_XS_GLOBAL 0
+#endif
+#if ACZ_SPEC_XS_GLOBAL
+#define XAT(i) __ldg(xg + (i))
+#else
+#define XAT(i) S.xs[xoff + (i)]
+#endif
 
 // Instrumentation (counters + clock64 phase timing) is accumulated only with
 // -DACZ_SPEC_STATS=1 (development builds: ACZ_NVCC_EXTRA=-DACZ_SPEC_STATS=1); the product
@@ -172,7 +182,7 @@ struct alignas(16) Smem {
     int forced[kW];       // range start is not an anchor-aligned guess
     // staged input window (plane index j*kSeg - 1 + i); LAST: everything before it is the
     // segment state the decoupled phase-A kernel persists for the walk kernel
-    float xs[kWin];
+    float xs[ACZ_SPEC_XS_GLOBAL ? 4 : kWin];
 };
 
 // Per-segment header of the decoupled path (phase-A kernel -> walk kernel).
@@ -186,14 +196,14 @@ struct SegHdr {
 // Phase A, pass 1: the speculative chain over range k from its guess (one lane per range):
 // the reference step only (symbols + chain states), the tightest dependent chain.
 template <typename SymT>
-__device__ void spec_range(Smem<SymT>& S, int xoff, uint64_t seg0, int k, const SP& p,
-                           const QParams& qp, unsigned* flags) {
+__device__ void spec_range(Smem<SymT>& S, int xoff, const float* __restrict__ xg, uint64_t seg0,
+                           int k, const SP& p, const QParams& qp, unsigned* flags) {
     const int b = S.rstart[k], e = S.rstart[k + 1];
     double r = (double)S.guess[k];
     bool bad = false;
 #pragma unroll 4
     for (int i = b; i < e; ++i) {
-        const float xf = S.xs[xoff + i];
+        const float xf = XAT(i);
         bad |= !isfinite(xf);
         const double pred = (seg0 + (uint64_t)i == 0) ? 0.0 : r;
         double v;
@@ -215,8 +225,8 @@ __device__ void spec_range(Smem<SymT>& S, int xoff, uint64_t seg0, int k, const 
 // pre-value is not exactly prev + q*step, re-expansions without a certificate, sidecar
 // points. lvl[L-1] marks outputs with exponent > B - L (fine offsets, see levelD).
 template <typename SymT>
-__device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len, const SP& p,
-                         uint64_t plane_flat0) {
+__device__ void classify(Smem<SymT>& S, int xoff, const float* __restrict__ xg, uint64_t seg0,
+                         int i0, int len, const SP& p, uint64_t plane_flat0) {
     const int lane = threadIdx.x;
     auto range_of = [&](int q) {
         const int w = q >> 5;
@@ -272,7 +282,7 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
                 cur = i >> 5;
             }
             const bool start = (S.rsb[i >> 5] >> (i & 31)) & 1u;
-            const float xf = S.xs[xoff + i];
+            const float xf = XAT(i);
             const double outd = (double)S.s[i];
             const uint32_t sy = (uint32_t)S.sym[i];
             const bool tiny = sy != 0 && fabs(outd) < p.eb;
@@ -349,7 +359,7 @@ __device__ void classify(Smem<SymT>& S, int xoff, uint64_t seg0, int i0, int len
 // cache. The parameters are copied to registers on entry (the stack copies the call ABI
 // makes could alias the shared-memory stores of the chain and would be reloaded per step).
 template <typename SymT>
-__device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
+__device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, const float* __restrict__ xg, uint64_t seg0, int k0, double lam, bool lam_exact_k0,
                         float k0_entry, const SP& p_in, const QParams& qp_in, uint64_t plane_flat0,
                         unsigned* flags, int len) {
     const SP p = p_in;
@@ -363,13 +373,13 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, uint64_t seg0, int
         } else if (seg0 + (uint64_t)st == 0) {
             S.guess[k] = 0.0f;
         } else {
-            S.guess[k] = lattice_guess(lam, S.xs[xoff + st - 1], p);
+            S.guess[k] = lattice_guess(lam, XAT(st - 1), p);
         }
-        spec_range(S, xoff, seg0, k, p, qp, flags);
+        spec_range(S, xoff, xg, seg0, k, p, qp, flags);
     }
     __syncwarp();
     const long long t1 = sclock<1>();
-    classify(S, xoff, seg0, S.rstart[k0], len, p, plane_flat0);
+    classify(S, xoff, xg, seg0, S.rstart[k0], len, p, plane_flat0);
     __syncwarp();
     if (lane == 0) {
         sadd(&g_qclk[6], (unsigned long long)(t1 - t0));
@@ -497,6 +507,9 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
 
     // ---- stage the input window [j*kSeg - 1, (j+1)*kSeg + kExt) into shared memory ----
     const int64_t xbase = (int64_t)(j * kSeg) - 1;
+#if ACZ_SPEC_XS_GLOBAL
+    const float* xwin = xp + xbase;  // xwin[i] == plane position xbase + i
+#else
     for (int i = lane; i < kWin; i += kW) {
         const int64_t pi = xbase + i;
         if (pi >= 0 && pi < (int64_t)p.P) cp_async4(&S.xs[i], xp + pi);
@@ -505,6 +518,8 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
+    const float* xwin = S.xs;
+#endif
 
     // ---- segment geometry -------------------------------------------------------
     uint64_t b0, b1;
@@ -513,10 +528,12 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         b1 = b0 + (uint64_t)max(0, hdr->len);
         if (hdr->len <= 0) return tin_given;  // empty segment: state passes through
     } else {
-        b0 = seg_bound_w(S.xs, xbase, j, p);      // first range start
-        b1 = seg_bound_w(S.xs, xbase, j + 1, p);  // next segment's first start
+        b0 = seg_bound_w(xwin, xbase, j, p);      // first range start
+        b1 = seg_bound_w(xwin, xbase, j + 1, p);  // next segment's first start
     }
     const int xoff = (int)((int64_t)b0 - xbase);  // xs index of segment position 0
+    const float* __restrict__ xg = xp + b0;        // global input at segment position 0
+    (void)xg;
     const uint64_t seg0 = b0;
     const int len = (int)(b1 - b0);
     if (MODE == kFront && len <= 0) {
@@ -568,7 +585,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         const uint64_t nb = j * kSeg;
         for (int w = 0; w < kSeg / 32; ++w) {
             const uint64_t i = nb + (uint64_t)w * 32 + lane;
-            const bool a = i < p.P && is_anchor(S.xs[(int64_t)i - xbase], p.anchor_min);
+            const bool a = i < p.P && is_anchor(xwin[(int64_t)i - xbase], p.anchor_min);
             const unsigned m = __ballot_sync(0xffffffffu, a);
             if (lane == 0) S.abits[w] = m;
         }
@@ -605,7 +622,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         // the segment's first range starts at a forced (non-anchor) boundary?
         bool forced = false;
         if (j > 0) {
-            const float xa = S.xs[xoff - 1];
+            const float xa = XAT(-1);
             forced = !is_anchor(xa, p.anchor_min);
         }
         S.forced[0] = forced ? 1 : 0;
@@ -630,7 +647,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     __syncwarp();
 
     // ---- phase A: speculate all ranges (lattice origin 0: plane-start lattice) ----
-    phase_a(S, xoff, seg0, 0, 0.0, false, 0.0f, p, qp, plane_flat0, flags, len);
+    phase_a(S, xoff, xg, seg0, 0, 0.0, false, 0.0f, p, qp, plane_flat0, flags, len);
     }  // !kBack
 
     tphase(0);
@@ -688,7 +705,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     }
     if (j > 0 && lev < 0) {
         // lattice differs (escape upstream) or guess too far: re-speculate from tin
-        phase_a(S, xoff, seg0, 0, (double)tin, true, tin, p, qp, plane_flat0, flags, len);
+        phase_a(S, xoff, xg, seg0, 0, (double)tin, true, tin, p, qp, plane_flat0, flags, len);
         D = 0.0;
         lev = 0;
     }
@@ -727,7 +744,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 const double Dk = __dsub_rn((double)T, (double)S.guess[k]);
                 const int lk = levelD(Dk);
                 if (lk < 0) {
-                    phase_a(S, xoff, seg0, k, (double)T, true, T, p, qp, plane_flat0, flags, len);
+                    phase_a(S, xoff, xg, seg0, k, (double)T, true, T, p, qp, plane_flat0, flags, len);
                     D = 0.0;
                     lev = 0;
                 } else {
@@ -740,7 +757,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             }
             const uint64_t pi = seg0 + (uint64_t)pos;
             const float tprev = T;
-            const XS ex = xstep(S.xs[xoff + pos], pi == 0 ? 0.0 : (double)tprev, p);
+            const XS ex = xstep(XAT(pos), pi == 0 ? 0.0 : (double)tprev, p);
             if (lane == 0) {
                 S.sym[pos] = (SymT)ex.sym;
                 const uint64_t flat = plane_flat0 + pi;
@@ -823,7 +840,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 } else {
                     tprev = __double2float_rn(__dadd_rn((double)S.s[vp - 1], Dp));
                 }
-                ex = xstep(S.xs[xoff + vp], pi == 0 ? 0.0 : (double)tprev, p);
+                ex = xstep(XAT(vp), pi == 0 ? 0.0 : (double)tprev, p);
                 const uint32_t ssym = (uint32_t)S.sym[vp];
                 const float ss = S.s[vp];
                 if (ex.sym != ssym) {
@@ -868,7 +885,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 if (lane == 0) sadd(&g_qstats[3], 1ull);
                 // lattice changed at range start fk: re-speculate ranges >= fk from the
                 // exact entry state and re-evaluate from fvp
-                phase_a(S, xoff, seg0, fk, (double)ftp, true, ftp, p, qp, plane_flat0, flags, len);
+                phase_a(S, xoff, xg, seg0, fk, (double)ftp, true, ftp, p, qp, plane_flat0, flags, len);
                 D = 0.0;
                 lev = 0;
                 rcur = fk;
