@@ -120,9 +120,12 @@ __device__ __forceinline__ uint32_t qstep(double orig, float xf, double pred, co
                                           double* r) {
     (void)xf;
     const double d = __dsub_rn(orig, pred);
-    const double t = __dmul_rn(d, p.inv_step);
-    const double M52 = 6755399441055744.0;  // 1.5 * 2^52
-    double tm = __dadd_rn(t, M52);
+    const double t = __dmul_rn(d, p.inv_step);  // for the fragility guard (off the chain)
+    const double M52 = 6755399441055744.0;       // 1.5 * 2^52
+    // one fused op on the chain: round(d*inv) by the magic add, d*inv unrounded. It can
+    // differ from round(t) only when d*inv is within an ulp of a half-integer, where the
+    // guard below sees |t - q| ~ 0.5 and recomputes q by exact division
+    double tm = __fma_rn(d, p.inv_step, M52);
     double q = __dsub_rn(tm, M52);
     // plain F2F round trip: the shortest dependent chain measured on B200
     // (tools/microbench/qchain.cu: 162 cycles/step vs 190-282 for magic-add rounding)
