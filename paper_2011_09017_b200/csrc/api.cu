@@ -87,6 +87,8 @@ struct acz_gpu_ctx {
     size_t ws_io_cap = 0;
     void* ws_aux = nullptr;  // sequential-decode scratch (symbols, plane prefixes)
     size_t ws_aux_cap = 0;
+    void* ws_scan = nullptr;  // parallel stream-scan scratch (subsequence starts / counts)
+    size_t ws_scan_cap = 0;
     // profiling: events recorded around every launch when enabled
     bool prof = false;
     struct Pending {
@@ -402,7 +404,7 @@ int acz_gpu_ctx_create(int device, acz_gpu_ctx** out) {
 int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
     if (!ctx) return ACZ_ERR_INVALID;
     cudaDeviceSynchronize();
-    for (void* p : {ctx->ws_io, ctx->ws_aux})
+    for (void* p : {ctx->ws_io, ctx->ws_aux, ctx->ws_scan})
         if (p) cudaFree(p);
     for (Slot* sl : ctx->slots) free_slot(sl);
     for (auto st : ctx->pool) cudaStreamDestroy(st);
@@ -1318,7 +1320,8 @@ static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uin
     sa.flags = &sl->d_small->flags;
     {
         KTimer kt(ctx, ACZ_K_SCAN, s);
-        CKB(launch_scan_decode(sa, s, &ctx->launches));
+        CKB(grow(&ctx->ws_scan, &ctx->ws_scan_cap, scan_decode_scratch_bytes(bit_length)));
+        CKB(launch_scan_decode(sa, ctx->ws_scan, s, &ctx->launches));
     }
     CKB(cudaMemcpyAsync(&sl->h_small->flags, &sl->d_small->flags, sizeof(unsigned),
                         cudaMemcpyDeviceToHost, s));
@@ -1640,7 +1643,8 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
     sa.plane_outl = nullptr;
     sa.plane_size = count;
     sa.flags = &sl->d_small->flags;
-    CK(launch_scan_decode(sa, s, &ctx->launches));
+    CK(grow(&ctx->ws_scan, &ctx->ws_scan_cap, scan_decode_scratch_bytes(sa.bit_length)));
+    CK(launch_scan_decode(sa, ctx->ws_scan, s, &ctx->launches));
     CK(cudaMemcpyAsync(&sl->h_small->flags, &sl->d_small->flags, sizeof(unsigned),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaFreeAsync(tmpb.arena, s));

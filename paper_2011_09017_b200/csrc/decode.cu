@@ -10,6 +10,8 @@
 //                   foreign ACZ1 blob and to validate it exactly like the reference
 //                   (truncation / no-match DecodeError, outlier FormatErrors).
 // k_chain_states  : thread-per-plane chain replay producing the sidecar chain states.
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace acz_b200 {
@@ -399,14 +401,26 @@ __global__ void __launch_bounds__(128) k_chain_states(const uint32_t* __restrict
     float r = 0.0f;
     uint64_t to_side = base % interval;
     to_side = to_side == 0 ? 0 : interval - to_side;
+    // the symbols of a plane are read 16 at a time ahead of the chain (independent loads in
+    // flight instead of one memory round trip per step)
+    constexpr int kAhead = 16;
+    uint32_t sb[kAhead];
     for (uint64_t i = 0; i < P; ++i) {
         const uint64_t flat = base + i;
+        const int slot = (int)(i % kAhead);
+        if (slot == 0) {
+#pragma unroll
+            for (int k = 0; k < kAhead; ++k) sb[k] = i + k < P ? __ldg(sym + flat + k) : 0u;
+        }
         if (to_side == 0) {
             side_state[flat / interval] = i == 0 ? 0.0f : r;
             to_side = interval;
         }
         --to_side;
-        const uint32_t s = sym[flat];
+        uint32_t s = sb[0];
+#pragma unroll
+        for (int k = 1; k < kAhead; ++k)
+            if (slot == k) s = sb[k];
         float v;
         if (s == 0) {
             v = out_value[oi++];
@@ -418,6 +432,198 @@ __global__ void __launch_bounds__(128) k_chain_states(const uint32_t* __restrict
     }
 }
 
+// ---- parallel foreign-stream scan (ref src/huffman.cpp:137-189 + src/codec.cpp:138-169) ----
+// The bitstream is cut into subsequences of kPsBits bits; a thread decodes the codewords
+// that START in its subsequence. The true start of subsequence i is the end of the last
+// codeword that started in subsequence i-1, unknown up front: every thread first decodes from
+// its nominal start, then starts are replaced by the predecessors' exits and the changed
+// subsequences re-decoded until nothing changes. Canonical Huffman codes resynchronise within
+// a few codewords, so a wrong start only perturbs the first few symbols of a subsequence and
+// the fixed point is reached in a handful of passes (capped; the sequential scan is the
+// fallback). A last pass decodes every subsequence from its true start at its global symbol
+// index (a scan of the per-subsequence counts), writes what the sequential scan writes, and
+// records the first error of each kind in flat order.
+constexpr uint64_t kPsBits = 2048;
+constexpr int kPsThreads = 256;
+
+struct PsState {
+    unsigned long long err_dec;   // (flat << 1 | nomatch) of the first decode error, or ~0
+    unsigned long long err_out;   // (flat << 1 | index) of the first outlier error, or ~0
+    unsigned long long esc_n;     // escapes among the first n symbols
+    unsigned long long total;     // symbols in the stream (Σ counts)
+    unsigned int changed;
+};
+
+__global__ void __launch_bounds__(kPsThreads) k_ps_sync(ScanArgs a, unsigned long long* starts,
+                                                        unsigned long long* exits,
+                                                        uint32_t* cnt, uint32_t* esc,
+                                                        uint32_t* dirty, uint64_t M) {
+    extern __shared__ uint32_t s_lut[];
+    __shared__ CanonTables s_ct;
+    load_tables(a.lut, a.canon, s_lut, &s_ct);
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= M || !dirty[i]) return;
+    const uint64_t end = min((i + 1) * kPsBits, a.bit_length);
+    uint64_t pos = starts[i];
+    BitReader br;
+    br.init(a.words, a.nwords, pos);
+    uint32_t c = 0, e = 0;
+    while (pos < end) {
+        uint32_t sym = 0;
+        const uint64_t p0 = pos;
+        if (!decode_one(br, pos, s_lut, s_ct, a.book_sym, &sym)) {
+            pos = p0;
+            break;
+        }
+        ++c;
+        e += sym == 0;
+    }
+    exits[i] = pos;
+    cnt[i] = c;
+    esc[i] = e;
+    dirty[i] = 0;
+}
+
+__global__ void k_ps_fix(const unsigned long long* exits, unsigned long long* starts,
+                         uint32_t* dirty, uint64_t M, PsState* st) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + 1;
+    if (i >= M) return;
+    const unsigned long long e = exits[i - 1];
+    if (starts[i] != e) {
+        starts[i] = e;
+        dirty[i] = 1;
+        st->changed = 1;
+    }
+}
+
+// exclusive scans of the counts (single CTA; a foreign-blob path, not the hot path)
+__global__ void __launch_bounds__(1024) k_ps_scan(const uint32_t* cnt, const uint32_t* esc,
+                                                  unsigned long long* base_sym,
+                                                  unsigned long long* base_esc, uint64_t M,
+                                                  PsState* st) {
+    __shared__ unsigned long long s_a[32], s_b[32];
+    __shared__ unsigned long long s_run_a, s_run_b;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_run_a = 0;
+        s_run_b = 0;
+    }
+    __syncthreads();
+    for (uint64_t c0 = 0; c0 < M; c0 += 1024) {
+        const uint64_t i = c0 + tid;
+        const unsigned long long va = i < M ? cnt[i] : 0, vb = i < M ? esc[i] : 0;
+        unsigned long long ia = va, ib = vb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long xa = __shfl_up_sync(0xffffffffu, ia, o);
+            const unsigned long long xb = __shfl_up_sync(0xffffffffu, ib, o);
+            if (lane >= o) {
+                ia += xa;
+                ib += xb;
+            }
+        }
+        if (lane == 31) {
+            s_a[warp] = ia;
+            s_b[warp] = ib;
+        }
+        __syncthreads();
+        unsigned long long pa = s_run_a, pb = s_run_b, ta = 0, tb = 0;
+        for (int w = 0; w < 32; ++w) {
+            if (w < warp) {
+                pa += s_a[w];
+                pb += s_b[w];
+            }
+            ta += s_a[w];
+            tb += s_b[w];
+        }
+        if (i < M) {
+            base_sym[i] = pa + ia - va;
+            base_esc[i] = pb + ib - vb;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            s_run_a += ta;
+            s_run_b += tb;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) st->total = s_run_a;
+}
+
+__global__ void __launch_bounds__(kPsThreads) k_ps_final(ScanArgs a,
+                                                         const unsigned long long* starts,
+                                                         const unsigned long long* base_sym,
+                                                         const unsigned long long* base_esc,
+                                                         uint64_t M, PsState* st) {
+    extern __shared__ uint32_t s_lut[];
+    __shared__ CanonTables s_ct;
+    load_tables(a.lut, a.canon, s_lut, &s_ct);
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    uint64_t g = base_sym[i];
+    if (g >= a.n) return;
+    uint64_t oi = base_esc[i];
+    const uint64_t end = min((i + 1) * kPsBits, a.bit_length);
+    uint64_t pos = starts[i];
+    BitReader br;
+    br.init(a.words, a.nwords, pos);
+    while (pos < end && g < a.n) {
+        if (g % a.interval == 0 && a.side_bitoff) {
+            a.side_bitoff[g / a.interval] = pos;
+            if (a.side_outl) a.side_outl[g / a.interval] = (uint32_t)oi;
+        }
+        if (a.plane_outl && g % a.plane_size == 0) a.plane_outl[g / a.plane_size] = oi;
+        uint32_t sym = 0;
+        const uint64_t p0 = pos;
+        const uint32_t len = decode_one(br, pos, s_lut, s_ct, a.book_sym, &sym);
+        if (len == 0) {
+            atomicMin(&st->err_dec, ((unsigned long long)g << 1) | (p0 + 64 > a.bit_length ? 0ull : 1ull));
+            return;
+        }
+        if (pos > a.bit_length) {
+            atomicMin(&st->err_dec, (unsigned long long)g << 1);
+            return;
+        }
+        if (a.sym_out) a.sym_out[g] = sym;
+        if (sym == 0) {
+            if (a.out_index) {
+                if (oi >= a.n_outliers) atomicMin(&st->err_out, (unsigned long long)g << 1);
+                else if (a.out_index[oi] != g)
+                    atomicMin(&st->err_out, ((unsigned long long)g << 1) | 1ull);
+            }
+            ++oi;
+        }
+        ++g;
+        if (g == a.n) st->esc_n = oi;
+    }
+}
+
+// Flags exactly as the sequential scan would set them (first error in flat order).
+__global__ void k_ps_flags(ScanArgs a, const PsState* st) {
+    unsigned f = 0;
+    if (st->err_dec != ~0ull) f = (st->err_dec & 1ull) ? kDecNoMatch : kDecTruncated;
+    else if (st->total < a.n) f = kDecTruncated;
+    else if (a.out_index && st->err_out != ~0ull)
+        f = (st->err_out & 1ull) ? kDecOutlierIndex : kDecOutlierMissing;
+    else if (a.out_index && st->esc_n != a.n_outliers) f = kDecOutlierUnused;
+    if (f) atomicOr(a.flags, f);
+}
+
+__global__ void k_ps_init(unsigned long long* starts, uint32_t* dirty, uint64_t M, PsState* st) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < M) {
+        starts[i] = i * kPsBits;
+        dirty[i] = 1;
+    }
+    if (i == 0) {
+        st->err_dec = ~0ull;
+        st->err_out = ~0ull;
+        st->esc_n = 0;
+        st->total = 0;
+        st->changed = 0;
+    }
+}
+
 }  // namespace
 
 cudaError_t set_decode_attrs() {
@@ -425,6 +631,12 @@ cudaError_t set_decode_attrs() {
     if (done) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(k_decode_prev, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kDecSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_ps_sync, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 4 * kLutSize);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_ps_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 4 * kLutSize);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_decode_lorenzo, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  4 * kLutSize);
@@ -461,11 +673,56 @@ cudaError_t decode_stats(unsigned long long* out, bool reset) {
     return e;
 }
 
-cudaError_t launch_scan_decode(const ScanArgs& a, cudaStream_t s, uint64_t* launches) {
+size_t scan_decode_scratch_bytes(uint64_t bit_length) {
+    const uint64_t M = (bit_length + kPsBits - 1) / kPsBits;
+    return 256 + 8 * 4 * M + 4 * 3 * M + 1024;
+}
+
+cudaError_t launch_scan_decode(const ScanArgs& a, void* scratch, cudaStream_t s,
+                               uint64_t* launches) {
     cudaError_t e = set_decode_attrs();
     if (e != cudaSuccess) return e;
-    k_scan_decode<<<1, 128, 4 * kLutSize, s>>>(a);
+    const uint64_t M = (a.bit_length + kPsBits - 1) / kPsBits;
+    const bool force_seq = std::getenv("ACZ_SCAN_SEQUENTIAL") != nullptr;  // testing
+    if (!scratch || M < 64 || force_seq) {  // short streams: one sequential pass
+        k_scan_decode<<<1, 128, 4 * kLutSize, s>>>(a);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    char* p = static_cast<char*>(scratch);
+    PsState* st = reinterpret_cast<PsState*>(p);
+    unsigned long long* starts = reinterpret_cast<unsigned long long*>(p + 256);
+    unsigned long long* exits = starts + M;
+    unsigned long long* base_sym = exits + M;
+    unsigned long long* base_esc = base_sym + M;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(base_esc + M);
+    uint32_t* esc = cnt + M;
+    uint32_t* dirty = esc + M;
+    const unsigned blocks = (unsigned)((M + kPsThreads - 1) / kPsThreads);
+    k_ps_init<<<blocks, kPsThreads, 0, s>>>(starts, dirty, M, st);
     ++*launches;
+    bool converged = false;
+    for (int it = 0; it < 48 && !converged; ++it) {
+        k_ps_sync<<<blocks, kPsThreads, 4 * kLutSize, s>>>(a, starts, exits, cnt, esc, dirty, M);
+        e = cudaMemsetAsync(&st->changed, 0, sizeof(unsigned), s);
+        if (e != cudaSuccess) return e;
+        k_ps_fix<<<blocks, kPsThreads, 0, s>>>(exits, starts, dirty, M, st);
+        *launches += 2;
+        unsigned changed = 1;
+        e = cudaMemcpyAsync(&changed, &st->changed, sizeof(unsigned), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        converged = changed == 0;
+    }
+    if (!converged) {  // no resynchronisation (adversarial stream): sequential scan
+        k_scan_decode<<<1, 128, 4 * kLutSize, s>>>(a);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    k_ps_scan<<<1, 1024, 0, s>>>(cnt, esc, base_sym, base_esc, M, st);
+    k_ps_final<<<blocks, kPsThreads, 4 * kLutSize, s>>>(a, starts, base_sym, base_esc, M, st);
+    k_ps_flags<<<1, 1, 0, s>>>(a, st);
+    *launches += 3;
     return cudaGetLastError();
 }
 

@@ -165,7 +165,12 @@ struct ScanArgs {
     uint64_t plane_size;
     unsigned int* flags;
 };
-cudaError_t launch_scan_decode(const ScanArgs& a, cudaStream_t s, uint64_t* launches);
+// scratch: scan_decode_scratch_bytes(bit_length) bytes (nullptr: sequential single-thread
+// scan). Long streams are scanned in parallel (subsequence resynchronisation); may
+// synchronise the stream while iterating.
+size_t scan_decode_scratch_bytes(uint64_t bit_length);
+cudaError_t launch_scan_decode(const ScanArgs& a, void* scratch, cudaStream_t s,
+                               uint64_t* launches);
 // Rebuild per-chunk chain states (PrevValue) from decoded symbols: thread per plane.
 cudaError_t launch_chain_states(const uint32_t* sym, const unsigned long long* plane_outl,
                                 const float* out_value, PlaneGeom g, double step,

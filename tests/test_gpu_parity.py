@@ -303,3 +303,88 @@ def test_sidecar_roundtrip(acz):
     torch.cuda.synchronize()
     assert torch.equal(d1, d2) and torch.equal(d1, d3)
     assert c3.sidecar() == s
+
+
+
+def _err(fn):
+    """(reference-style error code, message) of a call; (0, "") when it succeeds."""
+    try:
+        fn()
+        return 0, ""
+    except Exception as e:  # noqa: BLE001
+        code = getattr(e, "code", None)
+        if code is None:
+            code = {"ParamError": 1, "DomainError": 2, "FormatError": 3, "DecodeError": 4,
+                    "ShapeError": 5}.get(type(e).__name__, 9)
+        return code, str(e)
+
+
+def _foreign_variants(good):
+    """Corrupted but parseable variants of an ACZ1 blob."""
+    import struct
+    b = bytearray(good)
+    rank = b[6]
+    hdr = 7 + 8 * rank + 8 + 4
+    nout = struct.unpack_from("<I", b, hdr)[0]
+    k = struct.unpack_from("<H", b, hdr + 4)[0]
+    bl_at = hdr + 6 + 5 * k
+    bit_length = struct.unpack_from("<Q", b, bl_at)[0]
+    bits_at = bl_at + 8
+    nbytes = (bit_length + 7) // 8
+    out_at = bits_at + nbytes
+    out = []
+    # flipped bits in the stream (misparses from there on, misaligned outliers)
+    for pos in (nbytes // 3, nbytes // 2, (9 * nbytes) // 10):
+        v = bytearray(b)
+        v[bits_at + pos] ^= 0x5A
+        out.append(bytes(v))
+    # truncated stream: bit_length cut by a quarter, bytes to match
+    nbl = bit_length * 3 // 4
+    out.append(bytes(b[:bl_at]) + struct.pack("<Q", nbl) +
+               bytes(b[bits_at:bits_at + (nbl + 7) // 8]) + bytes(b[out_at:]))
+    if nout >= 2:
+        # last outlier record dropped: an escape without a matching outlier
+        v = bytearray(b)
+        struct.pack_into("<I", v, hdr, nout - 1)
+        out.append(bytes(v[:-12]))
+        # first outlier index moved off its escape (still strictly increasing)
+        v = bytearray(b)
+        i0 = struct.unpack_from("<Q", v, out_at)[0]
+        i1 = struct.unpack_from("<Q", v, out_at + 12)[0]
+        if i1 - i0 > 1:
+            struct.pack_into("<Q", v, out_at, i0 + 1)
+            out.append(bytes(v))
+    return out
+
+
+@pytest.mark.parametrize("case", ["dense", "relu", "outliers"])
+def test_foreign_blob_parallel_scan(acz, reference, case, monkeypatch):
+    """Long foreign (reference-produced) blobs without a sidecar take the parallel
+    resynchronising stream scan: bit-exact decompression; on corrupted blobs the same error
+    code as the reference and the same error (code and message) as the sequential scan."""
+    import torch
+    rng = np.random.default_rng({"dense": 31, "relu": 32, "outliers": 33}[case])
+    radius = 32768
+    x = rng.standard_normal((2, 8, 128, 128)).astype(np.float32)
+    if case == "relu":
+        x = np.maximum(x, 0)
+    if case == "outliers":
+        x *= 3
+        radius = 256
+    good = reference.compress(x, 1e-3, radius)
+    assert acz.parse_acz1(good)["bit_length"] > 64 * 2048  # long enough for the parallel scan
+    fb = acz.blob_from_bytes(good)
+    for zf in (False, True):
+        d = acz.decompress(fb, zero_filter=zf)
+        torch.cuda.synchronize()
+        assert d.cpu().numpy().ravel().tobytes() == reference.decompress(good, x.size, zf).tobytes()
+    variants = _foreign_variants(good)
+    assert len(variants) >= 4
+    for v in variants:
+        ref = _err(lambda: reference.decompress(v, x.size))
+        par = _err(lambda: acz.decompress(acz.blob_from_bytes(v)))
+        monkeypatch.setenv("ACZ_SCAN_SEQUENTIAL", "1")
+        seq = _err(lambda: acz.decompress(acz.blob_from_bytes(v)))
+        monkeypatch.delenv("ACZ_SCAN_SEQUENTIAL")
+        assert par == seq
+        assert par[0] == ref[0], (par, ref)
