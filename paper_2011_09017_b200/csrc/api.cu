@@ -231,6 +231,14 @@ uint64_t sidecar_interval_default() {
     return v;
 }
 
+// Sidecar interval of a tensor: PrevValue and the Lorenzo2d wavefront path use fixed-size
+// chunks (chunk-parallel symbol decode); row-major Lorenzo2d (single-row or very tall planes)
+// one chunk per plane.
+bool lorenzo_wave(const PlaneGeom& g) { return g.rows > 1 && g.rows <= kLorenzoWaveRows; }
+uint64_t sidecar_interval_for(uint32_t pred, const PlaneGeom& g) {
+    return (pred == ACZ_PRED_PREV || lorenzo_wave(g)) ? sidecar_interval_default() : g.plane_size;
+}
+
 uint64_t acz1_size(uint32_t rank, uint32_t book, uint64_t bits, uint64_t nout) {
     // ref src/codec.cpp:177-199
     return 4 + 1 + 1 + 1 + 8ull * rank + 8 + 4 + 4 + 2 + 5ull * book + 8 + (bits + 7) / 8 +
@@ -540,7 +548,7 @@ int decompress_on(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, int zero_fi
     const acz_gpu_blob_info_t& in = b->info;
     const PlaneGeom g = plane_geom(in.shape, in.rank);
     if (in.predictor == ACZ_PRED_LORENZO2D)
-        CK(grow(&sl->ws_row, &sl->ws_row_cap, 4ull * g.planes * g.cols));
+        CK(grow(&sl->ws_row, &sl->ws_row_cap, 4ull * std::max(g.planes * g.cols, in.element_count)));
     DecodeArgs a;
     a.words = b->words;
     a.nwords = b->nwords;
@@ -565,6 +573,7 @@ int decompress_on(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, int zero_fi
     a.zero_filter = zero_filter;
     a.out = d_out;
     a.row_scratch = static_cast<float*>(sl->ws_row);
+    a.sym_scratch = static_cast<uint32_t*>(sl->ws_row);  // (the two Lorenzo paths exclusive)
     {
         KTimer kt(ctx, ACZ_K_DECODE, s);
         CK(launch_decode(a, ctx->sms, s, &ctx->launches));
@@ -610,7 +619,7 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     if (rc) return rc;
     const PlaneGeom g = plane_geom(shape, rank);
     const uint32_t alphabet = 2u * quant_radius;
-    const uint64_t interval = predictor == ACZ_PRED_PREV ? sidecar_interval_default() : g.plane_size;
+    const uint64_t interval = sidecar_interval_for(predictor, g);
     const uint64_t nchunks = (n + interval - 1) / interval;
 
     CK(grow(&sl->ws_sym, &sl->ws_sym_cap, 4ull * n));
@@ -1212,7 +1221,7 @@ static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uin
             dmsg = "invalid code length in codebook";
         }
     const PlaneGeom g = plane_geom(in.shape, in.rank);
-    const uint64_t interval = pred == ACZ_PRED_PREV ? sidecar_interval_default() : g.plane_size;
+    const uint64_t interval = sidecar_interval_for((uint32_t)pred, g);
     // sidecar supplied?
     bool have_side = false;
     uint64_t side_interval = interval, side_chunks = (count + interval - 1) / interval;
@@ -1227,7 +1236,7 @@ static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uin
             hdr[3] == (count + hdr[2] - 1) / hdr[2] && hdr[4] == blob_binding(in) &&
             hdr[5] == (want_outl ? 1ull : 0ull) &&
             sidecar_size == sidecar_bytes(hdr[3], want_outl) &&
-            (pred == ACZ_PRED_PREV || hdr[2] == g.plane_size)) {
+            (pred == ACZ_PRED_PREV || hdr[2] == sidecar_interval_for((uint32_t)pred, g))) {
             have_side = true;
             side_interval = hdr[2];
             side_chunks = hdr[3];

@@ -341,6 +341,81 @@ __global__ void __launch_bounds__(128) k_decode_lorenzo(DecodeArgs a) {
     }
 }
 
+// Lorenzo2d decode for the wavefront path: (1) a thread per plane decodes the plane's
+// symbols from its sidecar bit offset into a scratch array; (2) a warp per plane rebuilds
+// the values by anti-diagonals (see k_quant_lorenzo_wave), escapes taking their outlier by
+// binary search over the plane's slice of the (sorted) outlier list.
+__global__ void __launch_bounds__(128) k_lorenzo_syms(DecodeArgs a, uint32_t* __restrict__ syms) {
+    extern __shared__ uint32_t s_lut[];
+    __shared__ CanonTables s_ct;
+    load_tables(a.lut, a.canon, s_lut, &s_ct);
+    const uint64_t chunk = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (chunk >= a.nchunks) return;
+    const uint64_t start = chunk * a.interval;
+    const uint64_t cnt = min(a.interval, a.g.n - start);
+    uint64_t pos = a.side_bitoff[chunk];
+    BitReader br;
+    br.init(a.words, a.nwords, pos);
+    for (uint64_t i = 0; i < cnt; ++i) {
+        uint32_t sym = 0;
+        decode_one(br, pos, s_lut, s_ct, a.book_sym, &sym);
+        syms[start + i] = sym;
+    }
+}
+
+__global__ void __launch_bounds__(32) k_decode_lorenzo_wave(DecodeArgs a,
+                                                            const uint32_t* __restrict__ syms) {
+    extern __shared__ float diag[];  // 3 x rows
+    const uint64_t plane = blockIdx.x;
+    if (plane >= a.g.planes) return;
+    const int lane = threadIdx.x;
+    const int rows = (int)a.g.rows, cols = (int)a.g.cols;
+    const uint64_t base = plane * a.g.plane_size;
+    const uint32_t* sp = syms + base;
+    float* op = a.out + base;
+    // the plane's outliers lie between the prefixes of its first and one-past-last chunks
+    const uint64_t c0 = base / a.interval, c1 = (base + a.g.plane_size - 1) / a.interval + 1;
+    const uint32_t o0 = a.side_outl[c0];
+    const uint32_t o1 = c1 < a.nchunks ? a.side_outl[c1] : (uint32_t)a.n_outliers;
+    const long long R = a.radius;
+    const float zthr = a.zero_filter ? __double2float_rd(a.eb) : -1.0f;
+    float* d0 = diag;
+    float* d1 = diag + rows;
+    float* d2 = diag + 2 * rows;
+    for (int d = 0; d < rows + cols - 1; ++d) {
+        const int r_lo = d - (cols - 1) > 0 ? d - (cols - 1) : 0;
+        const int r_hi = d < rows - 1 ? d : rows - 1;
+        for (int r = r_lo + lane; r <= r_hi; r += 32) {
+            const int c = d - r;
+            const uint64_t off = (uint64_t)r * cols + c;
+            const uint32_t sym = __ldg(sp + off);
+            float v;
+            if (sym == 0) {
+                uint32_t lo = o0, hi = o1;  // the outlier record of flat index base + off
+                const unsigned long long key = base + off;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (__ldg(a.out_index + mid) < key) lo = mid + 1; else hi = mid;
+                }
+                v = __ldg(a.out_value + lo);
+            } else {
+                const double dl = c > 0 ? (double)d1[r] : 0.0;
+                const double dt = r > 0 ? (double)d1[r - 1] : 0.0;
+                const double dtl = (r > 0 && c > 0) ? (double)d2[r - 1] : 0.0;
+                const double pred = __dsub_rn(__dadd_rn(dl, dt), dtl);
+                v = recon_value(pred, (double)((long long)sym - R), a.step);
+            }
+            d0[r] = v;
+            op[off] = fabsf(v) <= zthr ? 0.0f : v;
+        }
+        __syncwarp();
+        float* t = d2;
+        d2 = d1;
+        d1 = d0;
+        d0 = t;
+    }
+}
+
 // Single-thread sequential decode of the whole stream (foreign blobs, generic Huffman).
 __global__ void k_scan_decode(ScanArgs a) {
     extern __shared__ uint32_t s_lut[];
@@ -643,6 +718,9 @@ cudaError_t set_decode_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_scan_decode, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  4 * kLutSize);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_lorenzo_syms, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 4 * kLutSize);
     done = e == cudaSuccess;
     return e;
 }
@@ -656,6 +734,11 @@ cudaError_t launch_decode(const DecodeArgs& a, int sms, cudaStream_t s, uint64_t
         uint64_t blocks = (tasks + kDW - 1) / kDW;
         if (blocks > (uint64_t)sms) blocks = sms;  // persistent: one CTA per SM
         k_decode_prev<<<(unsigned)blocks, kDW * 32, kDecSmem, s>>>(a);
+    } else if (a.g.rows > 1 && a.g.rows <= kLorenzoWaveRows && a.sym_scratch) {
+        const uint64_t blocks = (a.nchunks + threads - 1) / threads;
+        k_lorenzo_syms<<<(unsigned)blocks, threads, 4 * kLutSize, s>>>(a, a.sym_scratch);
+        k_decode_lorenzo_wave<<<(unsigned)a.g.planes, 32, 3 * 4 * a.g.rows, s>>>(a, a.sym_scratch);
+        ++*launches;
     } else {
         const uint64_t blocks = (a.g.planes + threads - 1) / threads;
         k_decode_lorenzo<<<(unsigned)blocks, threads, 4 * kLutSize, s>>>(a);

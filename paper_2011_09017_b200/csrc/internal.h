@@ -67,6 +67,9 @@ struct QuantArgs {
     float* row_scratch;       // planes*cols floats (Lorenzo2d only)
     unsigned int* flags;      // kFlagNonFinite
 };
+// Lorenzo2d planes of up to this many rows use the anti-diagonal wavefront kernels
+// (3 diagonals of floats in shared memory per warp: <= 48 KB).
+constexpr uint64_t kLorenzoWaveRows = 4096;
 cudaError_t launch_quant(const QuantArgs& a, int sms, cudaStream_t s, uint64_t* launches);
 // ---- quant_spec.cu (long planes, PrevValue) ----
 bool quant_spec_applicable(uint32_t predictor, uint64_t plane_size, uint64_t planes, int sms);
@@ -136,7 +139,8 @@ struct DecodeArgs {
     uint32_t predictor;
     int zero_filter;
     float* out;
-    float* row_scratch;              // Lorenzo2d
+    float* row_scratch;              // Lorenzo2d (row-major path)
+    uint32_t* sym_scratch;           // Lorenzo2d wavefront path: n symbols
 };
 cudaError_t launch_decode(const DecodeArgs& a, int sms, cudaStream_t s, uint64_t* launches);
 cudaError_t decode_stats(unsigned long long* out, bool reset);

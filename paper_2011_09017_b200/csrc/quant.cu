@@ -134,6 +134,52 @@ __global__ void __launch_bounds__(128) k_quant_lorenzo_serial(const float* __res
     if (bad) atomicOr(flags, kFlagNonFinite);
 }
 
+// Lorenzo2d by anti-diagonal wavefront: element (r, c) needs the
+// reconstructions of (r, c-1), (r-1, c) -- diagonal d-1 -- and (r-1, c-1) -- diagonal d-2 --
+// so all elements of one anti-diagonal are independent. A warp owns a plane and walks its
+// rows+cols-1 diagonals; the last two diagonals' reconstructions live in shared memory,
+// indexed by row. Bit-identical to the row-major recurrence (same expression per element).
+__global__ void __launch_bounds__(32) k_quant_lorenzo_wave(const float* __restrict__ x,
+                                                           PlaneGeom g, QParams qp,
+                                                           uint32_t* __restrict__ sym,
+                                                           unsigned int* flags) {
+    extern __shared__ float diag[];  // 3 x rows
+    const uint64_t plane = blockIdx.x;
+    if (plane >= g.planes) return;
+    const int lane = threadIdx.x;
+    const int rows = (int)g.rows, cols = (int)g.cols;
+    const uint64_t base = plane * g.plane_size;
+    const float* xp = x + base;
+    uint32_t* sp = sym + base;
+    float* d0 = diag;             // diagonal d   (being written)
+    float* d1 = diag + rows;      // diagonal d-1
+    float* d2 = diag + 2 * rows;  // diagonal d-2
+    bool bad = false;
+    for (int d = 0; d < rows + cols - 1; ++d) {
+        const int r_lo = d - (cols - 1) > 0 ? d - (cols - 1) : 0;
+        const int r_hi = d < rows - 1 ? d : rows - 1;
+        for (int r = r_lo + lane; r <= r_hi; r += 32) {
+            const int c = d - r;
+            const uint64_t off = (uint64_t)r * cols + c;
+            const float xf = __ldg(xp + off);
+            bad |= !isfinite(xf);
+            const double dl = c > 0 ? (double)d1[r] : 0.0;
+            const double dt = r > 0 ? (double)d1[r - 1] : 0.0;
+            const double dtl = (r > 0 && c > 0) ? (double)d2[r - 1] : 0.0;
+            const double pred = __dsub_rn(__dadd_rn(dl, dt), dtl);
+            double v;
+            sp[off] = qstep((double)xf, xf, pred, qp, &v);
+            d0[r] = (float)v;
+        }
+        __syncwarp();
+        float* t = d2;
+        d2 = d1;
+        d1 = d0;
+        d0 = t;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, kFlagNonFinite);
+}
+
 }  // namespace
 
 cudaError_t launch_quant(const QuantArgs& a, int sms, cudaStream_t s, uint64_t* launches) {
@@ -148,7 +194,11 @@ cudaError_t launch_quant(const QuantArgs& a, int sms, cudaStream_t s, uint64_t* 
         else
             k_quant_prev_serial<uint32_t><<<(unsigned)blocks, kQW * 32, 0, s>>>(
                 a.x, a.g, qp, a.sym, a.side_state, a.interval, a.flags);
-    } else {
+    } else if (a.g.rows > 1 && a.g.rows <= kLorenzoWaveRows) {
+        const QParams qp = make_qparams(a.eb, a.radius);
+        k_quant_lorenzo_wave<<<(unsigned)a.g.planes, 32, 3 * 4 * a.g.rows, s>>>(a.x, a.g, qp,
+                                                                              a.sym, a.flags);
+    } else {  // single rows (no wavefront) or very tall planes: row-major, thread per plane
         const unsigned threads = 128;
         const uint64_t blocks = (a.g.planes + threads - 1) / threads;
         k_quant_lorenzo_serial<<<(unsigned)blocks, threads, 0, s>>>(

@@ -388,3 +388,32 @@ def test_foreign_blob_parallel_scan(acz, reference, case, monkeypatch):
         monkeypatch.delenv("ACZ_SCAN_SEQUENTIAL")
         assert par == seq
         assert par[0] == ref[0], (par, ref)
+
+
+@pytest.mark.parametrize("case", ["relu_56", "dense_227", "tall_100x7", "wide_5x300", "tiny_2x2",
+                                  "rank2_70x90", "outliers_r16", "eb1e-2_smooth", "rows33"])
+def test_lorenzo_wavefront_parity(acz, oracle, case):
+    """Lorenzo2d through the anti-diagonal wavefront quantiser / decoder: every artefact and
+    both decompressions bit-exact against the oracle (row-major reference recurrence)."""
+    rng = np.random.default_rng(abs(hash(case)) % (1 << 32))
+    eb, radius = 1e-3, 32768
+    if case == "relu_56":
+        x = np.maximum(rng.standard_normal((2, 4, 56, 56)), 0)
+    elif case == "dense_227":
+        x = rng.standard_normal((1, 2, 227, 227))
+    elif case == "tall_100x7":
+        x = rng.standard_normal((3, 100, 7))
+    elif case == "wide_5x300":
+        x = rng.standard_normal((3, 5, 300))
+    elif case == "tiny_2x2":
+        x = rng.standard_normal((7, 2, 2))
+    elif case == "rank2_70x90":
+        x = rng.standard_normal((70, 90))
+    elif case == "outliers_r16":
+        x, radius = rng.standard_normal((2, 3, 40, 50)) * 4, 16
+    elif case == "eb1e-2_smooth":
+        y = rng.standard_normal((2, 3, 64, 64))
+        x, eb = np.cumsum(np.cumsum(y, axis=-1), axis=-2) * 0.05, 1e-2
+    elif case == "rows33":
+        x = np.maximum(rng.standard_normal((4, 33, 45)), 0)
+    _check_all(acz, oracle, x, eb, radius, 1)
