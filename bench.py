@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--eb", type=float, default=EB)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     return ap.parse_args()
 
 
