@@ -327,6 +327,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # ACZ_BENCH_ONE_GPU=1 (testing the multi-rank path on a one-GPU box): every rank on cuda:0,
+    # gloo for the barrier / max-reduction; the numbers are not a scaling measurement
+    one_gpu = os.environ.get("ACZ_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -334,7 +339,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         peak, kind = load_peaks()
