@@ -1486,7 +1486,10 @@ cudaError_t launch_histogram(const void* sym, int sym16, uint64_t n, uint32_t al
     const uint32_t win_n =
         alphabet - win_lo < (uint32_t)kHistWindow ? alphabet - win_lo : (uint32_t)kHistWindow;
     uint64_t blocks = (n / 4 + 511) / 512;
-    const uint64_t cap = (uint64_t)sms * 4;
+#ifndef ACZ_HIST_BPS
+#define ACZ_HIST_BPS 2  // blocks per SM (measured: fewer flush atomics, same read rate)
+#endif
+    const uint64_t cap = (uint64_t)sms * ACZ_HIST_BPS;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) blocks = 1;
     if (sym16)
