@@ -93,7 +93,8 @@ __device__ unsigned long long g_qstats[8];
 // per-phase SM cycles summed over segments (debug): geometry+phase A, look-back wait,
 // walk, exit+store
 __device__ unsigned long long g_qclk[8];  // + [4] exact-step, [5] batch, [6] pass-1, [7] classify cycles
-__device__ unsigned long long g_wclk[4];  // walk batch split (debug): gather, evaluate, resolve
+__device__ unsigned long long g_wclk[4];
+__device__ unsigned long long g_spec_fixes;  // symbols / sidecar states rewritten by the replay  // walk batch split (debug): gather, evaluate, resolve
 
 struct SP {
     double eb, step, inv_step, radius_d, Tmax;
@@ -103,6 +104,8 @@ struct SP {
     int B;  // anchor binade exponent
     uint64_t P, nseg, interval, planes;
     int ishift;  // log2(interval): PrevValue sidecar intervals are powers of two
+    unsigned long long* segbeg;  // verification: first position of every segment
+    float* vexit;                // verification: the walk's exit state of every segment
 };
 
 struct XS {
@@ -526,11 +529,15 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     if (MODE == kBack) {
         b0 = hdr->seg0;
         b1 = b0 + (uint64_t)max(0, hdr->len);
-        if (hdr->len <= 0) return tin_given;  // empty segment: state passes through
+        if (hdr->len <= 0) {  // empty segment: state passes through
+            if (lane == 0) p.vexit[sidx] = tin_given;
+            return tin_given;
+        }
     } else {
         b0 = seg_bound_w(xwin, xbase, j, p);      // first range start
         b1 = seg_bound_w(xwin, xbase, j + 1, p);  // next segment's first start
     }
+    if (MODE != kBack && lane == 0) p.segbeg[sidx] = b0;
     const int xoff = (int)((int64_t)b0 - xbase);  // xs index of segment position 0
     const float* __restrict__ xg = xp + b0;        // global input at segment position 0
     (void)xg;
@@ -563,6 +570,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 tin = *((volatile float*)exits + sidx - 1);
             }
             exits[sidx] = tin;
+            p.vexit[sidx] = tin;
             __threadfence();
             atomicExch(status + sidx, 1u);
         }
@@ -936,14 +944,14 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             texit = __double2float_rn(__dadd_rn((double)S.s[last], Dl));
         }
     }
+    if (lane == 0) p.vexit[sidx] = texit;
     if (MODE == kFused && lane == 0) {
         exits[sidx] = texit;
         __threadfence();
         atomicExch(status + sidx, 1u);
     }
-    // ---- symbols out (coalesced) ----------------------------------------------------
-    SymT* so = sym_out + plane_flat0 + seg0;
-    for (int i = lane; i < len; i += kW) so[i] = S.sym[i];
+    // (symbols and sidecar states leave through the exact replay, k_spec_verify)
+    (void)sym_out;
     tphase(3);
     return texit;
 }
@@ -1005,6 +1013,126 @@ __global__ void __launch_bounds__(kW) k_quant_spec_back(const float* __restrict_
     }
 }
 
+// ---- exactness net ------------------------------------------------------------------------
+// The certified walk's translation argument has rare holes (fuzzing with extreme error
+// bounds / radii finds chains that stay one ulp off while every symbol still matches, and a
+// few wrong symbols). The walk's job is therefore reduced to producing every segment's exit
+// state; the symbols and sidecar states are then produced by an exact replay: a thread per
+// segment runs the reference step serially from the segment's entry (its predecessor's walk
+// exit), 32 segments per warp through shared-memory tiles staged with cp.async (coalesced,
+// no load latency on the chain; the thread-per-plane quantiser's layout). A segment whose
+// replayed exit differs from its walk exit marks its plane: the successors started from a
+// wrong state and k_spec_fixup replays the rest of that plane serially from the first exact
+// exit. By induction over the segments of a plane (segment 0 starts from 0) the output is
+// the reference's.
+constexpr int kRW = 4;   // warps per replay CTA
+constexpr int kRT = 32;  // tile width
+template <typename SymT>
+__global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restrict__ x, SP p, const int* dB,
+                                                          SymT* __restrict__ sym_out,
+                                                          float* __restrict__ side_state,
+                                                          float* __restrict__ rexit,
+                                                          unsigned int* __restrict__ pfirst,
+                                                          unsigned long long* fixes) {
+    __shared__ uint32_t tile[kRW][2][32][kRT + 1];
+    QParams qp;
+    spec_params(p, qp, dB);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t total = p.planes * p.nseg;
+    const uint64_t s0 = ((uint64_t)blockIdx.x * kRW + w) * 32;
+    if (s0 >= total) return;
+    const uint64_t sidx = s0 + lane;
+    const bool active = sidx < total;
+    const uint64_t plane = active ? sidx / p.nseg : 0, j = active ? sidx % p.nseg : 0;
+    const uint64_t b = active ? p.segbeg[sidx] : 0;
+    const uint64_t e = !active ? 0 : (j + 1 < p.nseg ? p.segbeg[sidx + 1] : p.P);
+    const uint64_t len = e > b ? e - b : 0;
+    const uint64_t base = plane * p.P + b;  // flat index of my segment's first element
+    double r = (!active || j == 0) ? 0.0 : (double)p.vexit[sidx - 1];
+    uint64_t maxlen = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    const uint64_t ntiles = (maxlen + kRT - 1) / kRT;
+    auto issue = [&](uint64_t t) {
+        for (int q = 0; q < 32; ++q) {
+            const uint64_t lq = __shfl_sync(0xffffffffu, len, q);
+            const uint64_t bq = __shfl_sync(0xffffffffu, base, q);
+            const uint64_t k = t * kRT + lane;
+            if (k < lq) cp_async4(&tile[w][t & 1][q][lane], x + bq + k);
+        }
+        cp_async_commit();
+    };
+    unsigned long long nfix = 0;
+    if (ntiles) issue(0);
+    for (uint64_t t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) {
+            issue(t + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const uint64_t k0 = t * kRT;
+        const int cnt = k0 < len ? (int)min((uint64_t)kRT, len - k0) : 0;
+        uint32_t* tr = tile[w][t & 1][lane];
+        // the sidecar point of this tile, if any (interval >= 32: at most one)
+        const uint64_t f0 = base + k0;
+        const int ks = (int)((p.interval - (f0 & (p.interval - 1))) & (p.interval - 1));
+#pragma unroll 4
+        for (int k = 0; k < cnt; ++k) {
+            const float xf = __uint_as_float(tr[k]);
+            // the plane's first element (r == 0 then: segment 0 starts from 0) needs no reset
+            if (k == ks) side_state[(f0 + k) >> p.ishift] = (float)r;
+            double v;
+            tr[k] = qstep((double)xf, xf, r, qp, &v);
+            r = v;
+        }
+        __syncwarp();
+        for (int q = 0; q < 32; ++q) {  // symbols out, coalesced per segment
+            const uint64_t lq = __shfl_sync(0xffffffffu, len, q);
+            const uint64_t bq = __shfl_sync(0xffffffffu, base, q);
+            const uint64_t k = k0 + lane;
+            if (k < lq) sym_out[bq + k] = (SymT)tile[w][t & 1][q][lane];
+        }
+        __syncwarp();
+    }
+    if (active) {
+        const float ex = (float)r;
+        rexit[sidx] = ex;
+        if (j + 1 < p.nseg && __float_as_uint(ex) != __float_as_uint(p.vexit[sidx])) {
+            atomicMin(pfirst + plane, (unsigned)j);
+            ++nfix;
+        }
+    }
+    if (nfix) atomicAdd(fixes, nfix);
+}
+
+// Serial replay of a plane from the first segment whose exit disagreed (see k_spec_verify).
+template <typename SymT>
+__global__ void __launch_bounds__(128) k_spec_fixup(const float* __restrict__ x, SP p, const int* dB,
+                                                    SymT* __restrict__ sym_out,
+                                                    float* __restrict__ side_state,
+                                                    const float* __restrict__ rexit,
+                                                    const unsigned int* __restrict__ pfirst) {
+    const uint64_t plane = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (plane >= p.planes) return;
+    const unsigned jf = pfirst[plane];
+    if (jf == 0xFFFFFFFFu) return;
+    QParams qp;
+    spec_params(p, qp, dB);
+    const uint64_t sidx = plane * p.nseg + jf;  // its replayed exit is exact
+    double r = (double)rexit[sidx];
+    const uint64_t base = plane * p.P;
+    for (uint64_t i = p.segbeg[sidx + 1]; i < p.P; ++i) {
+        const uint64_t flat = base + i;
+        if ((flat & (p.interval - 1)) == 0) side_state[flat >> p.ishift] = (float)r;
+        const float xf = __ldg(x + flat);
+        double v;
+        sym_out[flat] = (SymT)qstep((double)xf, xf, r, qp, &v);
+        r = v;
+    }
+}
+
 }  // namespace
 
 // Scratch layout: [B | ticket | status (u32/segment) | exits (f32/segment) | segment states]
@@ -1015,6 +1143,35 @@ size_t spec_store_stride() {
 size_t spec_store_offset(uint64_t total) {
     return ((256 + 2 * ((4 * total + 255) & ~255ull)) + 255) & ~size_t(255);
 }
+// verification arrays after the decoupled path's segment states
+size_t spec_verify_offset(uint64_t total) {
+    return ((spec_store_offset(total) + total * spec_store_stride()) + 255) & ~size_t(255);
+}
+
+namespace {
+cudaError_t launch_spec_verify(const QuantArgs& a, const SP& p, const int* dB, float* rexit,
+                               unsigned* pfirst, cudaStream_t s, uint64_t* launches) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const unsigned long long total = (unsigned long long)a.g.planes * p.nseg;
+    unsigned long long* fixes = nullptr;
+    e = cudaGetSymbolAddress(reinterpret_cast<void**>(&fixes), g_spec_fixes);
+    if (e != cudaSuccess) return e;
+    const unsigned vb = (unsigned)((total + kRW * 32 - 1) / (kRW * 32));
+    const unsigned fb = (unsigned)((a.g.planes + 127) / 128);
+    if (a.sym16) {
+        k_spec_verify<uint16_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rexit,
+                                                   pfirst, fixes);
+        k_spec_fixup<uint16_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rexit, pfirst);
+    } else {
+        k_spec_verify<uint32_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rexit,
+                                                        pfirst, fixes);
+        k_spec_fixup<uint32_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rexit, pfirst);
+    }
+    *launches += 2;
+    return cudaGetLastError();
+}
+}  // namespace
 
 // Host launcher. `scratch` must hold quant_spec_scratch_bytes(planes, plane_size).
 cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
@@ -1042,6 +1199,13 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     float* exits = reinterpret_cast<float*>(sc + 256 + ((4 * total + 255) & ~255ull));
     cudaError_t e = cudaMemsetAsync(sc, 0, 256 + ((4 * total + 255) & ~255ull), s);
     if (e != cudaSuccess) return e;
+    char* vb = sc + spec_verify_offset(total);
+    p.segbeg = reinterpret_cast<unsigned long long*>(vb);
+    p.vexit = reinterpret_cast<float*>(vb + 8 * total);
+    float* rexit = reinterpret_cast<float*>(vb + 12 * total);
+    unsigned* pfirst = reinterpret_cast<unsigned*>(vb + 16 * total);
+    e = cudaMemsetAsync(pfirst, 0xFF, 4 * a.g.planes, s);
+    if (e != cudaSuccess) return e;
     static const unsigned qdiv = [] {
         const char* e = std::getenv("ACZ_ANCHOR_Q");
         const unsigned v = e ? (unsigned)std::strtoul(e, nullptr, 10) : 0u;
@@ -1060,7 +1224,7 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
             k_quant_spec<uint32_t><<<(unsigned)total, kW, 0, s>>>(
                 a.x, p, dB, a.sym, a.side_state, status, exits, ticket, a.flags, total);
         ++*launches;
-        return cudaGetLastError();
+        return launch_spec_verify(a, p, dB, rexit, pfirst, s, launches);
     }
     // decoupled: phase A of every segment (throughput), then one warp per plane walks its
     // segments in order (the only sequential part), from the persisted segment states
@@ -1077,25 +1241,27 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
             a.x, p, dB, a.sym, a.side_state, a.flags, store);
     }
     *launches += 2;
-    return cudaGetLastError();
+    return launch_spec_verify(a, p, dB, rexit, pfirst, s, launches);
 }
 
 cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
     cudaError_t e = cudaMemcpyFromSymbol(out, g_qstats, sizeof(g_qstats));
     if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 8, g_qclk, sizeof(g_qclk));  // 8 values
-    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 16, g_wclk, sizeof(g_wclk));  // 4 values
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 16, g_wclk, 3 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 19, g_spec_fixes, sizeof(g_spec_fixes));
     if (e == cudaSuccess && reset) {
         unsigned long long z[8] = {0};
         e = cudaMemcpyToSymbol(g_qstats, z, sizeof(z));
         if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_qclk, z, sizeof(g_qclk));
         if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_wclk, z, sizeof(g_wclk));
+        if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_spec_fixes, z, sizeof(g_spec_fixes));
     }
     return e;
 }
 
 size_t quant_spec_scratch_bytes(uint64_t planes, uint64_t plane_size) {
     const uint64_t total = planes * ((plane_size + kSeg - 1) / kSeg);
-    return spec_store_offset(total) + total * spec_store_stride();
+    return spec_verify_offset(total) + 16 * total + 4 * planes + 512;
 }
 
 // Speculative (K2b) vs thread-per-plane (K2a) quantiser, by a cost model calibrated on B200
