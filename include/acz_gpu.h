@@ -245,9 +245,9 @@ int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, vo
  * cycles summed over warps (table prologue, stream staging, symbol loop) and warp count;
  * when n >= 26, out[24..25]: speculative-quantiser walk cycles in exact steps / batches;
  * when n >= 28, out[26..27]: its phase-A pass-1 / classification cycles; when n >= 32,
- * out[28..30]: its walk batch cycles split into gather / evaluate / resolve, out[31]: symbols /
- * sidecar states the exact replay of the speculative quantiser rewrote (0 when the certified
- * walk was right; counted in every build). */
+ * out[28..30]: its walk batch cycles split into gather / evaluate / resolve, out[31]: sidecar
+ * chunks whose recorded walk state the exact replay of the speculative quantiser found wrong
+ * (their planes were recomputed serially; counted in every build). */
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset);
 /* Number of CUDA kernel launches issued by this context since creation. */
 uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx);

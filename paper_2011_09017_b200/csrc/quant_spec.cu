@@ -104,8 +104,6 @@ struct SP {
     int B;  // anchor binade exponent
     uint64_t P, nseg, interval, planes;
     int ishift;  // log2(interval): PrevValue sidecar intervals are powers of two
-    unsigned long long* segbeg;  // verification: first position of every segment
-    float* vexit;                // verification: the walk's exit state of every segment
 };
 
 struct XS {
@@ -529,15 +527,11 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     if (MODE == kBack) {
         b0 = hdr->seg0;
         b1 = b0 + (uint64_t)max(0, hdr->len);
-        if (hdr->len <= 0) {  // empty segment: state passes through
-            if (lane == 0) p.vexit[sidx] = tin_given;
-            return tin_given;
-        }
+        if (hdr->len <= 0) return tin_given;  // empty segment: state passes through
     } else {
         b0 = seg_bound_w(xwin, xbase, j, p);      // first range start
         b1 = seg_bound_w(xwin, xbase, j + 1, p);  // next segment's first start
     }
-    if (MODE != kBack && lane == 0) p.segbeg[sidx] = b0;
     const int xoff = (int)((int64_t)b0 - xbase);  // xs index of segment position 0
     const float* __restrict__ xg = xp + b0;        // global input at segment position 0
     (void)xg;
@@ -570,7 +564,6 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 tin = *((volatile float*)exits + sidx - 1);
             }
             exits[sidx] = tin;
-            p.vexit[sidx] = tin;
             __threadfence();
             atomicExch(status + sidx, 1u);
         }
@@ -944,7 +937,6 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             texit = __double2float_rn(__dadd_rn((double)S.s[last], Dl));
         }
     }
-    if (lane == 0) p.vexit[sidx] = texit;
     if (MODE == kFused && lane == 0) {
         exits[sidx] = texit;
         __threadfence();
@@ -1015,55 +1007,50 @@ __global__ void __launch_bounds__(kW) k_quant_spec_back(const float* __restrict_
 
 // ---- exactness net ------------------------------------------------------------------------
 // The certified walk's translation argument has rare holes (fuzzing with extreme error
-// bounds / radii finds chains that stay one ulp off while every symbol still matches, and a
-// few wrong symbols). The walk's job is therefore reduced to producing every segment's exit
-// state; the symbols and sidecar states are then produced by an exact replay: a thread per
-// segment runs the reference step serially from the segment's entry (its predecessor's walk
-// exit), 32 segments per warp through shared-memory tiles staged with cp.async (coalesced,
-// no load latency on the chain; the thread-per-plane quantiser's layout). A segment whose
-// replayed exit differs from its walk exit marks its plane: the successors started from a
-// wrong state and k_spec_fixup replays the rest of that plane serially from the first exact
-// exit. By induction over the segments of a plane (segment 0 starts from 0) the output is
-// the reference's.
+// bounds / radii finds chains left an ulp off while every symbol still matches, and a few
+// wrong symbols). The walk records the state before every sidecar point (every `interval`
+// elements; sidecar points are candidates, so the walk evaluates them exactly from its
+// state); an exact replay then recomputes every element: one thread per sidecar chunk runs
+// the reference step serially from the chunk's recorded entry state, 32 chunks per warp
+// through shared-memory tiles staged with cp.async, and rewrites the symbols. A chunk whose
+// replayed end state differs from the next chunk's recorded entry marks its plane, and
+// k_spec_fixup replays the rest of that plane serially from the first such chunk, whose
+// replayed end is exact. By induction over the chunks of a plane (its first element starts
+// from 0) the output is the reference's.
 constexpr int kRW = 4;   // warps per replay CTA
-constexpr int kRT = 32;  // tile width
+constexpr int kRT = 32;  // tile width (elements of a chunk per tile)
 template <typename SymT>
-__global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restrict__ x, SP p, const int* dB,
+__global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restrict__ x, SP p,
+                                                          const int* dB,
                                                           SymT* __restrict__ sym_out,
                                                           float* __restrict__ side_state,
-                                                          float* __restrict__ rexit,
-                                                          unsigned int* __restrict__ pfirst,
+                                                          float* __restrict__ rfix,
+                                                          unsigned long long* __restrict__ pfirst,
                                                           unsigned long long* fixes) {
     __shared__ uint32_t tile[kRW][2][32][kRT + 1];
     QParams qp;
     spec_params(p, qp, dB);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint64_t total = p.planes * p.nseg;
-    const uint64_t s0 = ((uint64_t)blockIdx.x * kRW + w) * 32;
-    if (s0 >= total) return;
-    const uint64_t sidx = s0 + lane;
-    const bool active = sidx < total;
-    const uint64_t plane = active ? sidx / p.nseg : 0, j = active ? sidx % p.nseg : 0;
-    const uint64_t b = active ? p.segbeg[sidx] : 0;
-    const uint64_t e = !active ? 0 : (j + 1 < p.nseg ? p.segbeg[sidx + 1] : p.P);
-    const uint64_t len = e > b ? e - b : 0;
-    const uint64_t base = plane * p.P + b;  // flat index of my segment's first element
-    double r = (!active || j == 0) ? 0.0 : (double)p.vexit[sidx - 1];
-    uint64_t maxlen = len;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
-    const uint64_t ntiles = (maxlen + kRT - 1) / kRT;
+    const uint64_t n = p.planes * p.P, I = p.interval;
+    const uint64_t nch = (n + I - 1) / I;
+    const uint64_t c0 = ((uint64_t)blockIdx.x * kRW + w) * 32;
+    if (c0 >= nch) return;
+    const uint64_t ch = c0 + lane;
+    const bool active = ch < nch;
+    const uint64_t f0 = ch * I;                            // my chunk's first flat index
+    const uint64_t len = active ? min(I, n - f0) : 0;
+    uint64_t pin = active ? f0 % p.P : 0;                  // position in the plane
+    double r = (active && pin != 0) ? (double)side_state[ch] : 0.0;
+    const uint64_t ntiles = (I + kRT - 1) / kRT;
     auto issue = [&](uint64_t t) {
         for (int q = 0; q < 32; ++q) {
+            const uint64_t fq = (c0 + q) * I + t * kRT + lane;
             const uint64_t lq = __shfl_sync(0xffffffffu, len, q);
-            const uint64_t bq = __shfl_sync(0xffffffffu, base, q);
-            const uint64_t k = t * kRT + lane;
-            if (k < lq) cp_async4(&tile[w][t & 1][q][lane], x + bq + k);
+            if (t * kRT + lane < lq) cp_async4(&tile[w][t & 1][q][lane], x + fq);
         }
         cp_async_commit();
     };
-    unsigned long long nfix = 0;
-    if (ntiles) issue(0);
+    issue(0);
     for (uint64_t t = 0; t < ntiles; ++t) {
         if (t + 1 < ntiles) {
             issue(t + 1);
@@ -1075,57 +1062,50 @@ __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restric
         const uint64_t k0 = t * kRT;
         const int cnt = k0 < len ? (int)min((uint64_t)kRT, len - k0) : 0;
         uint32_t* tr = tile[w][t & 1][lane];
-        // the sidecar point of this tile, if any (interval >= 32: at most one)
-        const uint64_t f0 = base + k0;
-        const int ks = (int)((p.interval - (f0 & (p.interval - 1))) & (p.interval - 1));
 #pragma unroll 4
         for (int k = 0; k < cnt; ++k) {
             const float xf = __uint_as_float(tr[k]);
-            // the plane's first element (r == 0 then: segment 0 starts from 0) needs no reset
-            if (k == ks) side_state[(f0 + k) >> p.ishift] = (float)r;
+            if (pin == 0) r = 0.0;  // plane start: the predictor resets
             double v;
             tr[k] = qstep((double)xf, xf, r, qp, &v);
             r = v;
+            pin = pin + 1 == p.P ? 0 : pin + 1;
         }
         __syncwarp();
-        for (int q = 0; q < 32; ++q) {  // symbols out, coalesced per segment
+        for (int q = 0; q < 32; ++q) {  // symbols out, coalesced per chunk
             const uint64_t lq = __shfl_sync(0xffffffffu, len, q);
-            const uint64_t bq = __shfl_sync(0xffffffffu, base, q);
-            const uint64_t k = k0 + lane;
-            if (k < lq) sym_out[bq + k] = (SymT)tile[w][t & 1][q][lane];
+            if (k0 + lane < lq) sym_out[(c0 + q) * I + k0 + lane] = (SymT)tile[w][t & 1][q][lane];
         }
         __syncwarp();
     }
-    if (active) {
-        const float ex = (float)r;
-        rexit[sidx] = ex;
-        if (j + 1 < p.nseg && __float_as_uint(ex) != __float_as_uint(p.vexit[sidx])) {
-            atomicMin(pfirst + plane, (unsigned)j);
-            ++nfix;
-        }
+    // the next chunk's recorded entry must be my exact end state (unless it starts a plane)
+    if (active && ch + 1 < nch && pin != 0 &&
+        __float_as_uint((float)r) != __float_as_uint(side_state[ch + 1])) {
+        rfix[ch + 1] = (float)r;
+        const uint64_t plane = (f0 + len) / p.P;
+        atomicMin(pfirst + plane, (unsigned long long)(ch + 1));
+        atomicAdd(fixes, 1ull);
     }
-    if (nfix) atomicAdd(fixes, nfix);
 }
 
-// Serial replay of a plane from the first segment whose exit disagreed (see k_spec_verify).
+// Serial replay of a plane from its first chunk whose recorded entry disagreed with the
+// replay (see k_spec_verify): symbols and sidecar states to the plane's end.
 template <typename SymT>
 __global__ void __launch_bounds__(128) k_spec_fixup(const float* __restrict__ x, SP p, const int* dB,
                                                     SymT* __restrict__ sym_out,
                                                     float* __restrict__ side_state,
-                                                    const float* __restrict__ rexit,
-                                                    const unsigned int* __restrict__ pfirst) {
+                                                    const float* __restrict__ rfix,
+                                                    const unsigned long long* __restrict__ pfirst) {
     const uint64_t plane = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (plane >= p.planes) return;
-    const unsigned jf = pfirst[plane];
-    if (jf == 0xFFFFFFFFu) return;
+    const unsigned long long cf = pfirst[plane];
+    if (cf == ~0ull) return;
     QParams qp;
     spec_params(p, qp, dB);
-    const uint64_t sidx = plane * p.nseg + jf;  // its replayed exit is exact
-    double r = (double)rexit[sidx];
-    const uint64_t base = plane * p.P;
-    for (uint64_t i = p.segbeg[sidx + 1]; i < p.P; ++i) {
-        const uint64_t flat = base + i;
-        if ((flat & (p.interval - 1)) == 0) side_state[flat >> p.ishift] = (float)r;
+    const uint64_t I = p.interval, end = (plane + 1) * p.P;
+    double r = (double)rfix[cf];
+    for (uint64_t flat = cf * I; flat < end; ++flat) {
+        if ((flat & (I - 1)) == 0) side_state[flat >> p.ishift] = (float)r;
         const float xf = __ldg(x + flat);
         double v;
         sym_out[flat] = (SymT)qstep((double)xf, xf, r, qp, &v);
@@ -1149,24 +1129,24 @@ size_t spec_verify_offset(uint64_t total) {
 }
 
 namespace {
-cudaError_t launch_spec_verify(const QuantArgs& a, const SP& p, const int* dB, float* rexit,
-                               unsigned* pfirst, cudaStream_t s, uint64_t* launches) {
+cudaError_t launch_spec_verify(const QuantArgs& a, const SP& p, const int* dB, float* rfix,
+                               unsigned long long* pfirst, cudaStream_t s, uint64_t* launches) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const unsigned long long total = (unsigned long long)a.g.planes * p.nseg;
     unsigned long long* fixes = nullptr;
     e = cudaGetSymbolAddress(reinterpret_cast<void**>(&fixes), g_spec_fixes);
     if (e != cudaSuccess) return e;
-    const unsigned vb = (unsigned)((total + kRW * 32 - 1) / (kRW * 32));
+    const uint64_t nch = (a.g.n + a.interval - 1) / a.interval;
+    const unsigned vb = (unsigned)((nch + kRW * 32 - 1) / (kRW * 32));
     const unsigned fb = (unsigned)((a.g.planes + 127) / 128);
     if (a.sym16) {
-        k_spec_verify<uint16_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rexit,
-                                                   pfirst, fixes);
-        k_spec_fixup<uint16_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rexit, pfirst);
-    } else {
-        k_spec_verify<uint32_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rexit,
+        k_spec_verify<uint16_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix,
                                                         pfirst, fixes);
-        k_spec_fixup<uint32_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rexit, pfirst);
+        k_spec_fixup<uint16_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix, pfirst);
+    } else {
+        k_spec_verify<uint32_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix,
+                                                        pfirst, fixes);
+        k_spec_fixup<uint32_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix, pfirst);
     }
     *launches += 2;
     return cudaGetLastError();
@@ -1200,11 +1180,10 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     cudaError_t e = cudaMemsetAsync(sc, 0, 256 + ((4 * total + 255) & ~255ull), s);
     if (e != cudaSuccess) return e;
     char* vb = sc + spec_verify_offset(total);
-    p.segbeg = reinterpret_cast<unsigned long long*>(vb);
-    p.vexit = reinterpret_cast<float*>(vb + 8 * total);
-    float* rexit = reinterpret_cast<float*>(vb + 12 * total);
-    unsigned* pfirst = reinterpret_cast<unsigned*>(vb + 16 * total);
-    e = cudaMemsetAsync(pfirst, 0xFF, 4 * a.g.planes, s);
+    const uint64_t nch = (a.g.n + a.interval - 1) / a.interval;
+    float* rfix = reinterpret_cast<float*>(vb);
+    unsigned long long* pfirst = reinterpret_cast<unsigned long long*>(vb + ((4 * nch + 255) & ~255ull));
+    e = cudaMemsetAsync(pfirst, 0xFF, 8 * a.g.planes, s);
     if (e != cudaSuccess) return e;
     static const unsigned qdiv = [] {
         const char* e = std::getenv("ACZ_ANCHOR_Q");
@@ -1224,7 +1203,7 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
             k_quant_spec<uint32_t><<<(unsigned)total, kW, 0, s>>>(
                 a.x, p, dB, a.sym, a.side_state, status, exits, ticket, a.flags, total);
         ++*launches;
-        return launch_spec_verify(a, p, dB, rexit, pfirst, s, launches);
+        return launch_spec_verify(a, p, dB, rfix, pfirst, s, launches);
     }
     // decoupled: phase A of every segment (throughput), then one warp per plane walks its
     // segments in order (the only sequential part), from the persisted segment states
@@ -1241,7 +1220,7 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
             a.x, p, dB, a.sym, a.side_state, a.flags, store);
     }
     *launches += 2;
-    return launch_spec_verify(a, p, dB, rexit, pfirst, s, launches);
+    return launch_spec_verify(a, p, dB, rfix, pfirst, s, launches);
 }
 
 cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
@@ -1261,7 +1240,8 @@ cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
 
 size_t quant_spec_scratch_bytes(uint64_t planes, uint64_t plane_size) {
     const uint64_t total = planes * ((plane_size + kSeg - 1) / kSeg);
-    return spec_verify_offset(total) + 16 * total + 4 * planes + 512;
+    const uint64_t nch = (planes * plane_size + 31) / 32;  // sidecar chunks (interval >= 32)
+    return spec_verify_offset(total) + ((4 * nch + 255) & ~255ull) + 8 * planes + 512;
 }
 
 // Speculative (K2b) vs thread-per-plane (K2a) quantiser, by a cost model calibrated on B200
