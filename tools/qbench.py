@@ -51,3 +51,4 @@ for nm in which:
     print("   codebook cycles: compact %.0f sort %.0f tree %.0f depths %.0f canon %.0f tables %.0f (books %d)" % tuple(
         [v[8 + i] / nb for i in range(6)] + [v[15]]))
     print("   spec cycles/elem (per segment-warp): phaseA %.1f wait %.1f walk %.1f out %.1f" % tuple(v[16 + i] / n for i in range(4)))
+    print("   exact replay: chunks whose walk state was wrong %d" % v[31])
