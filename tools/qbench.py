@@ -1,6 +1,7 @@
 """Times compress/decompress per kernel class for given shapes and prints the speculative
 quantiser's walk counters (development tool)."""
 import ctypes as C
+import os
 import sys
 import time
 
@@ -19,7 +20,7 @@ which = sys.argv[1:] or list(shapes)
 for nm in which:
     b, c, h, w, relu = shapes[nm]
     x = W.make_tensor((b, c, h, w), relu, 7)
-    p = acz.CodecParams(1e-3)
+    p = acz.CodecParams(float(os.environ.get("QB_EB", "1e-3")))
     for _ in range(2):
         blob = acz.compress(x, p)
         acz.decompress(blob, True)
