@@ -16,3 +16,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -f -o gpurun_
     -k regex:"k_decode_prev|k_encode|k_histogram|k_codebook_fast|k_quant_prev_serial" --launch-skip 6 --launch-count 7 \
     python tools/prof_codec.py conv1 > /dev/null 2>&1
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.json gpurun_out/bench_ref.json
+# BASELINE config 3: VGG-16 B256 error-bound sweep
+for eb in 1e-4 3e-4 1e-3 3e-3 1e-2; do
+  timeout 300 python bench.py --workload vgg16 --batch 256 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --eb $eb 2>/dev/null | tail -1
+done > gpurun_out/bench_vgg16_eb_sweep.jsonl
