@@ -43,7 +43,10 @@ constexpr int kExt = 2 * kL;
 constexpr int kCap = kSeg + kExt;
 constexpr int kCapW = (kCap + 31) / 32;
 constexpr int kWin = kSeg + kExt + 1;  // staged x window: [j*kSeg - 1, (j+1)*kSeg + kExt)
-constexpr int kLev = 3;                // fine offset levels (binades below the anchor grid)
+#ifndef ACZ_SPEC_LEV
+#define ACZ_SPEC_LEV 1  // measured: 1 level beats 2-4 since phase A and the walk were tightened
+#endif
+constexpr int kLev = ACZ_SPEC_LEV;     // fine offset levels (binades below the anchor grid)
 // ACZ_SPEC_XS_GLOBAL=1: read the input through L1/L2 instead of staging the segment's window
 // in shared memory (8.7 KB less per segment: more resident segments per SM).
 #ifndef ACZ_SPEC_XS_GLOBAL
