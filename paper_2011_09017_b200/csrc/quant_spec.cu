@@ -74,6 +74,9 @@ constexpr bool kStats = ACZ_SPEC_STATS != 0;
 #ifndef ACZ_SPEC_ADD
 #define ACZ_SPEC_ADD ACZ_SPEC_STATS
 #endif
+#ifndef ACZ_SPEC_TMAX_ULPS
+#define ACZ_SPEC_TMAX_ULPS 32  // largest offset the translation certifies, in anchor-grid ulps
+#endif
 #ifndef ACZ_SPEC_SYNC_PHASE
 #define ACZ_SPEC_SYNC_PHASE 0
 #endif
@@ -469,7 +472,7 @@ __device__ __forceinline__ void spec_params(SP& p, QParams& qp, const int* dB) {
     const int B = *dB;
     p.B = B;
     p.anchor_min = ldexpf(1.0f, B) * (1.0f + 1.0f / 64.0f);
-    p.Tmax = fmin(ldexp(1.0, B - 23) * 32.0, p.eb / 8.0);
+    p.Tmax = fmin(ldexp(1.0, B - 23) * (double)ACZ_SPEC_TMAX_ULPS, p.eb / 8.0);
     qp.eb = p.eb;
     qp.step = p.step;
     qp.inv_step = p.inv_step;
