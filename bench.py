@@ -361,7 +361,7 @@ def main():
         traffic = None  # measured DRAM bytes of that launch, from the committed ncu capture
         if args.workload == "alexnet" and dnm == "conv1_in" and dom == "quant" and args.eb == EB:
             try:
-                with open(os.path.join(ROOT, "profiles", "r01", "v9", "traffic.json")) as f:
+                with open(os.path.join(ROOT, "profiles", "r01", "v10", "traffic.json")) as f:
                     traffic = json.load(f)["dram_bytes_per_launch"]
             except Exception:  # noqa: BLE001
                 traffic = None
@@ -381,7 +381,7 @@ def main():
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_kind": kind,
                          "algorithmic_bytes_per_launch": dalg, "launch_ms": dms,
-                         "traffic_source": "profiles/r01/v9/traffic.json (ncu --set full)",
+                         "traffic_source": "profiles/r01/v10/traffic.json (ncu --set full)",
                          "roundtrip_frac": res["value"] / world / peak},
             "kernels": kern,
             "kernels_basis": "per class, summed over the tensors each compressed + decompressed "
