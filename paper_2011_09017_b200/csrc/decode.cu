@@ -106,6 +106,7 @@ __device__ __forceinline__ void load_tables(const uint32_t* lut, const CanonTabl
 struct Limits {
     unsigned long long nc[65];
     unsigned long long lim[65];
+    uint32_t off[65];  // first_index[l] - nc[l] (mod 2^32): book index = code + off[l]
     int maxlen;
 };
 
@@ -118,6 +119,7 @@ __device__ __forceinline__ void build_limits(const CanonTables& ct, Limits* L) {
             nc = (l == 1) ? 0 : ((L->nc[l - 1] + ct.count[l - 1]) << 1);
             L->nc[l] = nc;
             L->lim[l] = nc + ct.count[l];
+            L->off[l] = ct.first_index[l] - (uint32_t)nc;
             if (ct.count[l]) L->maxlen = l;
         }
     }
@@ -188,10 +190,12 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
             const uint32_t w2 = word(i + 2);
             const unsigned long long win =
                 ((unsigned long long)top << 32) | __funnelshift_l(w2, w1, o);
-            len = kLutBits + 1;
-            while (len < 64 && (win >> (64 - len)) >= lim.lim[len]) ++len;
+            // the LUT entry bounds the length for this prefix (huffman.cu write_tables)
+            len = (e >> 5) & 127;
+            const uint32_t lmax = e >> 12;
+            while (len < lmax && (win >> (64 - len)) >= lim.lim[len]) ++len;
             const unsigned long long c = win >> (64 - len);
-            const uint32_t idx = ct.first_index[len] + (uint32_t)(c - lim.nc[len]);
+            const uint32_t idx = (uint32_t)c + lim.off[len];
             sym = lbook ? lbook[idx - lfirst] : __ldg(a.book_sym + idx);
         }
         p += len;

@@ -198,9 +198,43 @@ __device__ void write_tables(const uint32_t* s_count, const unsigned long long* 
             s_lj[l] = (uint32_t)min(end << (kLutBits - l), (unsigned long long)kLutSize);
         }
     }
+    // Long-code prefixes: a LUT index v past the short codes is the kLutBits-bit prefix of a
+    // code longer than kLutBits; its length lies in [lmin(v), lmax(v)], lmin = the smallest l
+    // with v < ceil(end(l) / 2^(l - kLutBits)), lmax = the smallest l with
+    // v < floor(end(l) / 2^(l - kLutBits)) (every window with that prefix ends by then).
+    // The entry keeps len = 0 (long) and carries lmin | lmax << 7 above the length field so
+    // the sidecar decoder starts its limit search at lmin and stops at lmax.
+    __shared__ uint32_t s_bc[65], s_bf[65];
+    if (tid > kLutBits && tid <= 64) {  // one thread per length: end(l) = end(j) << (l - j),
+        const int l = tid;               // j = the longest used length <= l
+        int j = l;
+        while (j > 0 && s_count[j] == 0) --j;
+        const unsigned long long endj = j ? s_first_code[j] + s_count[j] : 0ull;
+        const int sh = l - kLutBits;
+        const unsigned long long hi = (endj << (l - j)) >> sh;  // l < 64: no overflow
+        const bool big = l == 64 || hi >= (unsigned long long)kLutSize;
+        const bool frac = ((endj << (l - j)) & ((1ull << sh) - 1)) != 0;
+        s_bf[l] = big ? (uint32_t)kLutSize : (uint32_t)hi;
+        s_bc[l] = big ? (uint32_t)kLutSize : (uint32_t)hi + (frac ? 1u : 0u);
+    }
     __syncthreads();
     for (uint32_t v = tid; v < kLutSize; v += blockDim.x) {
         uint32_t e = 0;
+        if (v >= s_lj[kLutBits]) {
+            // both bounds are nondecreasing in l (end(l+1) >= 2 end(l)): binary searches
+            uint32_t lo = kLutBits + 1, hi = 64;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (v < s_bc[mid]) hi = mid; else lo = mid + 1;
+            }
+            const uint32_t lmin = lo;
+            hi = 64;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (v < s_bf[mid]) hi = mid; else lo = mid + 1;
+            }
+            e = (lmin << 5) | (lo << 12);
+        }
         if (v < s_lj[kLutBits]) {
             int lo = 1, hi = kLutBits;  // smallest l with v < lj[l]
             while (lo < hi) {
