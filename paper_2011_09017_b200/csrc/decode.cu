@@ -132,15 +132,18 @@ __device__ __forceinline__ void build_limits(const CanonTables& ct, Limits* L) {
 // asynchronous 16-byte copies; every lane then decodes its chunk from its sidecar bit offset
 // with two shared loads + a funnel shift per symbol and reconstructs it with the exact
 // reference expression from the sidecar chain state (ref src/codec.cpp:143-164). Outputs go
-// through a transposed 32x32 shared tile, so every global store is one coalesced 128-byte
-// line of one chunk. The outlier cursor of a chunk is found by binary search over the
+// through a transposed 32 x kTW shared tile, so every global store writes one 64-byte run of
+// each of two chunks (the narrow tile and u16 long-code entries fit 16 warps per SM). The outlier cursor of a chunk is found by binary search over the
 // (sorted) outlier indices at its first escape. A span larger than the staging window
 // (very long codes) decodes from global memory through the same code.
-constexpr int kDW = 12;           // warps per CTA (one CTA per SM)
+constexpr int kDW = 16;           // warps per CTA (one CTA per SM)
+constexpr int kTW = 16;           // output tile: kTW elements of each of the 32 chunks
 constexpr int kDStage = 1792;     // staged stream words per warp (7 KiB, a multiple of 4:
                                   // 32 x 128 symbols at up to 14 bits/symbol)
 constexpr int kLongCap = 6144;    // book entries of codes longer than kLutBits kept in smem
-constexpr size_t kDecSmem = 4ull * kLutSize + 4ull * kLongCap + 4ull * kDW * (kDStage + 32 * 33);
+                                  // (as u16: symbols of a radius <= 32768 alphabet)
+constexpr size_t kDecSmem =
+    4ull * kLutSize + 2ull * kLongCap + 4ull * kDW * (kDStage + 32 * (kTW + 1));
 __device__ unsigned long long g_dclk[4];  // debug: prologue, staging, loop cycles; tasks
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
@@ -155,11 +158,11 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a,
 
 template <bool kStaged, typename PosT>
 __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t* bits, PosT p,
-                                             const uint32_t* s_lut, const uint32_t* lbook,
+                                             const uint32_t* s_lut, const uint16_t* lbook,
                                              uint32_t lfirst, const Limits& lim,
                                              const CanonTables& ct, uint32_t cnt,
                                              uint64_t start, double r, uint32_t to_reset,
-                                             float* tile, float (*s_out)[33], uint64_t chunk0,
+                                             float* tile, float (*s_out)[kTW + 1], uint64_t chunk0,
                                              int lane) {
     const uint32_t I = (uint32_t)a.interval;
     const uint32_t P32 = (uint32_t)min(a.g.plane_size, (uint64_t)0xFFFFFFFFu);
@@ -213,9 +216,9 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
         r = (double)v;
         return fabsf(v) <= zthr ? 0.0f : v;
     };
-    for (uint32_t t0 = 0; t0 < I; t0 += 32) {
+    for (uint32_t t0 = 0; t0 < I; t0 += kTW) {
         if (t0 < cnt) {
-            const uint32_t m = min(32u, cnt - t0);
+            const uint32_t m = min((uint32_t)kTW, cnt - t0);
             // (a per-lane fast path without the plane-start test diverges across the warp's
             // lanes on small planes and measured slower)
 #pragma unroll 4
@@ -225,16 +228,17 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
             }
         }
         __syncwarp();
-        // coalesced stores: line c of the tile = elements [t0, t0+32) of chunk chunk0 + c
+        // coalesced stores: half-warp h writes elements [t0, t0+kTW) of chunk chunk0 + 2c + h
         {
-            float* dst = a.out + chunk0 * I + t0 + lane;
-            const float* src = &s_out[0][lane];
+            const uint32_t h = (uint32_t)lane / kTW, e0 = (uint32_t)lane % kTW;
+            float* dst = a.out + (chunk0 + h) * I + t0 + e0;
+            const float* src = &s_out[h][e0];
             if ((chunk0 + 32) * I <= a.g.n) {  // all 32 chunks complete (every task but the last)
 #pragma unroll 8
-                for (int c = 0; c < 32; ++c, dst += I, src += 33) *dst = *src;
+                for (int c = 0; c < 32; c += 2, dst += 2 * I, src += 2 * (kTW + 1)) *dst = *src;
             } else {
-                for (int c = 0; c < 32; ++c, dst += I, src += 33) {
-                    const uint64_t e = (chunk0 + c) * I + t0 + lane;
+                for (int c = 0; c < 32; c += 2, dst += 2 * I, src += 2 * (kTW + 1)) {
+                    const uint64_t e = (chunk0 + c + h) * I + t0 + e0;
                     if (e < a.g.n) *dst = *src;
                 }
             }
@@ -247,21 +251,21 @@ __global__ void __launch_bounds__(kDW * 32, 1) k_decode_prev(DecodeArgs a) {
     extern __shared__ uint32_t dsm[];
     const long long tk0 = clock64();
     uint32_t* s_lut = dsm;                // 64 KiB
-    uint32_t* s_lbook = dsm + kLutSize;   // book entries of long codes (canonical order)
+    uint16_t* s_lbook = reinterpret_cast<uint16_t*>(dsm + kLutSize);  // long-code book entries
     __shared__ CanonTables s_ct;
     __shared__ Limits s_lim;
     const uint32_t lfirst = __ldg(&a.canon->first_index[kLutBits + 1]);
-    const bool lstaged = a.book_size - lfirst <= (uint32_t)kLongCap;
+    const bool lstaged = a.book_size - lfirst <= (uint32_t)kLongCap && a.radius <= 32768u;
     if (lstaged)
         for (uint32_t i = threadIdx.x; i < a.book_size - lfirst; i += blockDim.x)
-            cp_async4(s_lbook + i, a.book_sym + lfirst + i);
+            s_lbook[i] = (uint16_t)__ldg(a.book_sym + lfirst + i);
     load_tables(a.lut, a.canon, s_lut, &s_ct);  // commits and waits for all async copies
     build_limits(s_ct, &s_lim);
     __syncthreads();
-    const uint32_t* lbook = lstaged ? s_lbook : nullptr;
+    const uint16_t* lbook = lstaged ? s_lbook : nullptr;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t* s_bits = dsm + kLutSize + kLongCap + w * (kDStage + 32 * 33);
-    float(*s_out)[33] = reinterpret_cast<float(*)[33]>(s_bits + kDStage);
+    uint32_t* s_bits = dsm + kLutSize + kLongCap / 2 + w * (kDStage + 32 * (kTW + 1));
+    float(*s_out)[kTW + 1] = reinterpret_cast<float(*)[kTW + 1]>(s_bits + kDStage);
     float* tile = s_out[lane];
     if (lane == 0) atomicAdd(&g_dclk[0], (unsigned long long)(clock64() - tk0));
     const uint64_t ntasks = (a.nchunks + 31) / 32;
