@@ -132,12 +132,13 @@ __device__ __forceinline__ void build_limits(const CanonTables& ct, Limits* L) {
 // asynchronous 16-byte copies; every lane then decodes its chunk from its sidecar bit offset
 // with two shared loads + a funnel shift per symbol and reconstructs it with the exact
 // reference expression from the sidecar chain state (ref src/codec.cpp:143-164). Outputs go
-// through a transposed 32 x kTW shared tile, so every global store writes one 64-byte run of
-// each of two chunks (the narrow tile and u16 long-code entries fit 16 warps per SM). The outlier cursor of a chunk is found by binary search over the
+// through a transposed 32 x kTW shared tile, so every global store writes one 32-byte sector
+// of each of four chunks (the narrow tile and u16 long-code entries fit 18 warps per SM). The outlier cursor of a chunk is found by binary search over the
 // (sorted) outlier indices at its first escape. A span larger than the staging window
 // (very long codes) decodes from global memory through the same code.
-constexpr int kDW = 16;           // warps per CTA (one CTA per SM)
-constexpr int kTW = 16;           // output tile: kTW elements of each of the 32 chunks
+constexpr int kDW = 18;           // warps per CTA (one CTA per SM)
+constexpr int kTW = 8;            // output tile: kTW elements of each of the 32 chunks
+constexpr int kTR = 32 / kTW;     // chunks one store instruction covers
 constexpr int kDStage = 1792;     // staged stream words per warp (7 KiB, a multiple of 4:
                                   // 32 x 128 symbols at up to 14 bits/symbol)
 constexpr int kLongCap = 6144;    // book entries of codes longer than kLutBits kept in smem
@@ -228,16 +229,16 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
             }
         }
         __syncwarp();
-        // coalesced stores: half-warp h writes elements [t0, t0+kTW) of chunk chunk0 + 2c + h
+        // coalesced stores: lane group h writes elements [t0, t0+kTW) of chunk chunk0 + c + h
         {
             const uint32_t h = (uint32_t)lane / kTW, e0 = (uint32_t)lane % kTW;
             float* dst = a.out + (chunk0 + h) * I + t0 + e0;
             const float* src = &s_out[h][e0];
             if ((chunk0 + 32) * I <= a.g.n) {  // all 32 chunks complete (every task but the last)
-#pragma unroll 8
-                for (int c = 0; c < 32; c += 2, dst += 2 * I, src += 2 * (kTW + 1)) *dst = *src;
+#pragma unroll
+                for (int c = 0; c < 32; c += kTR, dst += kTR * I, src += kTR * (kTW + 1)) *dst = *src;
             } else {
-                for (int c = 0; c < 32; c += 2, dst += 2 * I, src += 2 * (kTW + 1)) {
+                for (int c = 0; c < 32; c += kTR, dst += kTR * I, src += kTR * (kTW + 1)) {
                     const uint64_t e = (chunk0 + c + h) * I + t0 + e0;
                     if (e < a.g.n) *dst = *src;
                 }
