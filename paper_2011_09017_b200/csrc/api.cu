@@ -29,7 +29,7 @@ struct SmallBlock {
     unsigned long long nnz;
     double sumabs;
     unsigned int maxsym;
-    unsigned int pad;
+    unsigned int hist_done;  // histogram CTA arrivals (fused codebook), zero between calls
     CanonTables canon;
     uint32_t lut[kLutSize];
 };
@@ -45,6 +45,9 @@ struct Slot {
     void* ws_enc = nullptr;
     size_t ws_enc_cap = 0;
     uint32_t enc_alphabet = 0;
+    uint32_t book_alphabet = 0;     // the last build_book's alphabet / leaf bound (book_wait)
+    uint64_t book_max_leaves = 0;
+    bool book_pending = false;      // a build_book whose book_wait has not run (dirty bins)
     void* ws_cb = nullptr;
     size_t ws_cb_cap = 0;
     void* ws_status = nullptr;
@@ -311,6 +314,7 @@ uint64_t blob_binding(const acz_gpu_blob_info_t& in) {
 int ensure_small(acz_gpu_ctx* ctx, Slot* sl) {
     if (sl->d_small) return ACZ_OK;
     CK(cudaMalloc(&sl->d_small, sizeof(SmallBlock)));
+    CK(cudaMemset(sl->d_small, 0, sizeof(SmallBlock)));
     CK(cudaHostAlloc(&sl->h_small, sizeof(SmallBlock), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(&sl->h_small_dev, sl->h_small, 0));
     CK(cudaEventCreateWithFlags(&sl->ev_book, cudaEventDisableTiming));
@@ -501,7 +505,7 @@ int build_book(acz_gpu_ctx* ctx, Slot* sl, const void* d_sym, int sym16, uint64_
                uint32_t alphabet, uint32_t center, cudaStream_t s) {
     const uint64_t max_leaves = std::min<uint64_t>(alphabet, n);
     const size_t hist_bytes = 8ull * alphabet + 4ull * ((alphabet + 31) / 32);
-    if (hist_bytes > sl->ws_hist_cap) sl->hist_clean = false;
+    if (hist_bytes > sl->ws_hist_cap || sl->book_pending) sl->hist_clean = false;
     CK(grow(&sl->ws_hist, &sl->ws_hist_cap, hist_bytes));
     if (!sl->hist_clean) {
         CK(cudaMemsetAsync(sl->ws_hist, 0, sl->ws_hist_cap, s));
@@ -514,19 +518,40 @@ int build_book(acz_gpu_ctx* ctx, Slot* sl, const void* d_sym, int sym16, uint64_
     CK(grow(&sl->ws_cb, &sl->ws_cb_cap, codebook_scratch_bytes(max_leaves)));
     CK(grow(&sl->ws_book, &sl->ws_book_cap, 5ull * max_leaves + 64));
     CK(grow(&sl->ws_status, &sl->ws_status_cap, encode_scratch_bytes(n, ctx->sms)));
+    uint32_t* wb_sym = static_cast<uint32_t*>(sl->ws_book);
+    uint8_t* wb_len = reinterpret_cast<uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
+    unsigned long long* enc = static_cast<unsigned long long*>(sl->ws_enc);
+    // K3 + K4 fused (the last histogram CTA builds books of <= 8192 symbols); larger books
+    // set info.slow and the host runs the global-scratch codebook (book_wait). ACZ_BOOK_UNFUSED=1
+    // launches the separate kernels (development A/B).
+    static const bool unfused = [] {
+        const char* e = std::getenv("ACZ_BOOK_UNFUSED");
+        return e && e[0] == '1';
+    }();
+    CbArgs cb{};
+    if (!unfused) {
+        cb.done = &sl->d_small->hist_done;
+        cb.book_sym = wb_sym;
+        cb.book_len = wb_len;
+        cb.enc = enc;
+        cb.canon = &sl->d_small->canon;
+        cb.lut = sl->d_small->lut;
+        cb.info = &sl->d_small->info;
+    }
+    sl->book_alphabet = alphabet;
+    sl->book_max_leaves = max_leaves;
+    sl->book_pending = true;
     {
     KTimer kt(ctx, ACZ_K_HIST, s);
     sl->hist_clean = false;  // until the codebook kernels have consumed the bins
-    CK(launch_histogram(d_sym, sym16, n, alphabet, center, hist, touched, ctx->sms, s,
+    CK(launch_histogram(d_sym, sym16, n, alphabet, center, hist, touched, cb, ctx->sms, s,
                         &ctx->launches));
     }
-    uint32_t* wb_sym = static_cast<uint32_t*>(sl->ws_book);
-    uint8_t* wb_len = reinterpret_cast<uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
-    {
+    if (unfused) {
     KTimer kt(ctx, ACZ_K_BOOK, s);
-    CK(launch_codebook(hist, touched, alphabet, max_leaves, sl->ws_cb, wb_sym, wb_len,
-                       static_cast<unsigned long long*>(sl->ws_enc), &sl->d_small->canon,
-                       sl->d_small->lut, &sl->d_small->info, s, &ctx->launches));
+    CK(launch_codebook(hist, touched, alphabet, max_leaves, sl->ws_cb, wb_sym, wb_len, enc,
+                       &sl->d_small->canon, sl->d_small->lut, &sl->d_small->info, false, s,
+                       &ctx->launches));
     }
     sl->hist_clean = true;
     // BookInfo + flags straight into the mapped pinned mirror (no copy-engine queueing)
@@ -669,8 +694,39 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     return ACZ_OK;
 }
 
-int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz_gpu_blob** out) {
+// Waits for the codebook (ev_book). A book of more than 8192 symbols leaves info.slow set
+// by the fused kernel: the global-scratch codebook then runs here, followed by a second
+// BookInfo read-back (small error bounds only).
+int book_wait(acz_gpu_ctx* ctx, Slot* sl, cudaStream_t s) {
     CK(cudaEventSynchronize(sl->ev_book));
+    sl->book_pending = false;
+    if (!sl->h_small->info.slow) return ACZ_OK;
+    sl->book_pending = true;
+    unsigned long long* hist = static_cast<unsigned long long*>(sl->ws_hist);
+    uint32_t* touched = reinterpret_cast<uint32_t*>(hist + sl->book_alphabet);
+    uint32_t* wb_sym = static_cast<uint32_t*>(sl->ws_book);
+    uint8_t* wb_len = reinterpret_cast<uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
+    {
+    KTimer kt(ctx, ACZ_K_BOOK, s);
+    CK(launch_codebook(hist, touched, sl->book_alphabet, sl->book_max_leaves, sl->ws_cb, wb_sym,
+                       wb_len, static_cast<unsigned long long*>(sl->ws_enc), &sl->d_small->canon,
+                       sl->d_small->lut, &sl->d_small->info, true, s, &ctx->launches));
+    }
+    CopyRegions cr{};
+    cr.src[0] = sl->d_small;
+    cr.dst[0] = sl->h_small_dev;
+    cr.bytes[0] = offsetof(SmallBlock, canon);
+    cr.n = 1;
+    cr.to_host = 1;
+    CK(launch_copy_regions(cr, ctx->sms, s, &ctx->launches));
+    CK(cudaEventRecord(sl->ev_book, s));
+    CK(cudaEventSynchronize(sl->ev_book));
+    sl->book_pending = false;
+    return ACZ_OK;
+}
+
+int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz_gpu_blob** out) {
+    if (int rc = book_wait(ctx, sl, s)) return rc;
     const BookInfo bi = sl->h_small->info;
     const unsigned flags = sl->h_small->flags | bi.flags;
     // precedence follows the reference: Tensor ctor (DomainError), huffman_encode
@@ -1584,7 +1640,7 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
     const uint32_t alphabet = maxsym + 1;
     int rc = build_book(ctx, sl, d_symbols, 0, n, alphabet, 0, s);
     if (rc) return rc;
-    CK(cudaEventSynchronize(sl->ev_book));
+    if ((rc = book_wait(ctx, sl, s))) return rc;
     const BookInfo bi = sl->h_small->info;
     if (bi.flags & kFlagDepth64) return fail(ctx, ACZ_ERR_DECODE, "huffman code length exceeds 64 bits");
     if (bi.flags & kFlagLenTooLong) return fail(ctx, ACZ_ERR_FORMAT, "code length > 56 bits unsupported");

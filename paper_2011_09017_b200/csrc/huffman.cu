@@ -38,12 +38,21 @@ constexpr int kHistThreads = 1024;
 // --------------------------------------------------------------------------- K3 ----
 // The histogram buffer is self-cleaning: the codebook kernel zeroes every bin it reads and
 // the `touched` bitmap, so no per-call memset of the 2R-bin table is needed.
+__device__ __forceinline__ void codebook_fast_body(
+    unsigned long long* __restrict__ hist, uint32_t* __restrict__ touched, uint32_t alphabet,
+    uint32_t* __restrict__ book_sym, uint8_t* __restrict__ book_len,
+    unsigned long long* __restrict__ enc, CanonTables* __restrict__ canon,
+    uint32_t* __restrict__ lut, BookInfo* __restrict__ info);
+
+// With cb.done set, the last histogram CTA to finish builds the codebook (K3+K4 fused): the
+// single-CTA codebook then needs no SM of its own -- launched separately it waited for a
+// whole SM to drain of other tensors' kernels (~20 us on the AlexNet critical path).
 template <typename SymT>
 __global__ void __launch_bounds__(kHistThreads) k_histogram(const SymT* __restrict__ sym, uint64_t n,
                                                    uint32_t alphabet, uint32_t win_lo,
                                                    uint32_t win_n, uint32_t center,
                                                    unsigned long long* __restrict__ hist,
-                                                   uint32_t* __restrict__ touched) {
+                                                   uint32_t* __restrict__ touched, CbArgs cb) {
     extern __shared__ unsigned int bins[];  // kHistWindow
     for (uint32_t i = threadIdx.x; i < kHistWindow; i += blockDim.x) bins[i] = 0;
     __syncthreads();
@@ -94,6 +103,17 @@ __global__ void __launch_bounds__(kHistThreads) k_histogram(const SymT* __restri
         const unsigned m = __ballot_sync(0xffffffffu, b != 0);
         if ((threadIdx.x & 31) == 0 && m) atomicOr(&touched[(win_lo + i) >> 5], m);
     }
+    if (!cb.done) return;
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(cb.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) *cb.done = 0;  // ready for the next call on this slot
+    codebook_fast_body(hist, touched, alphabet, cb.book_sym, cb.book_len, cb.enc, cb.canon,
+                       cb.lut, cb.info);
 }
 
 // --------------------------------------------------------------------------- K4 ----
@@ -266,11 +286,11 @@ constexpr size_t kFastSmem = kFastLeaves * 8 /*keys*/ + kFastLeaves * 8 /*ifreq*
                              2 * kFastLeaves * 2 /*parent*/ + 2 * kFastLeaves /*depth*/ +
                              kFastLeaves * 4 /*leaf symbols*/;
 
-__global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
+__device__ __forceinline__ void codebook_fast_body(
     unsigned long long* __restrict__ hist, uint32_t* __restrict__ touched, uint32_t alphabet,
-    uint32_t* __restrict__ leaf_sym, uint32_t* __restrict__ book_sym,
-    uint8_t* __restrict__ book_len, unsigned long long* __restrict__ enc,
-    CanonTables* __restrict__ canon, uint32_t* __restrict__ lut, BookInfo* __restrict__ info) {
+    uint32_t* __restrict__ book_sym, uint8_t* __restrict__ book_len,
+    unsigned long long* __restrict__ enc, CanonTables* __restrict__ canon,
+    uint32_t* __restrict__ lut, BookInfo* __restrict__ info) {
     extern __shared__ unsigned long long dyn[];
     unsigned long long* key = dyn;                         // [kFastLeaves]
     unsigned long long* ifreq = dyn + kFastLeaves;         // [kFastLeaves]
@@ -732,6 +752,14 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
         info->flags = s_flags;
         info->slow = 0;
     }
+}
+
+__global__ void __launch_bounds__(kCbThreads, 1) k_codebook_fast(
+    unsigned long long* __restrict__ hist, uint32_t* __restrict__ touched, uint32_t alphabet,
+    uint32_t* __restrict__ book_sym, uint8_t* __restrict__ book_len,
+    unsigned long long* __restrict__ enc, CanonTables* __restrict__ canon,
+    uint32_t* __restrict__ lut, BookInfo* __restrict__ info) {
+    codebook_fast_body(hist, touched, alphabet, book_sym, book_len, enc, canon, lut, info);
 }
 
 // Slow K4 (books larger than kFastLeaves): global-memory scratch. Runs only when the fast
@@ -1522,7 +1550,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_write(EncodeArgs a, uint
 
 cudaError_t launch_histogram(const void* sym, int sym16, uint64_t n, uint32_t alphabet,
                              uint32_t center, unsigned long long* hist, uint32_t* touched,
-                             int sms, cudaStream_t s, uint64_t* launches) {
+                             const CbArgs& cb, int sms, cudaStream_t s, uint64_t* launches) {
     const uint32_t win_lo = center > kHistWindow / 2 ? ((center - kHistWindow / 2) & ~31u) : 0u;
     const uint32_t win_n =
         alphabet - win_lo < (uint32_t)kHistWindow ? alphabet - win_lo : (uint32_t)kHistWindow;
@@ -1533,21 +1561,23 @@ cudaError_t launch_histogram(const void* sym, int sym16, uint64_t n, uint32_t al
     const uint64_t cap = (uint64_t)sms * ACZ_HIST_BPS;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) blocks = 1;
-    const size_t smem = 4ull * kHistWindow;
+    const size_t smem = cb.done ? std::max<size_t>(4ull * kHistWindow, kFastSmem)
+                                : 4ull * kHistWindow;
     static bool attr = false;
     if (!attr) {
         for (const void* f : {(const void*)k_histogram<uint16_t>, (const void*)k_histogram<uint32_t>}) {
-            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)std::max<size_t>(4ull * kHistWindow, kFastSmem));
             if (e != cudaSuccess) return e;
         }
         attr = true;
     }
     if (sym16)
         k_histogram<uint16_t><<<(unsigned)blocks, kHistThreads, smem, s>>>(
-            static_cast<const uint16_t*>(sym), n, alphabet, win_lo, win_n, center, hist, touched);
+            static_cast<const uint16_t*>(sym), n, alphabet, win_lo, win_n, center, hist, touched, cb);
     else
         k_histogram<uint32_t><<<(unsigned)blocks, kHistThreads, smem, s>>>(
-            static_cast<const uint32_t*>(sym), n, alphabet, win_lo, win_n, center, hist, touched);
+            static_cast<const uint32_t*>(sym), n, alphabet, win_lo, win_n, center, hist, touched, cb);
     ++*launches;
     return cudaGetLastError();
 }
@@ -1569,7 +1599,8 @@ size_t codebook_scratch_bytes(uint64_t k) {
 cudaError_t launch_codebook(unsigned long long* hist, uint32_t* touched, uint32_t alphabet,
                             uint64_t max_leaves, void* scratch, uint32_t* book_sym,
                             uint8_t* book_len, unsigned long long* enc, CanonTables* canon,
-                            uint32_t* lut, BookInfo* info, cudaStream_t s, uint64_t* launches) {
+                            uint32_t* lut, BookInfo* info, bool slow_only, cudaStream_t s,
+                            uint64_t* launches) {
     const size_t smem_slow = kSmemQueue * sizeof(unsigned long long);  // 128 KiB (>= radix table)
     static bool attr = false;
     if (!attr) {
@@ -1582,11 +1613,11 @@ cudaError_t launch_codebook(unsigned long long* hist, uint32_t* touched, uint32_
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    // the leaf symbols of the fast path live at the start of the slow path's scratch
-    k_codebook_fast<<<1, kCbThreads, kFastSmem, s>>>(hist, touched, alphabet,
-                                                     static_cast<uint32_t*>(scratch), book_sym,
-                                                     book_len, enc, canon, lut, info);
-    ++*launches;
+    if (!slow_only) {
+        k_codebook_fast<<<1, kCbThreads, kFastSmem, s>>>(hist, touched, alphabet, book_sym,
+                                                         book_len, enc, canon, lut, info);
+        ++*launches;
+    }
     if (max_leaves > (uint64_t)kFastLeaves) {
         k_codebook_slow<<<1, kCbThreads, smem_slow, s>>>(hist, touched, alphabet, max_leaves,
                                                          scratch, book_sym, book_len, enc, canon,

@@ -81,9 +81,19 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
 // ---- huffman.cu ----
 // hist (u64 x alphabet) and touched (1 bit per bin) must be zero on entry; the codebook
 // kernels leave them zero again (self-cleaning).
+// Codebook outputs for the fused histogram + codebook (done == nullptr: histogram only).
+struct CbArgs {
+    unsigned int* done;  // CTA arrival counter, zero between calls
+    uint32_t* book_sym;
+    uint8_t* book_len;
+    unsigned long long* enc;
+    CanonTables* canon;
+    uint32_t* lut;
+    BookInfo* info;
+};
 cudaError_t launch_histogram(const void* sym, int sym16, uint64_t n, uint32_t alphabet,
                              uint32_t center, unsigned long long* hist, uint32_t* touched,
-                             int sms, cudaStream_t s, uint64_t* launches);
+                             const CbArgs& cb, int sms, cudaStream_t s, uint64_t* launches);
 // Workspace needed by launch_codebook for an alphabet of `alphabet` symbols and at most
 // `max_leaves` distinct symbols.
 size_t codebook_scratch_bytes(uint64_t max_leaves);
@@ -91,7 +101,8 @@ cudaError_t codebook_stats(unsigned long long* out, bool reset);
 cudaError_t launch_codebook(unsigned long long* hist, uint32_t* touched, uint32_t alphabet,
                             uint64_t max_leaves, void* scratch, uint32_t* book_sym,
                             uint8_t* book_len, unsigned long long* enc, CanonTables* canon,
-                            uint32_t* lut, BookInfo* info, cudaStream_t s, uint64_t* launches);
+                            uint32_t* lut, BookInfo* info, bool slow_only, cudaStream_t s,
+                            uint64_t* launches);
 struct EncodeArgs {
     const void* sym;                 // u16 (sym16) or u32 symbols
     int sym16;
