@@ -13,7 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -f -o gpurun_out/ncu_full_quant \
     -k regex:k_quant_spec --launch-skip 1 --launch-count 1 python tools/prof_codec.py conv1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -f -o gpurun_out/ncu_full_rest \
-    -k regex:"k_decode_prev|k_encode|k_histogram|k_codebook_fast|k_quant_prev_serial" --launch-skip 6 --launch-count 7 \
+    -k regex:"k_decode_prev|k_encode|k_histogram|k_codebook_fast|k_quant_prev_serial" --launch-skip 4 --launch-count 4 \
     python tools/prof_codec.py conv1 > /dev/null 2>&1
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.json gpurun_out/bench_ref.json
 # BASELINE config 3: VGG-16 B256 error-bound sweep
