@@ -1045,8 +1045,12 @@ __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restric
     const bool active = ch < nch;
     const uint64_t f0 = ch * I;                            // my chunk's first flat index
     const uint64_t len = active ? min(I, n - f0) : 0;
-    uint64_t pin = active ? f0 % p.P : 0;                  // position in the plane
+    const uint64_t pin = active ? f0 % p.P : 0;            // position in the plane
     double r = (active && pin != 0) ? (double)side_state[ch] : 0.0;
+    // chunk offsets of plane starts (the predictor resets): the first one, then every P
+    const uint32_t pstep = (uint32_t)min(p.P, (uint64_t)0xFFFFFFFFu);
+    uint32_t snext = pin == 0 ? 0u : (uint32_t)min(p.P - pin, (uint64_t)0xFFFFFFFFu);
+    const bool full32 = (c0 + 32) * I <= n && (I % kRT) == 0;  // 32 whole chunks of whole tiles
     const uint64_t ntiles = (I + kRT - 1) / kRT;
     auto issue = [&](uint64_t t) {
         for (int q = 0; q < 32; ++q) {
@@ -1071,21 +1075,34 @@ __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restric
 #pragma unroll 4
         for (int k = 0; k < cnt; ++k) {
             const float xf = __uint_as_float(tr[k]);
-            if (pin == 0) r = 0.0;  // plane start: the predictor resets
+            if ((uint32_t)k0 + k == snext) {  // plane start: the predictor resets
+                r = 0.0;
+                snext += pstep;
+            }
             double v;
             tr[k] = qstep((double)xf, xf, r, qp, &v);
             r = v;
-            pin = pin + 1 == p.P ? 0 : pin + 1;
         }
         __syncwarp();
-        for (int q = 0; q < 32; ++q) {  // symbols out, coalesced per chunk
-            const uint64_t lq = __shfl_sync(0xffffffffu, len, q);
-            if (k0 + lane < lq) sym_out[(c0 + q) * I + k0 + lane] = (SymT)tile[w][t & 1][q][lane];
+        if (sizeof(SymT) == 2 && full32) {
+            // symbols out: lane group g (8 lanes) writes 4 symbols x 8 lanes = 32 elements of
+            // chunk c0 + q + g as 8-byte stores
+            const int g = lane >> 3, e = (lane & 7) * 4;
+            for (int q = 0; q < 32; q += 4) {
+                const uint32_t* tq = tile[w][t & 1][q + g] + e;
+                const uint2 v = make_uint2(tq[0] | (tq[1] << 16), tq[2] | (tq[3] << 16));
+                *reinterpret_cast<uint2*>(sym_out + (c0 + q + g) * I + k0 + e) = v;
+            }
+        } else {
+            for (int q = 0; q < 32; ++q) {  // symbols out, coalesced per chunk
+                const uint64_t lq = __shfl_sync(0xffffffffu, len, q);
+                if (k0 + lane < lq) sym_out[(c0 + q) * I + k0 + lane] = (SymT)tile[w][t & 1][q][lane];
+            }
         }
         __syncwarp();
     }
     // the next chunk's recorded entry must be my exact end state (unless it starts a plane)
-    if (active && ch + 1 < nch && pin != 0 &&
+    if (active && ch + 1 < nch && (f0 + len) % p.P != 0 &&
         __float_as_uint((float)r) != __float_as_uint(side_state[ch + 1])) {
         rfix[ch + 1] = (float)r;
         const uint64_t plane = (f0 + len) / p.P;
