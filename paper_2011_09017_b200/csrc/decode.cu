@@ -162,7 +162,7 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
                                              const uint32_t* s_lut, const uint16_t* lbook,
                                              uint32_t lfirst, const Limits& lim,
                                              const CanonTables& ct, uint32_t cnt,
-                                             uint64_t start, double r, uint32_t to_reset,
+                                             uint64_t start, double r, uint32_t snext,
                                              float* tile, float (*s_out)[kTW + 1], uint64_t chunk0,
                                              int lane) {
     const uint32_t I = (uint32_t)a.interval;
@@ -224,8 +224,9 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
             // lanes on small planes and measured slower)
 #pragma unroll 4
             for (uint32_t j = 0; j < m; ++j) {
-                tile[j] = step_one(t0 + j, to_reset == 0);
-                to_reset = to_reset + 1 == P32 ? 0u : to_reset + 1;
+                const bool reset = t0 + j == snext;  // plane start: the predictor resets
+                if (reset) snext += P32;
+                tile[j] = step_one(t0 + j, reset);
             }
         }
         __syncwarp();
@@ -281,7 +282,10 @@ __global__ void __launch_bounds__(kDW * 32, 1) k_decode_prev(DecodeArgs a) {
         const uint32_t cnt = active ? (uint32_t)min(I, a.g.n - start) : 0u;
         const uint64_t pos = active ? a.side_bitoff[chunk] : 0;
         const double r = active ? (double)a.side_state[chunk] : 0.0;
-        const uint32_t pin = (uint32_t)(start % a.g.plane_size);
+        // chunk offset of the first plane start in the chunk (the next ones follow every P)
+        const uint64_t pin64 = start % a.g.plane_size;
+        const uint32_t pin =
+            pin64 == 0 ? 0u : (uint32_t)min(a.g.plane_size - pin64, (uint64_t)0xFFFFFFFFu);
         // the task's stream span [b0, b1) in bits, staged as words [w0, w0 + nw)
         const uint64_t b0 = __shfl_sync(0xffffffffu, pos, 0);
         const uint64_t b1 = chunk0 + 32 < a.nchunks ? a.side_bitoff[chunk0 + 32] : a.bit_length;
