@@ -1431,17 +1431,23 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_write(EncodeArgs a, uint
         load_chunk_syms<SymT, true>(symp, a.n, my0, vec_ok, sy);
         const unsigned long long cbit = a.chunk_off[2 * c];
         const unsigned long long cesc = a.chunk_off[2 * c + 1];
-        unsigned long long code[kEncPer];  // (code << 8) | len
+        // mode 0: the compact entry (code | len << 27, upper half zero); else (code << 8) | len
+        unsigned long long code[kEncPer];
+        auto clen = [&](int i) -> uint32_t {
+            return kMode == 0 ? (uint32_t)code[i] >> 27 : (uint32_t)(code[i] & 0xFF);
+        };
+        auto cval = [&](int i) -> unsigned long long {
+            return kMode == 0 ? (unsigned long long)((uint32_t)code[i] & 0x7FFFFFFu) : code[i] >> 8;
+        };
         uint32_t my_bits = 0, escmask = 0;
 #pragma unroll
         for (int i = 0; i < kEncPer; ++i) {
             if (kMode == 0) {
-                const uint32_t e = i < cnt ? __ldg(a.enc32 + sy[i]) : 0u;
-                code[i] = ((unsigned long long)(e & 0x7FFFFFFu) << 8) | (e >> 27);
+                code[i] = i < cnt ? __ldg(a.enc32 + sy[i]) : 0u;
             } else {
                 code[i] = i < cnt ? __ldg(a.enc + sy[i]) : 0ull;
             }
-            my_bits += (uint32_t)(code[i] & 0xFF);
+            my_bits += clen(i);
             if (i < cnt && sy[i] == 0) escmask |= 1u << i;
         }
         const uint32_t my_esc = __popc(escmask);
@@ -1471,14 +1477,16 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_write(EncodeArgs a, uint
                 }
             } else {
                 uint32_t lb = 0, le = 0;
-                for (int i = 0; i < cnt; ++i) {
+#pragma unroll
+                for (int i = 0; i < kEncPer; ++i) {  // static indices: code[] stays in registers
+                    if (i >= cnt) break;
                     const uint64_t g = my0 + i;
                     if ((ipow2 ? (g & imask) : g % a.interval) == 0) {
                         const uint64_t si = ipow2 ? (g >> ishift) : g / a.interval;
                         a.side_bitoff[si] = cbit + ex_bits + lb;
                         if (a.side_outl) a.side_outl[si] = (uint32_t)(cesc + ex_esc + le);
                     }
-                    lb += (uint32_t)(code[i] & 0xFF);
+                    lb += clen(i);
                     le += (escmask >> i) & 1u;
                 }
             }
@@ -1512,7 +1520,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_write(EncodeArgs a, uint
         };
 #pragma unroll
         for (int i = 0; i < kEncPer; ++i) {
-            const int len = (int)(code[i] & 0xFF);
+            const int len = (int)clen(i);
             if (kMode == 2 && len > 32) {
                 const unsigned long long cv = code[i] >> 8;
                 acc |= (cv >> 32) << (64 - nacc - (len - 32));
@@ -1522,7 +1530,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_write(EncodeArgs a, uint
                 nacc += 32;
                 emit();
             } else {
-                acc |= (code[i] >> 8) << (64 - nacc - len);
+                acc |= cval(i) << (64 - nacc - len);
                 nacc += len;
                 if (nacc >= 32) emit();
             }
