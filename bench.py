@@ -381,7 +381,7 @@ def main():
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_kind": kind,
                          "algorithmic_bytes_per_launch": dalg, "launch_ms": dms,
-                         "traffic_source": "profiles/r01/v11/traffic.json (ncu --set full)",
+                         "traffic_source": "profiles/r01/v12/traffic.json (ncu --set full)",
                          "roundtrip_frac": res["value"] / world / peak},
             "kernels": kern,
             "kernels_basis": "per class, summed over the tensors each compressed + decompressed "
