@@ -417,3 +417,22 @@ def test_lorenzo_wavefront_parity(acz, oracle, case):
     elif case == "rows33":
         x = np.maximum(rng.standard_normal((4, 33, 45)), 0)
     _check_all(acz, oracle, x, eb, radius, 1)
+
+
+def test_large_codebook_on_demand(acz, oracle):
+    """Books of more than 8192 symbols: the fused histogram/codebook kernel flags them and
+    the host runs the global-scratch codebook after the BookInfo read-back (api.cu
+    book_wait); small and large books alternate on the same slot (clean histogram bins)."""
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((64, 4096)).astype(np.float32)
+    c, _ = _check_all(acz, oracle, x, 1e-4)
+    assert c.codebook_size > 8192
+    y = np.maximum(rng.standard_normal((16, 56, 56)), 0).astype(np.float32)
+    c2, _ = _check_all(acz, oracle, y, 1e-2)
+    assert c2.codebook_size <= 8192
+    c3, _ = _check_all(acz, oracle, x, 1e-4)
+    assert c3.to_bytes() == c.to_bytes()
+    blobs = acz.compress_many([_gpu(x), _gpu(y), _gpu(x)], acz.CodecParams(1e-4))
+    for b, src in zip(blobs, (x, y, x)):
+        ref = oracle.compress(src, 1e-4, 32768, 0, shape=src.shape)
+        assert b.to_bytes() == ref.blob
