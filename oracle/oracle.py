@@ -205,6 +205,13 @@ class Reference:
         L.ref_roundtrip_sharded.argtypes = [_f32p, _u64p, C.c_int, C.c_double, C.c_uint32,
                                             C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64),
                                             C.POINTER(C.c_double), C.c_char_p, C.c_int]
+        if hasattr(L, "ref_controller_run_ex"):
+            L.ref_controller_run_ex.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double,
+                                                C.c_double, _f32p, _u64p, C.c_int, _f32p,
+                                                C.c_uint64, _f32p, C.c_uint64, C.c_uint64,
+                                                C.c_int, C.c_int, C.c_int, _f32p,
+                                                C.POINTER(C.c_double), C.POINTER(C.c_char_p),
+                                                C.c_char_p, C.c_int]
         if hasattr(L, "ref_controller_run"):
             L.ref_controller_run.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double,
                                              C.c_double, _f32p, _u64p, C.c_int, _f32p,
@@ -214,28 +221,34 @@ class Reference:
         self.L = L
 
     def controller_run(self, act, loss, mom, batch, W=1000, sigma_fraction=0.01,
-                       coefficient_a=0.32, eb_min=1e-8, eb_max=1e-1, wraps=0):
+                       coefficient_a=0.32, eb_min=1e-8, eb_max=1e-1, wraps=0,
+                       relu_recompute=False, is_post_relu=True):
         """The unmodified reference Controller (src/controller.cpp) on one layer: collect at
         iteration 0, `wraps` wrap/unwrap passes at iteration 1, finalize. Returns a dict
-        with l_bar, r, m_avg, degenerate, eb, active, held_bytes and the ledger CSV."""
+        with l_bar, r, m_avg, degenerate, eb, active, held_bytes, the ledger CSV and the
+        last unwrapped tensor ("back"; zero_restoration = relu-recompute when
+        relu_recompute)."""
         act = np.ascontiguousarray(act, dtype=np.float32)
         loss = np.ascontiguousarray(loss, dtype=np.float32).ravel()
         mom = np.ascontiguousarray(mom, dtype=np.float32).ravel()
         shp = np.asarray(act.shape, dtype=np.uint64)
+        back = np.zeros(act.shape, dtype=np.float32)
         out = (C.c_double * 8)()
         csv = C.c_char_p()
         err = C.create_string_buffer(512)
-        rc = self.L.ref_controller_run(int(W), sigma_fraction, coefficient_a, eb_min, eb_max,
-                                       act.ctypes.data_as(_f32p), shp.ctypes.data_as(_u64p),
-                                       act.ndim, loss.ctypes.data_as(_f32p), loss.size,
-                                       mom.ctypes.data_as(_f32p), mom.size, int(batch), int(wraps),
-                                       out, C.byref(csv), err, 512)
+        rc = self.L.ref_controller_run_ex(int(W), sigma_fraction, coefficient_a, eb_min, eb_max,
+                                          act.ctypes.data_as(_f32p), shp.ctypes.data_as(_u64p),
+                                          act.ndim, loss.ctypes.data_as(_f32p), loss.size,
+                                          mom.ctypes.data_as(_f32p), mom.size, int(batch),
+                                          int(wraps), int(bool(relu_recompute)),
+                                          int(bool(is_post_relu)), back.ctypes.data_as(_f32p),
+                                          out, C.byref(csv), err, 512)
         if rc:
             raise OracleError(rc, err.value.decode())
         text = csv.value.decode()
         self.L.ref_free(csv)
         return dict(l_bar=out[0], r=out[1], m_avg=out[2], degenerate=bool(out[3]), eb=out[4],
-                    active=bool(out[5]), held_bytes=int(out[6]), csv=text)
+                    active=bool(out[5]), held_bytes=int(out[6]), csv=text, back=back)
 
     def compress(self, x: np.ndarray, eb: float, radius: int = 32768, predictor: int = 0,
                  shape=None) -> bytes:

@@ -198,11 +198,13 @@ int ref_roundtrip_sharded(const float* x, const std::uint64_t* shape, int rank, 
 // collection at iteration 0 with host activation/loss/momentum, then `wraps` forward
 // passes at iteration 1 (compress-or-pass-through + unwrap); returns the layer stats, the
 // window's bound and sigma, and the ledger CSV after finalize() (malloc'd).
-int ref_controller_run(std::int64_t W, double sigma_fraction, double coefficient_a,
-                       double eb_min, double eb_max, const float* act, const std::uint64_t* shape,
-                       int rank, const float* loss, std::uint64_t nloss, const float* mom,
-                       std::uint64_t nmom, std::uint64_t batch, int wraps, double* stats_out,
-                       char** csv, char* err, int errcap) {
+int ref_controller_run_ex(std::int64_t W, double sigma_fraction, double coefficient_a,
+                          double eb_min, double eb_max, const float* act,
+                          const std::uint64_t* shape, int rank, const float* loss,
+                          std::uint64_t nloss, const float* mom, std::uint64_t nmom,
+                          std::uint64_t batch, int wraps, int relu_recompute, int is_post_relu,
+                          float* back_out, double* stats_out, char** csv, char* err,
+                          int errcap) {
     return guarded(err, errcap, [&] {
         acz::ControllerConfig cfg;
         cfg.collect_interval = W;
@@ -210,6 +212,7 @@ int ref_controller_run(std::int64_t W, double sigma_fraction, double coefficient
         cfg.coefficient_a = coefficient_a;
         cfg.eb_min = eb_min;
         cfg.eb_max = eb_max;
+        if (relu_recompute) cfg.zero_restoration = acz::ZeroRestoration::ReluRecompute;
         acz::Controller c(cfg, 1);
         const std::size_t n = volume(shape, rank);
         acz::Tensor ta(to_shape(shape, rank), std::vector<float>(act, act + n));
@@ -226,16 +229,26 @@ int ref_controller_run(std::int64_t W, double sigma_fraction, double coefficient
         stats_out[5] = c.layer_active(0) ? 1.0 : 0.0;
         for (int i = 0; i < wraps; ++i) {
             acz::Tensor copy = ta;
-            acz::ActivationHandle h = c.wrap_forward(0, std::move(copy), true);
+            acz::ActivationHandle h = c.wrap_forward(0, std::move(copy), is_post_relu != 0);
             stats_out[6] = static_cast<double>(h.held_bytes);
             acz::Tensor back = c.unwrap_backward(h);
-            (void)back;
+            if (back_out) std::memcpy(back_out, back.data(), back.size() * sizeof(float));
         }
         c.finalize();
         const std::string s = c.ledger().to_csv();
         *csv = static_cast<char*>(std::malloc(s.size() + 1));
         std::memcpy(*csv, s.c_str(), s.size() + 1);
     });
+}
+
+int ref_controller_run(std::int64_t W, double sigma_fraction, double coefficient_a,
+                       double eb_min, double eb_max, const float* act, const std::uint64_t* shape,
+                       int rank, const float* loss, std::uint64_t nloss, const float* mom,
+                       std::uint64_t nmom, std::uint64_t batch, int wraps, double* stats_out,
+                       char** csv, char* err, int errcap) {
+    return ref_controller_run_ex(W, sigma_fraction, coefficient_a, eb_min, eb_max, act, shape,
+                                 rank, loss, nloss, mom, nmom, batch, wraps, 0, 1, nullptr,
+                                 stats_out, csv, err, errcap);
 }
 
 } // extern "C"

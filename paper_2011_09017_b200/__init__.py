@@ -9,6 +9,6 @@ from .codec import (CodebookEntry, CodecParams, CompressedTensor, Context, CudaE
                     ParamError, Predictor, ShapeError, blob_from_bytes, blob_to_bytes, compress,
                     compress_host, compress_host_many, compress_many, compression_ratio, debug_last_symbols,
                     decompress, decompress_host, decompress_host_many, decompress_many, default_context, huffman_decode, huffman_encode, mean_abs,
-                    nonzero_ratio, parse_acz1, zero_bitmap)
+                    nonzero_ratio, parse_acz1, relu_, zero_bitmap)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -320,8 +320,10 @@ def compress(t, p: CodecParams = CodecParams(), stream=None,
     return CompressedTensor(h, ctx)
 
 
-def decompress(c: CompressedTensor, zero_filter: bool = False, out=None, stream=None):
-    """ref include/acz/codec.hpp:59 / src/codec.cpp:122-171. Returns a CUDA fp32 tensor."""
+def decompress(c: CompressedTensor, zero_filter: bool = False, out=None, stream=None,
+               ctx: Optional[Context] = None):
+    """ref include/acz/codec.hpp:59 / src/codec.cpp:122-171. Returns a CUDA fp32 tensor.
+    (ctx: accepted for symmetry; the blob's own context runs the decode.)"""
     import torch
     if out is None:
         out = torch.empty(c.shape, dtype=torch.float32, device=f"cuda:{c._ctx.device}")
@@ -383,6 +385,19 @@ def decompress_many(blobs: Sequence[CompressedTensor], zero_filter: bool = False
                                                  _stream_handle(stream))
     _check(rc, ctx)
     return outs
+
+
+def relu_(t, stream=None, ctx: Optional[Context] = None):
+    """In-place x = x > 0 ? x : 0 on the GPU (ref nn::recompute_relu,
+    include/acz/nn/layers.hpp:134-157): the controller's relu-recompute zero restoration
+    after an unfiltered decompress (src/controller.cpp:210-213,244)."""
+    t2 = _require_cuda_f32(t)
+    if t2.data_ptr() != t.data_ptr():
+        raise ValueError("relu_ needs a contiguous tensor")
+    ctx = ctx or default_context(t.device.index)
+    _check(_native.load().acz_gpu_relu(ctx.handle, _dev_ptr(t), t.numel(),
+                                       _stream_handle(stream)), ctx)
+    return t
 
 
 def compression_ratio(c: CompressedTensor) -> float:
@@ -477,22 +492,47 @@ def compress_host_many(hosts: Sequence, p: CodecParams = CodecParams(), blob_buf
     if side_bufs is None:
         side_bufs = [torch.empty(h.numel() // 8 + (1 << 20), dtype=torch.uint8, pin_memory=True)
                      for h in hs]
-    ptrs = (C.c_void_p * k)(*[h.data_ptr() for h in hs])
-    ranks = (C.c_uint32 * k)(*[h.dim() for h in hs])
-    flat = [int(e) for h in hs for e in h.shape]
-    shapes = (C.c_uint64 * max(1, len(flat)))(*flat)
-    bp = (C.c_void_p * k)(*[b.data_ptr() for b in blob_bufs])
-    bc = (C.c_uint64 * k)(*[b.numel() for b in blob_bufs])
-    bs = (C.c_uint64 * k)()
-    sp = (C.c_void_p * k)(*[b.data_ptr() for b in side_bufs])
-    sc = (C.c_uint64 * k)(*[b.numel() for b in side_bufs])
-    ss = (C.c_uint64 * k)()
-    st = (C.c_int * k)()
-    rc = _native.load().acz_gpu_compress_host_batch(ctx.handle, k, ptrs, shapes, ranks,
-                                                    float(p.eb), int(p.quant_radius),
-                                                    int(p.predictor), bp, bc, bs, sp, sc, ss, st)
-    _check(rc, ctx)
-    return [(blob_bufs[i][:bs[i]].numpy(), side_bufs[i][:ss[i]].numpy()) for i in range(k)]
+    blob_bufs, side_bufs = list(blob_bufs), list(side_bufs)
+    sizes_b, sizes_s = [0] * k, [0] * k
+
+    def run(idx):
+        m = len(idx)
+        ptrs = (C.c_void_p * m)(*[hs[i].data_ptr() for i in idx])
+        ranks = (C.c_uint32 * m)(*[hs[i].dim() for i in idx])
+        flat = [int(e) for i in idx for e in hs[i].shape]
+        shapes = (C.c_uint64 * max(1, len(flat)))(*flat)
+        bp = (C.c_void_p * m)(*[blob_bufs[i].data_ptr() for i in idx])
+        bc = (C.c_uint64 * m)(*[blob_bufs[i].numel() for i in idx])
+        bs = (C.c_uint64 * m)()
+        sp = (C.c_void_p * m)(*[side_bufs[i].data_ptr() for i in idx])
+        sc = (C.c_uint64 * m)(*[side_bufs[i].numel() for i in idx])
+        ss = (C.c_uint64 * m)()
+        st = (C.c_int * m)()
+        rc = _native.load().acz_gpu_compress_host_batch(ctx.handle, m, ptrs, shapes, ranks,
+                                                        float(p.eb), int(p.quant_radius),
+                                                        int(p.predictor), bp, bc, bs, sp, sc, ss,
+                                                        st)
+        for j, i in enumerate(idx):
+            sizes_b[i], sizes_s[i] = int(bs[j]), int(ss[j])
+        return rc, [int(st[j]) for j in range(m)]
+
+    rc, st = run(list(range(k)))
+    if rc:
+        # a destination smaller than the blob (small error bounds: mostly outliers, up to
+        # 12 B + the code per element) reports the size it needs: grow those buffers, redo
+        # only those tensors
+        retry = [i for i in range(k) if st[i] == 8 and (sizes_b[i] > blob_bufs[i].numel() or
+                                                        sizes_s[i] > side_bufs[i].numel())]
+        if retry and all(st[i] in (0, 8) for i in range(k)):
+            for i in retry:
+                if sizes_b[i] > blob_bufs[i].numel():
+                    blob_bufs[i] = torch.empty(sizes_b[i], dtype=torch.uint8, pin_memory=True)
+                if sizes_s[i] > side_bufs[i].numel():
+                    side_bufs[i] = torch.empty(sizes_s[i], dtype=torch.uint8, pin_memory=True)
+            rc, st2 = run(retry)
+        _check(rc, ctx)
+    return [(blob_bufs[i][:sizes_b[i]].numpy(), side_bufs[i][:sizes_s[i]].numpy())
+            for i in range(k)]
 
 
 def decompress_host_many(blobs, zero_filter: bool = False, outs=None,

@@ -275,9 +275,9 @@ class Controller:
         if h.raw is not None:
             t, h.raw = h.raw, None
         elif h.blob is not None:
-            t = _codec.decompress(h.blob, zero_filter=h.zero_filter)
+            t = _codec.decompress(h.blob, zero_filter=h.zero_filter, ctx=self.ctx)
             if h.apply_relu:
-                t.clamp_(min=0.0)  # nn::recompute_relu (layers.hpp:152-157)
+                _codec.relu_(t, ctx=self.ctx)  # nn::recompute_relu (layers.hpp:152-157)
             h.blob = None
         else:
             raise _codec.ParamError("unwrap_backward: handle already consumed")
@@ -314,35 +314,121 @@ def suggest_batch(batch: int, peak_stash_bytes: int, budget_bytes: int, granular
     return max(granularity, min(b, max_batch))
 
 
-class SavedActivationHooks:
-    """torch.autograd.graph.saved_tensors_hooks that route every fp32 CUDA tensor autograd
-    saves (conv inputs, post-ReLU activations) through the controller: layer ids are the
-    save order within an iteration (call :meth:`new_iteration` each step)."""
+class _Stash:
+    """One controller handle shared by every saved-tensor slot that aliases the same storage
+    (a ReLU's saved output and the next conv's saved input are one tensor: compressing it
+    once and dropping every raw reference is what actually frees the activation)."""
 
-    def __init__(self, controller: Controller, min_numel: int = 1 << 14):
+    __slots__ = ("ctl", "handle", "cache")
+
+    def __init__(self, ctl: "Controller", handle: ActivationHandle):
+        self.ctl, self.handle, self.cache = ctl, handle, None
+
+    def get(self):
+        # decompressed once (Controller.unwrap_backward consumes the handle); the result is
+        # kept while any slot referencing it lives, so a second unpack of the same saved
+        # tensor (retain_graph, double backward, grad_fn._saved_*) sees the same values
+        if self.cache is None:
+            self.cache = self.ctl.unwrap_backward(self.handle)
+        return self.cache
+
+
+class _Saved:
+    """What pack() returns: the raw tensor, or (after the storage became a conv input) the
+    shared stash."""
+
+    __slots__ = ("raw", "stash", "__weakref__")
+
+    def __init__(self, raw=None, stash=None):
+        self.raw, self.stash = raw, stash
+
+
+class SavedActivationHooks:
+    """torch.autograd.graph.saved_tensors_hooks that compress the INPUT of every
+    convolution of `model` between its forward and backward pass, and nothing else (ref
+    SPEC.md:420 "only convolutional-layer activations are compressed";
+    Controller::wrap_forward / unwrap_backward, src/controller.cpp:194-249).
+
+    * Layer ids are the convolutions' order in ``model.modules()`` (stable across
+      iterations, so every layer's statistics window keeps its id).
+    * A forward pre-hook on each conv marks its input; the first time autograd saves that
+      storage for the conv, it is compressed through the controller. Earlier or later
+      saves of the same storage (ReLU's output, a pooling input) share the compressed stash
+      instead of keeping a raw reference.
+    * Parameters and other leaf tensors that require grad (weights) are never compressed.
+    * is_post_relu for the relu-recompute zero restoration is read from the tensor's
+      autograd node (ReluBackward / ThresholdBackward), with no device synchronisation.
+    Call :meth:`new_iteration` at the start of every step."""
+
+    def __init__(self, controller: Controller, model, min_numel: int = 0):
+        import torch.nn as nn
         self.ctl = controller
         self.min_numel = min_numel
-        self.next_layer = 0
+        self.convs = [m for m in model.modules()
+                      if isinstance(m, (nn.Conv1d, nn.Conv2d, nn.Conv3d))]
+        if len(self.convs) > len(controller.windows):
+            raise _codec.ParamError(f"controller has {len(controller.windows)} layers, model "
+                                    f"has {len(self.convs)} convolutions")
+        self._hooks = [m.register_forward_pre_hook(self._mark(i))
+                       for i, m in enumerate(self.convs)]
+        self._marked = {}   # storage key -> conv layer id (forward order)
+        self._stash = {}    # storage key -> _Stash (this iteration)
+        self._raw = {}      # storage key -> [_Saved] raw saves that may alias a conv input
+        self.compressed = 0
+
+    @staticmethod
+    def _key(t):
+        return (t.data_ptr(), tuple(t.shape))
+
+    def _mark(self, layer: int):
+        def hook(_module, args):
+            if args and hasattr(args[0], "data_ptr") and args[0].is_cuda:
+                self._marked.setdefault(self._key(args[0]), layer)
+        return hook
+
+    def remove(self) -> None:
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
 
     def new_iteration(self, iteration: int) -> None:
         self.ctl.begin_iteration(iteration)
-        self.next_layer = 0
+        self._marked.clear()
+        self._stash.clear()
+        self._raw.clear()
+
+    @staticmethod
+    def _post_relu(t) -> bool:
+        fn = t.grad_fn
+        name = type(fn).__name__ if fn is not None else ""
+        return "Relu" in name or "Threshold" in name
 
     def pack(self, t):
         import torch
-        if not (t.is_cuda and t.dtype == torch.float32 and t.numel() >= self.min_numel
-                and t.is_contiguous() and self.next_layer < len(self.ctl.windows)):
-            return ("raw", t)
-        layer = self.next_layer
-        self.next_layer += 1
-        post_relu = bool(t.min().item() >= 0) if self.ctl.cfg.zero_restoration == RELU_RECOMPUTE else False
-        return ("acz", self.ctl.wrap_forward(layer, t.detach(), post_relu))
+        if (isinstance(t, torch.nn.Parameter) or (t.is_leaf and t.requires_grad)
+                or not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous()
+                or t.numel() < max(1, self.min_numel)):
+            return _Saved(raw=t)
+        key = self._key(t)
+        st = self._stash.get(key)
+        if st is not None:
+            return _Saved(stash=st)
+        layer = self._marked.pop(key, None)
+        if layer is None:
+            s = _Saved(raw=t)
+            self._raw.setdefault(key, []).append(s)
+            return s
+        relu = self.ctl.cfg.zero_restoration == RELU_RECOMPUTE and self._post_relu(t)
+        st = _Stash(self.ctl, self.ctl.wrap_forward(layer, t.detach(), relu))
+        self._stash[key] = st
+        if st.handle.blob is not None:
+            self.compressed += 1
+        for s in self._raw.pop(key, []):  # earlier saves of the same storage share it
+            s.raw, s.stash = None, st
+        return _Saved(stash=st)
 
-    def unpack(self, packed):
-        kind, v = packed
-        if kind == "raw":
-            return v
-        return self.ctl.unwrap_backward(v)
+    def unpack(self, s):
+        return s.raw if s.stash is None else s.stash.get()
 
     def __enter__(self):
         import torch

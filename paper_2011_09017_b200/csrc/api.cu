@@ -30,6 +30,7 @@ struct SmallBlock {
     double sumabs;
     unsigned int maxsym;
     unsigned int hist_done;  // histogram CTA arrivals (fused codebook), zero between calls
+    unsigned long long binding;  // sidecar binding computed on the device (sidecar export)
     CanonTables canon;
     uint32_t lut[kLutSize];
 };
@@ -70,6 +71,11 @@ struct Slot {
     cudaEvent_t ev_book = nullptr;  // recorded after the codebook read-back
     cudaEvent_t ev_up = nullptr;    // host-input upload complete (serialises batch uploads)
     cudaEvent_t ev_dec = nullptr;   // host-batch decode complete (download may start)
+    // Stream hand-over: the slot's workspaces are read by kernels still in flight on the
+    // stream of its last call; a call on another stream waits for that work first.
+    cudaEvent_t ev_last = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool has_last = false;
     uint64_t last_n = 0;
     bool last_sym16 = false;
 };
@@ -86,6 +92,14 @@ struct acz_gpu_ctx {
     std::vector<cudaStream_t> pool;     // internal streams of the batched entry points
     std::vector<cudaEvent_t> pool_ev;   // one per pool stream (join)
     cudaEvent_t ev_fork = nullptr;
+    // Sticky internal-error word in mapped pinned memory: kernels that detect an internal
+    // consistency failure after the host has stopped waiting (the encoder's look-back) OR
+    // kFlagInternal into it; every entry point reports it (ACZ_ERR_CUDA) and clears it.
+    unsigned int* h_sticky = nullptr;
+    unsigned int* d_sticky = nullptr;
+    // K1 fixed-order reduction of sum|x| (deterministic mean_abs): per-CTA partials + ticket
+    double* d_partials = nullptr;
+    unsigned int* d_ticket = nullptr;
     void* ws_io = nullptr;  // host-API staging (input / output floats)
     size_t ws_io_cap = 0;
     void* ws_aux = nullptr;  // sequential-decode scratch (symbols, plane prefixes)
@@ -190,6 +204,21 @@ int fail(acz_gpu_ctx* c, int code, const std::string& msg) {
     return code;
 }
 
+// No exception crosses the C-ABI: host allocation failures (std::bad_alloc from the
+// per-call vectors, e.g. sized by an untrusted blob) map to ACZ_ERR_NOMEM.
+template <class F>
+int guarded(acz_gpu_ctx* c, F&& f) {
+    try {
+        return f();
+    } catch (const std::bad_alloc&) {
+        return fail(c, ACZ_ERR_NOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(c, ACZ_ERR_INVALID, std::string("unexpected exception: ") + e.what());
+    } catch (...) {
+        return fail(c, ACZ_ERR_INVALID, "unexpected exception");
+    }
+}
+
 int cuda_fail(acz_gpu_ctx* c, cudaError_t e, const char* where) {
     return fail(c, ACZ_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
@@ -284,7 +313,7 @@ cudaError_t blob_alloc(acz_gpu_blob* b, uint32_t book, uint64_t nwords, uint64_t
     return cudaSuccess;
 }
 
-// ACZS v2: "ACZS" u32 version, u64 {count, bit_length, interval, nchunks, binding, has_outl},
+// ACZS v3: "ACZS" u32 version, u64 {count, bit_length, interval, nchunks, binding, has_outl},
 // u64 bit offset x nchunks, [u32 outlier prefix x nchunks if has_outl], f32 state x nchunks.
 uint64_t sidecar_bytes(uint64_t nchunks, bool has_outl) {
     return 4 + 4 + 8 * 6 + nchunks * (8 + (has_outl ? 4 : 0) + 4);
@@ -298,8 +327,11 @@ uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h = 1469598103934665603ull) 
     return h;
 }
 
-// Binds a sidecar to its blob: header + codebook + bit length + outlier count.
-uint64_t blob_binding(const acz_gpu_blob_info_t& in) {
+constexpr uint32_t kSidecarVersion = 3;
+
+// Header part of the sidecar binding (acz_binding in common.cuh adds the codebook and a
+// sampled bitstream digest): rank, extents, eb, radius, predictor, sizes.
+uint64_t blob_binding_h0(const acz_gpu_blob_info_t& in) {
     uint64_t h = fnv1a(reinterpret_cast<const uint8_t*>(&in.rank), sizeof(in.rank));
     h = fnv1a(reinterpret_cast<const uint8_t*>(in.shape), 8ull * in.rank, h);
     h = fnv1a(reinterpret_cast<const uint8_t*>(&in.eb), 8, h);
@@ -320,7 +352,33 @@ int ensure_small(acz_gpu_ctx* ctx, Slot* sl) {
     CK(cudaEventCreateWithFlags(&sl->ev_book, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sl->ev_up, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&sl->ev_dec, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sl->ev_last, cudaEventDisableTiming));
     return ACZ_OK;
+}
+
+// Orders a call's use of slot sl on stream s after the slot's previous call when that one
+// ran on another stream (single-tensor entry points share slot 0 whatever the stream).
+int slot_enter(acz_gpu_ctx* ctx, Slot* sl, cudaStream_t s) {
+    if (sl->has_last && sl->last_stream != s) CK(cudaStreamWaitEvent(s, sl->ev_last, 0));
+    return ACZ_OK;
+}
+// Marks the end of the work a call enqueued on s for slot sl.
+int slot_leave(acz_gpu_ctx* ctx, Slot* sl, cudaStream_t s) {
+    CK(cudaEventRecord(sl->ev_last, s));
+    sl->last_stream = s;
+    sl->has_last = true;
+    return ACZ_OK;
+}
+
+// Reports (and clears) an internal failure a kernel recorded after the host stopped
+// waiting for it (see acz_gpu_ctx::h_sticky).
+int check_sticky(acz_gpu_ctx* ctx) {
+    if (!ctx->h_sticky) return ACZ_OK;
+    const unsigned v = *(volatile unsigned*)ctx->h_sticky;
+    if (!v) return ACZ_OK;
+    *(volatile unsigned*)ctx->h_sticky = 0;
+    return fail(ctx, ACZ_ERR_CUDA, "internal: encoder look-back timeout (a previous blob on "
+                                   "this context may be corrupt)");
 }
 
 // Slot i (created on first use).
@@ -334,6 +392,7 @@ void free_slot(Slot* sl) {
     for (void* p : {sl->ws_sym, sl->ws_hist, sl->ws_enc, sl->ws_cb, sl->ws_status, sl->ws_row,
                     sl->ws_book, sl->ws_side, sl->ws_qs, sl->ws_in, sl->ws_pack})
         if (p) cudaFree(p);
+    if (sl->ev_last) cudaEventDestroy(sl->ev_last);
     if (sl->d_small) cudaFree(sl->d_small);
     if (sl->h_small) cudaFreeHost(sl->h_small);
     if (sl->ev_book) cudaEventDestroy(sl->ev_book);
@@ -348,14 +407,17 @@ int run_stats(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, uint32_t* d_bitma
     Slot* sl = get_slot(ctx, 0);
     int rc = ensure_small(ctx, sl);
     if (rc) return rc;
+    if ((rc = slot_enter(ctx, sl, s))) return rc;
     CK(cudaMemsetAsync(&sl->d_small->flags, 0, sizeof(unsigned), s));
     CK(cudaMemsetAsync(&sl->d_small->nnz, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(&sl->d_small->sumabs, 0, sizeof(double), s));
     {
         KTimer kt(ctx, ACZ_K_STATS, s);
         CK(launch_stats(d_in, n, d_bitmap, &sl->d_small->nnz, &sl->d_small->flags,
-                        &sl->d_small->sumabs, ctx->sms, s, &ctx->launches));
+                        sumabs ? &sl->d_small->sumabs : nullptr, ctx->d_partials, ctx->d_ticket,
+                        ctx->sms, s, &ctx->launches));
     }
+    if ((rc = slot_leave(ctx, sl, s))) return rc;
     CK(cudaMemcpyAsync(sl->h_small, sl->d_small, offsetof(SmallBlock, canon),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -404,8 +466,20 @@ int acz_gpu_ctx_create(int device, acz_gpu_ctx** out) {
         delete ctx;
         return ACZ_ERR_CUDA;
     }
+    void* sticky_dev = nullptr;
     if (ensure_small(ctx, get_slot(ctx, 0)) != ACZ_OK ||
-        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaHostAlloc(&ctx->h_sticky, sizeof(unsigned), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&sticky_dev, ctx->h_sticky, 0) != cudaSuccess ||
+        cudaMalloc(&ctx->d_partials, sizeof(double) * stats_partials(ctx->sms) + 256) !=
+            cudaSuccess) {
+        acz_gpu_ctx_destroy(ctx);
+        return ACZ_ERR_CUDA;
+    }
+    *ctx->h_sticky = 0;
+    ctx->d_sticky = static_cast<unsigned*>(sticky_dev);
+    ctx->d_ticket = reinterpret_cast<unsigned*>(ctx->d_partials + stats_partials(ctx->sms));
+    if (cudaMemset(ctx->d_ticket, 0, sizeof(unsigned)) != cudaSuccess) {
         acz_gpu_ctx_destroy(ctx);
         return ACZ_ERR_CUDA;
     }
@@ -416,8 +490,9 @@ int acz_gpu_ctx_create(int device, acz_gpu_ctx** out) {
 int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
     if (!ctx) return ACZ_ERR_INVALID;
     cudaDeviceSynchronize();
-    for (void* p : {ctx->ws_io, ctx->ws_aux, ctx->ws_scan})
+    for (void* p : {ctx->ws_io, ctx->ws_aux, ctx->ws_scan, (void*)ctx->d_partials})
         if (p) cudaFree(p);
+    if (ctx->h_sticky) cudaFreeHost(ctx->h_sticky);
     for (Slot* sl : ctx->slots) free_slot(sl);
     for (auto st : ctx->pool) cudaStreamDestroy(st);
     for (auto e : ctx->pool_ev) cudaEventDestroy(e);
@@ -491,7 +566,7 @@ int finish_encode(acz_gpu_ctx* ctx, Slot* sl, acz_gpu_blob* b, const void* d_sym
     ea.interval = interval ? interval : 1;
     ea.max_len = bi.max_len;
     ea.status = static_cast<TileStatus*>(sl->ws_status);
-    ea.ticket = &sl->d_small->ticket;
+    ea.sticky = ctx->d_sticky;
     {
         KTimer kt(ctx, ACZ_K_ENCODE, s);
         CK(launch_encode(ea, ctx->sms, s, &ctx->launches));
@@ -570,6 +645,8 @@ int decompress_on(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, int zero_fi
                   float* d_out, cudaStream_t s) {
     if (!b || !d_out || !sl) return ACZ_ERR_INVALID;
     if (b->invalid) return fail(ctx, b->invalid, b->invalid_msg);
+    if (int rc = check_sticky(ctx)) return rc;
+    if (int rc = slot_enter(ctx, sl, s)) return rc;
     const acz_gpu_blob_info_t& in = b->info;
     const PlaneGeom g = plane_geom(in.shape, in.rank);
     if (in.predictor == ACZ_PRED_LORENZO2D)
@@ -603,7 +680,7 @@ int decompress_on(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, int zero_fi
         KTimer kt(ctx, ACZ_K_DECODE, s);
         CK(launch_decode(a, ctx->sms, s, &ctx->launches));
     }
-    return ACZ_OK;
+    return slot_leave(ctx, sl, s);
 }
 
 
@@ -642,12 +719,15 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "compress: empty tensor");
     rc = ensure_small(ctx, sl);
     if (rc) return rc;
+    if ((rc = slot_enter(ctx, sl, s))) return rc;
     const PlaneGeom g = plane_geom(shape, rank);
     const uint32_t alphabet = 2u * quant_radius;
     const uint64_t interval = sidecar_interval_for(predictor, g);
     const uint64_t nchunks = (n + interval - 1) / interval;
 
-    CK(grow(&sl->ws_sym, &sl->ws_sym_cap, 4ull * n));
+    const int sym16 = (predictor == ACZ_PRED_PREV && quant_radius <= 32768) ? 1 : 0;
+    // u16 symbols take 2 bytes per element (+16: the encoder's vector loads of the tail)
+    CK(grow(&sl->ws_sym, &sl->ws_sym_cap, (sym16 ? 2ull : 4ull) * n + 16));
     CK(grow(&sl->ws_side, &sl->ws_side_cap, 4ull * nchunks));
     if (predictor == ACZ_PRED_LORENZO2D)
         CK(grow(&sl->ws_row, &sl->ws_row_cap, 4ull * g.planes * g.cols));
@@ -662,7 +742,6 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     qa.step = 2.0 * eb;
     qa.radius = quant_radius;
     qa.predictor = predictor;
-    const int sym16 = (predictor == ACZ_PRED_PREV && quant_radius <= 32768) ? 1 : 0;
     sl->last_sym16 = sym16 != 0;
     qa.sym = sym16 ? nullptr : static_cast<uint32_t*>(sl->ws_sym);
     qa.sym16 = sym16 ? static_cast<uint16_t*>(sl->ws_sym) : nullptr;
@@ -680,6 +759,7 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
         }
     }
     rc = build_book(ctx, sl, sl->ws_sym, sym16, n, alphabet, quant_radius, s);
+    if (const int lr = slot_leave(ctx, sl, s)) return lr;
     if (rc) return rc;
     pl->n = n;
     pl->g = g;
@@ -727,6 +807,7 @@ int book_wait(acz_gpu_ctx* ctx, Slot* sl, cudaStream_t s) {
 
 int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz_gpu_blob** out) {
     if (int rc = book_wait(ctx, sl, s)) return rc;
+    if (int rc = check_sticky(ctx)) return rc;
     const BookInfo bi = sl->h_small->info;
     const unsigned flags = sl->h_small->flags | bi.flags;
     // precedence follows the reference: Tensor ctor (DomainError), huffman_encode
@@ -742,6 +823,7 @@ int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz
     if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
     int rc = finish_encode(ctx, sl, b, sl->ws_sym, pl.sym16, pl.n, pl.d_in, pl.interval,
                            pl.predictor == ACZ_PRED_LORENZO2D, s);
+    if (const int lr = slot_leave(ctx, sl, s)) rc = rc ? rc : lr;
     if (rc) {
         if (b->arena) cudaFreeAsync(b->arena, s);
         delete b;
@@ -805,31 +887,40 @@ int blob_to_host_enqueue(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, uint
         return fail(ctx, ACZ_ERR_FORMAT, "internal: ACZ1 size mismatch");
     if (k || nout) {
         const size_t need = 5ull * k + 12ull * nout;
+        if (int rc = slot_enter(ctx, sl, s)) return rc;
         CK(grow(&sl->ws_pack, &sl->ws_pack_cap, need));
         uint8_t* pk = static_cast<uint8_t*>(sl->ws_pack);
         CK(launch_pack_acz1(b->book_sym, b->book_len, k, b->out_index, b->out_value, nout, pk,
                             pk + 5ull * k, ctx->sms, s, &ctx->launches));
         if (k) CK(cudaMemcpyAsync(book_at, pk, 5ull * k, cudaMemcpyDeviceToHost, s));
         if (nout) CK(cudaMemcpyAsync(outl_at, pk + 5ull * k, 12ull * nout, cudaMemcpyDeviceToHost, s));
+        return slot_leave(ctx, sl, s);
     }
     return ACZ_OK;
 }
 
-// Decode sidecar ("ACZS" v2) into host memory dst, async on s (see blob_to_host_enqueue).
-int sidecar_to_host_enqueue(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
-                            cudaStream_t s) {
+// Decode sidecar ("ACZS" v3) into host memory dst, async on s (see blob_to_host_enqueue).
+// The binding is computed on the device from the blob's codebook and bitstream.
+int sidecar_to_host_enqueue(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, uint8_t* dst,
+                            uint64_t cap, cudaStream_t s) {
     const bool has_outl = b->side_outl != nullptr;
     const uint64_t need = sidecar_bytes(b->nchunks, has_outl);
     if (cap < need) return fail(ctx, ACZ_ERR_INVALID, "destination too small");
     uint8_t* p = dst;
+    if (!sl) return fail(ctx, ACZ_ERR_NOMEM, "slot");
+    if (int rc = ensure_small(ctx, sl)) return rc;
+    if (int rc = slot_enter(ctx, sl, s)) return rc;
     std::memcpy(p, "ACZS", 4);
     p += 4;
-    const uint32_t ver = 2;
-    std::memcpy(p, &ver, 4);
+    std::memcpy(p, &kSidecarVersion, 4);
     p += 4;
     const uint64_t hdr[6] = {b->info.element_count, b->info.bit_length, b->interval, b->nchunks,
-                             blob_binding(b->info), has_outl ? 1ull : 0ull};
+                             0ull, has_outl ? 1ull : 0ull};
     std::memcpy(p, hdr, sizeof(hdr));
+    CK(launch_blob_digest(b->book_sym, b->book_len, b->info.codebook_size,
+                          reinterpret_cast<const uint8_t*>(b->words), (b->info.bit_length + 7) / 8,
+                          blob_binding_h0(b->info), &sl->d_small->binding, s, &ctx->launches));
+    CK(cudaMemcpyAsync(p + 4 * 8, &sl->d_small->binding, 8, cudaMemcpyDeviceToHost, s));
     p += sizeof(hdr);
     CK(cudaMemcpyAsync(p, b->side_bitoff, 8ull * b->nchunks, cudaMemcpyDeviceToHost, s));
     p += 8ull * b->nchunks;
@@ -838,7 +929,7 @@ int sidecar_to_host_enqueue(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* ds
         p += 4ull * b->nchunks;
     }
     CK(cudaMemcpyAsync(p, b->side_state, 4ull * b->nchunks, cudaMemcpyDeviceToHost, s));
-    return ACZ_OK;
+    return slot_leave(ctx, sl, s);
 }
 
 constexpr size_t kPoolStreams = 8;
@@ -896,6 +987,7 @@ extern "C" {
 int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape, uint32_t rank,
                      double eb, uint32_t quant_radius, uint32_t predictor, void* stream,
                      acz_gpu_blob** out) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !out) return ACZ_ERR_INVALID;
     *out = nullptr;
     ctx->err.clear();
@@ -905,12 +997,14 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
     int rc = compress_begin(ctx, sl, d_in, shape, rank, eb, quant_radius, predictor, s, &pl);
     if (rc) return rc;
     return compress_end(ctx, sl, pl, s, out);
+    });
 }
 
 int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const* d_in,
                            const uint64_t* shapes, const uint32_t* ranks, double eb,
                            uint32_t quant_radius, uint32_t predictor, void* stream,
                            acz_gpu_blob** out, int* status) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !out || (count && (!d_in || !shapes || !ranks))) return ACZ_ERR_INVALID;
     ctx->err.clear();
     cudaStream_t user = static_cast<cudaStream_t>(stream);
@@ -985,6 +1079,7 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
     if (rc) return rc;
     if (first_err) ctx->err = first_msg;
     return first_err;
+    });
 }
 
 int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const* h_in,
@@ -993,6 +1088,7 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
                                 const uint64_t* acz1_cap, uint64_t* acz1_size,
                                 uint8_t* const* sidecar, const uint64_t* sidecar_cap,
                                 uint64_t* sidecar_size, int* status) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || (count && (!h_in || !shapes || !ranks || !acz1 || !acz1_cap || !acz1_size)))
         return ACZ_ERR_INVALID;
     ctx->err.clear();
@@ -1050,6 +1146,8 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
         acz_gpu_blob* b = nullptr;
         if (st[i] == ACZ_OK) st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], s, &b);
         if (st[i] == ACZ_OK) {
+            acz1_size[i] = b->info.compressed_bytes;  // the needed size, also on failure
+            if (sidecar_size) sidecar_size[i] = b->info.sidecar_bytes;
             if (acz1_cap[i] < b->info.compressed_bytes)
                 st[i] = fail(ctx, ACZ_ERR_INVALID, "ACZ1 destination too small");
             else
@@ -1060,7 +1158,8 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
             if (!sidecar_cap || sidecar_cap[i] < b->info.sidecar_bytes)
                 st[i] = fail(ctx, ACZ_ERR_INVALID, "sidecar destination too small");
             else
-                st[i] = sidecar_to_host_enqueue(ctx, b, sidecar[i], sidecar_cap[i], s);
+                st[i] = sidecar_to_host_enqueue(ctx, get_slot(ctx, i), b, sidecar[i],
+                                                sidecar_cap[i], s);
             if (st[i] == ACZ_OK && sidecar_size) sidecar_size[i] = b->info.sidecar_bytes;
         }
         if (b) acz_gpu_blob_free(b);  // stream-ordered: the copies above complete first
@@ -1092,11 +1191,14 @@ int acz_gpu_compress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const float* c
     if (rc) return rc;
     CK(cudaStreamSynchronize(ctx->own));  // every ACZ1 / sidecar byte is in host memory
     if (first_err) ctx->err = first_msg;
+    if (!first_err) first_err = check_sticky(ctx);
     return first_err;
+    });
 }
 
 int acz_gpu_decompress_batch(acz_gpu_ctx* ctx, uint32_t count, const acz_gpu_blob* const* blobs,
                              int zero_filter, float* const* d_out, void* stream) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || (count && (!blobs || !d_out))) return ACZ_ERR_INVALID;
     ctx->err.clear();
     if (count == 0) return ACZ_OK;
@@ -1113,14 +1215,17 @@ int acz_gpu_decompress_batch(acz_gpu_ctx* ctx, uint32_t count, const acz_gpu_blo
     rc = pool_join(ctx, k, user);
     if (rc) return rc;
     return first_err;
+    });
 }
 
 int acz_gpu_decompress(acz_gpu_ctx* ctx, const acz_gpu_blob* b, int zero_filter, float* d_out,
                        void* stream) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !b || !d_out) return ACZ_ERR_INVALID;
     ctx->err.clear();
     return decompress_on(ctx, get_slot(ctx, 0), b, zero_filter, d_out,
                          static_cast<cudaStream_t>(stream));
+    });
 }
 
 int acz_gpu_blob_info(const acz_gpu_blob* b, acz_gpu_blob_info_t* info) {
@@ -1139,25 +1244,63 @@ int acz_gpu_blob_free(acz_gpu_blob* b) {
 // ------------------------------------------------------------------ serialisation --
 int acz_gpu_blob_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
                          uint64_t* written, void* stream) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !b || !dst) return ACZ_ERR_INVALID;
     ctx->err.clear();
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int rc = blob_to_host_enqueue(ctx, get_slot(ctx, 0), b, dst, cap, s);
     if (rc) return rc;
     CK(cudaStreamSynchronize(s));
+    if (int sr = check_sticky(ctx)) return sr;
     if (written) *written = b->info.compressed_bytes;
     return ACZ_OK;
+    });
 }
 
 int acz_gpu_sidecar_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* dst, uint64_t cap,
                             uint64_t* written, void* stream) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !b || !dst) return ACZ_ERR_INVALID;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int rc = sidecar_to_host_enqueue(ctx, b, dst, cap, s);
+    const int rc = sidecar_to_host_enqueue(ctx, get_slot(ctx, 0), b, dst, cap, s);
     if (rc) return rc;
     CK(cudaStreamSynchronize(s));
     if (written) *written = sidecar_bytes(b->nchunks, b->side_outl != nullptr);
     return ACZ_OK;
+    });
+}
+
+// Sidecar arrays the decoders index with (bit offsets, outlier prefixes) must be in range:
+// offsets start at 0, never decrease, advance at most 64 bits per symbol and stay within the
+// stream; prefixes start at 0, never decrease and stay within the outlier list; chain states
+// are finite (reference chain values always are). Anything else falls back to the rebuild.
+bool sidecar_arrays_ok(const uint8_t* p, uint64_t nchunks, uint64_t interval, bool has_outl,
+                       uint64_t bit_length, uint64_t nout) {
+    uint64_t prev = 0;
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        uint64_t v;
+        std::memcpy(&v, p + 8 * c, 8);
+        if ((c == 0 && v != 0) || v < prev || v > bit_length || v - prev > 64 * interval)
+            return false;
+        prev = v;
+    }
+    p += 8 * nchunks;
+    if (has_outl) {
+        uint32_t po = 0;
+        for (uint64_t c = 0; c < nchunks; ++c) {
+            uint32_t v;
+            std::memcpy(&v, p + 4 * c, 4);
+            if ((c == 0 && v != 0) || v < po || v > nout) return false;
+            po = v;
+        }
+        p += 4 * nchunks;
+    }
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        float f;
+        std::memcpy(&f, p + 4 * c, 4);
+        if (!std::isfinite(f)) return false;
+    }
+    return true;
 }
 
 // ACZ1 bytes (+ optional ACZS sidecar) in host memory -> device blob on stream s, with the
@@ -1166,9 +1309,9 @@ int acz_gpu_sidecar_to_host(acz_gpu_ctx* ctx, const acz_gpu_blob* b, uint8_t* ds
 // are page-locked); the codebook and outliers are de-interleaved on the device. async: do
 // not synchronise s when a valid sidecar was supplied (the caller keeps src/sidecar alive
 // and orders its own work after s).
-static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uint64_t size,
-                      const uint8_t* sidecar, uint64_t sidecar_size, cudaStream_t s,
-                      acz_gpu_blob** out, bool async) {
+static int blob_from_host_body(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uint64_t size,
+                               const uint8_t* sidecar, uint64_t sidecar_size, cudaStream_t s,
+                               acz_gpu_blob** out, bool async) {
     if (!ctx || !out || (!src && size)) return ACZ_ERR_INVALID;
     if (!sl) return fail(ctx, ACZ_ERR_NOMEM, "slot");
     *out = nullptr;
@@ -1240,9 +1383,13 @@ static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uin
     const uint8_t* bits = src + pos;
     pos += nbytes;
     const uint64_t outl_off = pos;
-    std::vector<unsigned long long> oidx(nout);
-    std::vector<float> oval(nout);
+    // the count is untrusted: parse record by record (the reference's error order), but
+    // never allocate for more records than the remaining bytes can hold
+    const uint64_t nfit = std::min<uint64_t>(nout, (size - pos) / 12 + 1);
+    std::vector<unsigned long long> oidx(nfit);
+    std::vector<float> oval(nfit);
     for (uint64_t i = 0; i < nout; ++i) {
+        if (i >= nfit) return fail(ctx, ACZ_ERR_FORMAT, "unexpected end of stream");
         oidx[i] = get(8);
         const uint32_t vb = (uint32_t)get(4);
         NEED();
@@ -1284,18 +1431,25 @@ static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uin
     const bool want_outl = pred == ACZ_PRED_LORENZO2D;
     uint32_t sver = 0;
     if (sidecar && sidecar_size >= 56) std::memcpy(&sver, sidecar + 4, 4);
-    if (sidecar && sidecar_size >= 56 && std::memcmp(sidecar, "ACZS", 4) == 0 && sver == 2) {
+    if (sidecar && sidecar_size >= 56 && std::memcmp(sidecar, "ACZS", 4) == 0 &&
+        sver == kSidecarVersion) {
         uint64_t hdr[6];
         std::memcpy(hdr, sidecar + 8, sizeof(hdr));
         if (hdr[0] == count && hdr[1] == bit_length && hdr[2] > 0 &&
-            (pred != ACZ_PRED_PREV || (hdr[2] % 32 == 0)) &&
-            hdr[3] == (count + hdr[2] - 1) / hdr[2] && hdr[4] == blob_binding(in) &&
-            hdr[5] == (want_outl ? 1ull : 0ull) &&
+            (pred != ACZ_PRED_PREV || (hdr[2] % 32 == 0 && (hdr[2] & (hdr[2] - 1)) == 0)) &&
+            hdr[3] == (count + hdr[2] - 1) / hdr[2] && hdr[5] == (want_outl ? 1ull : 0ull) &&
             sidecar_size == sidecar_bytes(hdr[3], want_outl) &&
             (pred == ACZ_PRED_PREV || hdr[2] == sidecar_interval_for((uint32_t)pred, g))) {
-            have_side = true;
-            side_interval = hdr[2];
-            side_chunks = hdr[3];
+            uint64_t book_sum = 0;
+            for (uint64_t i = 0; i < k; ++i) book_sum += acz_book_term(bsym[i], blen[i], i);
+            const uint64_t want = acz_binding(blob_binding_h0(in), book_sum,
+                                              acz_bits_digest(bits, nbytes));
+            if (hdr[4] == want && sidecar_arrays_ok(sidecar + 56, hdr[3], hdr[2], want_outl,
+                                                    bit_length, nout)) {
+                have_side = true;
+                side_interval = hdr[2];
+                side_chunks = hdr[3];
+            }
         }
     }
     acz_gpu_blob* b = new (std::nothrow) acz_gpu_blob();
@@ -1412,19 +1566,34 @@ static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uin
     return ACZ_OK;
 }
 
+static int blob_from_host_on(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, uint64_t size,
+                             const uint8_t* sidecar, uint64_t sidecar_size, cudaStream_t s,
+                             acz_gpu_blob** out, bool async) {
+    if (!ctx || !out || (!src && size)) return ACZ_ERR_INVALID;
+    if (!sl) return fail(ctx, ACZ_ERR_NOMEM, "slot");
+    if (int rc = ensure_small(ctx, sl)) return rc;
+    if (int rc = slot_enter(ctx, sl, s)) return rc;
+    const int rc = blob_from_host_body(ctx, sl, src, size, sidecar, sidecar_size, s, out, async);
+    const int lr = slot_leave(ctx, sl, s);
+    return rc ? rc : lr;
+}
+
 extern "C" int acz_gpu_blob_from_host(acz_gpu_ctx* ctx, const uint8_t* src, uint64_t size,
                                       const uint8_t* sidecar, uint64_t sidecar_size, void* stream,
                                       acz_gpu_blob** out) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !out || (!src && size)) return ACZ_ERR_INVALID;
     ctx->err.clear();
     return blob_from_host_on(ctx, get_slot(ctx, 0), src, size, sidecar, sidecar_size,
                              static_cast<cudaStream_t>(stream), out, false);
+    });
 }
 
 int acz_gpu_decompress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const uint8_t* const* acz1,
                                   const uint64_t* acz1_size, const uint8_t* const* sidecar,
                                   const uint64_t* sidecar_size, int zero_filter,
                                   float* const* h_out, const uint64_t* out_cap, int* status) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || (count && (!acz1 || !acz1_size || !h_out || !out_cap))) return ACZ_ERR_INVALID;
     ctx->err.clear();
     if (count == 0) return ACZ_OK;
@@ -1494,7 +1663,9 @@ int acz_gpu_decompress_host_batch(acz_gpu_ctx* ctx, uint32_t count, const uint8_
     CK(cudaStreamWaitEvent(ctx->own, ctx->io_ev, 0));
     CK(cudaStreamSynchronize(ctx->own));
     if (first_err) ctx->err = first_msg;
+    if (!first_err) first_err = check_sticky(ctx);
     return first_err;
+    });
 }
 
 // ------------------------------------------------------------------- host buffers --
@@ -1504,6 +1675,7 @@ int acz_gpu_compress_host(acz_gpu_ctx* ctx, const float* h_in, const uint64_t* s
                           uint32_t rank, double eb, uint32_t quant_radius, uint32_t predictor,
                           uint8_t** acz1, uint64_t* acz1_size, uint8_t** sidecar,
                           uint64_t* sidecar_size) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !acz1 || !acz1_size) return ACZ_ERR_INVALID;
     *acz1 = nullptr;
     if (sidecar) *sidecar = nullptr;
@@ -1544,11 +1716,13 @@ int acz_gpu_compress_host(acz_gpu_ctx* ctx, const float* h_in, const uint64_t* s
     *acz1 = buf;
     *acz1_size = sz;
     return ACZ_OK;
+    });
 }
 
 int acz_gpu_decompress_host(acz_gpu_ctx* ctx, const uint8_t* acz1, uint64_t acz1_size,
                             const uint8_t* sidecar, uint64_t sidecar_size, int zero_filter,
                             float* h_out, uint64_t n) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !h_out) return ACZ_ERR_INVALID;
     cudaStream_t s = ctx->own;
     acz_gpu_blob* b = nullptr;
@@ -1571,11 +1745,13 @@ int acz_gpu_decompress_host(acz_gpu_ctx* ctx, const uint8_t* acz1, uint64_t acz1
     }
     acz_gpu_blob_free(b);
     return rc;
+    });
 }
 
 // ---------------------------------------------------------------------- statistics --
 int acz_gpu_zero_bitmap(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, uint32_t* d_bitmap,
                         uint64_t* nonzero, void* stream) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || (!d_in && n)) return ACZ_ERR_INVALID;
     ctx->err.clear();
     if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "nonzero_ratio: empty tensor");
@@ -1586,6 +1762,7 @@ int acz_gpu_zero_bitmap(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, uint32_
     if (nonzero) *nonzero = nz;
     if (fl & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
     return ACZ_OK;
+    });
 }
 
 int acz_gpu_nonzero_ratio(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void* stream,
@@ -1599,6 +1776,7 @@ int acz_gpu_nonzero_ratio(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void*
 
 int acz_gpu_mean_abs(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void* stream,
                      double* mean) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || (!d_in && n)) return ACZ_ERR_INVALID;
     ctx->err.clear();
     if (n == 0) return fail(ctx, ACZ_ERR_DOMAIN, "mean_abs: empty tensor");
@@ -1609,6 +1787,7 @@ int acz_gpu_mean_abs(acz_gpu_ctx* ctx, const float* d_in, uint64_t n, void* stre
     if (fl & kFlagNonFinite) return fail(ctx, ACZ_ERR_DOMAIN, "tensor element is not finite");
     if (mean) *mean = sa / (double)n;
     return ACZ_OK;
+    });
 }
 
 // ------------------------------------------------------------------------- Huffman --
@@ -1616,6 +1795,7 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
                            uint32_t* book_sym, uint8_t* book_len, uint32_t book_cap,
                            uint32_t* book_size, uint8_t* bits, uint64_t bits_cap,
                            uint64_t* bit_length, void* stream) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx || !book_size || !bit_length) return ACZ_ERR_INVALID;
     ctx->err.clear();
     Slot* sl = get_slot(ctx, 0);
@@ -1660,11 +1840,13 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
     *book_size = bi.book_size;
     *bit_length = bi.total_bits;
     return ACZ_OK;
+    });
 }
 
 int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uint8_t* book_len,
                            uint32_t book_size, const uint8_t* bits, uint64_t bit_length,
                            uint64_t count, uint32_t* d_out, void* stream) {
+    return guarded(ctx, [&]() -> int {
     if (!ctx) return ACZ_ERR_INVALID;
     ctx->err.clear();
     Slot* sl = get_slot(ctx, 0);
@@ -1718,6 +1900,7 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
     if (fl & kDecTruncated) return fail(ctx, ACZ_ERR_DECODE, "truncated bitstream");
     if (fl & kDecNoMatch) return fail(ctx, ACZ_ERR_DECODE, "no codeword matches bitstream");
     return ACZ_OK;
+    });
 }
 
 // ------------------------------------------------------------------ memory helpers --

@@ -34,6 +34,35 @@ constexpr unsigned kFlagDepth64 = 4u;    // DecodeError (ref src/huffman.cpp:64)
 constexpr unsigned kFlagLenTooLong = 8u; // code length > 56: unsupported packing (never for n<2^44)
 constexpr unsigned kFlagInternal = 16u;  // internal consistency failure (look-back timeout)
 
+// Sidecar binding (ACZS v3): ties a decode sidecar to one blob. Host (blob_from_host) and
+// device (k_blob_digest, at sidecar export) compute the same value from the header hash h0,
+// the codebook (order-independent sum of per-entry mixes, so a CTA can reduce it) and 64
+// 8-byte samples of the bitstream at fixed positions plus its length.
+__host__ __device__ inline uint64_t acz_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t acz_book_term(uint32_t sym, uint32_t len, uint64_t i) {
+    return acz_mix64((((uint64_t)sym << 8) | len) + i * 0xD1B54A32D192ED03ull);
+}
+// bits: the bitstream's byte image (nbytes = ceil(bit_length / 8)).
+__host__ __device__ inline uint64_t acz_bits_digest(const uint8_t* bits, uint64_t nbytes) {
+    uint64_t h = acz_mix64(nbytes);
+    for (int i = 0; i < 64; ++i) {
+        const uint64_t pos = nbytes >= 8 ? (nbytes - 8) * (uint64_t)i / 63 : 0;
+        uint64_t v = 0;
+        for (int j = 0; j < 8; ++j)
+            if (pos + j < nbytes) v |= (uint64_t)bits[pos + j] << (8 * j);
+        h = acz_mix64(h ^ (v + (uint64_t)i));
+    }
+    return h;
+}
+__host__ __device__ inline uint64_t acz_binding(uint64_t h0, uint64_t book_sum, uint64_t bits_digest) {
+    return acz_mix64(h0 ^ acz_mix64(book_sum ^ acz_mix64(bits_digest)));
+}
+
 // Per-length canonical decode tables (ref src/huffman.cpp:152-166).
 struct CanonTables {
     unsigned long long first_code[65];

@@ -1341,6 +1341,12 @@ __global__ void __launch_bounds__(kCountThreads) k_encode_count(EncodeArgs a) {
                     do {
                         f = vst[j].flag;
                     } while (f == 0 && ++spins < (1ull << 30));
+                    if (f == 0 && a.sticky) {
+                        // the predecessor never published: the offsets below would be wrong.
+                        // Report it (the host checks the sticky word at every entry point)
+                        atomicOr(a.sticky, kFlagInternal);
+                        __threadfence_system();
+                    }
                     __threadfence();
                     if (f == 2) {
                         vb = vst[j].incl_bits;

@@ -29,9 +29,13 @@ struct PlaneGeom {
 PlaneGeom plane_geom(const uint64_t* shape, uint32_t rank);
 
 // ---- stats.cu ----
+// d_sumabs (optional): fixed-order reduction through d_partials (stats_partials(sms)
+// doubles) and d_ticket (zero between launches).
+size_t stats_partials(int sms);
 cudaError_t launch_stats(const float* x, uint64_t n, uint32_t* bitmap,
                          unsigned long long* d_nnz, unsigned int* d_flags, double* d_sumabs,
-                         int sms, cudaStream_t s, uint64_t* launches);
+                         double* d_partials, unsigned int* d_ticket, int sms, cudaStream_t s,
+                         uint64_t* launches);
 
 cudaError_t launch_relu(float* x, uint64_t n, int sms, cudaStream_t s, uint64_t* launches);
 struct CopyRegions {
@@ -50,6 +54,9 @@ cudaError_t launch_pack_acz1(const uint32_t* bsym, const uint8_t* blen, uint32_t
                              const unsigned long long* oidx, const float* oval, uint64_t nout,
                              uint8_t* book_out, uint8_t* outl_out, int sms, cudaStream_t s,
                              uint64_t* launches);
+cudaError_t launch_blob_digest(const uint32_t* bsym, const uint8_t* blen, uint32_t k,
+                               const uint8_t* bits, uint64_t nbytes, uint64_t h0,
+                               unsigned long long* out, cudaStream_t s, uint64_t* launches);
 cudaError_t launch_widen_u16(const uint16_t* a, uint32_t* b, uint64_t n, int sms, cudaStream_t s,
                              uint64_t* launches);
 
@@ -119,7 +126,7 @@ struct EncodeArgs {
     uint64_t interval;
     uint32_t max_len;
     TileStatus* status;              // encode_scratch_bytes(n, sms) of scratch (look-back + chunk offsets)
-    unsigned int* ticket;            // unused
+    unsigned int* sticky;            // mapped host word: kFlagInternal on a look-back timeout
     unsigned long long* chunk_off;   // set by the launcher (inside the scratch)
 };
 constexpr int kEncThreads = 256;

@@ -2,7 +2,11 @@
 // zero-bitmap and sparsity pass"). Predicates follow the reference exactly:
 //   nonzero  : v != 0.0f              (ref include/acz/tensor.hpp:91-99, -0.0 is zero)
 //   finite   : isfinite(v)            (ref include/acz/tensor.hpp:69-73 -> DomainError)
-//   sum |v|  : in double              (ref include/acz/tensor.hpp:82-89; parallel order)
+//   sum |v|  : in double              (ref include/acz/tensor.hpp:82-89). The reference sums
+//              sequentially; here every thread sums its grid-stride words in order, warps
+//              and CTAs combine in a fixed tree order and the last CTA adds the per-CTA
+//              partials in index order, so the result is deterministic (identical for
+//              identical inputs on a given grid), within 1e-12 relative of the reference.
 //
 // HBM-bound: 4 B read per element, 1/8 B written (bitmap). Each thread owns one 32-element
 // bitmap word and reads it as 8 x 128-bit loads; a warp therefore streams 4 KiB per
@@ -28,7 +32,10 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 __global__ void __launch_bounds__(256) k_stats(const float* __restrict__ x, uint64_t n,
                                                uint32_t* __restrict__ bitmap,
                                                unsigned long long* nnz, unsigned int* flags,
-                                               double* sumabs) {
+                                               double* sumabs, double* partials,
+                                               unsigned int* ticket) {
+    __shared__ double s_warp[8];
+    __shared__ bool s_last;
     const uint64_t nwords = (n + 31) / 32;
     const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     unsigned long long cnt = 0;
@@ -65,10 +72,31 @@ __global__ void __launch_bounds__(256) k_stats(const float* __restrict__ x, uint
     cnt = warp_sum_u64(cnt);
     sabs = warp_sum(sabs);
     const unsigned any_bad = __any_sync(0xffffffffu, bad);
-    if ((threadIdx.x & 31) == 0) {
-        if (cnt) atomicAdd(nnz, cnt);
-        if (sumabs) atomicAdd(sumabs, sabs);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        if (cnt) atomicAdd(nnz, cnt);  // integer: order-independent
         if (any_bad) atomicOr(flags, kFlagNonFinite);
+        s_warp[warp] = sabs;
+    }
+    if (!sumabs) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += s_warp[w];
+        partials[blockIdx.x] = b;
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || warp != 0) return;
+    // last CTA: lane l sums partials l, l+32, ... in order, then a fixed butterfly
+    __threadfence();
+    double t = 0.0;
+    for (unsigned i = lane; i < gridDim.x; i += 32) t += ((volatile double*)partials)[i];
+    t = warp_sum(t);
+    if (lane == 0) {
+        *sumabs = t;
+        *ticket = 0u;  // ready for the next launch (stream-ordered)
     }
 }
 
@@ -161,7 +189,31 @@ __global__ void k_unpack_acz1(const uint8_t* __restrict__ raw, uint32_t k, uint6
     }
 }
 
+// Sidecar binding of a device blob (acz_binding in common.cuh), written to *out.
+__global__ void __launch_bounds__(256) k_blob_digest(const uint32_t* __restrict__ bsym,
+                                                     const uint8_t* __restrict__ blen, uint32_t k,
+                                                     const uint8_t* __restrict__ bits,
+                                                     uint64_t nbytes, uint64_t h0,
+                                                     unsigned long long* out) {
+    __shared__ unsigned long long s_sum;
+    if (threadIdx.x == 0) s_sum = 0ull;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) t += acz_book_term(bsym[i], blen[i], i);
+    atomicAdd(&s_sum, t);  // integer sum mod 2^64: order-independent
+    __syncthreads();
+    if (threadIdx.x == 0) *out = acz_binding(h0, s_sum, acz_bits_digest(bits, nbytes));
+}
+
 }  // namespace
+
+cudaError_t launch_blob_digest(const uint32_t* bsym, const uint8_t* blen, uint32_t k,
+                               const uint8_t* bits, uint64_t nbytes, uint64_t h0,
+                               unsigned long long* out, cudaStream_t s, uint64_t* launches) {
+    k_blob_digest<<<1, 256, 0, s>>>(bsym, blen, k, bits, nbytes, h0, out);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_unpack_acz1(const uint8_t* raw, uint32_t k, uint64_t nout, uint32_t* bsym,
                                uint8_t* blen, unsigned long long* oidx, float* oval, int sms,
@@ -213,15 +265,19 @@ cudaError_t launch_widen_u16(const uint16_t* a, uint32_t* b, uint64_t n, int sms
     return cudaGetLastError();
 }
 
+size_t stats_partials(int sms) { return (size_t)sms * 8; }
+
 cudaError_t launch_stats(const float* x, uint64_t n, uint32_t* bitmap,
                          unsigned long long* d_nnz, unsigned int* d_flags, double* d_sumabs,
-                         int sms, cudaStream_t s, uint64_t* launches) {
+                         double* d_partials, unsigned int* d_ticket, int sms, cudaStream_t s,
+                         uint64_t* launches) {
     const uint64_t nwords = (n + 31) / 32;
     uint64_t blocks = (nwords + 255) / 256;
-    const uint64_t cap = (uint64_t)sms * 8;
+    const uint64_t cap = stats_partials(sms);
     if (blocks > cap) blocks = cap;
     if (blocks == 0) blocks = 1;
-    k_stats<<<(unsigned)blocks, 256, 0, s>>>(x, n, bitmap, d_nnz, d_flags, d_sumabs);
+    k_stats<<<(unsigned)blocks, 256, 0, s>>>(x, n, bitmap, d_nnz, d_flags, d_sumabs,
+                                             d_partials, d_ticket);
     ++*launches;
     return cudaGetLastError();
 }
