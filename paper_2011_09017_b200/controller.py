@@ -371,8 +371,12 @@ class SavedActivationHooks:
                                     f"has {len(self.convs)} convolutions")
         self._hooks = [m.register_forward_pre_hook(self._mark(i))
                        for i, m in enumerate(self.convs)]
-        self._marked = {}   # storage key -> conv layer id (forward order)
-        self._stash = {}    # storage key -> _Stash (this iteration)
+        # Keys are (data_ptr, shape); every entry also holds a weak reference to the storage
+        # it was taken from, so an address the caching allocator hands out again after the
+        # original activation was freed (e.g. a later ReLU output of the same shape) never
+        # matches a stale entry.
+        self._marked = {}   # storage key -> (storage weakref, conv layer id)
+        self._stash = {}    # storage key -> (storage weakref, _Stash) (this iteration)
         self._raw = {}      # storage key -> [_Saved] raw saves that may alias a conv input
         self.compressed = 0
 
@@ -380,10 +384,25 @@ class SavedActivationHooks:
     def _key(t):
         return (t.data_ptr(), tuple(t.shape))
 
+    @staticmethod
+    def _live(entry, t):
+        """entry = (storage weakref, value): the value if the entry was made for t's storage
+        and that storage is still alive, else None."""
+        if entry is None:
+            return None
+        ref, value = entry
+        st = ref()
+        return value if st is not None and st is t.untyped_storage() else None
+
     def _mark(self, layer: int):
+        import weakref
+
         def hook(_module, args):
             if args and hasattr(args[0], "data_ptr") and args[0].is_cuda:
-                self._marked.setdefault(self._key(args[0]), layer)
+                t = args[0]
+                key = self._key(t)
+                if self._live(self._marked.get(key), t) is None:
+                    self._marked[key] = (weakref.ref(t.untyped_storage()), layer)
         return hook
 
     def remove(self) -> None:
@@ -409,18 +428,19 @@ class SavedActivationHooks:
                 or not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous()
                 or t.numel() < max(1, self.min_numel)):
             return _Saved(raw=t)
+        import weakref
         key = self._key(t)
-        st = self._stash.get(key)
+        st = self._live(self._stash.get(key), t)
         if st is not None:
             return _Saved(stash=st)
-        layer = self._marked.pop(key, None)
+        layer = self._live(self._marked.pop(key, None), t)
         if layer is None:
             s = _Saved(raw=t)
             self._raw.setdefault(key, []).append(s)
             return s
         relu = self.ctl.cfg.zero_restoration == RELU_RECOMPUTE and self._post_relu(t)
         st = _Stash(self.ctl, self.ctl.wrap_forward(layer, t.detach(), relu))
-        self._stash[key] = st
+        self._stash[key] = (weakref.ref(t.untyped_storage()), st)
         if st.handle.blob is not None:
             self.compressed += 1
         for s in self._raw.pop(key, []):  # earlier saves of the same storage share it

@@ -63,20 +63,42 @@ def test_saved_tensor_hooks_train_step(gpu_lib, zr):
     x = torch.randn(8, 3, 32, 32, device="cuda")
     y = torch.randint(0, 10, (8,), device="cuda")
     g0 = torch.autograd.grad(nn.functional.cross_entropy(net(x), y), list(net.parameters()))
+    import paper_2011_09017_b200 as acz
     ctl = _active_controller(3, 1e-5, zr)
     hooks = SavedActivationHooks(ctl, net)
     hooks.new_iteration(1)
+    inputs = []  # every conv input as the conv saw it (the net's third ReLU is not in place
+    # and its output has conv3's input shape: an allocator address reuse must not alias it)
+    taps = [m.register_forward_pre_hook(lambda _m, a: inputs.append(a[0].detach().clone()))
+            for m in hooks.convs]
     with hooks:
         loss1 = nn.functional.cross_entropy(net(x), y)
+    for h in taps:
+        h.remove()
     assert hooks.compressed == 3  # conv1 (image), conv2 (post-ReLU), conv3 (post-pool)
     assert len(ctl.ledger.records) == 0 and ctl.current_bytes > 0
     # bytes accounted once per conv input (no double compression of aliased saves)
     sizes = [8 * 3 * 32 * 32, 8 * 16 * 32 * 32, 8 * 32 * 16 * 16]
     assert ctl.total_in == 4 * sum(sizes)
+    # every stash unpacks to exactly the codec round trip of its conv input, with the
+    # zero restoration of its handle (ref Controller::unwrap_backward src/controller.cpp:243-244)
+    stashes = sorted((st.handle.layer_id, st) for _ref, st in hooks._stash.values())
+    assert [i for i, _ in stashes] == [0, 1, 2]
+    expect_relu = [False, zr == "relu-recompute", False]  # conv3's input comes from a pool
+    for (i, st), relu in zip(stashes, expect_relu):
+        assert st.handle.apply_relu == relu and st.handle.zero_filter == (not relu)
+        want = acz.decompress(acz.compress(inputs[i], acz.CodecParams(1e-5)),
+                              zero_filter=not relu)
+        if relu:
+            want.clamp_(min=0)
+        assert torch.equal(st.get(), want)
     g1 = torch.autograd.grad(loss1, list(net.parameters()))
     assert ctl.current_bytes == 0
-    for a, b in zip(g0, g1):
-        assert torch.allclose(a, b, rtol=0, atol=1e-3 * float(a.abs().max()) + 1e-6)
+    if zr == "codec-filter":
+        # relu-recompute keeps zeros reconstructed as tiny positives positive (the
+        # reference's semantics), so ReLU masks and gradients may legitimately move
+        for a, b in zip(g0, g1):
+            assert torch.allclose(a, b, rtol=0, atol=1e-3 * float(a.abs().max()) + 1e-6)
     hooks.remove()
 
 
@@ -87,6 +109,8 @@ def test_saved_tensor_hooks_free_memory_and_retain_graph(gpu_lib):
     import torch.nn as nn
     from paper_2011_09017_b200.controller import SavedActivationHooks
     torch.manual_seed(1)
+    # cuDNN's weight-gradient kernels may sum in a different order on every call
+    torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
     net = nn.Sequential(nn.Conv2d(3, 64, 3, padding=1), nn.ReLU(inplace=True),
                         nn.Conv2d(64, 64, 3, padding=1), nn.ReLU(inplace=True),
                         nn.Conv2d(64, 64, 3, padding=1), nn.AdaptiveAvgPool2d(1),
@@ -118,8 +142,10 @@ def test_saved_tensor_hooks_free_memory_and_retain_graph(gpu_lib):
     gb = torch.autograd.grad(out1, list(net.parameters()))
     for a, b in zip(ga, gb):
         assert torch.equal(a, b)
+    # eb = 1e-2 moves ReLU masks (the zero filter clears |v| <= eb): measured 2-4 % of
+    # max |grad| on this net; the bound-following check is test_saved_tensor_hooks_train_step
     for a, b in zip(g0, ga):
-        assert torch.allclose(a, b, rtol=0, atol=2e-2 * float(a.abs().max()) + 1e-6)
+        assert torch.allclose(a, b, rtol=0, atol=1e-1 * float(a.abs().max()) + 1e-6)
 
 
 def test_relu_recompute_matches_reference(gpu_lib, reference):
