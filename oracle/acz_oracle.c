@@ -6,6 +6,7 @@
 #include "acz_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -114,17 +115,100 @@ static int cmp_entry(const void* a, const void* b) {
     return x->sym < y->sym ? -1 : x->sym > y->sym;
 }
 
+/* ---- thread helpers (the multi-threaded oracle splits work into contiguous ranges and
+ * joins the results in index order, so its outputs are those of the serial loops) ---- */
+typedef void (*range_fn)(void* arg, int t, int nt);
+typedef struct {
+    range_fn fn;
+    void* arg;
+    int t, nt;
+} range_job;
+static void* range_main(void* p) {
+    range_job* j = (range_job*)p;
+    j->fn(j->arg, j->t, j->nt);
+    return NULL;
+}
+/* runs fn(arg, t, nt) for t in [0, nt) on nt threads (thread 0 is the caller) */
+static void run_threads(range_fn fn, void* arg, int nt) {
+    if (nt <= 1) {
+        fn(arg, 0, 1);
+        return;
+    }
+    pthread_t th[256];
+    range_job jobs[256];
+    if (nt > 256) nt = 256;
+    int started[256] = {0};
+    for (int t = 1; t < nt; ++t) {
+        jobs[t] = (range_job){fn, arg, t, nt};
+        started[t] = pthread_create(&th[t], NULL, range_main, &jobs[t]) == 0;
+        if (!started[t]) fn(arg, t, nt);
+    }
+    fn(arg, 0, nt);
+    for (int t = 1; t < nt; ++t)
+        if (started[t]) pthread_join(th[t], NULL);
+}
+static void split(uint64_t n, int t, int nt, uint64_t* a, uint64_t* b) {
+    *a = n * (uint64_t)t / (uint64_t)nt;
+    *b = n * (uint64_t)(t + 1) / (uint64_t)nt;
+}
+
+typedef struct {
+    const uint32_t* syms;
+    uint64_t n;
+    uint32_t mx;
+    uint64_t* part; /* nt x (mx + 1) counts */
+} count_job;
+static void count_range(void* p, int t, int nt) {
+    count_job* j = (count_job*)p;
+    uint64_t a, b;
+    split(j->n, t, nt, &a, &b);
+    uint64_t* d = j->part + (uint64_t)t * ((uint64_t)j->mx + 1);
+    for (uint64_t i = a; i < b; ++i) d[j->syms[i]]++;
+}
+
+typedef struct {
+    const uint32_t* syms;
+    uint64_t n;
+    uint32_t* mx; /* per thread */
+} max_job;
+static void max_range(void* p, int t, int nt) {
+    max_job* j = (max_job*)p;
+    uint64_t a, b;
+    split(j->n, t, nt, &a, &b);
+    uint32_t m = 0;
+    for (uint64_t i = a; i < b; ++i)
+        if (j->syms[i] > m) m = j->syms[i];
+    j->mx[t] = m;
+}
+
 /* Frequencies in ascending symbol order: ref src/huffman.cpp:110-111 (std::map). */
 static int frequencies(const uint32_t* syms, uint64_t n, uint32_t** fsym, uint64_t** ffreq,
-                       uint64_t* k) {
+                       uint64_t* k, int nt) {
     uint32_t mx = 0;
-    for (uint64_t i = 0; i < n; ++i)
-        if (syms[i] > mx) mx = syms[i];
+    {
+        uint32_t m[256] = {0};
+        max_job mj = {syms, n, m};
+        run_threads(max_range, &mj, nt);
+        for (int t = 0; t < (nt > 256 ? 256 : nt); ++t)
+            if (m[t] > mx) mx = m[t];
+    }
     uint64_t cnt = 0;
     if (mx < (1u << 26)) {
         uint64_t* dense = calloc((size_t)mx + 1, sizeof(uint64_t));
         if (!dense) return E_NOMEM;
-        for (uint64_t i = 0; i < n; ++i) dense[syms[i]]++;
+        uint64_t* part = NULL;
+        if (nt > 1 && mx < (1u << 22))
+            part = calloc((size_t)nt * ((size_t)mx + 1), sizeof(uint64_t));
+        if (part) {
+            count_job cj = {syms, n, mx, part};
+            run_threads(count_range, &cj, nt);
+            for (int t = 0; t < nt; ++t)
+                for (uint64_t s2 = 0; s2 <= mx; ++s2)
+                    dense[s2] += part[(uint64_t)t * ((uint64_t)mx + 1) + s2];
+            free(part);
+        } else {
+            for (uint64_t i = 0; i < n; ++i) dense[syms[i]]++;
+        }
         for (uint64_t s = 0; s <= mx; ++s) cnt += dense[s] != 0;
         *fsym = malloc(sizeof(uint32_t) * (cnt + 1));
         *ffreq = malloc(sizeof(uint64_t) * (cnt + 1));
@@ -220,9 +304,50 @@ static void canonical_codes(const entry* book, uint64_t k, uint64_t* codes) {
 }
 
 /* ref src/huffman.cpp:107-135 (huffman_encode); BitWriter :88-103 (MSB-first). */
+typedef struct {
+    const uint32_t* syms;
+    uint64_t n;
+    const uint64_t* code_of_sym; /* dense: symbol -> code */
+    const uint8_t* len_of_sym;   /* dense: symbol -> length */
+    uint64_t* start;             /* per thread: first bit (filled by the caller) */
+    uint64_t* nbits;             /* per thread: bit count (first pass) */
+    uint8_t** local;             /* per thread: private bytes from byte start[t] / 8 */
+    int pass;
+    int nomem;
+} pack_job;
+/* MSB-first packing of a contiguous symbol range into a private buffer aligned like the
+ * shared stream (its first byte is byte start/8 of the stream): ref BitWriter,
+ * src/huffman.cpp:88-103, loop :127-131. */
+static void pack_range(void* p, int t, int nt) {
+    pack_job* j = (pack_job*)p;
+    uint64_t a, b;
+    split(j->n, t, nt, &a, &b);
+    if (j->pass == 0) {
+        uint64_t c = 0;
+        for (uint64_t i = a; i < b; ++i) c += j->len_of_sym[j->syms[i]];
+        j->nbits[t] = c;
+        return;
+    }
+    const uint64_t s0 = j->start[t];
+    const uint64_t nbytes = ((s0 & 7) + j->nbits[t] + 7) / 8 + 1;
+    uint8_t* out = calloc((size_t)nbytes, 1);
+    j->local[t] = out;
+    if (!out) {
+        j->nomem = 1;
+        return;
+    }
+    uint64_t pos = s0 & 7;
+    for (uint64_t i = a; i < b; ++i) {
+        const uint32_t s2 = j->syms[i];
+        const uint64_t code = j->code_of_sym[s2];
+        for (int bit = j->len_of_sym[s2] - 1; bit >= 0; --bit, ++pos)
+            if ((code >> bit) & 1) out[pos >> 3] |= (uint8_t)(0x80u >> (pos & 7));
+    }
+}
+
 static int huffman_encode_impl(const uint32_t* syms, uint64_t n, uint32_t* book_size,
                                uint32_t** book_sym, uint8_t** book_len, uint8_t** bits,
-                               uint64_t* bit_length, char* err, int cap) {
+                               uint64_t* bit_length, char* err, int cap, int nt) {
     *book_size = 0;
     *book_sym = NULL;
     *book_len = NULL;
@@ -232,7 +357,7 @@ static int huffman_encode_impl(const uint32_t* syms, uint64_t n, uint32_t* book_
     uint32_t* fsym = NULL;
     uint64_t* ffreq = NULL;
     uint64_t k = 0;
-    int rc = frequencies(syms, n, &fsym, &ffreq, &k);
+    int rc = frequencies(syms, n, &fsym, &ffreq, &k, nt);
     if (rc) return fail(err, cap, rc, "out of memory");
     uint8_t* len = malloc(k);
     rc = code_lengths(ffreq, k, len, err, cap);
@@ -267,6 +392,58 @@ static int huffman_encode_impl(const uint32_t* syms, uint64_t n, uint32_t* book_
     uint8_t* out = calloc((size_t)((total_bits + 7) / 8) + 1, 1);
     uint64_t pos = 0;
     uint64_t prev_sym_idx = 0;
+    const uint32_t mxs = fsym[k - 1];
+    uint64_t* dcode = NULL;
+    uint8_t* dlen = NULL;
+    if (nt > 1 && mxs < (1u << 26)) {
+        dcode = calloc((size_t)mxs + 1, sizeof(uint64_t));
+        dlen = calloc((size_t)mxs + 1, 1);
+    }
+    if (dcode && dlen) {
+        /* threaded packing: per-range bit counts, exclusive prefix, private aligned
+         * buffers OR-ed into the stream in range order (bytes shared by two ranges
+         * receive both ranges' bits) */
+        for (uint64_t i = 0; i < k; ++i) {
+            dcode[fsym[i]] = code_of[i];
+            dlen[fsym[i]] = len_of[i];
+        }
+        uint64_t start[256], nbits[256];
+        uint8_t* local[256] = {0};
+        int ntt = nt > 256 ? 256 : nt;
+        pack_job pj = {syms, n, dcode, dlen, start, nbits, local, 0, 0};
+        run_threads(pack_range, &pj, ntt);
+        uint64_t acc = 0;
+        for (int t = 0; t < ntt; ++t) {
+            start[t] = acc;
+            acc += nbits[t];
+        }
+        pj.pass = 1;
+        run_threads(pack_range, &pj, ntt);
+        for (int t = 0; t < ntt; ++t) {
+            if (local[t]) {
+                const uint64_t b0 = start[t] >> 3;
+                const uint64_t nb = ((start[t] & 7) + nbits[t] + 7) / 8;
+                for (uint64_t i = 0; i < nb; ++i) out[b0 + i] |= local[t][i];
+            }
+            free(local[t]);
+        }
+        pos = acc;
+        free(dcode);
+        free(dlen);
+        if (pj.nomem) {
+            free(out);
+            free(fsym);
+            free(ffreq);
+            free(len);
+            free(book);
+            free(codes);
+            free(code_of);
+            free(len_of);
+            return fail(err, cap, E_NOMEM, "out of memory");
+        }
+    } else {
+    free(dcode);
+    free(dlen);
     for (uint64_t i = 0; i < n; ++i) {
         uint32_t s = syms[i];
         uint64_t j;
@@ -285,6 +462,7 @@ static int huffman_encode_impl(const uint32_t* syms, uint64_t n, uint32_t* book_
         int l = len_of[j];
         for (int b = l - 1; b >= 0; --b, ++pos)
             if ((code >> b) & 1) out[pos >> 3] |= (uint8_t)(0x80u >> (pos & 7));
+    }
     }
     *book_size = (uint32_t)k;
     *book_sym = malloc(sizeof(uint32_t) * k);
@@ -309,7 +487,7 @@ int oracle_huffman_encode(const uint32_t* syms, uint64_t n, uint32_t* book_size,
                           uint32_t** book_sym, uint8_t** book_len, uint8_t** bits,
                           uint64_t* bit_length, char* err, int errcap) {
     return huffman_encode_impl(syms, n, book_size, book_sym, book_len, bits, bit_length, err,
-                               errcap);
+                               errcap, 1);
 }
 
 /* ref src/huffman.cpp:137-189 (huffman_decode), bit-serial canonical decode. */
@@ -403,40 +581,49 @@ static uint64_t r_uint(rbuf* r, int bytes) {
 
 /* ------------------------------------------------------------------ codec ---- */
 
-/* ref src/codec.cpp:61-120 (compress) + :177-199 (blob_to_bytes) */
-int oracle_compress(const float* x, const uint64_t* shape, int rank, double eb,
-                    uint32_t radius, int predictor, oracle_result* res, char* err, int cap) {
-    memset(res, 0, sizeof(*res));
-    /* Tensor construction (ref include/acz/tensor.hpp:27-34,58-73) runs before compress */
-    uint64_t n = rank == 0 ? 0 : 1;
-    for (int i = 0; i < rank; ++i) {
-        if (shape[i] == 0) return fail(err, cap, E_SHAPE, "tensor extents must be positive");
-        n *= shape[i];
-    }
-    for (uint64_t i = 0; i < n; ++i)
-        if (!isfinite(x[i])) return fail(err, cap, E_DOMAIN, "tensor element is not finite");
-    if (predictor != 0 && predictor != 1) return fail(err, cap, E_PARAM, "unknown predictor");
-    int rc = validate_params(eb, radius, err, cap);
-    if (rc) return rc;
-    if (n == 0) return fail(err, cap, E_DOMAIN, "compress: empty tensor");
-
-    const double step = 2.0 * eb;
-    const int64_t R = radius;
+/* The quantise loop of ref src/codec.cpp:76-104 over planes [pl0, pl1): symbols, chain
+ * values and this range's outliers (flat order). Planes are independent (the predictor
+ * resets at every plane start, src/codec.cpp:17-20), so ranges run on separate threads and
+ * their outlier lists concatenate in range order. */
+typedef struct {
+    const float* x;
     uint64_t planes, rows, cols;
-    plane_view(shape, rank, &planes, &rows, &cols);
+    double eb;
+    int64_t R;
+    int predictor;
+    uint32_t* symbols;
+    float* recon_all;
+    struct qpart {
+        uint64_t n_out, ocap;
+        uint64_t* oidx;
+        float* oval;
+        int nomem;
+    } part[256];
+} quant_job;
+
+static void quantise_range(void* p, int t, int nt) {
+    quant_job* j = (quant_job*)p;
+    struct qpart* o = &j->part[t];
+    uint64_t pl0, pl1;
+    split(j->planes, t, nt, &pl0, &pl1);
+    const uint64_t rows = j->rows, cols = j->cols;
+    const double eb = j->eb, step = 2.0 * eb;
+    const int64_t R = j->R;
     float* recon = malloc(sizeof(float) * rows * cols);
-    res->n = n;
-    res->symbols = malloc(sizeof(uint32_t) * n);
-    res->recon = malloc(sizeof(float) * n);
-    uint64_t ocap = 16;
-    res->out_index = malloc(sizeof(uint64_t) * ocap);
-    res->out_value = malloc(sizeof(float) * ocap);
-    uint64_t flat = 0;
-    for (uint64_t pl = 0; pl < planes; ++pl) {
+    o->ocap = 16;
+    o->oidx = malloc(sizeof(uint64_t) * o->ocap);
+    o->oval = malloc(sizeof(float) * o->ocap);
+    if (!recon || !o->oidx || !o->oval) {
+        o->nomem = 1;
+        free(recon);
+        return;
+    }
+    uint64_t flat = pl0 * rows * cols;
+    for (uint64_t pl = pl0; pl < pl1; ++pl) {
         for (uint64_t r = 0; r < rows; ++r) {
             for (uint64_t c = 0; c < cols; ++c, ++flat) {
-                const double orig = x[flat];
-                const double pred = predict(predictor, recon, cols, r, c);
+                const double orig = j->x[flat];
+                const double pred = predict(j->predictor, recon, cols, r, c);
                 const double q = round((orig - pred) / step); /* ties away from zero */
                 float value;
                 uint32_t sym = 0;
@@ -446,29 +633,120 @@ int oracle_compress(const float* x, const uint64_t* shape, int rank, double eb,
                         sym = (uint32_t)((int64_t)q + R);
                         value = cand;
                     } else {
-                        value = x[flat];
+                        value = j->x[flat];
                     }
                 } else {
-                    value = x[flat];
+                    value = j->x[flat];
                 }
                 if (sym == 0) {
-                    if (res->n_outliers == ocap) {
-                        ocap *= 2;
-                        res->out_index = realloc(res->out_index, sizeof(uint64_t) * ocap);
-                        res->out_value = realloc(res->out_value, sizeof(float) * ocap);
+                    if (o->n_out == o->ocap) {
+                        o->ocap *= 2;
+                        uint64_t* ni = realloc(o->oidx, sizeof(uint64_t) * o->ocap);
+                        float* nv = realloc(o->oval, sizeof(float) * o->ocap);
+                        if (ni) o->oidx = ni;
+                        if (nv) o->oval = nv;
+                        if (!ni || !nv) {
+                            o->nomem = 1;
+                            free(recon);
+                            return;
+                        }
                     }
-                    res->out_index[res->n_outliers] = flat;
-                    res->out_value[res->n_outliers++] = x[flat];
+                    o->oidx[o->n_out] = flat;
+                    o->oval[o->n_out++] = j->x[flat];
                 }
-                res->symbols[flat] = sym;
-                res->recon[flat] = value;
+                j->symbols[flat] = sym;
+                j->recon_all[flat] = value;
                 recon[r * cols + c] = value;
             }
         }
     }
     free(recon);
+}
+
+typedef struct {
+    const float* x;
+    uint64_t n;
+    int bad[256];
+} finite_job;
+static void finite_range(void* p, int t, int nt) {
+    finite_job* j = (finite_job*)p;
+    uint64_t a, b;
+    split(j->n, t, nt, &a, &b);
+    for (uint64_t i = a; i < b; ++i)
+        if (!isfinite(j->x[i])) {
+            j->bad[t] = 1;
+            return;
+        }
+}
+
+/* ref src/codec.cpp:61-120 (compress) + :177-199 (blob_to_bytes); nt threads */
+static int compress_impl(const float* x, const uint64_t* shape, int rank, double eb,
+                         uint32_t radius, int predictor, oracle_result* res, char* err, int cap,
+                         int nt) {
+    memset(res, 0, sizeof(*res));
+    if (nt < 1) nt = 1;
+    if (nt > 256) nt = 256;
+    /* Tensor construction (ref include/acz/tensor.hpp:27-34,58-73) runs before compress */
+    uint64_t n = rank == 0 ? 0 : 1;
+    for (int i = 0; i < rank; ++i) {
+        if (shape[i] == 0) return fail(err, cap, E_SHAPE, "tensor extents must be positive");
+        n *= shape[i];
+    }
+    {
+        finite_job* fj = calloc(1, sizeof(finite_job));
+        if (!fj) return fail(err, cap, E_NOMEM, "out of memory");
+        fj->x = x;
+        fj->n = n;
+        run_threads(finite_range, fj, nt);
+        int bad = 0;
+        for (int t = 0; t < nt; ++t) bad |= fj->bad[t];
+        free(fj);
+        if (bad) return fail(err, cap, E_DOMAIN, "tensor element is not finite");
+    }
+    if (predictor != 0 && predictor != 1) return fail(err, cap, E_PARAM, "unknown predictor");
+    int rc = validate_params(eb, radius, err, cap);
+    if (rc) return rc;
+    if (n == 0) return fail(err, cap, E_DOMAIN, "compress: empty tensor");
+
+    uint64_t planes, rows, cols;
+    plane_view(shape, rank, &planes, &rows, &cols);
+    res->n = n;
+    res->symbols = malloc(sizeof(uint32_t) * n);
+    res->recon = malloc(sizeof(float) * n);
+    quant_job* qj = calloc(1, sizeof(quant_job));
+    if (!res->symbols || !res->recon || !qj) {
+        free(qj);
+        return fail(err, cap, E_NOMEM, "out of memory");
+    }
+    *qj = (quant_job){.x = x, .planes = planes, .rows = rows, .cols = cols, .eb = eb,
+                      .R = radius, .predictor = predictor, .symbols = res->symbols,
+                      .recon_all = res->recon};
+    const int qt = (uint64_t)nt > planes ? (int)planes : nt;
+    run_threads(quantise_range, qj, qt);
+    uint64_t total = 0;
+    int nomem = 0;
+    for (int t = 0; t < qt; ++t) {
+        total += qj->part[t].n_out;
+        nomem |= qj->part[t].nomem;
+    }
+    res->out_index = malloc(sizeof(uint64_t) * (total + 1));
+    res->out_value = malloc(sizeof(float) * (total + 1));
+    for (int t = 0; t < qt; ++t) {
+        if (!nomem && res->out_index && res->out_value) {
+            memcpy(res->out_index + res->n_outliers, qj->part[t].oidx,
+                   sizeof(uint64_t) * qj->part[t].n_out);
+            memcpy(res->out_value + res->n_outliers, qj->part[t].oval,
+                   sizeof(float) * qj->part[t].n_out);
+            res->n_outliers += qj->part[t].n_out;
+        }
+        free(qj->part[t].oidx);
+        free(qj->part[t].oval);
+    }
+    free(qj);
+    if (nomem || !res->out_index || !res->out_value)
+        return fail(err, cap, E_NOMEM, "out of memory");
     rc = huffman_encode_impl(res->symbols, n, &res->book_size, &res->book_sym, &res->book_len,
-                             &res->bits, &res->bit_length, err, cap);
+                             &res->bits, &res->bit_length, err, cap, nt);
     if (rc) return rc;
     if (res->book_size > 0xFFFF)
         return fail(err, cap, E_FORMAT,
@@ -500,6 +778,17 @@ int oracle_compress(const float* x, const uint64_t* shape, int rank, double eb,
     res->blob = w.p;
     res->blob_size = w.n;
     return OK;
+}
+
+int oracle_compress(const float* x, const uint64_t* shape, int rank, double eb,
+                    uint32_t radius, int predictor, oracle_result* res, char* err, int cap) {
+    return compress_impl(x, shape, rank, eb, radius, predictor, res, err, cap, 1);
+}
+
+int oracle_compress_mt(const float* x, const uint64_t* shape, int rank, double eb,
+                       uint32_t radius, int predictor, int threads, oracle_result* res,
+                       char* err, int cap) {
+    return compress_impl(x, shape, rank, eb, radius, predictor, res, err, cap, threads);
 }
 
 void oracle_result_free(oracle_result* res) {

@@ -42,6 +42,12 @@ typedef struct {
 
 int oracle_compress(const float* x, const uint64_t* shape, int rank, double eb,
                     uint32_t radius, int predictor, oracle_result* res, char* err, int errcap);
+/* Same outputs as oracle_compress (byte for byte), computed on `threads` threads: planes
+ * quantised in contiguous ranges, counts per range, bit packing per symbol range. For the
+ * full-size parity tests (hundreds of millions of elements). */
+int oracle_compress_mt(const float* x, const uint64_t* shape, int rank, double eb,
+                       uint32_t radius, int predictor, int threads, oracle_result* res,
+                       char* err, int errcap);
 void oracle_result_free(oracle_result* res);
 
 /* ACZ1 bytes -> n floats. recon_out (optional) receives the unfiltered chain values. */

@@ -86,6 +86,9 @@ class Oracle:
         L.oracle_compress.argtypes = [_f32p, _u64p, C.c_int, C.c_double, C.c_uint32, C.c_int,
                                       C.POINTER(_oracle_result), C.c_char_p, C.c_int]
         L.oracle_result_free.argtypes = [C.POINTER(_oracle_result)]
+        L.oracle_compress_mt.argtypes = [_f32p, _u64p, C.c_int, C.c_double, C.c_uint32,
+                                         C.c_int, C.c_int, C.POINTER(_oracle_result),
+                                         C.c_char_p, C.c_int]
         L.oracle_decompress.argtypes = [_u8p, C.c_uint64, C.c_int, _f32p, C.c_uint64,
                                         C.c_char_p, C.c_int]
         L.oracle_huffman_encode.argtypes = [_u32p, C.c_uint64, C.POINTER(C.c_uint32),
@@ -126,6 +129,37 @@ class Oracle:
                 blob=bytes(_copy(res.blob, res.blob_size, np.uint8)))
         finally:
             self.L.oracle_result_free(C.byref(res))
+
+    def compress_mt(self, x: np.ndarray, eb: float, radius: int = 32768, predictor: int = 0,
+                    threads: Optional[int] = None, symbols: bool = False):
+        """oracle_compress on `threads` host threads (same bytes as compress(); the plane
+        ranges, counts and bit packing are split and joined in order). Returns
+        (ACZ1 blob bytes, chain values float32 [n], symbols uint32 [n] or None). The chain
+        values are what decompress reconstructs (ref src/codec.cpp:153-161 repeats the
+        compressor's expression), so filter(recon) is the decompressed output."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        shp = np.asarray(x.shape, dtype=np.uint64)
+        res = _oracle_result()
+        err = C.create_string_buffer(512)
+        nt = threads or min(64, os.cpu_count() or 1)
+        rc = self.L.oracle_compress_mt(_ptr(x, _f32p), _ptr(shp, _u64p), len(shp), eb, radius,
+                                       predictor, nt, C.byref(res), err, 512)
+        try:
+            if rc:
+                raise OracleError(rc, err.value.decode())
+            blob = np.ctypeslib.as_array(res.blob, shape=(res.blob_size,)).tobytes()
+            recon = _copy(res.recon, res.n, np.float32)
+            syms = _copy(res.symbols, res.n, np.uint32) if symbols else None
+            return blob, recon, syms
+        finally:
+            self.L.oracle_result_free(C.byref(res))
+
+    @staticmethod
+    def zero_filter(recon: np.ndarray, eb: float) -> np.ndarray:
+        """ref src/codec.cpp:162-164: |(double)v| <= eb -> 0.0f (on the chain values)."""
+        out = recon.copy()
+        out[np.abs(recon.astype(np.float64)) <= eb] = 0.0
+        return out
 
     def decompress(self, blob: bytes, n: int, zero_filter: bool = False) -> np.ndarray:
         b = np.frombuffer(blob, dtype=np.uint8).copy()
@@ -263,6 +297,37 @@ class Reference:
             raise OracleError(rc, err.value.decode())
         out = bytes(_copy(p, sz.value, np.uint8))
         self.L.ref_free(C.cast(p, C.c_void_p))
+        return out
+
+    def compress_mt(self, x: np.ndarray, eb: float, radius: int = 32768, predictor: int = 0,
+                    threads: Optional[int] = None, symbols: bool = False):
+        """oracle_compress on `threads` host threads (same bytes as compress(); the plane
+        ranges, counts and bit packing are split and joined in order). Returns
+        (ACZ1 blob bytes, chain values float32 [n], symbols uint32 [n] or None). The chain
+        values are what decompress reconstructs (ref src/codec.cpp:153-161 repeats the
+        compressor's expression), so filter(recon) is the decompressed output."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        shp = np.asarray(x.shape, dtype=np.uint64)
+        res = _oracle_result()
+        err = C.create_string_buffer(512)
+        nt = threads or min(64, os.cpu_count() or 1)
+        rc = self.L.oracle_compress_mt(_ptr(x, _f32p), _ptr(shp, _u64p), len(shp), eb, radius,
+                                       predictor, nt, C.byref(res), err, 512)
+        try:
+            if rc:
+                raise OracleError(rc, err.value.decode())
+            blob = np.ctypeslib.as_array(res.blob, shape=(res.blob_size,)).tobytes()
+            recon = _copy(res.recon, res.n, np.float32)
+            syms = _copy(res.symbols, res.n, np.uint32) if symbols else None
+            return blob, recon, syms
+        finally:
+            self.L.oracle_result_free(C.byref(res))
+
+    @staticmethod
+    def zero_filter(recon: np.ndarray, eb: float) -> np.ndarray:
+        """ref src/codec.cpp:162-164: |(double)v| <= eb -> 0.0f (on the chain values)."""
+        out = recon.copy()
+        out[np.abs(recon.astype(np.float64)) <= eb] = 0.0
         return out
 
     def decompress(self, blob: bytes, n: int, zero_filter: bool = False) -> np.ndarray:

@@ -12,10 +12,12 @@
 //   acz::compression_ratio include/acz/codec.hpp:61          compression_ratio(blob)
 //   acz::blob_to_bytes / blob_from_bytes  :69-70             CompressedTensor::bytes / blob_from_bytes
 //   acz::nonzero_ratio / mean_abs  include/acz/tensor.hpp:82-99   nonzero_ratio / mean_abs (device)
-//   acz::Controller       include/acz/controller.hpp:99-155  Controller (device activations)
 //
 // Device-resident activations (the training path) go through DeviceTensor / DeviceBlob;
 // host tensors (the reference's own calling convention) through Tensor / CompressedTensor.
+// The reference's Controller is not restated here: the proj/core drop-in
+// (proj_core/gpu_codec.cpp replacing src/codec.cpp) runs the reference's own
+// src/controller.cpp over the GPU codec (oracle/Makefile `dropin`, tests/test_gpu_dropin.py).
 #pragma once
 
 #include <algorithm>
@@ -326,270 +328,6 @@ inline uint64_t nonzero_count(const DeviceTensor& t, Context& ctx, void* stream 
     ctx.check(acz_gpu_zero_bitmap(ctx.get(), t.data(), t.size(), nullptr, &nz, stream));
     return nz;
 }
-
-// ------------------------------------------------------ controller (controller.hpp) --
-enum class ZeroRestoration { CodecFilter, ReluRecompute };
-
-struct ControllerConfig {
-    int64_t collect_interval = 1000;  // W
-    double sigma_fraction = 0.01;
-    double coefficient_a = 0.32;
-    double eb_min = 1e-8;
-    double eb_max = 1e-1;
-    ZeroRestoration zero_restoration = ZeroRestoration::CodecFilter;
-    Predictor predictor = Predictor::PrevValue;
-    uint32_t quant_radius = 32768;
-
-    // ref src/controller.cpp:14-21
-    void validate() const {
-        if (collect_interval < 1) throw ParamError("collect_interval (W) must be >= 1");
-        if (!(sigma_fraction > 0.0)) throw ParamError("sigma_fraction must be positive");
-        if (!(coefficient_a > 0.0)) throw ParamError("coefficient_a must be positive");
-        if (!(eb_min > 0.0) || !(eb_min <= eb_max))
-            throw ParamError("error-bound clamps must satisfy 0 < eb_min <= eb_max");
-        CodecParams{eb_min, quant_radius, predictor}.validate();
-    }
-};
-
-struct LayerStats {
-    int layer_id = -1;
-    double l_bar = 0.0;
-    double r = 0.0;
-    double m_avg = 0.0;
-    size_t batch = 0;
-    int64_t collected_at = -1;
-    bool degenerate = false;
-};
-
-struct LedgerRecord {
-    int64_t iteration;
-    int layer_id;
-    double eb, predicted_sigma, l_bar, r, m_avg, ratio;
-    bool fallback;
-};
-
-class CompressionLedger {
-public:
-    void append(const LedgerRecord& r) { records_.push_back(r); }
-    const std::vector<LedgerRecord>& records() const { return records_; }
-    // ref src/controller.cpp:67-76 (same header and %.17g formatting)
-    std::string to_csv() const {
-        std::string out = "iteration,layer,eb,predicted_sigma,L_bar,R,M_avg,ratio,fallback_flag\n";
-        char line[256];
-        for (const auto& r : records_) {
-            std::snprintf(line, sizeof(line), "%lld,%d,%.17g,%.17g,%.17g,%.17g,%.17g,%.17g,%d\n",
-                          (long long)r.iteration, r.layer_id, r.eb, r.predicted_sigma, r.l_bar,
-                          r.r, r.m_avg, r.ratio, r.fallback ? 1 : 0);
-            out += line;
-        }
-        return out;
-    }
-
-private:
-    std::vector<LedgerRecord> records_;
-};
-
-// Stashed activation: exactly one of raw / blob engaged (ref include/acz/controller.hpp:65-78).
-struct ActivationHandle {
-    std::optional<DeviceTensor> raw;
-    std::optional<DeviceBlob> blob;
-    bool apply_relu = false;
-    bool zero_filter = false;
-    int layer_id = -1;
-    size_t held_bytes = 0;
-    double achieved_ratio = 1.0;
-};
-
-// Sums that make the controller statistics global across data-parallel ranks. The local
-// sums are reduced by `reducer` (e.g. one ncclAllReduce of 7 doubles per layer every W
-// iterations) before the ratios are formed; single process: identity.
-using StatsReducer = std::function<void(double* sums, size_t count)>;
-
-// Four-phase adaptive scheme (ref src/controller.cpp:94-253) over device activations.
-class Controller {
-public:
-    Controller(const ControllerConfig& cfg, int num_layers, Context& ctx = Context::thread_default())
-        : cfg_(cfg), ctx_(&ctx) {
-        cfg_.validate();
-        if (num_layers < 0) throw ParamError("controller needs a non-negative layer count");
-        windows_.resize((size_t)num_layers);
-    }
-    void set_stats_reducer(StatsReducer r) { reducer_ = std::move(r); }
-
-    void begin_iteration(int64_t iteration) {
-        if (iteration < 0) throw ParamError("iteration must be >= 0");
-        iteration_ = iteration;
-    }
-    int64_t iteration() const { return iteration_; }
-    bool collecting() const { return iteration_ % cfg_.collect_interval == 0; }
-
-    // Phase 1 (ref src/controller.cpp:124-152). L_bar and M_avg are means of |.|, R the
-    // nonzero fraction; with a reducer they are global over ranks (sums then ratios).
-    LayerStats collect_stats(int layer, const DeviceTensor& activation, const DeviceTensor& loss,
-                             const DeviceTensor& momentum, size_t batch, void* stream = nullptr) {
-        if (layer < 0 || (size_t)layer >= windows_.size())
-            throw ParamError("collect_stats: unknown layer id");
-        if (!collecting()) throw ParamError("collect_stats invoked outside a collection iteration");
-        double sums[7] = {mean_abs(loss, *ctx_, stream) * (double)loss.size(), (double)loss.size(),
-                          (double)nonzero_count(activation, *ctx_, stream),
-                          (double)activation.size(),
-                          mean_abs(momentum, *ctx_, stream) * (double)momentum.size(),
-                          (double)momentum.size(), (double)batch};
-        if (reducer_) reducer_(sums, 7);
-        LayerStats st;
-        st.layer_id = layer;
-        st.l_bar = sums[1] > 0 ? sums[0] / sums[1] : 0.0;
-        st.r = sums[3] > 0 ? sums[2] / sums[3] : 0.0;
-        st.m_avg = sums[5] > 0 ? sums[4] / sums[5] : 0.0;
-        st.batch = (size_t)sums[6];
-        st.collected_at = iteration_;
-        st.degenerate = st.l_bar == 0.0 || st.m_avg == 0.0 || st.r == 0.0;
-        close_window(layer);
-        Window& w = windows_[(size_t)layer];
-        w = Window{};
-        w.stats = st;
-        w.open = true;
-        if (!st.degenerate) {
-            w.sigma = target_sigma(st, cfg_);
-            w.eb = compute_error_bound(st, w.sigma, cfg_);
-            w.fallback = false;
-        }
-        return st;
-    }
-
-    // Phase 2 (ref src/controller.cpp:154-157)
-    static double target_sigma(const LayerStats& s, const ControllerConfig& cfg) {
-        if (!(s.m_avg > 0.0)) throw ParamError("target_sigma: degenerate M_avg");
-        return cfg.sigma_fraction * s.m_avg;
-    }
-    // Phase 3 (ref src/controller.cpp:159-168): eb = sigma / (a * L_bar * sqrt(N * R)), clamped
-    static double compute_error_bound(const LayerStats& s, double sigma, const ControllerConfig& cfg) {
-        if (!(sigma > 0.0)) throw ParamError("compute_error_bound: sigma must be positive");
-        if (!(s.l_bar > 0.0) || !(s.r > 0.0)) throw ParamError("compute_error_bound: degenerate stats");
-        const double eb = sigma / (cfg.coefficient_a * s.l_bar * std::sqrt((double)s.batch * s.r));
-        return std::clamp(eb, cfg.eb_min, cfg.eb_max);
-    }
-
-    bool layer_active(int layer) const {
-        if (layer < 0 || (size_t)layer >= windows_.size()) return false;
-        const Window& w = windows_[(size_t)layer];
-        return w.open && !w.fallback && iteration_ > w.stats.collected_at;
-    }
-    double layer_eb(int layer) const { return layer_active(layer) ? windows_[(size_t)layer].eb : 0.0; }
-    const LayerStats* layer_stats(int layer) const {
-        if (layer < 0 || (size_t)layer >= windows_.size()) return nullptr;
-        const Window& w = windows_[(size_t)layer];
-        return w.open ? &w.stats : nullptr;
-    }
-
-    // Phase 4, forward (ref src/controller.cpp:194-232): compress on the GPU or pass through;
-    // a codec failure degrades to pass-through with a warning.
-    ActivationHandle wrap_forward(int layer, DeviceTensor&& act, bool is_post_relu,
-                                  void* stream = nullptr) {
-        if (layer < 0 || (size_t)layer >= windows_.size())
-            throw ParamError("wrap_forward: unknown layer id");
-        const uint64_t in_bytes = 4ull * act.size();
-        ActivationHandle h;
-        h.layer_id = layer;
-        auto pass = [&]() {
-            h.held_bytes = in_bytes;
-            h.raw = std::move(act);
-            h.achieved_ratio = 1.0;
-        };
-        if (!layer_active(layer)) {
-            pass();
-        } else {
-            const Window& w = windows_[(size_t)layer];
-            try {
-                CodecParams params{w.eb, cfg_.quant_radius, cfg_.predictor};
-                DeviceBlob b = compress(act, params, *ctx_, stream);
-                h.held_bytes = b.compressed_bytes();
-                h.achieved_ratio = b.ratio();
-                if (cfg_.zero_restoration == ZeroRestoration::ReluRecompute && is_post_relu)
-                    h.apply_relu = true;
-                else
-                    h.zero_filter = true;
-                h.blob = std::move(b);
-                act.reset();  // release the original buffer
-            } catch (const Error& e) {
-                std::cerr << "warning: compression failed for layer " << layer << " (" << e.what()
-                          << "); passing through\n";
-                pass();
-            }
-        }
-        Window& w = windows_[(size_t)layer];
-        if (w.open) {
-            w.bytes_in += in_bytes;
-            w.bytes_stored += h.held_bytes;
-        }
-        total_in_ += in_bytes;
-        total_stored_ += h.held_bytes;
-        current_bytes_ += h.held_bytes;
-        peak_bytes_ = std::max(peak_bytes_, current_bytes_);
-        return h;
-    }
-
-    // Phase 4, backward (ref src/controller.cpp:234-249)
-    DeviceTensor unwrap_backward(ActivationHandle& h, void* stream = nullptr) {
-        if (h.raw) {
-            DeviceTensor t = std::move(*h.raw);
-            h.raw.reset();
-            current_bytes_ -= h.held_bytes;
-            h.held_bytes = 0;
-            return t;
-        }
-        if (!h.blob) throw ParamError("unwrap_backward: handle already consumed");
-        DeviceTensor t = decompress(*h.blob, h.zero_filter, *ctx_, stream);
-        if (h.apply_relu) ctx_->check(acz_gpu_relu(ctx_->get(), t.data(), t.size(), stream));
-        h.blob.reset();
-        current_bytes_ -= h.held_bytes;
-        h.held_bytes = 0;
-        return t;
-    }
-
-    void finalize() {
-        for (size_t i = 0; i < windows_.size(); ++i) close_window((int)i);
-    }
-    const CompressionLedger& ledger() const { return ledger_; }
-    size_t current_stash_bytes() const { return current_bytes_; }
-    size_t peak_stash_bytes() const { return peak_bytes_; }
-    uint64_t total_bytes_in() const { return total_in_; }
-    uint64_t total_bytes_stored() const { return total_stored_; }
-
-private:
-    struct Window {
-        LayerStats stats;
-        double eb = 0.0, sigma = 0.0;
-        bool fallback = true, open = false;
-        uint64_t bytes_in = 0, bytes_stored = 0;
-    };
-    // ref src/controller.cpp:98-122
-    void close_window(int layer) {
-        Window& w = windows_[(size_t)layer];
-        if (!w.open) return;
-        LedgerRecord r;
-        r.iteration = w.stats.collected_at;
-        r.layer_id = layer;
-        r.eb = w.fallback ? 0.0 : w.eb;
-        r.predicted_sigma = w.fallback ? 0.0 : w.sigma;
-        r.l_bar = w.stats.l_bar;
-        r.r = w.stats.r;
-        r.m_avg = w.stats.m_avg;
-        r.ratio = w.bytes_stored == 0 ? 1.0 : (double)w.bytes_in / (double)w.bytes_stored;
-        r.fallback = w.fallback;
-        ledger_.append(r);
-        w.open = false;
-    }
-
-    ControllerConfig cfg_;
-    Context* ctx_;
-    StatsReducer reducer_;
-    std::vector<Window> windows_;
-    CompressionLedger ledger_;
-    int64_t iteration_ = 0;
-    size_t current_bytes_ = 0, peak_bytes_ = 0;
-    uint64_t total_in_ = 0, total_stored_ = 0;
-};
 
 // Batch-size scheme (BASELINE config 5; the reference leaves it as a non-goal, SPEC.md:431,
 // PAPER.md:531-533): the largest batch whose stashed bytes fit the activation budget, given

@@ -94,65 +94,6 @@ int main(int argc, char** argv) {
     CHECK(dd.data == d1.data);
     CHECK(std::fabs(nonzero_ratio(dt, ctx) - 0.5) < 0.01);
 
-    // ---- controller (ref src/controller.cpp) ----
-    ControllerConfig cfg;
-    cfg.collect_interval = 2;
-    Controller ctl(cfg, 2, ctx);
-    CHECK(throws<ParamError>([&] { Controller(ControllerConfig{0}, 1, ctx); }));
-    Tensor loss = relu_tensor({4, 16, 56, 56}, 7), mom = relu_tensor({64, 16, 3, 3}, 8);
-    for (auto& v : loss.data) v *= 1e-3f;
-    for (auto& v : mom.data) v *= 1e-2f;
-    DeviceTensor dl = DeviceTensor::from_host(loss, ctx), dm = DeviceTensor::from_host(mom, ctx);
-    ctl.begin_iteration(0);
-    CHECK(ctl.collecting());
-    LayerStats st = ctl.collect_stats(0, dt, dl, dm, 4);
-    CHECK(!st.degenerate);
-    double la = 0, ma = 0;
-    size_t nz = 0;
-    for (float v : loss.data) la += std::fabs((double)v);
-    for (float v : mom.data) ma += std::fabs((double)v);
-    for (float v : t.data) nz += v != 0.0f;
-    la /= loss.size();
-    ma /= mom.size();
-    CHECK(std::fabs(st.l_bar - la) <= 1e-12 * la);
-    CHECK(std::fabs(st.m_avg - ma) <= 1e-12 * ma);
-    CHECK(st.r == (double)nz / (double)t.size());
-    const double sigma = cfg.sigma_fraction * st.m_avg;
-    const double eb_expect =
-        std::clamp(sigma / (cfg.coefficient_a * st.l_bar * std::sqrt(4.0 * st.r)), cfg.eb_min, cfg.eb_max);
-    CHECK(!ctl.layer_active(0));  // the collection iteration itself runs uncompressed
-    ctl.begin_iteration(1);
-    CHECK(ctl.layer_active(0) && !ctl.layer_active(1));
-    CHECK(std::fabs(ctl.layer_eb(0) - eb_expect) <= 1e-15 * eb_expect);
-    {
-        DeviceTensor a = DeviceTensor::from_host(t, ctx);
-        ActivationHandle h = ctl.wrap_forward(0, std::move(a), true);
-        CHECK(h.blob.has_value() && !h.raw.has_value() && a.empty());
-        CHECK(ctl.current_stash_bytes() == h.held_bytes && h.achieved_ratio > 1.0);
-        Tensor back = ctl.unwrap_backward(h).to_host();
-        for (size_t i = 0; i < t.size(); ++i)
-            CHECK(std::fabs((double)t.data[i] - (double)back.data[i]) <= 2 * ctl.layer_eb(0));
-        CHECK(ctl.current_stash_bytes() == 0);
-        CHECK(throws<ParamError>([&] { ctl.unwrap_backward(h); }));
-        DeviceTensor a2 = DeviceTensor::from_host(t, ctx);
-        ActivationHandle h2 = ctl.wrap_forward(1, std::move(a2), true);  // inactive: pass-through
-        CHECK(h2.raw.has_value() && h2.held_bytes == 4 * t.size());
-        ctl.unwrap_backward(h2);
-    }
-    ctl.finalize();
-    CHECK(ctl.ledger().records().size() == 1);
-    CHECK(ctl.ledger().to_csv().rfind("iteration,layer,eb,predicted_sigma,L_bar,R,M_avg,ratio,fallback_flag\n", 0) == 0);
-    // distributed statistics: two identical ranks (sums doubled) -> same ratios, batch 2N
-    Controller ctl2(cfg, 1, ctx);
-    ctl2.set_stats_reducer([](double* s, size_t n) {
-        for (size_t i = 0; i < n; ++i) s[i] *= 2.0;
-    });
-    ctl2.begin_iteration(0);
-    LayerStats s2 = ctl2.collect_stats(0, dt, dl, dm, 4);
-    CHECK(s2.batch == 8 && std::fabs(s2.l_bar - st.l_bar) <= 1e-15 * st.l_bar && s2.r == st.r);
-    ctl2.begin_iteration(1);
-    CHECK(std::fabs(ctl2.layer_eb(0) * std::sqrt(2.0) - ctl.layer_eb(0)) <= 1e-12 * ctl.layer_eb(0) ||
-          ctl.layer_eb(0) == 0.0);
     // batch-size scheme
     CHECK(suggest_batch(256, 1000u << 20, 4000u << 20) == 1024);
 
@@ -160,7 +101,6 @@ int main(int argc, char** argv) {
         std::fprintf(stderr, "%d check(s) failed\n", fails);
         return 1;
     }
-    std::printf("cpp host layer OK: ratio %.3f, max err %.3g, eb %.3g\n", compression_ratio(c), maxerr,
-                eb_expect);
+    std::printf("cpp host layer OK: ratio %.3f, max err %.3g\n", compression_ratio(c), maxerr);
     return 0;
 }

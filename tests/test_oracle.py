@@ -157,3 +157,26 @@ def test_zero_bitmap_oracle(oracle):
     assert bits == (x != 0).astype(int).tolist()
     assert nz == int((x != 0).sum())
     assert oracle.nonzero_ratio(x) == nz / x.size
+
+
+def test_oracle_mt_equals_serial(oracle):
+    """oracle_compress_mt (the full-size parity checker) == oracle_compress byte for byte:
+    ACZ1, chain values and symbols; plane ranges, counts and bit packing split over threads
+    (including more threads than planes, Lorenzo2d, outliers and a > 2^22 symbol range)."""
+    rng = np.random.default_rng(11)
+    cases = [((6, 16, 40, 40), 1e-3, 32768, 0, True), ((2, 3, 97, 131), 1e-3, 32768, 0, False),
+             ((3, 5, 33, 41), 1e-4, 32768, 1, True), ((3, 1000), 1e-2, 32768, 0, True),
+             ((7,), 0.1, 32768, 0, False), ((4, 8, 20, 20), 1e-3, 8, 0, False),
+             ((2, 4, 64, 64), 1e-6, 1 << 24, 0, False)]
+    for shape, eb, radius, pred, relu in cases:
+        x = rng.standard_normal(shape).astype(np.float32)
+        if relu:
+            np.maximum(x, 0, out=x)
+        a = oracle.compress(x, eb, radius, pred)
+        for t in (2, 5, 16):
+            blob, recon, syms = oracle.compress_mt(x, eb, radius, pred, threads=t, symbols=True)
+            assert blob == a.blob, (shape, t)
+            assert np.array_equal(recon.view(np.uint32), a.recon.view(np.uint32)), (shape, t)
+            assert np.array_equal(syms, a.symbols), (shape, t)
+        dec = oracle.decompress(a.blob, x.size, True)
+        assert np.array_equal(dec, oracle.zero_filter(a.recon, eb))
