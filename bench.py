@@ -219,7 +219,10 @@ def run_ours(args, rank, world, local_rank):
         ratios_in += c.uncompressed_bytes
         ratios_out += c.compressed_bytes
 
-    res = dict(value=value, ms_per_step=ms_max / args.steps, n=n_total, cbytes=cbytes,
+    host = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        host = host_set(args, tensors)  # the CPU baseline runs on these exact bytes
+    res = dict(host=host, value=value, ms_per_step=ms_max / args.steps, n=n_total, cbytes=cbytes,
                B_step=8 * n_total + 2 * cbytes, launches=launches, clocks=clk, kernels=kern,
                detail=detail, ratio=ratios_in / ratios_out, batch=batch, per_tensor=per_tensor)
 
@@ -263,29 +266,74 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------------------ CPU reference ----
-def cpu_reference_sample(args, threads=None):
-    """Times the reference CPU codec (oracle/_ref) on a bounded sample of the workload,
-    batch-sharded over `threads` host threads. Returns (GB/s on basis B, detail)."""
-    import numpy as np
+TRAFFIC_JSON = os.path.join("profiles", "r01", "v12", "traffic.json")
+ONE_THREAD_SAMPLES = 16  # 1-thread leg: the first 16 samples of every tensor (~2-3 s)
 
-    from oracle.oracle import Reference
+
+def _cuda() -> bool:
+    import torch
+    return torch.cuda.is_available()
+
+
+def host_set(args, tensors=None):
+    """The GPU arm's exact input bytes on the host: workloads.make_set (torch Philox on
+    cuda:0, seed 20201118 + tensor index) copied down, or the given device tensors."""
+    import torch
     from paper_2011_09017_b200 import workloads as W
+    if tensors is None:
+        batch = args.batch or DEFAULT_BATCH[args.workload]
+        dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+        tensors = [x for _, x in W.make_set(args.workload, batch, device=dev)]
+    return [x.cpu().numpy() for x in tensors]
+
+
+def cpu_reference_sample(args, host, threads=None):
+    """The reference CPU codec (oracle/_ref, compiled from the reference sources) on the
+    whole per-GPU batch of every tensor (the GPU arm's bytes), compress + decompress with the
+    zero filter, batch-sharded into `threads` shards on `threads` host threads (the
+    reference's functions are pure; one codebook per shard).
+    Returns (GB/s on basis B = 8n + 2C, detail)."""
+    from oracle.oracle import Reference
     R = Reference()
     threads = threads or os.cpu_count() or 1
-    batch = args.batch or DEFAULT_BATCH[args.workload]
-    sample = batch  # the full per-GPU batch of every tensor (~1.5 s of 16-thread CPU work)
-    rng = np.random.default_rng(W.SEED)
     tot_B, tot_s, n_tot = 0, 0.0, 0
-    for nm, (c, h, w), relu in W.activation_set(args.workload):
-        x = rng.standard_normal((sample, c, h, w), dtype=np.float32)
-        if relu:
-            np.maximum(x, 0, out=x)
-        cb, sec = R.roundtrip_sharded(x, args.eb, shards=sample, threads=threads)
+    for x in host:
+        cb, sec = R.roundtrip_sharded(x, args.eb, shards=threads, threads=threads)
         tot_B += 8 * x.size + 2 * cb
         tot_s += sec
         n_tot += x.size
-    return tot_B / tot_s / 1e9, {"threads": threads, "samples_per_tensor": sample,
+    return tot_B / tot_s / 1e9, {"threads": threads, "samples_per_tensor": host[0].shape[0],
                                  "elements": n_tot, "seconds": tot_s}
+
+
+def cpu_reference_one_thread(args, host, samples=ONE_THREAD_SAMPLES):
+    """The reference's own usage, one thread: acz::compress + acz::decompress of each
+    (whole, unsharded) tensor of a bounded sample (the first `samples` samples of every
+    tensor, same bytes as the GPU arm). Returns (GB/s on basis B, detail)."""
+    from oracle.oracle import Reference
+    R = Reference()
+    tot_B, tot_s, n_tot = 0, 0.0, 0
+    for x in host:
+        xs = x[:samples]
+        cb, sec = R.roundtrip_sharded(xs, args.eb, shards=1, threads=1)
+        tot_B += 8 * xs.size + 2 * cb
+        tot_s += sec
+        n_tot += xs.size
+    return tot_B / tot_s / 1e9, {"threads": 1, "samples_per_tensor": samples,
+                                 "elements": n_tot, "seconds": tot_s}
+
+
+def cpu_baseline_lines(args, host):
+    v, info = cpu_reference_sample(args, host)
+    v1, info1 = cpu_reference_one_thread(args, host)
+    return {"value": v, "unit": "GB/s", "cores": info["threads"], "kind": "reference",
+            "sample": f"all {info['samples_per_tensor']} samples of every {args.workload} tensor "
+                      f"(the GPU arm's input bytes), {info['threads']} batch shards on "
+                      f"{info['threads']} threads ({info['seconds']:.2f} s)",
+            "one_thread": {"value": v1, "unit": "GB/s", "cores": 1,
+                           "sample": f"first {info1['samples_per_tensor']} samples of every "
+                                     f"tensor, whole-tensor compress+decompress "
+                                     f"({info1['seconds']:.2f} s)"}}
 
 
 def run_reference(args, rank, world):
@@ -296,26 +344,35 @@ def run_reference(args, rank, world):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
     batch = args.batch or DEFAULT_BATCH[args.workload]
+    host = host_set(args)
     vals = []
     info = None
     for i in range(args.warmup + args.steps):
-        v, info = cpu_reference_sample(args)
+        v, info = cpu_reference_sample(args, host)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.mean(vals)
-    peak, kind = load_peaks()
+    v1, info1 = cpu_reference_one_thread(args, host)
     line = {
         "metric": "compress+decompress GB/s per B200 at eb=1e-3 (% of HBM peak); compression ratio",
         "impl": "reference", "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.workload} saved-activation set batch {batch}, eb={args.eb}",
+        "config": {"workload": f"{args.workload} saved-activation set, batch {batch} per GPU, "
+                               f"fp32, eb={args.eb}, zero filter on decompress",
+                   "input": ("the GPU arm's bytes (workloads.make_set, Philox on cuda:0)"
+                             if _cuda() else "workloads.make_set on the CPU generator "
+                                              "(no GPU: not the GPU arm's bytes)"),
                    "sample": f"{info['samples_per_tensor']} samples per tensor per step"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": info["threads"],
                          "kind": "reference",
-                         "sample": f"{info['samples_per_tensor']} samples of each of the "
-                                   f"{args.workload} tensors ({info['elements']} elements), "
-                                   f"batch-sharded over {info['threads']} threads"},
+                         "sample": f"all {info['samples_per_tensor']} samples of every "
+                                   f"{args.workload} tensor ({info['elements']} elements), "
+                                   f"{info['threads']} batch shards on {info['threads']} threads",
+                         "one_thread": {"value": v1, "unit": "GB/s", "cores": 1,
+                                        "sample": f"first {info1['samples_per_tensor']} samples "
+                                                  f"of every tensor, whole-tensor compress + "
+                                                  f"decompress"}},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -361,7 +418,7 @@ def main():
         traffic = None  # measured DRAM bytes of that launch, from the committed ncu capture
         if args.workload == "alexnet" and dnm == "conv1_in" and dom == "quant" and args.eb == EB:
             try:
-                with open(os.path.join(ROOT, "profiles", "r01", "v10", "traffic.json")) as f:
+                with open(os.path.join(ROOT, TRAFFIC_JSON)) as f:
                     traffic = json.load(f)["dram_bytes_per_launch"]
             except Exception:  # noqa: BLE001
                 traffic = None
@@ -381,7 +438,7 @@ def main():
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_kind": kind,
                          "algorithmic_bytes_per_launch": dalg, "launch_ms": dms,
-                         "traffic_source": "profiles/r01/v12/traffic.json (ncu --set full)",
+                         "traffic_source": f"{TRAFFIC_JSON} (ncu --set full)",
                          "roundtrip_frac": res["value"] / world / peak},
             "kernels": kern,
             "kernels_basis": "per class, summed over the tensors each compressed + decompressed "
@@ -394,12 +451,7 @@ def main():
             line["e2e"] = res["e2e"]
         if world == 1 and not args.no_cpu_baseline:
             try:
-                v, info = cpu_reference_sample(args)
-                line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": info["threads"],
-                                        "kind": "reference",
-                                        "sample": f"{info['samples_per_tensor']} samples of each "
-                                                  f"{args.workload} tensor, batch-sharded over "
-                                                  f"{info['threads']} threads ({info['seconds']:.1f} s)"}
+                line["cpu_baseline"] = cpu_baseline_lines(args, res["host"])
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"unavailable": str(e)}
         print(json.dumps(line))
