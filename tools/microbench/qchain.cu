@@ -10,6 +10,28 @@ using namespace acz_b200;
 
 constexpr int N = 256;
 
+// variant P: predicted-quotient step (tools/proto/dchain.c): q from the lattice index,
+// certified off the chain; measured 99 vs 148 cycles/step latency, 139 vs 115 Gstep/s, but
+// slower inside the real kernels (more instructions, more registers): not used
+__device__ __forceinline__ uint32_t pq_fast(double xd, double lam, double& r, int& Kp,
+                                            const QParams& p, bool& ok) {
+    const double M52 = 6755399441055744.0;
+    const double tK = __dmul_rn(__dsub_rn(xd, lam), p.inv_step);
+    const double km = __dadd_rn(tK, M52);
+    const int K = __double2loint(km);
+    const int qi = K - Kp;
+    const double q = __dsub_rn(__dsub_rn(km, M52), (double)Kp);
+    const double w = __dmul_rn(q, p.step);
+    const float cf = __double2float_rn(__dadd_rn(r, w));
+    const double c = (double)cf;
+    const double t = __dmul_rn(__dsub_rn(xd, r), p.inv_step);
+    ok = fabs(__dsub_rn(t, q)) < 0.5 - 0x1p-20 && fabs(tK) < 0x1p30 &&
+         fabs(q) < p.radius_d && fabs(__dsub_rn(xd, c)) <= p.eb && isfinite(cf) && !p.exact_div;
+    r = c;
+    Kp = K;
+    return (uint32_t)(qi + (int)p.R);
+}
+
 // variant B: branchless rn32 (both paths, select)
 __device__ __forceinline__ double rn32d_sel(double y) {
     const int hi = __double2hiint(y);
@@ -63,13 +85,22 @@ __global__ void k_chain(const float* __restrict__ x, uint32_t* sym, QParams p, l
     const int plane = blockIdx.x * 32 + lane;
     for (int i = 0; i < N; ++i) xs[lane][i] = x[(size_t)(plane % nplanes) * N + i];
     __syncwarp();
-    double r = 0.0;
+    double r = 0.0, lam = 0.0;
+    int Kp = 0;
+    bool okall = true;
     uint32_t acc = 0;
     long long t0 = clock64();
     for (int i = 0; i < N; ++i) {
         const float xf = xs[lane][i];
         double v;
         uint32_t s;
+        if (V == 3) {
+            bool ok;
+            s = pq_fast((double)xf, lam, r, Kp, p, ok);
+            okall &= ok;
+            acc = acc * 31 + s;
+            continue;
+        }
         if (V == 0) s = qstep((double)xf, xf, r, p, &v);
         else if (V == 1) s = qstep_B((double)xf, r, p, &v);
         else s = qstep_D((double)xf, r, p, &v);
@@ -77,7 +108,7 @@ __global__ void k_chain(const float* __restrict__ x, uint32_t* sym, QParams p, l
         acc = acc * 31 + s;
     }
     long long t1 = clock64();
-    sym[blockIdx.x * 32 + lane] = acc + (uint32_t)(r * 1000);
+    sym[blockIdx.x * 32 + lane] = acc + (uint32_t)(r * 1000) + okall;
     if (lane == 0 && blockIdx.x == 0) *cyc = t1 - t0;
 }
 
@@ -97,8 +128,8 @@ int main() {
     cudaMemcpy(d, h, sizeof(float) * nplanes * N, cudaMemcpyHostToDevice);
     QParams p = make_qparams(1e-3, 32768);
     cudaFuncSetAttribute(k_chain<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 0);
-    const char* names[3] = {"A current qstep", "B branchless rn32", "D plain F2F"};
-    for (int v = 0; v < 3; ++v) {
+    const char* names[4] = {"A current qstep", "B branchless rn32", "D plain F2F", "P pq_fast"};
+    for (int v = 0; v < 4; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             long long c = 0;
             cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -106,6 +137,7 @@ int main() {
             if (v == 0) k_chain<0><<<1, 32>>>(d, sy, p, cyc, nplanes);
             if (v == 1) k_chain<1><<<1, 32>>>(d, sy, p, cyc, nplanes);
             if (v == 2) k_chain<2><<<1, 32>>>(d, sy, p, cyc, nplanes);
+            if (v == 3) k_chain<3><<<1, 32>>>(d, sy, p, cyc, nplanes);
             cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
             // throughput: 148*2 blocks of 1 warp each... use many warps per SM
             const int blocks = 148 * 8;  // 8 warps/SM (smem-limited)
@@ -113,6 +145,7 @@ int main() {
             if (v == 0) k_chain<0><<<blocks, 32>>>(d, sy, p, cyc + 0, nplanes);
             if (v == 1) k_chain<1><<<blocks, 32>>>(d, sy, p, cyc + 0, nplanes);
             if (v == 2) k_chain<2><<<blocks, 32>>>(d, sy, p, cyc + 0, nplanes);
+            if (v == 3) k_chain<3><<<blocks, 32>>>(d, sy, p, cyc + 0, nplanes);
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);
             if (rep) printf("%-22s latency %.1f cyc/step (1 warp); %d warps: %.3f ms = %.2f Gstep/s\n", names[v],
