@@ -252,6 +252,21 @@ int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int rese
 /* Number of CUDA kernel launches issued by this context since creation. */
 uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx);
 
+/* ---- memory (the codec exists to free HBM: report what it holds) ---- */
+/* workspace_bytes: device scratch held by this context (per-tensor slots: symbols,
+ * histogram, tables, look-back scratch; host-API staging). blob_live_bytes /
+ * blob_peak_bytes: device memory of live blobs in this process (ACZ1 payload + decode
+ * sidecar + tables), the stash a training step keeps in HBM; reset_peak != 0 restarts the
+ * peak at the live value. (Reference counterpart: Controller::current_stash_bytes /
+ * peak_stash_bytes, include/acz/controller.hpp:140-141, which count ACZ1 bytes.) */
+int acz_gpu_memory_info(const acz_gpu_ctx* ctx, uint64_t* workspace_bytes,
+                        uint64_t* blob_live_bytes, uint64_t* blob_peak_bytes, int reset_peak);
+/* Synchronises the device and frees every workspace of the context (slots are recreated on
+ * demand by the next call) and trims the stream-ordered pool: call between the forward
+ * pass (compress) and the backward pass, or after a batched step, to return the scratch to
+ * the training framework. No blob is affected. */
+int acz_gpu_ctx_trim(acz_gpu_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,8 @@ SIGNATURES = [
     ("acz_gpu_debug_counters", C.c_int, [_vp, _u64p, C.c_uint32, C.c_int]),
     ("acz_gpu_debug_last_symbols", C.c_int, [_vp, _vp, C.c_uint64, _vp]),
     ("acz_gpu_launch_count", C.c_uint64, [_vp]),
+    ("acz_gpu_memory_info", C.c_int, [_vp, _u64p, _u64p, _u64p, C.c_int]),
+    ("acz_gpu_ctx_trim", C.c_int, [_vp]),
 ]
 
 _lib = None

@@ -121,6 +121,19 @@ class Context:
     def launches(self) -> int:
         return int(_native.load().acz_gpu_launch_count(self.handle))
 
+    def memory_info(self, reset_peak: bool = False) -> dict:
+        """Device memory held by the codec: this context's workspace, and the live / peak
+        bytes of blobs in the process (acz_gpu_memory_info)."""
+        ws, live, peak = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(_native.load().acz_gpu_memory_info(self.handle, C.byref(ws), C.byref(live),
+                                                  C.byref(peak), int(reset_peak)), self)
+        return {"workspace_bytes": int(ws.value), "blob_live_bytes": int(live.value),
+                "blob_peak_bytes": int(peak.value)}
+
+    def trim(self) -> None:
+        """Free every workspace of this context (acz_gpu_ctx_trim); blobs are unaffected."""
+        _check(_native.load().acz_gpu_ctx_trim(self.handle), self)
+
 
 _tls = threading.local()
 

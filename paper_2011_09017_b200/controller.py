@@ -319,7 +319,7 @@ class _Stash:
     (a ReLU's saved output and the next conv's saved input are one tensor: compressing it
     once and dropping every raw reference is what actually frees the activation)."""
 
-    __slots__ = ("ctl", "handle", "cache")
+    __slots__ = ("ctl", "handle", "cache", "__weakref__")
 
     def __init__(self, ctl: "Controller", handle: ActivationHandle):
         self.ctl, self.handle, self.cache = ctl, handle, None
@@ -375,9 +375,12 @@ class SavedActivationHooks:
         # it was taken from, so an address the caching allocator hands out again after the
         # original activation was freed (e.g. a later ReLU output of the same shape) never
         # matches a stale entry.
+        # Only weak references: autograd's saved-variable slots own the _Saved / _Stash
+        # objects, so a stash (and its decompressed cache) dies with the last graph node that
+        # saved it, and raw saves are not kept alive past the backward pass.
         self._marked = {}   # storage key -> (storage weakref, conv layer id)
-        self._stash = {}    # storage key -> (storage weakref, _Stash) (this iteration)
-        self._raw = {}      # storage key -> [_Saved] raw saves that may alias a conv input
+        self._stash = {}    # storage key -> (storage weakref, weakref to _Stash)
+        self._raw = {}      # storage key -> [weakref to _Saved] raw saves that may alias a conv input
         self.compressed = 0
 
     @staticmethod
@@ -430,21 +433,24 @@ class SavedActivationHooks:
             return _Saved(raw=t)
         import weakref
         key = self._key(t)
-        st = self._live(self._stash.get(key), t)
+        wst = self._live(self._stash.get(key), t)
+        st = wst() if wst is not None else None
         if st is not None:
             return _Saved(stash=st)
         layer = self._live(self._marked.pop(key, None), t)
         if layer is None:
             s = _Saved(raw=t)
-            self._raw.setdefault(key, []).append(s)
+            self._raw.setdefault(key, []).append(weakref.ref(s))
             return s
         relu = self.ctl.cfg.zero_restoration == RELU_RECOMPUTE and self._post_relu(t)
         st = _Stash(self.ctl, self.ctl.wrap_forward(layer, t.detach(), relu))
-        self._stash[key] = (weakref.ref(t.untyped_storage()), st)
+        self._stash[key] = (weakref.ref(t.untyped_storage()), weakref.ref(st))
         if st.handle.blob is not None:
             self.compressed += 1
-        for s in self._raw.pop(key, []):  # earlier saves of the same storage share it
-            s.raw, s.stash = None, st
+        for ws in self._raw.pop(key, []):  # earlier saves of the same storage share it
+            s = ws()
+            if s is not None:
+                s.raw, s.stash = None, st
         return _Saved(stash=st)
 
     def unpack(self, s):

@@ -7,6 +7,7 @@
 // ACZ1 (ref src/codec.cpp:177-262): header assembled on the host, bitstream copied
 //            device->host straight into place (device bytes already are ACZ1 order).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -174,6 +175,25 @@ struct acz_gpu_blob {
 };
 
 namespace acz_b200 {
+// Device memory held by live blobs (process-wide; arenas come from the stream-ordered pool):
+// what a training step actually stashes in HBM, incl. decode sidecars and tables.
+std::atomic<uint64_t> g_blob_live{0}, g_blob_peak{0};
+
+void blob_bytes_add(uint64_t b) {
+    const uint64_t v = g_blob_live.fetch_add(b) + b;
+    uint64_t pk = g_blob_peak.load();
+    while (v > pk && !g_blob_peak.compare_exchange_weak(pk, v)) {
+    }
+}
+
+// Releases a blob's arena (stream-ordered) and its accounting.
+void blob_arena_free(acz_gpu_blob* b, cudaStream_t s) {
+    if (!b->arena) return;
+    cudaFreeAsync(b->arena, s);
+    g_blob_live.fetch_sub(b->arena_bytes);
+    b->arena = nullptr;
+}
+
 PlaneGeom plane_geom(const uint64_t* shape, uint32_t rank) {
     PlaneGeom g{1, 1, 1, 1, 0};
     if (rank == 0) {
@@ -299,6 +319,7 @@ cudaError_t blob_alloc(acz_gpu_blob* b, uint32_t book, uint64_t nwords, uint64_t
     char* c = static_cast<char*>(p);
     b->arena = p;
     b->arena_bytes = off;
+    blob_bytes_add(off);
     b->book_sym = reinterpret_cast<uint32_t*>(c + o_sym);
     b->book_len = reinterpret_cast<uint8_t*>(c + o_len);
     b->words = reinterpret_cast<uint32_t*>(c + o_words);
@@ -513,6 +534,47 @@ int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
 const char* acz_gpu_last_error(const acz_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
 uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int acz_gpu_memory_info(const acz_gpu_ctx* ctx, uint64_t* workspace_bytes,
+                        uint64_t* blob_live_bytes, uint64_t* blob_peak_bytes, int reset_peak) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    uint64_t ws = ctx->ws_io_cap + ctx->ws_aux_cap + ctx->ws_scan_cap;
+    for (const Slot* sl : ctx->slots) {
+        if (!sl) continue;
+        ws += sl->ws_sym_cap + sl->ws_hist_cap + sl->ws_enc_cap + sl->ws_cb_cap +
+              sl->ws_status_cap + sl->ws_row_cap + sl->ws_book_cap + sl->ws_side_cap +
+              sl->ws_qs_cap + sl->ws_in_cap + sl->ws_pack_cap + (sl->d_small ? sizeof(SmallBlock) : 0);
+    }
+    if (workspace_bytes) *workspace_bytes = ws;
+    if (blob_live_bytes) *blob_live_bytes = g_blob_live.load();
+    if (blob_peak_bytes) *blob_peak_bytes = g_blob_peak.load();
+    if (reset_peak) g_blob_peak.store(g_blob_live.load());
+    return ACZ_OK;
+}
+
+int acz_gpu_ctx_trim(acz_gpu_ctx* ctx) {
+    if (!ctx) return ACZ_ERR_INVALID;
+    return guarded(ctx, [&]() -> int {
+    ctx->err.clear();
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());  // nothing of this context may still read its workspaces
+    for (Slot*& sl : ctx->slots) {
+        free_slot(sl);
+        sl = new (std::nothrow) Slot();  // recreated lazily (events, small block, buffers)
+        if (!sl) return fail(ctx, ACZ_ERR_NOMEM, "slot");
+    }
+    for (void** p : {&ctx->ws_io, &ctx->ws_aux, &ctx->ws_scan}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    ctx->ws_io_cap = ctx->ws_aux_cap = ctx->ws_scan_cap = 0;
+    // hand the freed blob arenas of the stream-ordered pool back to the device
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess)
+        CK(cudaMemPoolTrimTo(pool, 0));
+    return check_sticky(ctx);
+    });
+}
 
 }  // extern "C"
 
@@ -825,7 +887,7 @@ int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz
                            pl.predictor == ACZ_PRED_LORENZO2D, s);
     if (const int lr = slot_leave(ctx, sl, s)) rc = rc ? rc : lr;
     if (rc) {
-        if (b->arena) cudaFreeAsync(b->arena, s);
+        blob_arena_free(b, s);
         delete b;
         return rc;
     }
@@ -1236,7 +1298,7 @@ int acz_gpu_blob_info(const acz_gpu_blob* b, acz_gpu_blob_info_t* info) {
 
 int acz_gpu_blob_free(acz_gpu_blob* b) {
     if (!b) return ACZ_ERR_INVALID;
-    if (b->arena) cudaFreeAsync(b->arena, b->stream);
+    blob_arena_free(b, b->stream);
     delete b;
     return ACZ_OK;
 }
@@ -1468,7 +1530,7 @@ static int blob_from_host_body(acz_gpu_ctx* ctx, Slot* sl, const uint8_t* src, u
     b->info.device_bytes = b->arena_bytes;
     b->info.sidecar_bytes = sidecar_bytes(side_chunks, want_outl);
     auto cleanup = [&](int rc) {
-        cudaFreeAsync(b->arena, s);
+        blob_arena_free(b, s);
         delete b;
         return rc;
     };
@@ -1829,13 +1891,13 @@ int acz_gpu_huffman_encode(acz_gpu_ctx* ctx, const uint32_t* d_symbols, uint64_t
     acz_gpu_blob tmpb;
     rc = finish_encode(ctx, sl, &tmpb, d_symbols, 0, n, nullptr, 0, false, s);
     if (rc) {
-        if (tmpb.arena) cudaFreeAsync(tmpb.arena, s);
+        blob_arena_free(&tmpb, s);
         return rc;
     }
     CK(cudaMemcpyAsync(book_sym, tmpb.book_sym, 4ull * bi.book_size, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(book_len, tmpb.book_len, bi.book_size, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(bits, tmpb.words, (bi.total_bits + 7) / 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaFreeAsync(tmpb.arena, s));
+    blob_arena_free(&tmpb, s);
     CK(cudaStreamSynchronize(s));
     *book_size = bi.book_size;
     *bit_length = bi.total_bits;
@@ -1894,7 +1956,7 @@ int acz_gpu_huffman_decode(acz_gpu_ctx* ctx, const uint32_t* book_sym, const uin
     CK(launch_scan_decode(sa, ctx->ws_scan, s, &ctx->launches));
     CK(cudaMemcpyAsync(&sl->h_small->flags, &sl->d_small->flags, sizeof(unsigned),
                        cudaMemcpyDeviceToHost, s));
-    CK(cudaFreeAsync(tmpb.arena, s));
+    blob_arena_free(&tmpb, s);
     CK(cudaStreamSynchronize(s));
     const unsigned fl = sl->h_small->flags;
     if (fl & kDecTruncated) return fail(ctx, ACZ_ERR_DECODE, "truncated bitstream");

@@ -82,7 +82,8 @@ def test_saved_tensor_hooks_train_step(gpu_lib, zr):
     assert ctl.total_in == 4 * sum(sizes)
     # every stash unpacks to exactly the codec round trip of its conv input, with the
     # zero restoration of its handle (ref Controller::unwrap_backward src/controller.cpp:243-244)
-    stashes = sorted((st.handle.layer_id, st) for _ref, st in hooks._stash.values())
+    stashes = sorted(((st().handle.layer_id, st()) for _ref, st in hooks._stash.values()),
+                     key=lambda e: e[0])
     assert [i for i, _ in stashes] == [0, 1, 2]
     expect_relu = [False, zr == "relu-recompute", False]  # conv3's input comes from a pool
     for (i, st), relu in zip(stashes, expect_relu):
