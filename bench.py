@@ -222,7 +222,21 @@ def run_ours(args, rank, world, local_rank):
     host = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         host = host_set(args, tensors)  # the CPU baseline runs on these exact bytes
+    # memory the codec holds (what compression is for): blobs of one step (ACZ1 payload +
+    # decode sidecars + tables) and this context's workspace after the batched step
+    blobs = acz.compress_many(tensors, params, stream=stream, ctx=ctx)
+    torch.cuda.synchronize()
+    mem = ctx.memory_info()
+    memory = {"activation_bytes": 4 * n_total,
+              "acz1_bytes": sum(c.compressed_bytes for c in blobs),
+              "blob_device_bytes": sum(c.device_bytes for c in blobs),
+              "workspace_bytes": mem["workspace_bytes"],
+              "workspace_breakdown": mem["workspace_breakdown"]}
+    del blobs
+    ctx.trim()
+    memory["workspace_bytes_after_trim"] = ctx.memory_info()["workspace_bytes"]
     res = dict(host=host, value=value, ms_per_step=ms_max / args.steps, n=n_total, cbytes=cbytes,
+               memory=memory,
                B_step=8 * n_total + 2 * cbytes, launches=launches, clocks=clk, kernels=kern,
                detail=detail, ratio=ratios_in / ratios_out, batch=batch, per_tensor=per_tensor)
 
@@ -444,6 +458,7 @@ def main():
             "kernels_basis": "per class, summed over the tensors each compressed + decompressed "
                              "alone with CUDA events around every launch",
             "gpu_launches": res["launches"],
+            "memory": res["memory"],
             "clocks": res["clocks"],
             "detail": res["detail"],
         }

@@ -261,6 +261,15 @@ uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx);
  * peak_stash_bytes, include/acz/controller.hpp:140-141, which count ACZ1 bytes.) */
 int acz_gpu_memory_info(const acz_gpu_ctx* ctx, uint64_t* workspace_bytes,
                         uint64_t* blob_live_bytes, uint64_t* blob_peak_bytes, int reset_peak);
+/* Workspace by category (out[i] for i < n): */
+#define ACZ_MEM_SYMBOLS 0  /* quantisation symbols (2 or 4 B per element, per tensor slot) */
+#define ACZ_MEM_TABLES 1   /* histogram bins, code tables, codebook scratch per slot      */
+#define ACZ_MEM_QUANT 2    /* sidecar chain states, K2b look-back / replay scratch       */
+#define ACZ_MEM_ENCODE 3   /* encoder chunk offsets, ACZ1 packing buffers                */
+#define ACZ_MEM_STAGING 4  /* device copies of host inputs (host-buffer entry points)    */
+#define ACZ_MEM_DECODE 5   /* foreign-blob scan scratch                                  */
+#define ACZ_MEM_COUNT 6
+int acz_gpu_memory_breakdown(const acz_gpu_ctx* ctx, uint64_t* out, uint32_t n);
 /* Synchronises the device and frees every workspace of the context (slots are recreated on
  * demand by the next call) and trims the stream-ordered pool: call between the forward
  * pass (compress) and the backward pass, or after a batched step, to return the scratch to

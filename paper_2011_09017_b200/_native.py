@@ -83,6 +83,7 @@ SIGNATURES = [
     ("acz_gpu_launch_count", C.c_uint64, [_vp]),
     ("acz_gpu_memory_info", C.c_int, [_vp, _u64p, _u64p, _u64p, C.c_int]),
     ("acz_gpu_ctx_trim", C.c_int, [_vp]),
+    ("acz_gpu_memory_breakdown", C.c_int, [_vp, _u64p, C.c_uint32]),
 ]
 
 _lib = None

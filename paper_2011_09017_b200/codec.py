@@ -127,8 +127,12 @@ class Context:
         ws, live, peak = C.c_uint64(), C.c_uint64(), C.c_uint64()
         _check(_native.load().acz_gpu_memory_info(self.handle, C.byref(ws), C.byref(live),
                                                   C.byref(peak), int(reset_peak)), self)
+        br = (C.c_uint64 * 6)()
+        _check(_native.load().acz_gpu_memory_breakdown(self.handle, br, 6), self)
+        names = ["symbols", "tables", "quant", "encode", "staging", "decode"]
         return {"workspace_bytes": int(ws.value), "blob_live_bytes": int(live.value),
-                "blob_peak_bytes": int(peak.value)}
+                "blob_peak_bytes": int(peak.value),
+                "workspace_breakdown": {k: int(v) for k, v in zip(names, br)}}
 
     def trim(self) -> None:
         """Free every workspace of this context (acz_gpu_ctx_trim); blobs are unaffected."""

@@ -552,6 +552,23 @@ int acz_gpu_memory_info(const acz_gpu_ctx* ctx, uint64_t* workspace_bytes,
     return ACZ_OK;
 }
 
+int acz_gpu_memory_breakdown(const acz_gpu_ctx* ctx, uint64_t* out, uint32_t n) {
+    if (!ctx || !out) return ACZ_ERR_INVALID;
+    uint64_t v[ACZ_MEM_COUNT] = {0};
+    for (const Slot* sl : ctx->slots) {
+        if (!sl) continue;
+        v[ACZ_MEM_SYMBOLS] += sl->ws_sym_cap;
+        v[ACZ_MEM_TABLES] += sl->ws_hist_cap + sl->ws_enc_cap + sl->ws_cb_cap + sl->ws_book_cap;
+        v[ACZ_MEM_QUANT] += sl->ws_side_cap + sl->ws_qs_cap + sl->ws_row_cap;
+        v[ACZ_MEM_ENCODE] += sl->ws_status_cap + sl->ws_pack_cap;
+        v[ACZ_MEM_STAGING] += sl->ws_in_cap;
+    }
+    v[ACZ_MEM_STAGING] += ctx->ws_io_cap;
+    v[ACZ_MEM_DECODE] += ctx->ws_aux_cap + ctx->ws_scan_cap;
+    for (uint32_t i = 0; i < n && i < ACZ_MEM_COUNT; ++i) out[i] = v[i];
+    return ACZ_OK;
+}
+
 int acz_gpu_ctx_trim(acz_gpu_ctx* ctx) {
     if (!ctx) return ACZ_ERR_INVALID;
     return guarded(ctx, [&]() -> int {

@@ -187,6 +187,9 @@ struct alignas(16) Smem {
     double C[kW];         // prefix of (send[k-1] - guess[k])
     int nr;
     int forced[kW];       // range start is not an anchor-aligned guess
+    // classification job posted by warp 0 for the helper warp (two-warp CTA)
+    int job_i0, job_len, job_xoff, job_exit;
+    uint64_t job_seg0, job_flat0;
     // staged input window (plane index j*kSeg - 1 + i); LAST: everything before it is the
     // segment state the decoupled phase-A kernel persists for the walk kernel
     float xs[ACZ_SPEC_XS_GLOBAL ? 4 : kWin];
@@ -231,10 +234,16 @@ __device__ void spec_range(Smem<SymT>& S, int xoff, const float* __restrict__ xg
 // anchor binade or within 2 Tmax of a binade edge, exact RNE ties, collapse starts whose
 // pre-value is not exactly prev + q*step, re-expansions without a certificate, sidecar
 // points. lvl[L-1] marks outputs with exponent > B - L (fine offsets, see levelD).
+// Named barriers of the two-warp segment CTA (warp 0 runs the segment, warp 1 helps with
+// the classification): 1 = job posted, 2 = job done, 3 = masks reset inside a job.
+__device__ __forceinline__ void bar_pair(int id) {
+    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
 template <typename SymT>
 __device__ void classify(Smem<SymT>& S, int xoff, const float* __restrict__ xg, uint64_t seg0,
-                         int i0, int len, const SP& p, uint64_t plane_flat0) {
-    const int lane = threadIdx.x;
+                         int i0, int len, const SP& p, uint64_t plane_flat0, int tid, int NT) {
+    const int lane = tid;
     auto range_of = [&](int q) {
         const int w = q >> 5;
         return (int)S.rsp[w] + __popc(S.rsb[w] & (0xFFFFFFFFu >> (31 - (q & 31)))) - 1;
@@ -248,20 +257,20 @@ __device__ void classify(Smem<SymT>& S, int xoff, const float* __restrict__ xg, 
     const uint32_t sc_off = ph > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)ph;
     const uint32_t sc_mask = p.interval > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)(p.interval - 1);
     // Masks of positions >= i0 are rebuilt (OR-ed below); positions < i0 keep theirs.
-    for (int w = (i0 >> 5) + lane; w < kCapW; w += kW) {
+    for (int w = (i0 >> 5) + lane; w < kCapW; w += NT) {
         const uint32_t keep = w == (i0 >> 5) ? ((1u << (i0 & 31)) - 1u) : 0u;
         S.cand[w] &= keep;
 #pragma unroll
         for (int L = 0; L < kLev; ++L) S.lvl[L][w] &= keep;
     }
-    __syncwarp();
+    if (NT > kW) bar_pair(3); else __syncwarp();
     // Lane-sequential over a contiguous window of an odd number of positions (odd strides
     // between the lanes' shared-memory accesses are bank-conflict free): no warp-synchronous
     // step per element, so a lane's consecutive elements overlap. Carried in registers: the
     // previous position's output and "tiny accepted" flag, and the last position that is not
     // an identity continuation of a collapsed run (id[c]: sym[c] == R and position c-1 tiny
     // accepted), which the re-expansion certificate needs.
-    const int wl = ((len - i0 + kW - 1) / kW) | 1;
+    const int wl = ((len - i0 + NT - 1) / NT) | 1;
     const int b = i0 + lane * wl, e = min(len, b + wl);
     if (b < e) {
         double prev_out = 0.0;
@@ -386,8 +395,23 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, const float* __res
     }
     __syncwarp();
     const long long t1 = sclock<1>();
-    classify(S, xoff, xg, seg0, S.rstart[k0], len, p, plane_flat0);
-    __syncwarp();
+    if (blockDim.x > kW) {
+        // two-warp CTA: post the job, classify the first half, wait for the helper's half
+        if (lane == 0) {
+            S.job_i0 = S.rstart[k0];
+            S.job_len = len;
+            S.job_xoff = xoff;
+            S.job_seg0 = seg0;
+            S.job_flat0 = plane_flat0;
+            S.job_exit = 0;
+        }
+        bar_pair(1);
+        classify(S, xoff, xg, seg0, S.rstart[k0], len, p, plane_flat0, lane, 2 * kW);
+        bar_pair(2);
+    } else {
+        classify(S, xoff, xg, seg0, S.rstart[k0], len, p, plane_flat0, lane, kW);
+        __syncwarp();
+    }
     if (lane == 0) {
         sadd(&g_qclk[6], (unsigned long long)(t1 - t0));
         sadd(&g_qclk[7], (unsigned long long)(sclock<1>() - t1));
@@ -481,6 +505,12 @@ __device__ __forceinline__ void spec_params(SP& p, QParams& qp, const int* dB) {
     qp.exact_div = p.exact_div;
 }
 
+// threads per segment CTA of the fused kernel: warp 0 runs the segment, warp 1 (when
+// present) takes half of every candidate classification (ACZ_SPEC_HELPER=0: one warp)
+#ifndef ACZ_SPEC_HELPER
+#define ACZ_SPEC_HELPER 1
+#endif
+constexpr int kThreadsSpec = ACZ_SPEC_HELPER ? 2 * kW : kW;
 constexpr int kFused = 0;  // one kernel, segments chained by a decoupled look-back
 constexpr int kFront = 1;  // phase A only; the segment state is persisted to `store`
 constexpr int kBack = 2;   // walk only, from the persisted state and the given entry state
@@ -955,7 +985,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
 }
 
 template <typename SymT>
-__global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, SP p, const int* dB,
+__global__ void __maxnreg__(112) k_quant_spec(const float* __restrict__ x, SP p, const int* dB,
                                                    SymT* __restrict__ sym_out,
                                                    float* __restrict__ side_state,
                                                    unsigned int* __restrict__ status,
@@ -967,13 +997,28 @@ __global__ void __launch_bounds__(kW) k_quant_spec(const float* __restrict__ x, 
     QParams qp;
     spec_params(p, qp, dB);
     if (threadIdx.x == 0) s_tk = atomicAdd(ticket, 1u);
-    __syncwarp();
+    __syncthreads();
     const unsigned long long seg_id = s_tk;
     if (seg_id >= total_segs) return;
+    if (threadIdx.x >= kW) {
+        // helper warp: the second half of every classification job of this segment
+        const int tid = threadIdx.x;
+        for (;;) {
+            bar_pair(1);
+            if (S.job_exit) return;
+            classify(S, S.job_xoff, nullptr, S.job_seg0, S.job_i0, S.job_len, p, S.job_flat0,
+                     tid, 2 * kW);
+            bar_pair(2);
+        }
+    }
     // segment-major order: all planes' segment j before any segment j+1, so a segment's
     // predecessor (same plane, j-1) always holds an earlier ticket and is usually done
     spec_segment<SymT, kFused>(S, x, p, qp, seg_id % p.planes, seg_id / p.planes, sym_out,
                                side_state, status, exits, flags, nullptr, 0.0f);
+    if (blockDim.x > kW) {
+        if (threadIdx.x == 0) S.job_exit = 1;
+        bar_pair(1);  // release the helper
+    }
 }
 
 // Decoupled path, kernel A: phase A of every segment (no waiting), state persisted.
@@ -1146,9 +1191,16 @@ size_t spec_store_stride() {
 size_t spec_store_offset(uint64_t total) {
     return ((256 + 2 * ((4 * total + 255) & ~255ull)) + 255) & ~size_t(255);
 }
+// The decoupled path (opt-in) persists every segment's state: ~15 KB per segment (300 MB
+// for AlexNet conv1), reserved only when that path is selected.
+bool spec_decoupled() {
+    static const bool d = std::getenv("ACZ_SPEC_DECOUPLED") != nullptr;
+    return d;
+}
 // verification arrays after the decoupled path's segment states
 size_t spec_verify_offset(uint64_t total) {
-    return ((spec_store_offset(total) + total * spec_store_stride()) + 255) & ~size_t(255);
+    const size_t store = spec_decoupled() ? total * spec_store_stride() : 0;
+    return ((spec_store_offset(total) + store) + 255) & ~size_t(255);
 }
 
 namespace {
@@ -1218,12 +1270,12 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     // Fused kernel by default. The decoupled pair (ACZ_SPEC_DECOUPLED=1) is bit-identical;
     // measured slower on B200 (AlexNet conv1: 2.59 vs 2.36 ms): phase A costs the same and an
     // isolated walk batch still takes ~3.3k cycles, so the per-plane walk chain dominates.
-    if (!std::getenv("ACZ_SPEC_DECOUPLED")) {
+    if (!spec_decoupled()) {
         if (a.sym16)
-            k_quant_spec<uint16_t><<<(unsigned)total, kW, 0, s>>>(
+            k_quant_spec<uint16_t><<<(unsigned)total, kThreadsSpec, 0, s>>>(
                 a.x, p, dB, a.sym16, a.side_state, status, exits, ticket, a.flags, total);
         else
-            k_quant_spec<uint32_t><<<(unsigned)total, kW, 0, s>>>(
+            k_quant_spec<uint32_t><<<(unsigned)total, kThreadsSpec, 0, s>>>(
                 a.x, p, dB, a.sym, a.side_state, status, exits, ticket, a.flags, total);
         ++*launches;
         return launch_spec_verify(a, p, dB, rfix, pfirst, s, launches);
