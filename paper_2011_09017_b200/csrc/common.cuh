@@ -171,6 +171,55 @@ __device__ __forceinline__ uint32_t qstep(double orig, float xf, double pred, co
     return ok ? (uint32_t)(__double2loint(tm) + (int)p.R) : 0u;
 }
 
+// N reference steps from chain value r, speculating that every step is accepted and has a
+// non-fragile quotient (the common case): the chain carries each step's candidate
+// reconstruction straight into the next prediction, so the dependent path per step is
+// DADD, DFMA, DADD, DMUL, DADD and the F2F round trip (~80 cycles on B200), while the
+// acceptance test, the radius test and the fragility guard -- which qstep() has to resolve
+// before it can select the chain value -- run off the chain. xat(u) returns input u of the
+// block, emit(u, sym, value) receives every step's symbol and chain value (speculatively:
+// on a miss the caller's qexact() emits the same positions again). Returns true (and
+// advances r) when no step escaped, was rejected or needed the exact quotient: the emitted
+// values then equal what qstep() gives step by step.
+template <int N, class XAt, class Emit>
+__device__ __forceinline__ bool qspec(XAt xat, Emit emit, double& r, const QParams& p) {
+    const double M52 = 6755399441055744.0;  // 1.5 * 2^52
+    bool good = !p.exact_div;
+    double rr = r;
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+        const float xf = xat(u);
+        const double orig = (double)xf;
+        const double d = __dsub_rn(orig, rr);
+        const double tm = __fma_rn(d, p.inv_step, M52);
+        const double q = __dsub_rn(tm, M52);
+        const float cf = __double2float_rn(__dadd_rn(rr, __dmul_rn(q, p.step)));
+        const double c = (double)cf;
+        // off the chain: qstep's fragility guard and acceptance test
+        const double t = __dmul_rn(d, p.inv_step);
+        const bool frag = 0.5 - fabs(t - q) <= fabs(t) * 0x1p-44 + 0x1p-60;
+        const bool ok = fabs(q) < p.radius_d && isfinite(cf) && fabs(__dsub_rn(orig, c)) <= p.eb;
+        good &= ok & !frag;
+        emit(u, (uint32_t)(__double2loint(tm) + (int)p.R), cf);
+        rr = c;
+    }
+    if (good) r = rr;
+    return good;
+}
+
+// The same block step by step with qstep() (the fallback of qspec()).
+template <int N, class XAt, class Emit>
+__device__ __forceinline__ void qexact(XAt xat, Emit emit, double& r, const QParams& p) {
+#pragma unroll 1
+    for (int u = 0; u < N; ++u) {
+        const float xf = xat(u);
+        double v;
+        const uint32_t s = qstep((double)xf, xf, r, p, &v);
+        emit(u, s, (float)v);
+        r = v;
+    }
+}
+
 __host__ inline QParams make_qparams(double eb, uint32_t radius) {
     QParams p;
     p.eb = eb;

@@ -76,6 +76,39 @@ __global__ void __launch_bounds__(kQW * 32) k_quant_prev_serial(const float* __r
             // sidecar point inside this tile (interval >= 32: at most one)
             const int js = next_side - j0 < (uint64_t)cnt ? (int)(next_side - j0) : -1;
             if (js >= 0) next_side += interval;
+            if (cnt == kQT) {
+                // whole tile: blocks of 8 speculative steps (qspec), exact redo on a miss
+#pragma unroll 1
+                for (int jb = 0; jb < kQT; jb += 8) {
+                    float xv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        xv[u] = __uint_as_float(xr[jb + u]);
+                        bad |= !isfinite(xv[u]);
+                    }
+                    const float r0 = (float)r;
+                    float st = r0;  // chain value before element js (if js is in this block)
+                    uint32_t sy[8];
+                    auto emit = [&](int u, uint32_t s, float sv) {
+                        sy[u] = s;
+                        if (js == jb + u + 1) st = sv;
+                    };
+                    if (qspec<8>([&](int u) { return xv[u]; }, emit, r, qp)) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) xr[jb + u] = sy[u];
+                    } else {
+                        // exact redo from the tile (x is still in place)
+                        st = r0;
+                        qexact<8>([&](int u) { return __uint_as_float(xr[jb + u]); },
+                                  [&](int u, uint32_t s, float sv) {
+                                      xr[jb + u] = s;
+                                      if (js == jb + u + 1) st = sv;
+                                  },
+                                  r, qp);
+                    }
+                    if ((unsigned)(js - jb) < 8u) side_state[(base + j0 + js) / interval] = st;
+                }
+            } else {
 #pragma unroll 4
             for (int j = 0; j < cnt; ++j) {
                 const float xf = __uint_as_float(xr[j]);
@@ -84,6 +117,7 @@ __global__ void __launch_bounds__(kQW * 32) k_quant_prev_serial(const float* __r
                 double v;
                 xr[j] = qstep((double)xf, xf, r, qp, &v);  // r == 0 at the plane start
                 r = v;
+            }
             }
         }
         __syncwarp();

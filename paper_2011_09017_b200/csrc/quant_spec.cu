@@ -46,7 +46,11 @@ constexpr int kWin = kSeg + kExt + 1;  // staged x window: [j*kSeg - 1, (j+1)*kS
 #ifndef ACZ_SPEC_LEV
 #define ACZ_SPEC_LEV 1  // measured: 1 level beats 2-4 since phase A and the walk were tightened
 #endif
-constexpr int kLev = ACZ_SPEC_LEV;     // fine offset levels (binades below the anchor grid)
+constexpr int kLev = ACZ_SPEC_LEV;
+// speculative block length of the phase-A chains (qspec)
+#ifndef ACZ_SPEC_QB
+#define ACZ_SPEC_QB 4
+#endif     // fine offset levels (binades below the anchor grid)
 // ACZ_SPEC_XS_GLOBAL=1: read the input through L1/L2 instead of staging the segment's window
 // in shared memory (8.7 KB less per segment: more resident segments per SM).
 #ifndef ACZ_SPEC_XS_GLOBAL
@@ -209,10 +213,29 @@ template <typename SymT>
 __device__ void spec_range(Smem<SymT>& S, int xoff, const float* __restrict__ xg, uint64_t seg0,
                            int k, const SP& p, const QParams& qp, unsigned* flags) {
     const int b = S.rstart[k], e = S.rstart[k + 1];
-    double r = (double)S.guess[k];
+    double r = (seg0 + (uint64_t)b == 0) ? 0.0 : (double)S.guess[k];
     bool bad = false;
+    // blocks of 8 speculative steps (qspec: the acceptance / fragility checks off the
+    // chain); a block with an escape, a rejection or a fragile quotient is redone exactly.
+    // (A range never contains plane position 0 except as its first element, whose guess
+    // is then 0.0 == the reference's prediction.)
+    constexpr int kB = ACZ_SPEC_QB;
+    int i0 = b;
+#pragma unroll 1
+    for (; i0 + kB <= e; i0 += kB) {
+        auto xat = [&](int u) { return XAT(i0 + u); };
+        auto emit = [&](int u, uint32_t sy, float sv) {
+            S.sym[i0 + u] = (SymT)sy;
+            S.s[i0 + u] = sv;
+        };
+        if (!qspec<kB>(xat, emit, r, qp)) {
+#pragma unroll 1
+            for (int u = 0; u < kB; ++u) bad |= !isfinite(XAT(i0 + u));
+            qexact<kB>(xat, emit, r, qp);
+        }
+    }
 #pragma unroll 4
-    for (int i = b; i < e; ++i) {
+    for (int i = i0; i < e; ++i) {
         const float xf = XAT(i);
         bad |= !isfinite(xf);
         const double pred = (seg0 + (uint64_t)i == 0) ? 0.0 : r;
@@ -1117,8 +1140,28 @@ __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restric
         const uint64_t k0 = t * kRT;
         const int cnt = k0 < len ? (int)min((uint64_t)kRT, len - k0) : 0;
         uint32_t* tr = tile[w][t & 1][lane];
+        int kb = 0;
+        if (cnt == kRT) {
+            // blocks of 8 speculative steps (qspec) between plane starts
+#pragma unroll 1
+            for (; kb < kRT; kb += 8) {
+                if (snext - ((uint32_t)k0 + kb) < 8u) break;  // a plane starts in this block
+                float xv[8];
+                uint32_t sy[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) xv[u] = __uint_as_float(tr[kb + u]);
+                if (qspec<8>([&](int u) { return xv[u]; },
+                             [&](int u, uint32_t s, float) { sy[u] = s; }, r, qp)) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) tr[kb + u] = sy[u];
+                } else {
+                    qexact<8>([&](int u) { return __uint_as_float(tr[kb + u]); },
+                              [&](int u, uint32_t s, float) { tr[kb + u] = s; }, r, qp);
+                }
+            }
+        }
 #pragma unroll 4
-        for (int k = 0; k < cnt; ++k) {
+        for (int k = kb; k < cnt; ++k) {
             const float xf = __uint_as_float(tr[k]);
             if ((uint32_t)k0 + k == snext) {  // plane start: the predictor resets
                 r = 0.0;
