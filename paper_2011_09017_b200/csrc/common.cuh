@@ -128,6 +128,11 @@ __device__ __forceinline__ double rn32d(double y) {
     return __dsub_rn(__dadd_rn(y, M), M);
 }
 
+// ACZ_QSPEC_F2F=0: qspec rounds the chain with the magic add (rn32d) instead of the F2F round trip
+#ifndef ACZ_QSPEC_F2F
+#define ACZ_QSPEC_F2F 1  // measured: F2F 1.26 ms vs magic add 1.32 ms (AlexNet conv1 K2b)
+#endif
+
 // Parameters of the reference quantisation step.
 struct QParams {
     double eb, step, inv_step, radius_d;
@@ -171,20 +176,31 @@ __device__ __forceinline__ uint32_t qstep(double orig, float xf, double pred, co
     return ok ? (uint32_t)(__double2loint(tm) + (int)p.R) : 0u;
 }
 
+// float bits of a double that holds an exact normal float value (integer pipe only)
+__device__ __forceinline__ float f32_of_exact(double c) {
+    const unsigned hi = (unsigned)__double2hiint(c), lo = (unsigned)__double2loint(c);
+    const unsigned t = hi - (896u << 20);  // rebias the exponent (1023 - 127)
+    return __uint_as_float((t & 0x80000000u) | ((t << 3) & 0x7FFFFFF8u) | (lo >> 29));
+}
+
 // N reference steps from chain value r, speculating that every step is accepted and has a
 // non-fragile quotient (the common case): the chain carries each step's candidate
-// reconstruction straight into the next prediction, so the dependent path per step is
-// DADD, DFMA, DADD, DMUL, DADD and the F2F round trip (~80 cycles on B200), while the
-// acceptance test, the radius test and the fragility guard -- which qstep() has to resolve
-// before it can select the chain value -- run off the chain. xat(u) returns input u of the
-// block, emit(u, sym, value) receives every step's symbol and chain value (speculatively:
-// on a miss the caller's qexact() emits the same positions again). Returns true (and
-// advances r) when no step escaped, was rejected or needed the exact quotient: the emitted
-// values then equal what qstep() gives step by step.
+// reconstruction straight into the next prediction, and the acceptance test, the radius
+// test and the fragility guard -- which qstep() has to resolve before it can select the
+// chain value -- run off the chain: the dependent path per step is DADD, DFMA, DADD, DMUL,
+// DADD and the F2F round trip. (The magic-add rounding of rn32d instead of F2F, which keeps
+// the chain off the 7.4/clk/SM conversion pipe, measured slower: AlexNet conv1 K2b 1.32 vs
+// 1.26 ms; ACZ_QSPEC_F2F=0 selects it.) Off the chain the fragility guard is one DFMA: |d*inv - q| >= 0.5 - 2^-19 covers qstep's
+// 0.5 - |t - q| <= |t| 2^-44 + 2^-60 for every |t| < 2^24 (larger quotients exceed any
+// radius and are redone anyway). xat(u) returns input u of the block, emit(u, sym, value)
+// receives every step's symbol and chain value (speculatively: on a miss the caller's
+// qexact() emits the same positions again). Returns true (and advances r) when no step
+// escaped, was rejected, needed the exact quotient or left the normal float range: the
+// emitted values then equal what qstep() gives step by step.
 template <int N, class XAt, class Emit>
 __device__ __forceinline__ bool qspec(XAt xat, Emit emit, double& r, const QParams& p) {
     const double M52 = 6755399441055744.0;  // 1.5 * 2^52
-    bool good = !p.exact_div;
+    bool bad = p.exact_div != 0;
     double rr = r;
 #pragma unroll
     for (int u = 0; u < N; ++u) {
@@ -193,18 +209,27 @@ __device__ __forceinline__ bool qspec(XAt xat, Emit emit, double& r, const QPara
         const double d = __dsub_rn(orig, rr);
         const double tm = __fma_rn(d, p.inv_step, M52);
         const double q = __dsub_rn(tm, M52);
-        const float cf = __double2float_rn(__dadd_rn(rr, __dmul_rn(q, p.step)));
+        const double y = __dadd_rn(rr, __dmul_rn(q, p.step));
+#if ACZ_QSPEC_F2F
+        const float cf = __double2float_rn(y);
         const double c = (double)cf;
-        // off the chain: qstep's fragility guard and acceptance test
-        const double t = __dmul_rn(d, p.inv_step);
-        const bool frag = 0.5 - fabs(t - q) <= fabs(t) * 0x1p-44 + 0x1p-60;
-        const bool ok = fabs(q) < p.radius_d && isfinite(cf) && fabs(__dsub_rn(orig, c)) <= p.eb;
-        good &= ok & !frag;
+        bad |= !isfinite(cf);
+#else
+        const int ex = (__double2hiint(y) >> 20) & 0x7FF;
+        bad |= (unsigned)(ex - (1023 - 126)) > 252u;  // zero, subnormal, overflow: qstep
+        const double M = __hiloint2double((ex << 20) + ((29 << 20) | (1 << 19)), 0);
+        const double c = __dsub_rn(__dadd_rn(y, M), M);
+        const float cf = f32_of_exact(c);
+#endif
+        // off the chain: fragility guard, radius and acceptance tests
+        bad |= fabs(__fma_rn(d, p.inv_step, -q)) >= 0.5 - 0x1p-19;
+        bad |= !(fabs(q) < p.radius_d);
+        bad |= !(fabs(__dsub_rn(orig, c)) <= p.eb);
         emit(u, (uint32_t)(__double2loint(tm) + (int)p.R), cf);
         rr = c;
     }
-    if (good) r = rr;
-    return good;
+    if (!bad) r = rr;
+    return !bad;
 }
 
 // The same block step by step with qstep() (the fallback of qspec()).
