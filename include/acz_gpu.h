@@ -247,7 +247,9 @@ int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, vo
  * when n >= 28, out[26..27]: its phase-A pass-1 / classification cycles; when n >= 32,
  * out[28..30]: its walk batch cycles split into gather / evaluate / resolve, out[31]: sidecar
  * chunks whose recorded walk state the exact replay of the speculative quantiser found wrong
- * (their planes were recomputed serially; counted in every build). */
+ * (their planes were recomputed serially; counted in every build); when n >= 128,
+ * out[32 + 24 p + b]: number of speculative-quantiser segments whose phase p (0 phase A,
+ * 1 look-back wait, 2 walk, 3 exit) took [2^b, 2^(b+1)) cycles (stats builds). */
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset);
 /* Number of CUDA kernel launches issued by this context since creation. */
 uint64_t acz_gpu_launch_count(const acz_gpu_ctx* ctx);

@@ -2080,6 +2080,11 @@ int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int rese
         for (int i = 0; i < 2; ++i) out[24 + i] = v[12 + i];
     if (n >= 32)
         for (int i = 0; i < 4; ++i) out[28 + i] = v[16 + i];
+    if (n >= 128) {  // per-segment phase durations of K2b, log2 buckets (stats builds)
+        unsigned long long h[96];
+        CK(quant_spec_hist(h, reset != 0));
+        for (int i = 0; i < 96; ++i) out[32 + i] = h[i];
+    }
     return ACZ_OK;
 }
 

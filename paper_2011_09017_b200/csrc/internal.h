@@ -81,6 +81,7 @@ cudaError_t launch_quant(const QuantArgs& a, int sms, cudaStream_t s, uint64_t* 
 // ---- quant_spec.cu (long planes, PrevValue) ----
 bool quant_spec_applicable(uint32_t predictor, uint64_t plane_size, uint64_t planes, int sms);
 size_t quant_spec_scratch_bytes(uint64_t planes, uint64_t plane_size);
+cudaError_t quant_spec_hist(unsigned long long* out, bool reset);
 cudaError_t quant_spec_stats(unsigned long long* out, bool reset);
 cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
                               uint64_t* launches);

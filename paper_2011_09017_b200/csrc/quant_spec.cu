@@ -47,6 +47,16 @@ constexpr int kWin = kSeg + kExt + 1;  // staged x window: [j*kSeg - 1, (j+1)*kS
 #define ACZ_SPEC_LEV 1  // measured: 1 level beats 2-4 since phase A and the walk were tightened
 #endif
 constexpr int kLev = ACZ_SPEC_LEV;
+// exact steps the walk takes at once in exact mode (qspec block)
+#ifndef ACZ_SPEC_XB
+#define ACZ_SPEC_XB 8
+#endif
+constexpr int kXB = ACZ_SPEC_XB;
+// state changes after which the walk re-speculates at the next range start
+#ifndef ACZ_SPEC_RESPEC
+#define ACZ_SPEC_RESPEC 12
+#endif
+constexpr int kRespecChanges = ACZ_SPEC_RESPEC;
 // speculative block length of the phase-A chains (qspec)
 #ifndef ACZ_SPEC_QB
 #define ACZ_SPEC_QB 4
@@ -104,6 +114,8 @@ __device__ unsigned long long g_qstats[8];
 // walk, exit+store
 __device__ unsigned long long g_qclk[8];  // + [4] exact-step, [5] batch, [6] pass-1, [7] classify cycles
 __device__ unsigned long long g_wclk[4];
+// per-segment phase durations, log2 buckets (debug, ACZ_SPEC_STATS): [phase][bucket]
+__device__ unsigned long long g_qhist[4][24];
 __device__ unsigned long long g_spec_fixes;  // symbols / sidecar states rewritten by the replay  // walk batch split (debug): gather, evaluate, resolve
 
 struct SP {
@@ -561,6 +573,11 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         if (lane == 0) {
             const long long t = sclock<2>();
             sadd(&g_qclk[slot], (unsigned long long)(t - tck));
+            if (kStats) {
+                const unsigned long long dt = (unsigned long long)(t - tck) | 1ull;
+                const int bk = min(23, 63 - __clzll((long long)dt));
+                atomicAdd(&g_qhist[slot][bk], 1ull);
+            }
             tck = t;
         }
     };
@@ -706,8 +723,29 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     }
     __syncwarp();
 
-    // ---- phase A: speculate all ranges (lattice origin 0: plane-start lattice) ----
-    phase_a(S, xoff, xg, seg0, 0, 0.0, false, 0.0f, p, qp, plane_flat0, flags, len);
+    // ---- phase A: speculate all ranges ---------------------------------------------
+    // Lattice origin: the exact exit of the closest predecessor segment of this plane that
+    // is already published (non-blocking look; segment-major tickets make j-2 usually
+    // done), else the plane-start lattice (0). The chain's phase drifts from any exact
+    // origin by rounding (a random walk of ulps), so a recent origin keeps the entry
+    // offset D within the translation bound where the plane-start lattice, tens of
+    // thousands of elements back, often does not (then phase A is redone from the exact
+    // entry state).
+    double lam = 0.0;
+    if (MODE == kFused && j > 0) {
+        if (lane == 0) {
+            const uint64_t dmax = j < 4 ? j : 4;
+            for (uint64_t d = 1; d <= dmax; ++d) {
+                if (*((volatile unsigned*)status + sidx - d) != 0) {
+                    __threadfence();
+                    lam = (double)*((volatile float*)exits + sidx - d);
+                    break;
+                }
+            }
+        }
+        lam = __shfl_sync(0xffffffffu, lam, 0);
+    }
+    phase_a(S, xoff, xg, seg0, 0, lam, false, 0.0f, p, qp, plane_flat0, flags, len);
     }  // !kBack
 
     tphase(0);
@@ -770,6 +808,8 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         lev = 0;
     }
     int rcur = 0;          // range the offset D refers to
+    int nchg = 0;          // state changes since the last (re-)speculation
+    bool force_rebase = false;
     bool exact_mode = false;  // EXACT: the true state T is tracked explicitly
     float T = 0.0f;
     int pos = 0;           // next position to consider
@@ -803,7 +843,9 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 // exact entry T at a range start: resume translation (rebase if needed)
                 const double Dk = __dsub_rn((double)T, (double)S.guess[k]);
                 const int lk = levelD(Dk);
-                if (lk < 0) {
+                if (lk < 0 || force_rebase) {
+                    force_rebase = false;
+                    nchg = 0;
                     phase_a(S, xoff, xg, seg0, k, (double)T, true, T, p, qp, plane_flat0, flags, len);
                     D = 0.0;
                     lev = 0;
@@ -816,6 +858,55 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 continue;
             }
             const uint64_t pi = seg0 + (uint64_t)pos;
+            if (pi != 0 && min(S.rstart[k + 1], len) - pos >= kXB) {
+                // kXB exact steps at once (qspec, exact redo on a miss; every lane runs the
+                // same chain), then the first element after which translation may resume
+                // (both outputs non-tiny, representable offset) ends the stretch; elements
+                // up to it are committed. Element by element this took ~1.3-1.6k cycles per
+                // step, and post-ReLU planes have stretches of thousands of exact steps.
+                float* sT = reinterpret_cast<float*>(s_vis);            // chain values
+                uint32_t* sS = reinterpret_cast<uint32_t*>(s_vis) + kXB;  // symbols
+                double rr = (double)T;
+                auto xat = [&](int u) { return XAT(pos + u); };
+                auto emit = [&](int u, uint32_t sy, float v) {
+                    if (lane == 0) {
+                        sT[u] = v;
+                        sS[u] = sy;
+                    }
+                };
+                if (!qspec<kXB>(xat, emit, rr, qp)) qexact<kXB>(xat, emit, rr, qp);
+                __syncwarp();
+                bool can = false;
+                double Dn = 0.0;
+                int ln = -1;
+                if (lane < kXB && !force_rebase) {
+                    const float Tu = sT[lane], ssu = S.s[pos + lane];
+                    if (fabs((double)Tu) >= p.eb && fabs((double)ssu) >= p.eb) {
+                        Dn = __dsub_rn((double)Tu, (double)ssu);
+                        ln = levelD(Dn);
+                        can = ln >= 0;
+                    }
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, can);
+                const int cut = m ? __ffs(m) - 1 : kXB - 1;  // last committed element
+                if (lane <= cut) {
+                    S.sym[pos + lane] = (SymT)sS[lane];
+                    const uint64_t flat = plane_flat0 + pi + (uint64_t)lane;
+                    if ((flat & (p.interval - 1)) == 0)
+                        side_state[flat >> p.ishift] = lane == 0 ? T : sT[lane - 1];
+                }
+                T = sT[cut];
+                if (m) {
+                    D = __shfl_sync(0xffffffffu, Dn, cut);
+                    lev = __shfl_sync(0xffffffffu, ln, cut);
+                    rcur = k;
+                    exact_mode = false;
+                }
+                __syncwarp();
+                if (lane == 0) sadd(&g_qstats[2], (unsigned long long)cut);  // (+1 above)
+                pos += cut + 1;
+                continue;
+            }
             const float tprev = T;
             const XS ex = xstep(XAT(pos), pi == 0 ? 0.0 : (double)tprev, p);
             if (lane == 0) {
@@ -826,7 +917,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             __syncwarp();
             T = ex.out;
             const float ss = S.s[pos];
-            if (fabs((double)T) >= p.eb && fabs((double)ss) >= p.eb) {
+            if (!force_rebase && fabs((double)T) >= p.eb && fabs((double)ss) >= p.eb) {
                 const double Dn = __dsub_rn((double)T, (double)ss);
                 const int ln = levelD(Dn);
                 if (ln >= 0) {
@@ -946,6 +1037,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 // lattice changed at range start fk: re-speculate ranges >= fk from the
                 // exact entry state and re-evaluate from fvp
                 phase_a(S, xoff, xg, seg0, fk, (double)ftp, true, ftp, p, qp, plane_flat0, flags, len);
+                nchg = 0;
                 D = 0.0;
                 lev = 0;
                 rcur = fk;
@@ -964,11 +1056,16 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             rcur = fk;
             const double Dn = __dsub_rn((double)fout, (double)fss);
             const int ln = levelD(Dn);
-            if (fabs((double)fout) >= p.eb && fabs((double)fss) >= p.eb && ln >= 0) {
+            // Many state changes since the last speculation (a nonzero offset through
+            // post-ReLU collapse/re-expansion cycles can fail at nearly every candidate):
+            // step exactly to the next range start and re-speculate from there (D = 0).
+            const bool respec = ++nchg >= kRespecChanges;
+            if (!respec && fabs((double)fout) >= p.eb && fabs((double)fss) >= p.eb && ln >= 0) {
                 D = Dn;
                 lev = ln;
             } else {
                 exact_mode = true;
+                force_rebase = respec;
                 T = fout;
             }
             pos = fvp + 1;
@@ -1341,6 +1438,15 @@ cudaError_t launch_quant_spec(const QuantArgs& a, void* scratch, cudaStream_t s,
     return launch_spec_verify(a, p, dB, rfix, pfirst, s, launches);
 }
 
+cudaError_t quant_spec_hist(unsigned long long* out, bool reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_qhist, sizeof(g_qhist));
+    if (e == cudaSuccess && reset) {
+        static const unsigned long long z[4 * 24] = {0};
+        e = cudaMemcpyToSymbol(g_qhist, z, sizeof(z));
+    }
+    return e;
+}
+
 cudaError_t quant_spec_stats(unsigned long long* out, bool reset) {
     cudaError_t e = cudaMemcpyFromSymbol(out, g_qstats, sizeof(g_qstats));
     if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out + 8, g_qclk, sizeof(g_qclk));  // 8 values
@@ -1373,8 +1479,11 @@ bool quant_spec_applicable(uint32_t predictor, uint64_t plane_size, uint64_t pla
     if (std::getenv("ACZ_SERIAL_QUANT")) return false;
     if (std::getenv("ACZ_SPEC_QUANT")) return true;
     const double n = (double)plane_size * (double)planes;
-    const double t_serial = fmax((double)plane_size * 330.0, n * 1.2 / sms);
-    const double t_spec = n * 25.0 / sms;
+    // cycles: K2a walks a plane at ~180-200 cycles per element (qspec chain, latency bound
+    // with few planes) or ~1.2 SM-cycles per element when planes are plentiful; K2b costs
+    // ~8 (dense image planes) to ~19 (post-ReLU planes) SM-cycles per element
+    const double t_serial = fmax((double)plane_size * 200.0, n * 1.2 / sms);
+    const double t_spec = n * 14.0 / sms;
     return t_spec < t_serial;
 }
 

@@ -24,8 +24,8 @@ for nm in which:
     for _ in range(2):
         blob = acz.compress(x, p)
         acz.decompress(blob, True)
-    v = (C.c_uint64 * 32)()
-    lib.acz_gpu_debug_counters(ctx.handle, v, 32, 1)
+    v = (C.c_uint64 * 128)()
+    lib.acz_gpu_debug_counters(ctx.handle, v, 128, 1)
     lib.acz_gpu_profile_enable(ctx.handle, 1)
     blob = acz.compress(x, p)
     out = acz.decompress(blob, True)
@@ -34,7 +34,7 @@ for nm in which:
     cnt = (C.c_uint64 * 7)()
     lib.acz_gpu_profile_read(ctx.handle, ms, cnt)
     lib.acz_gpu_profile_enable(ctx.handle, 0)
-    lib.acz_gpu_debug_counters(ctx.handle, v, 32, 1)
+    lib.acz_gpu_debug_counters(ctx.handle, v, 128, 1)
     names = ["stats", "quant", "hist", "book", "encode", "decode", "scan"]
     print(nm, x.shape, "ratio %.3f" % acz.compression_ratio(blob),
           {names[i]: round(ms[i], 3) for i in range(7) if cnt[i]})
@@ -53,3 +53,7 @@ for nm in which:
         [v[8 + i] / nb for i in range(6)] + [v[15]]))
     print("   spec cycles/elem (per segment-warp): phaseA %.1f wait %.1f walk %.1f out %.1f" % tuple(v[16 + i] / n for i in range(4)))
     print("   exact replay: chunks whose walk state was wrong %d" % v[31])
+    if os.environ.get("QB_HIST"):
+        for ph, nmph in enumerate(["phaseA", "wait", "walk", "out"]):
+            h = [v[32 + 24 * ph + b] for b in range(24)]
+            print("   hist %-6s" % nmph, " ".join("2^%d:%d" % (b, c) for b, c in enumerate(h) if c))
