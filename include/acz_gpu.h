@@ -237,7 +237,9 @@ int acz_gpu_profile_read(acz_gpu_ctx* ctx, double* ms, uint64_t* launches);
 /* ---- parity / debug ---- */
 /* Copy the quantisation symbols of the last compress on this context (device, n u32). */
 int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, void* stream);
-/* Debug counters; reset != 0 clears them. out[0..7]: speculative-quantiser walk counters
+/* Debug counters of development builds (the product build counts nothing and returns zeros:
+ * -DACZ_SPEC_STATS=1 quantiser, -DACZ_CB_STATS=1 codebook, -DACZ_DEC_STATS=1 decoder, via
+ * ACZ_NVCC_EXTRA); reset != 0 clears them. out[0..7]: speculative-quantiser walk counters
  * (batches, state changes, exact steps, rebases, speculated elements, visits); when n >= 16,
  * out[8..15]: codebook phase cycles (compaction, sort, rounds, depths, canonical, tables),
  * round count, calls; when n >= 20, out[16..19]: speculative-quantiser cycles summed over
@@ -247,7 +249,7 @@ int acz_gpu_debug_last_symbols(acz_gpu_ctx* ctx, uint32_t* d_out, uint64_t n, vo
  * when n >= 28, out[26..27]: its phase-A pass-1 / classification cycles; when n >= 32,
  * out[28..30]: its walk batch cycles split into gather / evaluate / resolve, out[31]: sidecar
  * chunks whose recorded walk state the exact replay of the speculative quantiser found wrong
- * (their planes were recomputed serially; counted in every build); when n >= 128,
+ * (their planes were recomputed serially); when n >= 128,
  * out[32 + 24 p + b]: number of speculative-quantiser segments whose phase p (0 phase A,
  * 1 look-back wait, 2 walk, 3 exit) took [2^b, 2^(b+1)) cycles (stats builds). */
 int acz_gpu_debug_counters(acz_gpu_ctx* ctx, uint64_t* out, uint32_t n, int reset);

@@ -1,10 +1,13 @@
 // K6 Huffman decode + K7 reconstruction (ref src/huffman.cpp:137-189, src/codec.cpp:122-171).
 //
-// k_decode_prev   : one thread per sidecar chunk (`interval` symbols). The sidecar gives
-//                   the chunk's bit offset, outlier prefix and the chain state before its
-//                   first element, so every chunk decodes and reconstructs independently and
-//                   bit-exactly. Canonical decode via a 4096-entry shared-memory LUT
-//                   (codes <= 12 bits), per-length canonical ranges for longer codes.
+// k_decode_prev   : one lane per sidecar chunk (`interval` symbols, 32 chunks per warp, a
+//                   persistent CTA of 18 warps per SM). The sidecar gives the chunk's bit
+//                   offset and the chain state before its first element, so every chunk
+//                   decodes and reconstructs independently and bit-exactly. Canonical decode
+//                   via a 16384-entry shared-memory LUT (codes <= kLutBits = 14 bits; entries
+//                   of longer-code prefixes carry the code-length range), per-length
+//                   canonical limits for longer codes; outputs leave through a transposed
+//                   32 x 8 tile (coalesced stores).
 // k_decode_lorenzo: Lorenzo2d, one thread per plane (sidecar interval = plane size).
 // k_scan_decode   : sequential whole-stream decode used to (re)build the sidecar of a
 //                   foreign ACZ1 blob and to validate it exactly like the reference
@@ -145,7 +148,11 @@ constexpr int kLongCap = 6144;    // book entries of codes longer than kLutBits 
                                   // (as u16: symbols of a radius <= 32768 alphabet)
 constexpr size_t kDecSmem =
     4ull * kLutSize + 2ull * kLongCap + 4ull * kDW * (kDStage + 32 * (kTW + 1));
-__device__ unsigned long long g_dclk[4];  // debug: prologue, staging, loop cycles; tasks
+// debug (development builds, -DACZ_DEC_STATS=1): prologue, staging, loop cycles; tasks
+#ifndef ACZ_DEC_STATS
+#define ACZ_DEC_STATS 0
+#endif
+__device__ unsigned long long g_dclk[4];
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const unsigned long long* a, uint32_t n,
                                                     unsigned long long key) {
@@ -269,7 +276,7 @@ __global__ void __launch_bounds__(kDW * 32, 1) k_decode_prev(DecodeArgs a) {
     uint32_t* s_bits = dsm + kLutSize + kLongCap / 2 + w * (kDStage + 32 * (kTW + 1));
     float(*s_out)[kTW + 1] = reinterpret_cast<float(*)[kTW + 1]>(s_bits + kDStage);
     float* tile = s_out[lane];
-    if (lane == 0) atomicAdd(&g_dclk[0], (unsigned long long)(clock64() - tk0));
+    if (ACZ_DEC_STATS && lane == 0) atomicAdd(&g_dclk[0], (unsigned long long)(clock64() - tk0));
     const uint64_t ntasks = (a.nchunks + 31) / 32;
     const uint64_t I = a.interval;
     for (uint64_t task = (uint64_t)blockIdx.x * kDW + w; task < ntasks;
@@ -301,7 +308,7 @@ __global__ void __launch_bounds__(kDW * 32, 1) k_decode_prev(DecodeArgs a) {
             const long long tk2 = clock64();
             decode_chunk<true, uint32_t>(a, s_bits, (uint32_t)(pos - w0 * 32), s_lut, lbook, lfirst,
                                          s_lim, s_ct, cnt, start, r, pin, tile, s_out, chunk0, lane);
-            if (lane == 0) {
+            if (ACZ_DEC_STATS && lane == 0) {
                 atomicAdd(&g_dclk[1], (unsigned long long)(tk2 - tk1));
                 atomicAdd(&g_dclk[2], (unsigned long long)(clock64() - tk2));
                 atomicAdd(&g_dclk[3], 1ull);

@@ -1,9 +1,11 @@
 // K3 histogram, K4 codebook, K5 encode: the canonical Huffman coder of the reference
 // (ref src/huffman.cpp:22-135), bit-exact.
 //
-// K3  k_histogram   : shared-memory privatised histogram over a window of 8192 bins
-//                     centred on the zero-residual symbol (quant_radius); out-of-window
-//                     symbols go straight to global u64 atomics.
+// K3  k_histogram   : shared-memory privatised histogram over a window of 32768 bins
+//                     centred on the zero-residual symbol (quant_radius; one 1024-thread CTA
+//                     per SM), the zero-residual symbol itself counted in registers;
+//                     out-of-window symbols go straight to global u64 atomics. The last CTA
+//                     to finish builds the codebook (K4 fused).
 // K4  k_codebook    : single 1024-thread CTA. Compaction of non-zero bins (ascending
 //                     symbol order == the reference's std::map order, huffman.cpp:110),
 //                     stable LSD radix sort of the leaves by frequency, two-queue merge
@@ -12,11 +14,12 @@
 //                     (huffman.cpp:25-54), depths by pointer jumping, canonical
 //                     (length, symbol) order by a stable counting sort (huffman.cpp:116-125),
 //                     canonical codes (huffman.cpp:75-86), decode LUT.
-// K5  k_encode      : 4096 symbols per CTA; per-thread code lengths, CTA scan, decoupled
-//                     look-back over tiles for the global bit offset and escape count,
-//                     bit concatenation in shared memory, coalesced word stores (boundary
-//                     words by atomicOr). Also writes the outlier list and the decode
-//                     sidecar (bit offset / outlier prefix every `interval` symbols).
+// K5  k_encode_count: per-256-symbol-chunk bit / escape counts (persistent 1024-thread
+//                     CTAs, one decoupled look-back across CTAs, CTA scan -> absolute chunk
+//                     offsets); k_encode_write: a warp per chunk, bit concatenation in a
+//                     per-warp shared stage, coalesced word stores (boundary words by
+//                     atomicOr). Also writes the outlier list and the decode sidecar (bit
+//                     offset / outlier prefix every `interval` symbols).
 #include <algorithm>
 #include <type_traits>
 
@@ -281,6 +284,11 @@ __device__ void write_tables(const uint32_t* s_count, const unsigned long long* 
 constexpr int kFastLeaves = 8192;
 // phase timing of the fast codebook (debug; acz_gpu_debug_counters slots 8..15):
 // compaction, sort, rounds, depths, canonical, tables (SM cycles), round count, calls
+// Counted only in development builds (-DACZ_CB_STATS=1): the product build keeps no
+// device-global mutable state.
+#ifndef ACZ_CB_STATS
+#define ACZ_CB_STATS 0
+#endif
 __device__ unsigned long long g_cbstats[8];
 constexpr size_t kFastSmem = kFastLeaves * 8 /*keys*/ + kFastLeaves * 8 /*ifreq*/ +
                              2 * kFastLeaves * 2 /*parent*/ + 2 * kFastLeaves /*depth*/ +
@@ -308,7 +316,7 @@ __device__ __forceinline__ void codebook_fast_body(
     auto phase = [&](int slot) {
         if (tid == 0) {
             const long long t = clock64();
-            atomicAdd(&g_cbstats[slot], (unsigned long long)(t - tclk));
+            if (ACZ_CB_STATS) atomicAdd(&g_cbstats[slot], (unsigned long long)(t - tclk));
             tclk = t;
         }
     };
@@ -538,7 +546,7 @@ __device__ __forceinline__ void codebook_fast_body(
                     }
                 }
                 const unsigned long long fx = f2[0] + f2[1];
-                atomicAdd(&g_cbstats[6], 1ull);
+                if (ACZ_CB_STATS) atomicAdd(&g_cbstats[6], 1ull);
                 ifreq[m] = fx;
                 par[id2[0]] = (uint16_t)(k + m);
                 par[id2[1]] = (uint16_t)(k + m);
@@ -744,7 +752,7 @@ __device__ __forceinline__ void codebook_fast_body(
     __syncthreads();
     phase(5);
     if (tid == 0) {
-        atomicAdd(&g_cbstats[7], 1ull);
+        if (ACZ_CB_STATS) atomicAdd(&g_cbstats[7], 1ull);
         info->book_size = k;
         info->total_bits = s_total_bits;
         info->n_escapes = s_esc;

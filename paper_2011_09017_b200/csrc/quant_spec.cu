@@ -1292,7 +1292,7 @@ __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restric
         rfix[ch + 1] = (float)r;
         const uint64_t plane = (f0 + len) / p.P;
         atomicMin(pfirst + plane, (unsigned long long)(ch + 1));
-        atomicAdd(fixes, 1ull);
+        if (kStats) atomicAdd(fixes, 1ull);
     }
 }
 
