@@ -282,6 +282,52 @@ __device__ void write_tables(const uint32_t* s_count, const unsigned long long* 
 //      computed by binary search instead of a materialised merge;
 //   4. depths by pointer jumping; 5. canonical (length, symbol) order; 6. decode tables.
 constexpr int kFastLeaves = 8192;
+
+// Block-wide bottom-up merge sort of n <= kPer * kCbThreads unique u64 keys in shared memory
+// (ping-pong between a and b): every element finds its rank in the partner run by a
+// fixed-step binary search, the kPer elements of a thread searching together (independent
+// chains); one barrier per level. Returns the buffer that holds the sorted keys.
+template <int kPer>
+__device__ unsigned long long* block_merge_sort(unsigned long long* a, unsigned long long* b,
+                                                uint32_t n) {
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t run = 1; run < n; run <<= 1) {
+        unsigned long long v[kPer];
+        uint32_t lo[kPer], pe[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t i = tid + j * kCbThreads;
+            v[j] = i < n ? a[i] : 0ull;
+            const uint32_t base = i & ~(2 * run - 1);
+            const uint32_t pb = (i & run) ? base : base + run;  // partner run
+            lo[j] = pb;
+            pe[j] = i < n ? min(pb + run, n) : pb;
+        }
+        for (uint32_t st = run; st > 0; st >>= 1) {
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                const uint32_t q = lo[j] + st - 1;
+                if (q < pe[j] && a[q] < v[j]) lo[j] += st;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t i = tid + j * kCbThreads;
+            if (i < n) {
+                const uint32_t base = i & ~(2 * run - 1);
+                const bool second = (i & run) != 0;
+                const uint32_t own = i - (second ? base + run : base);
+                const uint32_t pb = second ? base : base + run;
+                b[base + own + (lo[j] - pb)] = v[j];
+            }
+        }
+        __syncthreads();
+        unsigned long long* t = a;
+        a = b;
+        b = t;
+    }
+    return a;
+}
 // phase timing of the fast codebook (debug; acz_gpu_debug_counters slots 8..15):
 // compaction, sort, rounds, depths, canonical, tables (SM cycles), round count, calls
 // Counted only in development builds (-DACZ_CB_STATS=1): the product build keeps no
@@ -310,7 +356,8 @@ __device__ __forceinline__ void codebook_fast_body(
     __shared__ uint32_t s_wcnt[kCbWarps][65];
     __shared__ unsigned long long s_total_bits, s_esc;
     __shared__ uint32_t s_max_len, s_flags;
-    __shared__ uint32_t sh_li, sh_ii, sh_m, sh_nl, sh_ni, sh_xm, sh_done;
+    __shared__ uint32_t sh_li, sh_ii, sh_nl;
+    __shared__ unsigned long long sh_fx;
     const int tid = threadIdx.x;
     long long tclk = clock64();
     auto phase = [&](int slot) {
@@ -322,28 +369,16 @@ __device__ __forceinline__ void codebook_fast_body(
     };
 
     uint32_t* lsym = reinterpret_cast<uint32_t*>(dep + 2 * kFastLeaves);  // [kFastLeaves]
-    // (1) compaction -------------------------------------------------------------------
-    // The touched bitmap is staged into shared memory and every touched bin is fetched
-    // with an asynchronous 8-byte copy straight into its compacted slot: the whole gather
-    // costs about two memory round trips. Warp wp owns bitmap words [wp*per, (wp+1)*per);
-    // positions = block prefix of set bits (ascending symbol order).
     const int lane = tid & 31, warp = tid >> 5;
+    // (1) compaction -------------------------------------------------------------------
+    // Thread t owns bitmap words [t*wpt, (t+1)*wpt): its touched-bin count, a block scan for
+    // its first position (ascending symbol order == the reference's std::map order), then
+    // every touched bin is fetched with an asynchronous 8-byte copy into its slot.
     const uint32_t nwords = (alphabet + 31) / 32;
-    const bool staged = nwords <= 2 * kFastLeaves;  // fits the ifreq region (64 KiB)
-    uint32_t* s_bm = reinterpret_cast<uint32_t*>(ifreq);
-    if (staged) {
-        for (uint32_t w = tid; w < nwords; w += kCbThreads) cp_async4(s_bm + w, touched + w);
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-    }
-    const uint32_t* bm = staged ? s_bm : touched;
-    const uint32_t per = (nwords + kCbWarps - 1) / kCbWarps;
-    const uint32_t w0 = min(nwords, warp * per), w1 = min(nwords, w0 + per);
+    const uint32_t wpt = (nwords + kCbThreads - 1) / kCbThreads;
+    const uint32_t w0 = min(nwords, (uint32_t)tid * wpt), w1 = min(nwords, w0 + wpt);
     uint32_t mine = 0;
-    for (uint32_t w = w0 + lane; w < w1; w += 32) mine += __popc(bm[w]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    for (uint32_t w = w0; w < w1; ++w) mine += __popc(touched[w]);
     if (tid == 0) {
         s_flags = 0;
         s_total_bits = 0;
@@ -351,41 +386,32 @@ __device__ __forceinline__ void codebook_fast_body(
         s_esc = 0;
     }
     uint32_t k;
-    uint32_t pos = block_scan_u32(lane == 0 ? mine : 0u, scan_tmp, &k);
-    pos = __shfl_sync(0xffffffffu, pos, 0);
+    uint32_t pos = block_scan_u32(mine, scan_tmp, &k);
     if (k > kFastLeaves) {
         if (tid == 0) info->slow = 1;  // k_codebook_slow takes over (bins left intact)
         return;
     }
-    const unsigned lt = (1u << lane) - 1u;
     for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t m = bm[w];
-        if ((m >> lane) & 1u) {
-            const uint32_t p = pos + __popc(m & lt);
-            const uint32_t sy = w * 32 + lane;
-            cp_async8(&key[p], &hist[sy]);
-            lsym[p] = sy;
+        for (uint32_t m = touched[w]; m; m &= m - 1) {
+            const uint32_t sy = w * 32 + (__ffs(m) - 1);
+            cp_async8(&key[pos], &hist[sy]);
+            lsym[pos] = sy;
+            ++pos;
         }
-        pos += __popc(m);
     }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    for (uint32_t p = tid; p < kFastLeaves; p += kCbThreads) {
-        if (p < k) {
-            const unsigned long long f = key[p];
-            if (lsym[p] == 0) s_esc = f;
-            key[p] = (f << 16) | p;
-        } else {
-            key[p] = ~0ull;  // padding sorts last
-        }
+    for (uint32_t p = tid; p < k; p += kCbThreads) {
+        const unsigned long long f = key[p];
+        if (lsym[p] == 0) s_esc = f;
+        key[p] = (f << 16) | p;
     }
     // self-cleaning: zero the consumed bins and the bitmap (the copies above have landed)
     for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t m = bm[w];
-        if ((m >> lane) & 1u) hist[w * 32 + lane] = 0;
+        for (uint32_t m = touched[w]; m; m &= m - 1) hist[w * 32 + (__ffs(m) - 1)] = 0;
+        touched[w] = 0;
     }
-    for (uint32_t w = w0 + lane; w < w1; w += 32) touched[w] = 0;
     __syncthreads();
     phase(0);
     if (k == 0) {
@@ -513,172 +539,164 @@ __device__ __forceinline__ void codebook_fast_body(
         }
     }
 
+    unsigned long long* skey = key;
+    unsigned long long* iq = ifreq;  // internal-node frequencies
     phase(1);
     // (3) tree by parallel rounds -------------------------------------------------------
     // node ids: leaf (symbol-order index) j -> j, internal t -> k + t; par[] = parent id.
+    // Round: X = the two smallest (leaf wins frequency ties, internals FIFO: the reference
+    // heap's (freq, creation index) order, huffman.cpp:42-54); every leaf with freq <= fx
+    // and every queued internal (all <= fx) -- the set S -- precede X, and the pairs
+    // S[2q], S[2q+1] are the next merges (each >= fx), an odd last element pairing with X.
+    // Warp 0 forms X and counts S's leaves (32-way probes); then every thread places one S
+    // element by binary search in the other list. Two barriers per round; the internal
+    // frequencies accumulate by atomics into a pre-zeroed queue.
     const uint32_t root = k == 1 ? 0 : 2 * k - 2;
-    if (tid == 0) {
-        sh_li = 0;
-        sh_ii = 0;
-        sh_m = 0;
-        sh_done = 0;
-        if (k == 1) par[0] = 0;
+    if (k == 1) {
+        if (tid == 0) par[0] = 0;
     }
+    for (uint32_t i = tid; i < k; i += kCbThreads) iq[i] = 0;
     __syncthreads();
-    while (k > 1) {
-        if (tid == 0) {
-            uint32_t li = sh_li, ii = sh_ii, m = sh_m;
-            if ((k - li) + (m - ii) <= 1) {
-                sh_done = 1;
-            } else {
-                unsigned long long f2[2];
-                uint32_t id2[2];
-                for (int t = 0; t < 2; ++t) {
-                    const unsigned long long fl = li < k ? (key[li] >> 16) : ~0ull;
-                    if (li < k && (ii >= m || fl <= ifreq[ii])) {  // leaf wins ties
-                        f2[t] = fl;
-                        id2[t] = (uint32_t)(key[li] & 0xFFFF);
-                        ++li;
-                    } else {
-                        f2[t] = ifreq[ii];
-                        id2[t] = k + ii;
-                        ++ii;
+    {
+        uint32_t li = 0, ii = 0, m = 0;  // queue state (uniform over the block)
+        while (k > 1 && (k - li) + (m - ii) > 1) {
+            if (tid < 32) {
+                uint32_t l2 = li, i2 = ii;
+                unsigned long long fx = 0;
+                if (lane == 0) {
+                    unsigned long long f2[2];
+                    uint32_t id2[2];
+                    for (int t = 0; t < 2; ++t) {
+                        const unsigned long long fl = l2 < k ? (skey[l2] >> 16) : ~0ull;
+                        if (l2 < k && (i2 >= m || fl <= iq[i2])) {  // leaf wins ties
+                            f2[t] = fl;
+                            id2[t] = (uint32_t)(skey[l2] & 0xFFFF);
+                            ++l2;
+                        } else {
+                            f2[t] = iq[i2];
+                            id2[t] = k + i2;
+                            ++i2;
+                        }
                     }
+                    fx = f2[0] + f2[1];
+                    if (ACZ_CB_STATS) atomicAdd(&g_cbstats[6], 1ull);
+                    iq[m] = fx;
+                    par[id2[0]] = (uint16_t)(k + m);
+                    par[id2[1]] = (uint16_t)(k + m);
                 }
-                const unsigned long long fx = f2[0] + f2[1];
-                if (ACZ_CB_STATS) atomicAdd(&g_cbstats[6], 1ull);
-                ifreq[m] = fx;
-                par[id2[0]] = (uint16_t)(k + m);
-                par[id2[1]] = (uint16_t)(k + m);
-                // leaves with freq <= fx (their keys precede X's)
-                uint32_t lo = li, hi = k;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if ((key[mid] >> 16) <= fx) lo = mid + 1; else hi = mid;
+                fx = __shfl_sync(0xffffffffu, fx, 0);
+                l2 = __shfl_sync(0xffffffffu, l2, 0);
+                i2 = __shfl_sync(0xffffffffu, i2, 0);
+                // first leaf in [l2, k) with freq > fx: 32-way probes of strides 1024, 32, 1
+                uint32_t lo = l2;
+#pragma unroll
+                for (int lev = 0; lev < 3; ++lev) {
+                    const uint32_t st = lev == 0 ? 1024u : lev == 1 ? 32u : 1u;
+                    const uint32_t q = lo + (uint32_t)lane * st + st - 1;  // last of block `lane`
+                    const bool le = q < k && (skey[q] >> 16) <= fx;
+                    lo += (uint32_t)__popc(__ballot_sync(0xffffffffu, le)) * st;
                 }
-                sh_nl = lo - li;
-                sh_ni = m - ii;  // queued internals (all precede X)
-                sh_xm = m;
-                sh_li = li;
-                sh_ii = ii;
-                sh_m = m + 1;
+                if (lane == 0) {
+                    sh_li = l2;
+                    sh_ii = i2;
+                    sh_nl = min(lo, k) - l2;
+                    sh_fx = fx;
+                }
             }
-        }
-        __syncthreads();
-        if (sh_done) break;
-        const uint32_t li = sh_li, ii = sh_ii, nl = sh_nl, ni = sh_ni, xm = sh_xm;
-        const uint32_t ns = nl + ni, np = ns >> 1, m1 = xm + 1;
-        const bool odd = ns & 1;
-        for (uint32_t q = tid; q < np + (odd ? 1u : 0u); q += kCbThreads) ifreq[m1 + q] = 0;
-        __syncthreads();
-        // S = merge(leaves[li, li+nl), internals[ii, ii+ni)) by key; S[2q], S[2q+1] -> Y_q;
-        // an odd last element pairs with X.
-        for (uint32_t t = tid; t < ns; t += kCbThreads) {
-            unsigned long long f;
-            uint32_t node, p;
-            if (t < nl) {
-                f = key[li + t] >> 16;
-                node = (uint32_t)(key[li + t] & 0xFFFF);
-                uint32_t lo = 0, hi = ni;  // internals with freq < f precede the leaf
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (ifreq[ii + mid] < f) lo = mid + 1; else hi = mid;
+            __syncthreads();
+            const uint32_t l2 = sh_li, i2 = sh_ii, nl = sh_nl, xm = m;
+            const unsigned long long fx = sh_fx;
+            const uint32_t ni = xm - i2;  // queued internals (all precede X)
+            const uint32_t ns = nl + ni, np = ns >> 1, m1 = xm + 1;
+            const bool odd = ns & 1;
+            for (uint32_t t = tid; t < ns; t += kCbThreads) {
+                unsigned long long f;
+                uint32_t node, p;
+                if (t < nl) {
+                    f = skey[l2 + t] >> 16;
+                    node = (uint32_t)(skey[l2 + t] & 0xFFFF);
+                    uint32_t lo = 0, hi = ni;  // internals with freq < f precede the leaf
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (iq[i2 + mid] < f) lo = mid + 1; else hi = mid;
+                    }
+                    p = t + lo;
+                } else {
+                    const uint32_t i = t - nl;
+                    f = iq[i2 + i];
+                    node = k + i2 + i;
+                    uint32_t lo = 0, hi = nl;  // leaves with freq <= f precede the internal
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if ((skey[l2 + mid] >> 16) <= f) lo = mid + 1; else hi = mid;
+                    }
+                    p = i + lo;
                 }
-                p = t + lo;
-            } else {
-                const uint32_t i = t - nl;
-                f = ifreq[ii + i];
-                node = k + ii + i;
-                uint32_t lo = 0, hi = nl;  // leaves with freq <= f precede the internal
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if ((key[li + mid] >> 16) <= f) lo = mid + 1; else hi = mid;
+                const uint32_t q = p >> 1;  // p == ns - 1 with odd ns -> q == np (pairs with X)
+                par[node] = (uint16_t)(k + m1 + q);
+                if (odd && p == ns - 1) {
+                    atomicAdd(&iq[m1 + q], f + fx);
+                    par[k + xm] = (uint16_t)(k + m1 + q);
+                } else {
+                    atomicAdd(&iq[m1 + q], f);
                 }
-                p = i + lo;
             }
-            const uint32_t q = p >> 1;  // p == ns - 1 with odd ns -> q == np (pairs with X)
-            par[node] = (uint16_t)(k + m1 + q);
-            atomicAdd(&ifreq[m1 + q], f);
+            li = l2 + nl;
+            ii = odd ? xm + 1 : xm;  // X is consumed, or stays at the queue front
+            m = m1 + np + (odd ? 1u : 0u);
+            __syncthreads();
         }
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t m = m1 + np;
-            uint32_t iin = xm;  // X becomes the queue front
-            if (odd) {
-                atomicAdd(&ifreq[m], ifreq[xm]);
-                par[k + xm] = (uint16_t)(k + m);
-                ++m;
-                iin = xm + 1;
-            }
-            sh_li = li + nl;
-            sh_ii = iin;
-            sh_m = m;
-        }
-        __syncthreads();
     }
     if (tid == 0 && k > 1) par[root] = (uint16_t)root;
     __syncthreads();
     phase(2);
 
-    // (4) depths by pointer jumping (register-staged, in place) --------------------------
-    const uint32_t nodes = k == 1 ? 1 : 2 * k - 1;
-    constexpr int kNpt = 2 * kFastLeaves / kCbThreads;  // nodes per thread
-    for (uint32_t i = tid; i < nodes; i += kCbThreads) dep[i] = (k == 1) ? 1 : (i == root ? 0 : 1);
-    __syncthreads();
-    if (k > 1) {
-        for (int it = 0; it < 16; ++it) {
-            uint16_t na[kNpt];
-            uint8_t nd[kNpt];
-            int changed = 0;
-#pragma unroll
-            for (int j = 0; j < kNpt; ++j) {
-                const uint32_t i = tid + j * kCbThreads;
-                if (i < nodes) {
-                    const uint32_t a = par[i];
-                    if (a != root) {
-                        nd[j] = (uint8_t)min(255u, (uint32_t)dep[i] + dep[a]);
-                        na[j] = par[a];
-                        changed = 1;
-                    } else {
-                        nd[j] = dep[i];
-                        na[j] = (uint16_t)a;
-                    }
-                }
-            }
-            const int any = __syncthreads_or(changed);
-#pragma unroll
-            for (int j = 0; j < kNpt; ++j) {
-                const uint32_t i = tid + j * kCbThreads;
-                if (i < nodes) {
-                    dep[i] = nd[j];
-                    par[i] = na[j];
-                }
-            }
-            __syncthreads();
-            if (!any) break;
-        }
-    }
-
-    phase(3);
-    // (5) canonical order: stable counting sort by length over ascending symbols ---------
-    if (tid < 65) {
-        s_count[tid] = 0;
-        s_base[tid] = 0;
-    }
+    // (4) code lengths: every leaf walks its parent chain to the root (the kPer leaves of a
+    // thread walk together), plus the per-length counts, total bits and the longest code --
+    constexpr int kPer = kFastLeaves / kCbThreads;
+    if (tid < 65) s_count[tid] = 0;
     __syncthreads();
     unsigned long long bits_part = 0;
     uint32_t maxl = 0;
     bool too_deep = false;
-    for (uint32_t p = tid; p < k; p += kCbThreads) {
-        const unsigned long long kk = key[p];
-        uint32_t l = dep[kk & 0xFFFF];
-        if (l > 64) {
-            too_deep = true;
-            l = 64;
+    {
+        uint32_t nd[kPer], d[kPer];
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t r = tid + j * kCbThreads;  // rank in frequency order
+            nd[j] = r < k ? (uint32_t)(skey[r] & 0xFFFF) : root;
+            d[j] = 0;
         }
-        atomicAdd(&s_count[l], 1u);
-        bits_part += (kk >> 16) * l;
-        maxl = max(maxl, l);
+        if (k > 1) {
+            for (int it = 0; it < 65; ++it) {
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < kPer; ++j) {
+                    if (nd[j] != root) {
+                        nd[j] = par[nd[j]];
+                        ++d[j];
+                        any = true;
+                    }
+                }
+                if (!any) break;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t r = tid + j * kCbThreads;
+            if (r < k) {
+                const unsigned long long kk = skey[r];
+                uint32_t l = k == 1 ? 1u : d[j];
+                if (nd[j] != root || l > 64) {
+                    too_deep = true;
+                    l = 64;
+                }
+                dep[kk & 0xFFFF] = (uint8_t)l;
+                atomicAdd(&s_count[l], 1u);
+                bits_part += (kk >> 16) * l;
+                maxl = max(maxl, l);
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bits_part += __shfl_xor_sync(0xffffffffu, bits_part, o);
@@ -688,6 +706,7 @@ __device__ __forceinline__ void codebook_fast_body(
         atomicMax(&s_max_len, maxl);
     }
     if (too_deep) atomicOr(&s_flags, kFlagDepth64);
+    phase(3);
     __syncthreads();
     if (tid == 0) {
         unsigned long long code = 0;
@@ -708,6 +727,8 @@ __device__ __forceinline__ void codebook_fast_body(
         s_first_index[0] = 0;
         if (s_max_len > 56) s_flags |= kFlagLenTooLong;
     }
+    // (5) canonical order: stable counting sort by length over ascending symbols ---------
+    if (tid < 65) s_base[tid] = 0;
     __syncthreads();
     const unsigned lanemask_lt = (1u << lane) - 1;
     uint32_t* s_book = reinterpret_cast<uint32_t*>(key);  // keys are dead from here on
