@@ -148,6 +148,10 @@ constexpr int kLongCap = 6144;    // book entries of codes longer than kLutBits 
                                   // (as u16: symbols of a radius <= 32768 alphabet)
 constexpr size_t kDecSmem =
     4ull * kLutSize + 2ull * kLongCap + 4ull * kDW * (kDStage + 32 * (kTW + 1));
+// ACZ_DEC_MAGIC=1: the decoder rounds the chain by the magic add (no F2F; A/B)
+#ifndef ACZ_DEC_MAGIC
+#define ACZ_DEC_MAGIC 0  // measured slower: AlexNet step decode 0.46 -> 0.54 ms
+#endif
 // debug (development builds, -DACZ_DEC_STATS=1): prologue, staging, loop cycles; tasks
 #ifndef ACZ_DEC_STATS
 #define ACZ_DEC_STATS 0
@@ -216,12 +220,29 @@ __device__ __forceinline__ void decode_chunk(const DecodeArgs& a, const uint32_t
                 oi = lower_bound_u64(a.out_index, (uint32_t)a.n_outliers, start + gidx);
             v = __ldg(a.out_value + oi);
             ++oi;
+            r = (double)v;
         } else {
             const double q = __dsub_rn(__hiloint2double(0x43380000, (int)sym), magic);
             const double pred = reset ? 0.0 : r;
-            v = __double2float_rn(__dadd_rn(pred, __dmul_rn(q, step)));
+            const double y = __dadd_rn(pred, __dmul_rn(q, step));
+#if ACZ_DEC_MAGIC
+            // RN32(y) as an exact double by the magic add (rn32d) and its float bits on the
+            // integer pipe: no F2F conversion per symbol (7.4/clk/SM); zero, subnormal and
+            // huge results take the conversions
+            const int ex = (__double2hiint(y) >> 20) & 0x7FF;
+            if ((unsigned)(ex - (1023 - 126)) <= 252u) {
+                const double M = __hiloint2double((ex << 20) + ((29 << 20) | (1 << 19)), 0);
+                r = __dsub_rn(__dadd_rn(y, M), M);
+                v = f32_of_exact(r);
+            } else {
+                v = __double2float_rn(y);
+                r = (double)v;
+            }
+#else
+            v = __double2float_rn(y);
+            r = (double)v;
+#endif
         }
-        r = (double)v;
         return fabsf(v) <= zthr ? 0.0f : v;
     };
     for (uint32_t t0 = 0; t0 < I; t0 += kTW) {

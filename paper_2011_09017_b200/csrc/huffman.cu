@@ -1270,7 +1270,10 @@ __device__ __forceinline__ void load_chunk_syms(const SymT* __restrict__ symp, u
     }
 }
 
-constexpr int kCountThreads = 1024;  // one counting CTA per SM: a short look-back chain
+constexpr int kCountThreads = 1024;  // counting CTAs of 1024 threads, ACZ_ENC_COUNT_CTAS per SM
+#ifndef ACZ_ENC_COUNT_CTAS
+#define ACZ_ENC_COUNT_CTAS 1
+#endif
 
 // code length of symbol v: the compact table when every code is <= 27 bits
 template <bool kCompact>
@@ -1680,19 +1683,19 @@ cudaError_t launch_build_tables(const uint32_t* book_sym, const uint8_t* book_le
 
 size_t encode_scratch_bytes(uint64_t n, int sms) {
     const uint64_t chunks = (n + kChunk - 1) / kChunk;
-    return align256(sizeof(TileStatus) * (uint64_t)sms) + 16 * chunks + 256;
+    return align256(sizeof(TileStatus) * (uint64_t)sms * ACZ_ENC_COUNT_CTAS) + 16 * chunks + 256;
 }
 
 cudaError_t launch_encode(const EncodeArgs& a0, int sms, cudaStream_t s, uint64_t* launches) {
     EncodeArgs a = a0;
     const uint64_t chunks = (a.n + kChunk - 1) / kChunk;
-    uint64_t grid = (uint64_t)sms;  // persistent counting pass: one 1024-thread CTA per SM
+    uint64_t grid = (uint64_t)sms * ACZ_ENC_COUNT_CTAS;  // persistent counting pass
     if (grid > chunks) grid = chunks;
     if (grid == 0) grid = 1;
     cudaError_t e = cudaMemsetAsync(a.status, 0, sizeof(TileStatus) * grid, s);
     if (e != cudaSuccess) return e;
     a.chunk_off = reinterpret_cast<unsigned long long*>(
-        reinterpret_cast<char*>(a.status) + align256(sizeof(TileStatus) * (uint64_t)sms));
+        reinterpret_cast<char*>(a.status) + align256(sizeof(TileStatus) * (uint64_t)sms * ACZ_ENC_COUNT_CTAS));
     const int mode = a.max_len <= 27 ? 0 : a.max_len <= 32 ? 1 : 2;
     if (a.sym16) {
         if (mode == 0) k_encode_count<uint16_t, true><<<(unsigned)grid, kCountThreads, 0, s>>>(a);
