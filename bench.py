@@ -44,6 +44,9 @@ def parse():
                     choices=["alexnet", "config1", "vgg16", "resnet18", "resnet50"])
     ap.add_argument("--batch", type=int, default=0, help="per-rank batch (0: workload default)")
     ap.add_argument("--eb", type=float, default=EB)
+    ap.add_argument("--data", default="iid", choices=["iid", "smooth", "model"],
+                    help="synthetic activations: iid (default), smooth (box-filtered), or "
+                         "model (a random-initialised AlexNet/VGG-16 forward pass)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -125,12 +128,9 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     batch = args.batch or DEFAULT_BATCH[args.workload]
-    tensors = [x for _, x in W.make_set(args.workload, batch, device=dev, shard=(rank, max(world, 1)))]
-    # weak scaling: every rank holds a full per-rank batch; regenerate with rank seed
-    if world > 1:
-        tensors = [W.make_tensor((batch,) + tuple(x.shape[1:]),
-                                 W.activation_set(args.workload)[i][2], i * 1000 + rank, dev)
-                   for i, x in enumerate(tensors)]
+    # weak scaling: every rank holds a full per-rank batch (rank-seeded)
+    tensors = [x for _, x in W.make_set(args.workload, batch * max(world, 1), device=dev,
+                                        shard=(rank, max(world, 1)), data=args.data)]
     names = [nm for nm, _, _ in W.activation_set(args.workload)]
     n_total = sum(x.numel() for x in tensors)
     outs = [torch.empty_like(x) for x in tensors]
@@ -297,7 +297,7 @@ def host_set(args, tensors=None):
     if tensors is None:
         batch = args.batch or DEFAULT_BATCH[args.workload]
         dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
-        tensors = [x for _, x in W.make_set(args.workload, batch, device=dev)]
+        tensors = [x for _, x in W.make_set(args.workload, batch, device=dev, data=args.data)]
     return [x.cpu().numpy() for x in tensors]
 
 
@@ -371,7 +371,7 @@ def run_reference(args, rank, world):
         "metric": "compress+decompress GB/s per B200 at eb=1e-3 (% of HBM peak); compression ratio",
         "impl": "reference", "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic ({args.data})",
         "config": {"workload": f"{args.workload} saved-activation set, batch {batch} per GPU, "
                                f"fp32, eb={args.eb}, zero filter on decompress",
                    "input": ("the GPU arm's bytes (workloads.make_set, Philox on cuda:0)"
@@ -440,7 +440,7 @@ def main():
             "metric": "compress+decompress GB/s per B200 at eb=1e-3 (% of HBM peak); compression ratio",
             "value": res["value"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": f"synthetic ({args.data})",
             "config": {"workload": f"{args.workload} saved-activation set, batch {res['batch']} per "
                                    f"GPU, fp32, eb={args.eb}, zero filter on decompress",
                        "parallelism": f"dp{world} (batch-sharded, no data-path collective)",
