@@ -183,6 +183,15 @@ __device__ __forceinline__ float f32_of_exact(double c) {
     return __uint_as_float((t & 0x80000000u) | ((t << 3) & 0x7FFFFFF8u) | (lo >> 29));
 }
 
+// (double)f on the integer pipe for zero and normal floats; subnormal / inf / nan set `special`
+__device__ __forceinline__ double f64_of_f32(float f, bool& special) {
+    const unsigned u = __float_as_uint(f);
+    const unsigned e = (u >> 23) & 0xFFu;
+    special |= e == 0xFFu || (e == 0 && (u << 1) != 0);
+    const unsigned hi = (u & 0x80000000u) | (e ? ((u & 0x7FFFFFFFu) >> 3) + (896u << 20) : 0u);
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
+
 // N reference steps from chain value r, speculating that every step is accepted and has a
 // non-fragile quotient (the common case): the chain carries each step's candidate
 // reconstruction straight into the next prediction, and the acceptance test, the radius
@@ -190,14 +199,16 @@ __device__ __forceinline__ float f32_of_exact(double c) {
 // chain value -- run off the chain: the dependent path per step is DADD, DFMA, DADD, DMUL,
 // DADD and the F2F round trip. (The magic-add rounding of rn32d instead of F2F, which keeps
 // the chain off the 7.4/clk/SM conversion pipe, measured slower: AlexNet conv1 K2b 1.32 vs
-// 1.26 ms; ACZ_QSPEC_F2F=0 selects it.) Off the chain the fragility guard is one DFMA: |d*inv - q| >= 0.5 - 2^-19 covers qstep's
+// 1.26 ms; ACZ_QSPEC_F2F=0 selects it by default, kMagic per call site, where the input
+// widening runs on the integer pipe too; it also measured slower in the exact replay and in
+// K2a, whose chains are throughput- rather than latency-bound.) Off the chain the fragility guard is one DFMA: |d*inv - q| >= 0.5 - 2^-19 covers qstep's
 // 0.5 - |t - q| <= |t| 2^-44 + 2^-60 for every |t| < 2^24 (larger quotients exceed any
 // radius and are redone anyway). xat(u) returns input u of the block, emit(u, sym, value)
 // receives every step's symbol and chain value (speculatively: on a miss the caller's
 // qexact() emits the same positions again). Returns true (and advances r) when no step
 // escaped, was rejected, needed the exact quotient or left the normal float range: the
 // emitted values then equal what qstep() gives step by step.
-template <int N, class XAt, class Emit>
+template <int N, bool kMagic = ACZ_QSPEC_F2F == 0, class XAt, class Emit>
 __device__ __forceinline__ bool qspec(XAt xat, Emit emit, double& r, const QParams& p) {
     const double M52 = 6755399441055744.0;  // 1.5 * 2^52
     bool bad = p.exact_div != 0;
@@ -205,22 +216,24 @@ __device__ __forceinline__ bool qspec(XAt xat, Emit emit, double& r, const QPara
 #pragma unroll
     for (int u = 0; u < N; ++u) {
         const float xf = xat(u);
-        const double orig = (double)xf;
+        const double orig = kMagic ? f64_of_f32(xf, bad) : (double)xf;
         const double d = __dsub_rn(orig, rr);
         const double tm = __fma_rn(d, p.inv_step, M52);
         const double q = __dsub_rn(tm, M52);
         const double y = __dadd_rn(rr, __dmul_rn(q, p.step));
-#if ACZ_QSPEC_F2F
-        const float cf = __double2float_rn(y);
-        const double c = (double)cf;
-        bad |= !isfinite(cf);
-#else
-        const int ex = (__double2hiint(y) >> 20) & 0x7FF;
-        bad |= (unsigned)(ex - (1023 - 126)) > 252u;  // zero, subnormal, overflow: qstep
-        const double M = __hiloint2double((ex << 20) + ((29 << 20) | (1 << 19)), 0);
-        const double c = __dsub_rn(__dadd_rn(y, M), M);
-        const float cf = f32_of_exact(c);
-#endif
+        double c;
+        float cf;
+        if (!kMagic) {
+            cf = __double2float_rn(y);
+            c = (double)cf;
+            bad |= !isfinite(cf);
+        } else {
+            const int ex = (__double2hiint(y) >> 20) & 0x7FF;
+            bad |= (unsigned)(ex - (1023 - 126)) > 252u;  // zero, subnormal, overflow: qstep
+            const double M = __hiloint2double((ex << 20) + ((29 << 20) | (1 << 19)), 0);
+            c = __dsub_rn(__dadd_rn(y, M), M);
+            cf = f32_of_exact(c);
+        }
         // off the chain: fragility guard, radius and acceptance tests
         bad |= fabs(__fma_rn(d, p.inv_step, -q)) >= 0.5 - 0x1p-19;
         bad |= !(fabs(q) < p.radius_d);

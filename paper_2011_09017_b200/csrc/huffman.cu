@@ -37,6 +37,10 @@ namespace {
 #endif
 constexpr int kHistWindow = ACZ_HIST_WINDOW;
 constexpr int kHistThreads = 1024;
+#ifndef ACZ_HIST_LOADS
+#define ACZ_HIST_LOADS 4
+#endif
+constexpr int kHistLoads = ACZ_HIST_LOADS;
 
 // --------------------------------------------------------------------------- K3 ----
 // The histogram buffer is self-cleaning: the codebook kernel zeroes every bin it reads and
@@ -79,8 +83,7 @@ __global__ void __launch_bounds__(kHistThreads) k_histogram(const SymT* __restri
     constexpr int V = 16 / sizeof(SymT);  // symbols per 128-bit load
     const uint64_t nv = ((reinterpret_cast<uintptr_t>(sym) & 15) == 0) ? n / V : 0;
     const uint4* s4 = reinterpret_cast<const uint4*>(sym);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
-        const uint4 v = __ldcs(s4 + i);
+    auto count4 = [&](const uint4 v) {
         const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -91,7 +94,18 @@ __global__ void __launch_bounds__(kHistThreads) k_histogram(const SymT* __restri
                 count(w[k]);
             }
         }
+    };
+    // kHistLoads 128-bit loads per thread in flight before counting (one CTA per SM: the
+    // loads in flight, not the counting, bound the pass)
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    for (; i + (kHistLoads - 1) * stride < nv; i += kHistLoads * stride) {
+        uint4 v[kHistLoads];
+#pragma unroll
+        for (int u = 0; u < kHistLoads; ++u) v[u] = __ldcs(s4 + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < kHistLoads; ++u) count4(v[u]);
     }
+    for (; i < nv; i += stride) count4(__ldcs(s4 + i));
     for (uint64_t i = nv * V + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += stride)
         count((uint32_t)sym[i]);
@@ -1297,12 +1311,23 @@ __global__ void __launch_bounds__(kCountThreads) k_encode_count(EncodeArgs a) {
 
     // ---- per-chunk counts (two chunks in flight per warp) -----------------------------
     unsigned long long wb = 0, we = 0;
+    // the next pair of chunks is loaded while the current pair is counted (four chunks in
+    // flight per warp: the loads, not the counting, bound this pass)
+    uint32_t sy[kEncPer], sy2[kEncPer];
+    {
+        const uint64_t c = cb + warp;
+        if (c < ce) load_chunk_syms<SymT, false>(symp, a.n, c * kChunk + (uint64_t)lane * kEncPer, vec_ok, sy);
+        if (c + W < ce)
+            load_chunk_syms<SymT, false>(symp, a.n, (c + W) * kChunk + (uint64_t)lane * kEncPer, vec_ok, sy2);
+    }
     for (uint64_t c = cb + warp; c < ce; c += 2 * W) {
         const uint64_t c2 = c + W;
-        uint32_t sy[kEncPer], sy2[kEncPer];
-        load_chunk_syms<SymT, false>(symp, a.n, c * kChunk + (uint64_t)lane * kEncPer, vec_ok, sy);
-        if (c2 < ce)
-            load_chunk_syms<SymT, false>(symp, a.n, c2 * kChunk + (uint64_t)lane * kEncPer, vec_ok, sy2);
+        uint32_t nx[kEncPer], nx2[kEncPer];
+        const uint64_t cn = c + 2 * W;
+        if (cn < ce)
+            load_chunk_syms<SymT, false>(symp, a.n, cn * kChunk + (uint64_t)lane * kEncPer, vec_ok, nx);
+        if (cn + W < ce)
+            load_chunk_syms<SymT, false>(symp, a.n, (cn + W) * kChunk + (uint64_t)lane * kEncPer, vec_ok, nx2);
         uint32_t b1 = 0, e1 = 0, b2 = 0, e2 = 0;
 #pragma unroll
         for (int i = 0; i < kEncPer; ++i) {
@@ -1332,6 +1357,11 @@ __global__ void __launch_bounds__(kCountThreads) k_encode_count(EncodeArgs a) {
         }
         wb += b1 + (c2 < ce ? b2 : 0u);
         we += e1 + (c2 < ce ? e2 : 0u);
+#pragma unroll
+        for (int i = 0; i < kEncPer; ++i) {
+            sy[i] = nx[i];
+            sy2[i] = nx2[i];
+        }
     }
     if (lane == 0) {
         s_red_bits[warp] = wb;

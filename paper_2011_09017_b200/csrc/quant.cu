@@ -21,6 +21,10 @@ namespace {
 // coalesced stores. The chain itself (about 90 cycles of dependent FP64 latency per element)
 // is the reference recurrence, exact.
 constexpr int kQW = 4;    // warps per CTA
+// qspec rounding of the thread-per-plane chains: magic add (1) or F2F (0)
+#ifndef ACZ_SERIAL_MAGIC
+#define ACZ_SERIAL_MAGIC 0
+#endif
 constexpr int kQT = 32;   // tile width (elements per plane)
 
 // x tiles, double-buffered; a lane overwrites the x slot it has just consumed with the
@@ -93,7 +97,7 @@ __global__ void __launch_bounds__(kQW * 32) k_quant_prev_serial(const float* __r
                         sy[u] = s;
                         if (js == jb + u + 1) st = sv;
                     };
-                    if (qspec<8>([&](int u) { return xv[u]; }, emit, r, qp)) {
+                    if (qspec<8, ACZ_SERIAL_MAGIC != 0>([&](int u) { return xv[u]; }, emit, r, qp)) {
 #pragma unroll
                         for (int u = 0; u < 8; ++u) xr[jb + u] = sy[u];
                     } else {

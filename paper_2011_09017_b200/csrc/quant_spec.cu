@@ -451,13 +451,18 @@ __device__ __noinline__ void phase_a(Smem<SymT>& S, int xoff, const float* __res
         sadd(&g_qclk[6], (unsigned long long)(t1 - t0));
         sadd(&g_qclk[7], (unsigned long long)(sclock<1>() - t1));
     }
-    // prefix C[k] = sum_{j<=k, j>0} (send[j-1] - guess[j])
-    if (lane == 0) {
-        double acc = 0.0;
-        for (int k = 0; k < S.nr; ++k) {
-            if (k > 0) acc += (double)S.send[k - 1] - (double)S.guess[k];
-            S.C[k] = acc;
+    // prefix C[k] = sum_{j<=k, j>0} (send[j-1] - guess[j]) by a warp scan (one range per
+    // lane; the terms are exact float differences on the grids of their anchors, so the
+    // partial sums are exact in any association)
+    {
+        const int nr = S.nr;
+        double tk = (lane > 0 && lane < nr) ? (double)S.send[lane - 1] - (double)S.guess[lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, tk, o);
+            if (lane >= o) tk += t;
         }
+        if (lane < nr) S.C[lane] = tk;
     }
     __syncwarp();
 }
@@ -714,11 +719,27 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     // range-start bitmap + per-word prefix: range_of() in O(1)
     if (my_start >= 0) atomicOr(&S.rsb[my_start >> 5], 1u << (my_start & 31));
     __syncwarp();
-    if (lane == 0) {
-        int run = 0;
-        for (int w = 0; w < kCapW; ++w) {
-            S.rsp[w] = (uint8_t)run;
-            run += __popc(S.rsb[w]);
+    {  // per-word prefix of range starts: warp scan over kPW words per lane
+        constexpr int kPW = (kCapW + 31) / 32;
+        int cnt[kPW], tot = 0;
+#pragma unroll
+        for (int q = 0; q < kPW; ++q) {
+            const int w = lane * kPW + q;
+            cnt[q] = w < kCapW ? __popc(S.rsb[w]) : 0;
+            tot += cnt[q];
+        }
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        int run = incl - tot;
+#pragma unroll
+        for (int q = 0; q < kPW; ++q) {
+            const int w = lane * kPW + q;
+            if (w < kCapW) S.rsp[w] = (uint8_t)run;
+            run += cnt[q];
         }
     }
     __syncwarp();
@@ -733,17 +754,20 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     // entry state).
     double lam = 0.0;
     if (MODE == kFused && j > 0) {
-        if (lane == 0) {
-            const uint64_t dmax = j < 4 ? j : 4;
-            for (uint64_t d = 1; d <= dmax; ++d) {
-                if (*((volatile unsigned*)status + sidx - d) != 0) {
-                    __threadfence();
-                    lam = (double)*((volatile float*)exits + sidx - d);
-                    break;
-                }
+        // lanes 1..4 look at predecessors j-1..j-4 at once; the nearest published one wins
+        const uint64_t dmax = j < 4 ? j : 4;
+        const bool pub = lane >= 1 && (uint64_t)lane <= dmax &&
+                         *((volatile unsigned*)status + sidx - lane) != 0;
+        const unsigned m = __ballot_sync(0xffffffffu, pub);
+        if (m) {
+            const int d = __ffs(m) - 1;
+            float e = 0.0f;
+            if (lane == d) {
+                __threadfence();
+                e = *((volatile float*)exits + sidx - d);
             }
+            lam = (double)__shfl_sync(0xffffffffu, e, d);
         }
-        lam = __shfl_sync(0xffffffffu, lam, 0);
     }
     phase_a(S, xoff, xg, seg0, 0, lam, false, 0.0f, p, qp, plane_flat0, flags, len);
     }  // !kBack
@@ -1189,6 +1213,10 @@ __global__ void __launch_bounds__(kW) k_quant_spec_back(const float* __restrict_
 // replayed end is exact. By induction over the chunks of a plane (its first element starts
 // from 0) the output is the reference's.
 constexpr int kRW = 4;   // warps per replay CTA
+// ACZ_VERIFY_MAGIC=1: the replay rounds its qspec chains by the magic add (no F2F pipe)
+#ifndef ACZ_VERIFY_MAGIC
+#define ACZ_VERIFY_MAGIC 0  // measured slower (AlexNet step 2.074 -> 2.095 ms)
+#endif
 constexpr int kRT = 32;  // tile width (elements of a chunk per tile)
 template <typename SymT>
 __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restrict__ x, SP p,
@@ -1247,7 +1275,7 @@ __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restric
                 uint32_t sy[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) xv[u] = __uint_as_float(tr[kb + u]);
-                if (qspec<8>([&](int u) { return xv[u]; },
+                if (qspec<8, ACZ_VERIFY_MAGIC != 0>([&](int u) { return xv[u]; },
                              [&](int u, uint32_t s, float) { sy[u] = s; }, r, qp)) {
 #pragma unroll
                     for (int u = 0; u < 8; ++u) tr[kb + u] = sy[u];
