@@ -52,6 +52,11 @@ constexpr int kLev = ACZ_SPEC_LEV;
 #define ACZ_SPEC_XB 8
 #endif
 constexpr int kXB = ACZ_SPEC_XB;
+// ACZ_SPEC_TMA=0: stage the segment window with per-lane cp.async instead of one bulk copy
+#ifndef ACZ_SPEC_TMA
+#define ACZ_SPEC_TMA 1
+#endif
+constexpr bool kSpecTma = ACZ_SPEC_TMA != 0;
 // state changes after which the walk re-speculates at the next range start
 #ifndef ACZ_SPEC_RESPEC
 #define ACZ_SPEC_RESPEC 12
@@ -208,7 +213,7 @@ struct alignas(16) Smem {
     uint64_t job_seg0, job_flat0;
     // staged input window (plane index j*kSeg - 1 + i); LAST: everything before it is the
     // segment state the decoupled phase-A kernel persists for the walk kernel
-    float xs[ACZ_SPEC_XS_GLOBAL ? 4 : kWin];
+    float xs[ACZ_SPEC_XS_GLOBAL ? 4 : kWin + 8];  // (+8: the bulk copy's 16-byte alignment)
 };
 
 // Per-segment header of the decoupled path (phase-A kernel -> walk kernel).
@@ -588,17 +593,47 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     };
 
     // ---- stage the input window [j*kSeg - 1, (j+1)*kSeg + kExt) into shared memory ----
-    const int64_t xbase = (int64_t)(j * kSeg) - 1;
+    // xs[i] holds plane position xbase + i
+    int64_t xbase = (int64_t)(j * kSeg) - 1;
 #if ACZ_SPEC_XS_GLOBAL
     const float* xwin = xp + xbase;  // xwin[i] == plane position xbase + i
 #else
-    for (int i = lane; i < kWin; i += kW) {
-        const int64_t pi = xbase + i;
-        if (pi >= 0 && pi < (int64_t)p.P) cp_async4(&S.xs[i], xp + pi);
-        else S.xs[i] = 0.0f;
+    {
+        // One bulk (TMA) copy of the 16-byte aligned span around the window's in-plane part
+        // [max(xbase, 0), min(xbase + kWin, P)), completed on an mbarrier; positions outside
+        // the plane are zeroed afterwards. Falls back to per-lane cp.async when the aligned
+        // span would run past the tensor's end.
+        const int64_t lo = xbase > 0 ? xbase : 0;
+        const int64_t hi = min(xbase + (int64_t)kWin, (int64_t)p.P);
+        const uintptr_t ga = reinterpret_cast<uintptr_t>(xp + lo) & ~(uintptr_t)15;
+        const uintptr_t gb = (reinterpret_cast<uintptr_t>(xp + hi) + 15) & ~(uintptr_t)15;
+        const uintptr_t gend = reinterpret_cast<uintptr_t>(x + p.planes * p.P);
+        if (kSpecTma && gb <= gend) {
+            __shared__ unsigned long long s_mbar;
+            const int64_t pa = lo - (int64_t)((reinterpret_cast<uintptr_t>(xp + lo) - ga) >> 2);
+            const unsigned bytes = (unsigned)(gb - ga);
+            if (lane == 0) {
+                mbar_init(&s_mbar, 1);
+                mbar_arrive_expect_tx(&s_mbar, bytes);
+                bulk_g2s(S.xs, reinterpret_cast<const void*>(ga), bytes, &s_mbar);
+            }
+            mbar_wait(&s_mbar, 0);
+            xbase = pa;
+            const int nld = (int)(bytes >> 2);
+            for (int i = lane; i < nld; i += kW) {
+                const int64_t pi = xbase + i;
+                if (pi < 0 || pi >= (int64_t)p.P) S.xs[i] = 0.0f;
+            }
+        } else {
+            for (int i = lane; i < kWin; i += kW) {
+                const int64_t pi = xbase + i;
+                if (pi >= 0 && pi < (int64_t)p.P) cp_async4(&S.xs[i], xp + pi);
+                else S.xs[i] = 0.0f;
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+        }
     }
-    cp_async_commit();
-    cp_async_wait<0>();
     __syncwarp();
     const float* xwin = S.xs;
 #endif
