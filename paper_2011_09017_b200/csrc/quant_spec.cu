@@ -802,6 +802,7 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
                 e = *((volatile float*)exits + sidx - d);
             }
             lam = (double)__shfl_sync(0xffffffffu, e, d);
+            if (!isfinite(lam)) lam = 0.0;  // non-finite input upstream (DomainError anyway)
         }
     }
     phase_a(S, xoff, xg, seg0, 0, lam, false, 0.0f, p, qp, plane_flat0, flags, len);
@@ -898,7 +899,9 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         if (exact_mode) {
             if (lane == 0) sadd(&g_qstats[2], 1ull);
             const int k = range_of(pos);
-            if (pos == S.rstart[k] && pos > 0) {
+            // (a non-finite state -- only after non-finite input, reported as DomainError --
+            // steps on exactly: translation from it could re-speculate forever)
+            if (pos == S.rstart[k] && pos > 0 && isfinite(T)) {
                 // exact entry T at a range start: resume translation (rebase if needed)
                 const double Dk = __dsub_rn((double)T, (double)S.guess[k]);
                 const int lk = levelD(Dk);
@@ -1091,6 +1094,14 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
             const int fk = __shfl_sync(0xffffffffu, kv, f);
             const int frb = __shfl_sync(0xffffffffu, (int)rebase, f);
             const float ftp = __shfl_sync(0xffffffffu, tprev, f);
+            if (frb && !isfinite(ftp)) {
+                // non-finite entry state (non-finite input): exact steps guarantee progress
+                exact_mode = true;
+                T = ftp;
+                rcur = fk;
+                pos = fvp;
+                continue;
+            }
             if (frb) {
                 if (lane == 0) sadd(&g_qstats[3], 1ull);
                 // lattice changed at range start fk: re-speculate ranges >= fk from the
