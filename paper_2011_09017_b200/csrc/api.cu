@@ -15,6 +15,7 @@
 #include <new>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.h"
@@ -50,6 +51,7 @@ struct Slot {
     uint32_t book_alphabet = 0;     // the last build_book's alphabet / leaf bound (book_wait)
     uint64_t book_max_leaves = 0;
     bool book_pending = false;      // a build_book whose book_wait has not run (dirty bins)
+    bool last_book_slow = false;    // the last book_wait ran the global-scratch codebook
     void* ws_cb = nullptr;
     size_t ws_cb_cap = 0;
     void* ws_status = nullptr;
@@ -93,6 +95,15 @@ struct acz_gpu_ctx {
     std::vector<cudaStream_t> pool;     // internal streams of the batched entry points
     std::vector<cudaEvent_t> pool_ev;   // one per pool stream (join)
     cudaEvent_t ev_fork = nullptr;
+    // Blob sizes of the last batched compress of each (shape, eb, radius, predictor): the
+    // next one launches its encode before the codebook read-back reaches the host, into a
+    // blob sized from these (see spec_encode).
+    struct SizePred {
+        uint32_t book;
+        uint64_t bits, nout;
+        uint32_t max_len;
+    };
+    std::unordered_map<std::string, SizePred> size_cache;
     // Sticky internal-error word in mapped pinned memory: kernels that detect an internal
     // consistency failure after the host has stopped waiting (the encoder's look-back) OR
     // kFlagInternal into it; every entry point reports it (ACZ_ERR_CUDA) and clears it.
@@ -775,6 +786,11 @@ struct Plan {
     uint64_t interval = 0;
     int sym16 = 0;
     const float* d_in = nullptr;
+    // speculative encode (spec_encode): the pre-sized blob and its capacities
+    acz_gpu_blob* spec = nullptr;
+    unsigned long long cap_bits = 0;
+    uint64_t cap_out = 0;
+    uint32_t cap_book = 0, cap_len = 0;
 };
 
 int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t* shape,
@@ -811,6 +827,7 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     if (predictor == ACZ_PRED_LORENZO2D)
         CK(grow(&sl->ws_row, &sl->ws_row_cap, 4ull * g.planes * g.cols));
     sl->last_n = n;
+    sl->last_book_slow = false;
 
     SmallBlock* sm = sl->d_small;
     CK(cudaMemsetAsync(&sm->flags, 0, sizeof(unsigned), s));
@@ -860,6 +877,7 @@ int book_wait(acz_gpu_ctx* ctx, Slot* sl, cudaStream_t s) {
     CK(cudaEventSynchronize(sl->ev_book));
     sl->book_pending = false;
     if (!sl->h_small->info.slow) return ACZ_OK;
+    sl->last_book_slow = true;
     sl->book_pending = true;
     unsigned long long* hist = static_cast<unsigned long long*>(sl->ws_hist);
     uint32_t* touched = reinterpret_cast<uint32_t*>(hist + sl->book_alphabet);
@@ -922,6 +940,139 @@ int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz
     in.compressed_bytes = acz1_size(pl.rank, bi.book_size, bi.total_bits, bi.n_escapes);
     in.device_bytes = b->arena_bytes;
     in.sidecar_bytes = sidecar_bytes(b->nchunks, b->side_outl != nullptr);
+    in.max_code_length = bi.max_len;
+    *out = b;
+    return ACZ_OK;
+}
+
+// Speculative encode (batched compress, PrevValue): the encode is enqueued right behind the
+// codebook on the tensor's stream, into a blob sized from the same tensor shape's previous
+// compress with margins (+6.25 % + 32 KB of bitstream, 2x + 4096 outliers, +1024 book
+// entries, the code-length class of the previous book). The kernels read the sizes from
+// the device BookInfo and write nothing if the book does not fit (or needed the global
+// codebook, or flagged an error); the host, which still reads every book back, then
+// re-encodes that tensor into an exactly sized blob (spec_finish). The GPU thus never waits
+// for the host between a tensor's codebook and its encode.
+std::string size_key(const Plan& pl) {
+    std::string k(reinterpret_cast<const char*>(pl.shape), 8 * pl.rank);
+    k.append(reinterpret_cast<const char*>(&pl.eb), 8);
+    k.append(reinterpret_cast<const char*>(&pl.radius), 4);
+    k.append(reinterpret_cast<const char*>(&pl.predictor), 4);
+    return k;
+}
+
+bool spec_encode_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ACZ_SPEC_ENCODE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+int spec_encode(acz_gpu_ctx* ctx, Slot* sl, Plan* pl, const acz_gpu_ctx::SizePred& pr,
+                cudaStream_t s) {
+    const uint64_t n = pl->n, interval = pl->interval;
+    const uint64_t nchunks = (n + interval - 1) / interval;
+    pl->cap_book = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(sl->book_max_leaves, kMaxBook),
+                                                 (uint64_t)pr.book + 1024);
+    pl->cap_bits = pr.bits + pr.bits / 16 + 262144;
+    pl->cap_out = pr.nout * 2 + 4096;
+    pl->cap_len = pr.max_len <= 27 ? 27u : pr.max_len <= 32 ? 32u : 56u;
+    const uint64_t nwords = (pl->cap_bits + 31) / 32;
+    acz_gpu_blob* b = new (std::nothrow) acz_gpu_blob();
+    if (!b) return fail(ctx, ACZ_ERR_NOMEM, "blob");
+    if (cudaError_t e = blob_alloc(b, pl->cap_book, nwords, pl->cap_out, nchunks, false, s)) {
+        delete b;
+        return cuda_fail(ctx, e, "spec blob");
+    }
+    b->interval = interval;
+    b->nchunks = nchunks;
+    const uint32_t* wb_sym = static_cast<const uint32_t*>(sl->ws_book);
+    const uint8_t* wb_len =
+        reinterpret_cast<const uint8_t*>(wb_sym + std::max<uint64_t>(sl->ws_book_cap / 5, 1));
+    CopyRegions cr{};
+    auto add = [&](const void* src, void* dst, uint64_t bytes) {
+        cr.src[cr.n] = src;
+        cr.dst[cr.n] = dst;
+        cr.bytes[cr.n] = bytes;
+        ++cr.n;
+    };
+    add(wb_sym, b->book_sym, 4ull * pl->cap_book);
+    add(wb_len, b->book_len, pl->cap_book);
+    add(sl->d_small->lut, b->lut, 4ull * kLutSize);
+    add(&sl->d_small->canon, b->canon, sizeof(CanonTables));
+    add(sl->ws_side, b->side_state, 4ull * nchunks);
+    int rc = ACZ_OK;
+    if (cudaError_t e = launch_copy_regions(cr, ctx->sms, s, &ctx->launches)) rc = cuda_fail(ctx, e, "spec copy");
+    EncodeArgs ea;
+    ea.sym = sl->ws_sym;
+    ea.sym16 = pl->sym16;
+    ea.n = n;
+    ea.enc = static_cast<const unsigned long long*>(sl->ws_enc);
+    ea.enc32 = reinterpret_cast<const uint32_t*>(ea.enc + sl->enc_alphabet);
+    ea.x = pl->d_in;
+    ea.words = b->words;
+    ea.nwords = nwords;
+    ea.out_index = b->out_index;
+    ea.out_value = b->out_value;
+    ea.side_bitoff = b->side_bitoff;
+    ea.side_outl = nullptr;
+    ea.interval = interval;
+    ea.max_len = pl->cap_len;
+    ea.status = static_cast<TileStatus*>(sl->ws_status);
+    ea.sticky = ctx->d_sticky;
+    ea.spec_info = &sl->d_small->info;
+    ea.cap_bits = pl->cap_bits;
+    ea.cap_out = pl->cap_out;
+    ea.cap_book = pl->cap_book;
+    ea.cap_len = pl->cap_len;
+    if (!rc) {
+        KTimer kt(ctx, ACZ_K_ENCODE, s);
+        if (cudaError_t e = launch_encode(ea, ctx->sms, s, &ctx->launches)) rc = cuda_fail(ctx, e, "spec encode");
+    }
+    if (const int lr = slot_leave(ctx, sl, s)) rc = rc ? rc : lr;
+    if (rc) {
+        blob_arena_free(b, s);
+        delete b;
+        return rc;
+    }
+    pl->spec = b;
+    return ACZ_OK;
+}
+
+// Second half of a speculatively encoded tensor: the book read-back decides whether the
+// blob holds the encode (fill in its sizes) or the tensor is re-encoded exactly.
+int spec_finish(acz_gpu_ctx* ctx, Slot* sl, Plan& pl, cudaStream_t s, acz_gpu_blob** out) {
+    acz_gpu_blob* b = pl.spec;
+    pl.spec = nullptr;
+    int rc = book_wait(ctx, sl, s);
+    if (!rc) rc = check_sticky(ctx);
+    const BookInfo bi = sl->h_small->info;
+    const unsigned flags = sl->h_small->flags | bi.flags;
+    const bool fits = !rc && !flags && !sl->last_book_slow && bi.book_size >= 1 &&
+                      bi.total_bits <= pl.cap_bits && bi.n_escapes <= pl.cap_out &&
+                      bi.book_size <= pl.cap_book && bi.max_len <= pl.cap_len;
+    if (!fits) {
+        blob_arena_free(b, s);
+        delete b;
+        return rc ? rc : compress_end(ctx, sl, pl, s, out);
+    }
+    b->nwords = (bi.total_bits + 31) / 32;
+    b->max_len = bi.max_len;
+    acz_gpu_blob_info_t& in = b->info;
+    in.rank = pl.rank;
+    for (uint32_t i = 0; i < pl.rank; ++i) in.shape[i] = pl.shape[i];
+    in.eb = pl.eb;
+    in.quant_radius = pl.radius;
+    in.predictor = pl.predictor;
+    in.element_count = pl.n;
+    in.codebook_size = bi.book_size;
+    in.bit_length = bi.total_bits;
+    in.outlier_count = bi.n_escapes;
+    in.uncompressed_bytes = 4ull * pl.n;
+    in.compressed_bytes = acz1_size(pl.rank, bi.book_size, bi.total_bits, bi.n_escapes);
+    in.device_bytes = b->arena_bytes;
+    in.sidecar_bytes = sidecar_bytes(b->nchunks, false);
     in.max_code_length = bi.max_len;
     *out = b;
     return ACZ_OK;
@@ -1114,6 +1265,10 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
         }
         st[i] = compress_begin(ctx, sl, d_in[i], shapes + off[i], ranks[i], eb, quant_radius,
                                predictor, ts[i], &plans[i]);
+        if (st[i] == ACZ_OK && predictor == ACZ_PRED_PREV && spec_encode_enabled()) {
+            auto it = ctx->size_cache.find(size_key(plans[i]));
+            if (it != ctx->size_cache.end()) st[i] = spec_encode(ctx, sl, &plans[i], it->second, ts[i]);
+        }
     }
     // second halves in completion order: a tensor's encode is launched as soon as its own
     // codebook read-back has landed, so short tensors do not queue behind a long quantiser
@@ -1122,8 +1277,16 @@ int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const*
     std::vector<char> done(count, 0);
     uint32_t remaining = count;
     auto finish = [&](uint32_t i) {
-        if (st[i] == ACZ_OK)
-            st[i] = compress_end(ctx, get_slot(ctx, i), plans[i], ts[i], &out[i]);
+        if (st[i] == ACZ_OK) {
+            Slot* sl = get_slot(ctx, i);
+            st[i] = plans[i].spec ? spec_finish(ctx, sl, plans[i], ts[i], &out[i])
+                                  : compress_end(ctx, sl, plans[i], ts[i], &out[i]);
+            if (st[i] == ACZ_OK && predictor == ACZ_PRED_PREV) {
+                const acz_gpu_blob_info_t& in = out[i]->info;
+                ctx->size_cache[size_key(plans[i])] = {in.codebook_size, in.bit_length,
+                                                       in.outlier_count, in.max_code_length};
+            }
+        }
         if (st[i] != ACZ_OK && first_err == ACZ_OK) {
             first_err = st[i];
             first_msg = ctx->err;

@@ -1308,6 +1308,8 @@ __global__ void __launch_bounds__(kCountThreads) k_encode_count(EncodeArgs a) {
     const uint64_t cb = (uint64_t)blockIdx.x * span, ce = min(chunks, cb + span);
     const bool vec_ok = (reinterpret_cast<uintptr_t>(symp) & 15) == 0;
     unsigned long long* coff = a.chunk_off;
+    uint64_t nwords_dev = a.nwords;
+    if (!encode_spec_ok(a, &nwords_dev)) return;  // speculative launch, book does not fit
 
     // ---- per-chunk counts (two chunks in flight per warp) -----------------------------
     unsigned long long wb = 0, we = 0;
@@ -1470,7 +1472,7 @@ __global__ void __launch_bounds__(kCountThreads) k_encode_count(EncodeArgs a) {
         // the stream's last partial word and the decoder's read-ahead padding
         const unsigned long long total = run_b;
         const uint64_t w0 = total >> 5;
-        for (uint64_t w = w0 + tid; w < a.nwords + 32; w += kCountThreads) a.words[w] = 0u;
+        for (uint64_t w = w0 + tid; w < nwords_dev + 32; w += kCountThreads) a.words[w] = 0u;
     }
 }
 
@@ -1484,6 +1486,10 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_write(EncodeArgs a, uint
     uint32_t* stage = stage_all + warp * stage_words;
     const uint64_t chunks = (a.n + kChunk - 1) / kChunk;
     const bool vec_ok = (reinterpret_cast<uintptr_t>(symp) & 15) == 0;
+    {
+        uint64_t nw;
+        if (!encode_spec_ok(a, &nw)) return;  // speculative launch, book does not fit
+    }
     // PrevValue sidecar intervals are powers of two >= kEncPer: at most one sidecar point per
     // lane, at its first symbol; other intervals (Lorenzo2d: the plane size) take the general
     // per-symbol path

@@ -129,7 +129,24 @@ struct EncodeArgs {
     TileStatus* status;              // encode_scratch_bytes(n, sms) of scratch (look-back + chunk offsets)
     unsigned int* sticky;            // mapped host word: kFlagInternal on a look-back timeout
     unsigned long long* chunk_off;   // set by the launcher (inside the scratch)
+    // Speculative launch (before the host has read the codebook back): the sizes come from
+    // the device BookInfo, and the kernels write nothing unless the book fits the blob's
+    // capacities (the host then re-encodes into an exactly sized blob). nullptr: host sizes.
+    const BookInfo* spec_info = nullptr;
+    unsigned long long cap_bits = 0;
+    uint64_t cap_out = 0;
+    uint32_t cap_book = 0, cap_len = 0;
 };
+// true when a speculatively launched encode may run (see EncodeArgs::spec_info); nwords out
+__device__ __forceinline__ bool encode_spec_ok(const EncodeArgs& a, uint64_t* nwords) {
+    if (!a.spec_info) return true;
+    const BookInfo& bi = *a.spec_info;
+    const bool ok = !bi.slow && !bi.flags && bi.book_size > 0 && bi.total_bits <= a.cap_bits &&
+                    bi.n_escapes <= a.cap_out && bi.book_size <= a.cap_book &&
+                    bi.max_len <= a.cap_len;
+    *nwords = (bi.total_bits + 31) / 32;
+    return ok;
+}
 constexpr int kEncThreads = 256;
 constexpr int kEncPer = 8;
 constexpr int kEncTile = kEncThreads * kEncPer;

@@ -101,3 +101,30 @@ def test_host_batch_decompress_errors(acz, oracle):
     # output buffer too small
     with pytest.raises(acz.ShapeError, match="output buffer too small"):
         acz.decompress_host_many([res[0]], True, outs=[torch.empty(3).pin_memory()])
+
+
+@pytest.mark.parametrize("order", ["grow", "shrink"])
+def test_batch_speculative_encode_sizes(acz, oracle, order):
+    """A repeated batched compress launches each tensor's encode before the host has read its
+    codebook back, into a blob sized from the previous call of the same shapes. A book that
+    outgrows that blob (far more bits / outliers / symbols than last time: "grow") is
+    re-encoded exactly; one that shrinks keeps the speculative blob. Either way the bytes are
+    the oracle's, the sizes reported are exact, and the blob decompresses bit-exactly."""
+    import torch
+    rng = np.random.default_rng(5)
+    shapes = [(4, 3, 97, 131), (16, 32, 27, 27), (3001,)]
+    calm = [np.maximum(rng.standard_normal(s), 0).astype(np.float32) * 1e-3 for s in shapes]
+    wild = [(rng.standard_normal(s) * np.exp(rng.standard_normal(s) * 2)).astype(np.float32)
+            for s in shapes]
+    first, second = (calm, wild) if order == "grow" else (wild, calm)
+    p = acz.CodecParams(1e-3, 64)  # small radius: the wild data escapes a lot
+    for xs in (first, second, second):
+        ts = [torch.from_numpy(x).cuda() for x in xs]
+        blobs = acz.compress_many(ts, p)
+        outs = acz.decompress_many(blobs, zero_filter=True)
+        torch.cuda.synchronize()
+        for x, c, o in zip(xs, blobs, outs):
+            ref = oracle.compress(x, 1e-3, 64)
+            assert c.to_bytes() == ref.blob
+            assert c.compressed_bytes == len(ref.blob)
+            assert o.cpu().numpy().ravel().tobytes() == oracle.decompress(ref.blob, x.size, True).tobytes()
