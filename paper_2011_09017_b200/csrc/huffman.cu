@@ -1331,15 +1331,26 @@ __global__ void __launch_bounds__(kCountThreads) k_encode_count(EncodeArgs a) {
         if (cn + W < ce)
             load_chunk_syms<SymT, false>(symp, a.n, (cn + W) * kChunk + (uint64_t)lane * kEncPer, vec_ok, nx2);
         uint32_t b1 = 0, e1 = 0, b2 = 0, e2 = 0;
+        if (c2 < ce && (c2 + 1) * kChunk <= a.n) {
+            // both chunks whole (every pair but the span's and the tensor's last): no bounds
 #pragma unroll
-        for (int i = 0; i < kEncPer; ++i) {
-            if (c * kChunk + (uint64_t)lane * kEncPer + i < a.n) {
+            for (int i = 0; i < kEncPer; ++i) {
                 b1 += code_len<kCompact>(a, sy[i]);
                 e1 += sy[i] == 0;
-            }
-            if (c2 < ce && c2 * kChunk + (uint64_t)lane * kEncPer + i < a.n) {
                 b2 += code_len<kCompact>(a, sy2[i]);
                 e2 += sy2[i] == 0;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kEncPer; ++i) {
+                if (c * kChunk + (uint64_t)lane * kEncPer + i < a.n) {
+                    b1 += code_len<kCompact>(a, sy[i]);
+                    e1 += sy[i] == 0;
+                }
+                if (c2 < ce && c2 * kChunk + (uint64_t)lane * kEncPer + i < a.n) {
+                    b2 += code_len<kCompact>(a, sy2[i]);
+                    e2 += sy2[i] == 0;
+                }
             }
         }
 #pragma unroll

@@ -700,11 +700,19 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     // [max(j*Seg + l*L, b0), j*Seg + (l+1)*L) if that start lies before b1
     {
         const uint64_t nb = j * kSeg;
+        // 32-position words, 16 at a time (independent loads in flight); word w goes to
+        // lane w % 32's register and is stored once per 32 words
+        const int64_t xl = (int64_t)nb + lane - xbase;
+        uint32_t mine = 0;
+#pragma unroll 16
         for (int w = 0; w < kSeg / 32; ++w) {
             const uint64_t i = nb + (uint64_t)w * 32 + lane;
-            const bool a = i < p.P && is_anchor(xwin[(int64_t)i - xbase], p.anchor_min);
+            const bool a = i < p.P && is_anchor(xwin[xl + (int64_t)w * 32], p.anchor_min);
             const unsigned m = __ballot_sync(0xffffffffu, a);
-            if (lane == 0) S.abits[w] = m;
+            if ((w & 31) == lane) mine = m;
+            if ((w & 31) == 31) {
+                S.abits[w - 31 + lane] = mine;
+            }
         }
         __syncwarp();
     }
