@@ -592,6 +592,17 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
         }
     };
 
+    // Lattice origin of phase A (see below): lanes 1..4 load the status and exit of the
+    // predecessors j-1..j-4 here, so the L2 round trip overlaps the window's bulk copy; the
+    // nearest published one is picked after the copy. (The exit is read without waiting for
+    // its status: a stale value only costs a worse origin -- the walk's entry offset is
+    // computed from the exit read under the look-back's ordering.)
+    unsigned pre_st = 0;
+    float pre_ex = 0.0f;
+    if (MODE == kFused && j > 0 && lane >= 1 && (uint64_t)lane <= (j < 4 ? j : 4)) {
+        pre_st = *((volatile unsigned*)status + sidx - lane);
+        pre_ex = *((volatile float*)exits + sidx - lane);
+    }
     // ---- stage the input window [j*kSeg - 1, (j+1)*kSeg + kExt) into shared memory ----
     // xs[i] holds plane position xbase + i
     int64_t xbase = (int64_t)(j * kSeg) - 1;
@@ -796,20 +807,10 @@ __device__ float spec_segment(Smem<SymT>& S, const float* __restrict__ x, const 
     // thousands of elements back, often does not (then phase A is redone from the exact
     // entry state).
     double lam = 0.0;
-    if (MODE == kFused && j > 0) {
-        // lanes 1..4 look at predecessors j-1..j-4 at once; the nearest published one wins
-        const uint64_t dmax = j < 4 ? j : 4;
-        const bool pub = lane >= 1 && (uint64_t)lane <= dmax &&
-                         *((volatile unsigned*)status + sidx - lane) != 0;
-        const unsigned m = __ballot_sync(0xffffffffu, pub);
+    {
+        const unsigned m = __ballot_sync(0xffffffffu, pre_st != 0);
         if (m) {
-            const int d = __ffs(m) - 1;
-            float e = 0.0f;
-            if (lane == d) {
-                __threadfence();
-                e = *((volatile float*)exits + sidx - d);
-            }
-            lam = (double)__shfl_sync(0xffffffffu, e, d);
+            lam = (double)__shfl_sync(0xffffffffu, pre_ex, __ffs(m) - 1);
             if (!isfinite(lam)) lam = 0.0;  // non-finite input upstream (DomainError anyway)
         }
     }
@@ -1193,8 +1194,8 @@ __global__ void __maxnreg__(112) k_quant_spec(const float* __restrict__ x, SP p,
     __shared__ Smem<SymT> S;
     __shared__ unsigned s_tk;
     QParams qp;
+    if (threadIdx.x == 0) s_tk = atomicAdd(ticket, 1u);  // (in flight with the B load)
     spec_params(p, qp, dB);
-    if (threadIdx.x == 0) s_tk = atomicAdd(ticket, 1u);
     __syncthreads();
     const unsigned long long seg_id = s_tk;
     if (seg_id >= total_segs) return;
