@@ -104,13 +104,14 @@ def test_host_batch_decompress_errors(acz, oracle):
 
 
 @pytest.mark.parametrize("order", ["grow", "shrink"])
-def test_batch_speculative_encode_sizes(acz, oracle, order):
+def test_batch_speculative_encode_sizes(acz, oracle, order, monkeypatch):
     """A repeated batched compress launches each tensor's encode before the host has read its
     codebook back, into a blob sized from the previous call of the same shapes. A book that
     outgrows that blob (far more bits / outliers / symbols than last time: "grow") is
     re-encoded exactly; one that shrinks keeps the speculative blob. Either way the bytes are
     the oracle's, the sizes reported are exact, and the blob decompresses bit-exactly."""
     import torch
+    monkeypatch.setenv("ACZ_SPEC_ENCODE", "1")
     rng = np.random.default_rng(5)
     shapes = [(4, 3, 97, 131), (16, 32, 27, 27), (3001,)]
     calm = [np.maximum(rng.standard_normal(s), 0).astype(np.float32) * 1e-3 for s in shapes]
