@@ -55,7 +55,12 @@ __global__ void __launch_bounds__(kQW * 32) k_quant_prev_serial(const float* __r
         if (lane < cnt) {
             const float* src = xw + j0 + lane;
             uint32_t* dst = &S.xs[w][t & 1][0][lane];
-            for (int p = 0; p < np; ++p, src += P, dst += kQT + 1) cp_async4(dst, src);
+            if (np == 32) {  // (every warp but the last: unrolled, all copies in flight)
+#pragma unroll
+                for (int p = 0; p < 32; ++p) cp_async4(dst + p * (kQT + 1), src + (uint64_t)p * P);
+            } else {
+                for (int p = 0; p < np; ++p, src += P, dst += kQT + 1) cp_async4(dst, src);
+            }
         }
         cp_async_commit();
     };
@@ -128,7 +133,15 @@ __global__ void __launch_bounds__(kQW * 32) k_quant_prev_serial(const float* __r
         if (lane < cnt) {
             SymT* dst = sw + j0 + lane;
             const uint32_t* src = &S.xs[w][t & 1][0][lane];
-            for (int p = 0; p < np; ++p, dst += P, src += kQT + 1) *dst = (SymT)*src;
+            if (np == 32) {  // unrolled: the 32 shared loads issue before the stores
+                SymT v[32];
+#pragma unroll
+                for (int p = 0; p < 32; ++p) v[p] = (SymT)src[p * (kQT + 1)];
+#pragma unroll
+                for (int p = 0; p < 32; ++p) dst[(uint64_t)p * P] = v[p];
+            } else {
+                for (int p = 0; p < np; ++p, dst += P, src += kQT + 1) *dst = (SymT)*src;
+            }
         }
         __syncwarp();
     }
