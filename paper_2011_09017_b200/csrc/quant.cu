@@ -25,6 +25,11 @@ constexpr int kQW = 4;    // warps per CTA
 #ifndef ACZ_SERIAL_MAGIC
 #define ACZ_SERIAL_MAGIC 0
 #endif
+// qspec blocks of a tile unrolled (the next block's loads overlap the current chain)
+#ifndef ACZ_SERIAL_BLOCK_UNROLL
+#define ACZ_SERIAL_BLOCK_UNROLL 4
+#endif
+constexpr int kSerialBlockUnroll = ACZ_SERIAL_BLOCK_UNROLL;
 constexpr int kQT = 32;   // tile width (elements per plane)
 
 // x tiles, double-buffered; a lane overwrites the x slot it has just consumed with the
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(kQW * 32) k_quant_prev_serial(const float* __r
             if (js >= 0) next_side += interval;
             if (cnt == kQT) {
                 // whole tile: blocks of 8 speculative steps (qspec), exact redo on a miss
-#pragma unroll 1
+#pragma unroll kSerialBlockUnroll
                 for (int jb = 0; jb < kQT; jb += 8) {
                     float xv[8];
 #pragma unroll
