@@ -183,6 +183,33 @@ def run_ours(args, rank, world, local_rank):
     B_all = tot.item()  # bytes per step over all ranks
     value = B_all * args.steps / (ms_max * 1e-3) / 1e9
 
+    # ---- compress and decompress timed separately (4n/T_c and 4n/T_d; an
+    # extra pass after the timed region, events on the launching stream) ----
+    split = None
+    if world == 1:
+        tc = td = 0.0
+        reps = max(3, min(args.steps, 10))
+        for _ in range(reps):
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a2 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            bl = acz.compress_many(tensors, params, stream=stream, ctx=ctx)
+            a1.record(stream)
+            acz.decompress_many(bl, zero_filter=True, outs=outs, stream=stream)
+            a2.record(stream)
+            torch.cuda.synchronize()
+            tc += a0.elapsed_time(a1)
+            td += a1.elapsed_time(a2)
+            del bl
+        tc /= reps
+        td /= reps
+        split = {"compress_ms": tc, "decompress_ms": td,
+                 "compress_gbps_4n": 4 * n_total / (tc * 1e-3) / 1e9,
+                 "decompress_gbps_4n": 4 * n_total / (td * 1e-3) / 1e9,
+                 "note": "compress_many and decompress_many timed separately (events); "
+                         "4n / T over the fp32 activation bytes (SURVEY 8(d))"}
+
     # ---- per-kernel times (separate passes with event timing around every launch) ----
     kms = (C.c_double * 7)()
     kn = (C.c_uint64 * 7)()
@@ -236,7 +263,7 @@ def run_ours(args, rank, world, local_rank):
     ctx.trim()
     memory["workspace_bytes_after_trim"] = ctx.memory_info()["workspace_bytes"]
     res = dict(host=host, value=value, ms_per_step=ms_max / args.steps, n=n_total, cbytes=cbytes,
-               memory=memory,
+               memory=memory, split=split,
                B_step=8 * n_total + 2 * cbytes, launches=launches, clocks=clk, kernels=kern,
                detail=detail, ratio=ratios_in / ratios_out, batch=batch, per_tensor=per_tensor)
 
@@ -280,7 +307,7 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------------------ CPU reference ----
-TRAFFIC_JSON = os.path.join("profiles", "r02", "v3", "traffic.json")
+TRAFFIC_JSON = os.path.join("profiles", "r02", "v5", "traffic.json")
 ONE_THREAD_SAMPLES = 16  # 1-thread leg: the first 16 samples of every tensor (~2-3 s)
 
 
@@ -459,6 +486,7 @@ def main():
                              "alone with CUDA events around every launch",
             "gpu_launches": res["launches"],
             "memory": res["memory"],
+            "compress_decompress_split": res.get("split"),
             "clocks": res["clocks"],
             "detail": res["detail"],
         }
