@@ -213,7 +213,7 @@ struct alignas(16) Smem {
     uint64_t job_seg0, job_flat0;
     // staged input window (plane index j*kSeg - 1 + i); LAST: everything before it is the
     // segment state the decoupled phase-A kernel persists for the walk kernel
-    float xs[ACZ_SPEC_XS_GLOBAL ? 4 : kWin + 8];  // (+8: the bulk copy's 16-byte alignment)
+    alignas(16) float xs[ACZ_SPEC_XS_GLOBAL ? 4 : kWin + 8];  // (+8: the bulk copy's 16-byte alignment)
 };
 
 // Per-segment header of the decoupled path (phase-A kernel -> walk kernel).
