@@ -268,7 +268,9 @@ def run_ours(args, rank, world, local_rank):
                detail=detail, ratio=ratios_in / ratios_out, batch=batch, per_tensor=per_tensor)
 
     # ---- e2e through the public host-buffer API (page-locked host memory in and out) ----
-    if not args.no_e2e and rank == 0:
+    # every rank runs it at once (each GPU through its own host link), timed per rank on the
+    # host around synchronised steps; the job's value is all ranks' bytes / the slowest rank
+    if not args.no_e2e:
         hin = [torch.empty(x.shape, dtype=torch.float32, pin_memory=True) for x in tensors]
         for h, x in zip(hin, tensors):
             h.copy_(x)
@@ -290,13 +292,23 @@ def run_ours(args, rank, world, local_rank):
 
         e2e_step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             h2d, d2h, cb = e2e_step()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        res["e2e"] = {"value": (8 * n_total + 2 * cb) * args.e2e_steps / dt / 1e9, "unit": "GB/s",
-                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+        agg = torch.tensor([dt, float(8 * n_total + 2 * cb), float(h2d), float(d2h)],
+                           dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = agg[:1].clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+            agg[0] = mx[0]
+        dt, b_all, h2d, d2h = agg[0].item(), agg[1].item(), int(agg[2].item()), int(agg[3].item())
+        res["e2e"] = {"value": b_all * args.e2e_steps / dt / 1e9, "unit": "GB/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ranks": world,
                       "path": "compress_host_many + decompress_host_many (C-ABI "
                               "acz_gpu_compress_host_batch / acz_gpu_decompress_host_batch; "
                               "page-locked host buffers, copies inside the timed region)"}
