@@ -196,13 +196,28 @@ __global__ void __launch_bounds__(256) k_blob_digest(const uint32_t* __restrict_
                                                      uint64_t nbytes, uint64_t h0,
                                                      unsigned long long* out) {
     __shared__ unsigned long long s_sum;
+    __shared__ uint64_t s_v[64];
     if (threadIdx.x == 0) s_sum = 0ull;
+    // the 64 bitstream samples of acz_bits_digest, loaded by 64 threads at once (one thread
+    // loading them in its mixing loop waits out 64 memory round trips)
+    if (threadIdx.x < 64) {
+        const uint64_t i = threadIdx.x;
+        const uint64_t pos = nbytes >= 8 ? (nbytes - 8) * i / 63 : 0;
+        uint64_t v = 0;
+        for (int j = 0; j < 8; ++j)
+            if (pos + j < nbytes) v |= (uint64_t)bits[pos + j] << (8 * j);
+        s_v[i] = v;
+    }
     __syncthreads();
     unsigned long long t = 0;
     for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) t += acz_book_term(bsym[i], blen[i], i);
     atomicAdd(&s_sum, t);  // integer sum mod 2^64: order-independent
     __syncthreads();
-    if (threadIdx.x == 0) *out = acz_binding(h0, s_sum, acz_bits_digest(bits, nbytes));
+    if (threadIdx.x == 0) {
+        uint64_t h = acz_mix64(nbytes);  // == acz_bits_digest(bits, nbytes)
+        for (int i = 0; i < 64; ++i) h = acz_mix64(h ^ (s_v[i] + (uint64_t)i));
+        *out = acz_binding(h0, s_sum, h);
+    }
 }
 
 }  // namespace

@@ -305,6 +305,25 @@ def test_sidecar_roundtrip(acz):
     assert c3.sidecar() == s
 
 
+def test_exported_sidecar_is_accepted(acz):
+    # the binding a blob's exported sidecar carries (k_blob_digest on the device) equals the
+    # one the parser recomputes on the host (acz_bits_digest): the sidecar is used as is,
+    # no kernel rebuilds it (a mismatch would fall back to the scan decode, same bytes)
+    rng = np.random.default_rng(8)
+    ctx = acz.default_context()
+    for shape in ((4, 8, 30, 30), (2, 3, 227, 227), (1, 1, 1, 5)):
+        x = _gpu(np.maximum(rng.standard_normal(shape), 0))
+        c = acz.compress(x, acz.CodecParams(1e-3))
+        b, s = c.to_bytes(), c.sidecar()
+        l0 = ctx.launches
+        acz.blob_from_bytes(b, s)
+        l1 = ctx.launches
+        acz.blob_from_bytes(b)
+        l2 = ctx.launches
+        assert l1 - l0 < l2 - l1, shape
+
+
+
 
 def _err(fn):
     """(reference-style error code, message) of a call; (0, "") when it succeeds."""
