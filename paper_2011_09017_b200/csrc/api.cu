@@ -49,6 +49,7 @@ struct Slot {
     size_t ws_enc_cap = 0;
     uint32_t enc_alphabet = 0;
     uint32_t book_alphabet = 0;     // the last build_book's alphabet / leaf bound (book_wait)
+    uint32_t book_center = 0;       // its centre symbol (the zero residual)
     uint64_t book_max_leaves = 0;
     bool book_pending = false;      // a build_book whose book_wait has not run (dirty bins)
     bool last_book_slow = false;    // the last book_wait ran the global-scratch codebook
@@ -609,6 +610,15 @@ int acz_gpu_ctx_trim(acz_gpu_ctx* ctx) {
 // ----------------------------------------------------------------------- compress --
 namespace {
 
+// Symbols whose code lengths the counting pass stages in shared memory: kEncLenWindow
+// symbols centred on the book's centre symbol (every symbol of a book at eb >= ~1e-4 on
+// unit-scale data; the rest are looked up in the global tables).
+void set_len_window(EncodeArgs& ea, const Slot* sl) {
+    const uint32_t a = sl->enc_alphabet, half = (uint32_t)kEncLenWindow / 2;
+    ea.len_lo = sl->book_center > half ? sl->book_center - half : 0u;
+    ea.len_n = ea.len_lo < a ? std::min<uint32_t>((uint32_t)kEncLenWindow, a - ea.len_lo) : 0u;
+}
+
 // Blob-side finalisation shared by compress and the generic Huffman encoder: after the
 // codebook sync, allocates the blob, copies the tables and runs K5.
 int finish_encode(acz_gpu_ctx* ctx, Slot* sl, acz_gpu_blob* b, const void* d_sym, int sym16,
@@ -646,6 +656,7 @@ int finish_encode(acz_gpu_ctx* ctx, Slot* sl, acz_gpu_blob* b, const void* d_sym
     ea.n = n;
     ea.enc = static_cast<const unsigned long long*>(sl->ws_enc);
     ea.enc32 = reinterpret_cast<const uint32_t*>(ea.enc + sl->enc_alphabet);
+    set_len_window(ea, sl);
     ea.x = d_x;
     ea.words = b->words;
     ea.nwords = nwords;
@@ -680,6 +691,7 @@ int build_book(acz_gpu_ctx* ctx, Slot* sl, const void* d_sym, int sym16, uint64_
     uint32_t* touched = reinterpret_cast<uint32_t*>(hist + alphabet);
     CK(grow(&sl->ws_enc, &sl->ws_enc_cap, 12ull * alphabet));  // u64 table + u32 compact table
     sl->enc_alphabet = alphabet;
+    sl->book_center = center;
     CK(grow(&sl->ws_cb, &sl->ws_cb_cap, codebook_scratch_bytes(max_leaves)));
     CK(grow(&sl->ws_book, &sl->ws_book_cap, 5ull * max_leaves + 64));
     CK(grow(&sl->ws_status, &sl->ws_status_cap, encode_scratch_bytes(n, ctx->sms)));
@@ -1010,6 +1022,7 @@ int spec_encode(acz_gpu_ctx* ctx, Slot* sl, Plan* pl, const acz_gpu_ctx::SizePre
     ea.n = n;
     ea.enc = static_cast<const unsigned long long*>(sl->ws_enc);
     ea.enc32 = reinterpret_cast<const uint32_t*>(ea.enc + sl->enc_alphabet);
+    set_len_window(ea, sl);
     ea.x = pl->d_in;
     ea.words = b->words;
     ea.nwords = nwords;

@@ -136,6 +136,9 @@ struct EncodeArgs {
     unsigned long long cap_bits = 0;
     uint64_t cap_out = 0;
     uint32_t cap_book = 0, cap_len = 0;
+    // symbols [len_lo, len_lo + len_n) (len_n <= kEncLenWindow) have their code lengths
+    // staged in shared memory by the counting pass; others are looked up in enc / enc32
+    uint32_t len_lo = 0, len_n = 0;
 };
 // true when a speculatively launched encode may run (see EncodeArgs::spec_info); nwords out
 __device__ __forceinline__ bool encode_spec_ok(const EncodeArgs& a, uint64_t* nwords) {
@@ -148,6 +151,10 @@ __device__ __forceinline__ bool encode_spec_ok(const EncodeArgs& a, uint64_t* nw
     return ok;
 }
 constexpr int kEncThreads = 256;
+#ifndef ACZ_ENC_LEN_WINDOW
+#define ACZ_ENC_LEN_WINDOW 16384
+#endif
+constexpr int kEncLenWindow = ACZ_ENC_LEN_WINDOW;  // 0: no staged code lengths
 constexpr int kEncPer = 8;
 constexpr int kEncTile = kEncThreads * kEncPer;
 size_t encode_scratch_bytes(uint64_t n, int sms);
