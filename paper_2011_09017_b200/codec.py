@@ -337,6 +337,72 @@ def compress(t, p: CodecParams = CodecParams(), stream=None,
     return CompressedTensor(h, ctx)
 
 
+class AsyncCompress:
+    """An asynchronous compress in flight (acz_gpu_compress_async): nothing waits for the
+    GPU until :meth:`settle`. The input tensor is kept referenced until then, so that a
+    blob that outgrew its predicted size can be compressed again from it."""
+
+    def __init__(self, t, p: CodecParams, stream, ctx: "Context", h, pending: bool):
+        self._ctx, self._p, self._stream = ctx, p, stream
+        self._h = h if pending else None
+        self._t = t if pending else None
+        self.result: Optional[CompressedTensor] = None if pending else CompressedTensor(h, ctx)
+        self.refits = 0
+
+    @property
+    def pending(self) -> bool:
+        return self.result is None
+
+    def settle(self, wait: bool = True) -> Optional[CompressedTensor]:
+        """The CompressedTensor (bit-identical to :func:`compress`), or None while the
+        compress has not finished (wait=False). Raises the errors compress() raises."""
+        if self.result is not None:
+            return self.result
+        st = C.c_int(0)
+        lib = _native.load()
+        rc = lib.acz_gpu_compress_settle(self._ctx.handle, self._h, int(bool(wait)), C.byref(st))
+        if rc == 0 and st.value == 0:
+            return None
+        if rc == 0 and st.value == 1:
+            self.result = CompressedTensor(self._h, self._ctx)
+            self._h = self._t = None
+            return self.result
+        # did not fit its predicted size (or failed): free it, compress synchronously
+        lib.acz_gpu_blob_free(self._h)
+        self._h = None
+        self.refits += 1
+        self.result = compress(self._t, self._p, stream=self._stream, ctx=self._ctx)
+        self._t = None
+        return self.result
+
+    def __del__(self):
+        try:
+            if self._h:
+                _native.load().acz_gpu_blob_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def compress_async(t, p: CodecParams = CodecParams(), stream=None,
+                   ctx: Optional[Context] = None) -> AsyncCompress:
+    """:func:`compress` without the host wait for the codebook (the training hooks' per-layer
+    path): once a tensor of the same shape and parameters was compressed on this context,
+    the whole compress is enqueued on the stream and the blob is sized from that earlier
+    one (acz_gpu_compress_async). Settle the result before using it."""
+    t = _require_cuda_f32(t)
+    ctx = ctx or default_context(t.device.index)
+    shape = (C.c_uint64 * max(1, t.dim()))(*t.shape)
+    h = C.c_void_p()
+    pend = C.c_int(0)
+    rc = _native.load().acz_gpu_compress_async(ctx.handle, _dev_ptr(t), shape, t.dim(),
+                                               float(p.eb), int(p.quant_radius),
+                                               int(p.predictor), _stream_handle(stream),
+                                               C.byref(h), C.byref(pend))
+    _check(rc, ctx)
+    return AsyncCompress(t, p, stream, ctx, h, bool(pend.value))
+
+
 def decompress(c: CompressedTensor, zero_filter: bool = False, out=None, stream=None,
                ctx: Optional[Context] = None):
     """ref include/acz/codec.hpp:59 / src/codec.cpp:122-171. Returns a CUDA fp32 tensor.

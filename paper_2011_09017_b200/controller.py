@@ -106,6 +106,11 @@ class ActivationHandle:
     layer_id: int = -1
     held_bytes: int = 0
     achieved_ratio: float = 1.0
+    # asynchronous compress in flight (Controller(async_compress=True)); settled -- blob,
+    # sizes and accounting filled in -- before anything reads the handle
+    pending: Optional[_codec.AsyncCompress] = None
+    post_relu: bool = False
+    in_bytes: int = 0
 
 
 @dataclass
@@ -159,7 +164,11 @@ class Controller:
 
     def __init__(self, cfg: ControllerConfig, num_layers: int,
                  reducer: Optional[Callable[[List[float]], List[float]]] = None,
-                 ctx: Optional[_codec.Context] = None):
+                 ctx: Optional[_codec.Context] = None, async_compress: bool = False):
+        """async_compress: wrap_forward enqueues the compress without waiting for its
+        codebook (codec.compress_async); the handles are settled in wrap order -- as they
+        finish, and all of them before any unwrap_backward, window change or ledger write --
+        so blobs, ledger and byte accounting are those of the synchronous path."""
         cfg.validate()
         if num_layers < 0:
             raise _codec.ParamError("controller needs a non-negative layer count")
@@ -169,15 +178,79 @@ class Controller:
         self.windows = [_Window() for _ in range(num_layers)]
         self.ledger = CompressionLedger()
         self.iteration = 0
-        self.current_bytes = 0
-        self.peak_bytes = 0
-        self.total_in = 0
-        self.total_stored = 0
+        self._cur = 0
+        self._peak = 0
+        self._tin = 0
+        self._tstored = 0
+        self.async_compress = async_compress
+        self._pending: List[ActivationHandle] = []
+        self.refits = 0
+
+    # byte accounting of the stashed activations (settles pending compresses first)
+    def _settled(name):
+        def get(self):
+            if self._pending:
+                self.settle()
+            return getattr(self, name)
+
+        def put(self, v):
+            setattr(self, name, v)
+        return property(get, put)
+    current_bytes = _settled("_cur")
+    peak_bytes = _settled("_peak")
+    total_in = _settled("_tin")
+    total_stored = _settled("_tstored")
+    del _settled
+
+    # ---- asynchronous compress: settling in wrap order ----------------------------------
+    def settle(self, wait: bool = True) -> None:
+        """Settles pending handles in wrap order; wait=False stops at the first one whose
+        compress has not finished."""
+        while self._pending:
+            h = self._pending[0]
+            try:
+                c = h.pending.settle(wait)
+            except _codec.Error as e:
+                print(f"warning: compression failed for layer {h.layer_id} ({e}); passing "
+                      "through", file=sys.stderr)
+                t = h.pending._t
+                c = None
+                h.raw = t
+            else:
+                if c is None:
+                    return
+            self.refits += h.pending.refits
+            self._pending.pop(0)
+            h.pending = None
+            if c is not None:
+                self._engage_blob(h, c)
+            self._account(h, h.in_bytes)
+
+    def _engage_blob(self, h: ActivationHandle, c) -> None:
+        h.blob, h.held_bytes = c, c.compressed_bytes
+        h.achieved_ratio = _codec.compression_ratio(c)
+        if self.cfg.zero_restoration == RELU_RECOMPUTE and h.post_relu:
+            h.apply_relu = True
+        else:
+            h.zero_filter = True
+
+    def _account(self, h: ActivationHandle, in_bytes: int) -> None:
+        if h.raw is not None:
+            h.held_bytes = in_bytes
+        w = self.windows[h.layer_id]
+        if w.open:
+            w.bytes_in += in_bytes
+            w.bytes_stored += h.held_bytes
+        self._tin += in_bytes
+        self._tstored += h.held_bytes
+        self._cur += h.held_bytes
+        self._peak = max(self._peak, self._cur)
 
     # ---- phases 1-3 ----------------------------------------------------------------
     def begin_iteration(self, iteration: int) -> None:
         if iteration < 0:
             raise _codec.ParamError("iteration must be >= 0")
+        self.settle()
         self.iteration = iteration
 
     def collecting(self) -> bool:
@@ -193,6 +266,7 @@ class Controller:
             raise _codec.ParamError("collect_stats: unknown layer id")
         if not self.collecting():
             raise _codec.ParamError("collect_stats invoked outside a collection iteration")
+        self.settle()
         if self.reducer is not None:
             sums = self.reducer(list(sums))
         st = LayerStats(layer_id=layer,
@@ -242,6 +316,25 @@ class Controller:
             raise _codec.ParamError("wrap_forward: unknown layer id")
         in_bytes = activation.numel() * 4
         h = ActivationHandle(layer_id=layer)
+        if self._pending:
+            self.settle(wait=False)
+        if self.async_compress and self.layer_active(layer):
+            w = self.windows[layer]
+            try:
+                a = _codec.compress_async(activation, _codec.CodecParams(
+                    w.eb, self.cfg.quant_radius, self.cfg.predictor), ctx=self.ctx)
+            except _codec.Error as e:
+                print(f"warning: compression failed for layer {layer} ({e}); passing through",
+                      file=sys.stderr)
+                h.raw = activation
+            else:
+                h.pending, h.post_relu, h.in_bytes = a, is_post_relu, in_bytes
+                self._pending.append(h)
+                if not a.pending and len(self._pending) == 1:
+                    self.settle()
+                return h
+            self._account(h, in_bytes)
+            return h
         if not self.layer_active(layer):
             h.raw, h.held_bytes = activation, in_bytes
         else:
@@ -264,14 +357,16 @@ class Controller:
         if w.open:
             w.bytes_in += in_bytes
             w.bytes_stored += h.held_bytes
-        self.total_in += in_bytes
-        self.total_stored += h.held_bytes
-        self.current_bytes += h.held_bytes
-        self.peak_bytes = max(self.peak_bytes, self.current_bytes)
+        self._tin += in_bytes
+        self._tstored += h.held_bytes
+        self._cur += h.held_bytes
+        self._peak = max(self._peak, self._cur)
         return h
 
     def unwrap_backward(self, h: ActivationHandle):
         """ref src/controller.cpp:234-249"""
+        if self._pending:
+            self.settle()
         if h.raw is not None:
             t, h.raw = h.raw, None
         elif h.blob is not None:
@@ -281,11 +376,12 @@ class Controller:
             h.blob = None
         else:
             raise _codec.ParamError("unwrap_backward: handle already consumed")
-        self.current_bytes -= h.held_bytes
+        self._cur -= h.held_bytes
         h.held_bytes = 0
         return t
 
     def finalize(self) -> None:
+        self.settle()
         for i in range(len(self.windows)):
             self._close_window(i)
 
@@ -445,7 +541,7 @@ class SavedActivationHooks:
         relu = self.ctl.cfg.zero_restoration == RELU_RECOMPUTE and self._post_relu(t)
         st = _Stash(self.ctl, self.ctl.wrap_forward(layer, t.detach(), relu))
         self._stash[key] = (weakref.ref(t.untyped_storage()), weakref.ref(st))
-        if st.handle.blob is not None:
+        if st.handle.blob is not None or st.handle.pending is not None:
             self.compressed += 1
         for ws in self._raw.pop(key, []):  # earlier saves of the same storage share it
             s = ws()

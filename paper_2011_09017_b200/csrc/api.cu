@@ -105,6 +105,12 @@ struct acz_gpu_ctx {
         uint32_t max_len;
     };
     std::unordered_map<std::string, SizePred> size_cache;
+    // Asynchronous compresses awaiting their settle (acz_gpu_compress_async): a ring of
+    // BookInfo + flags copies in mapped pinned memory (one entry per pending blob, written
+    // by the device right behind the codebook) and its free list.
+    void* async_host = nullptr;
+    void* async_dev = nullptr;
+    std::vector<uint32_t> async_free;
     // Sticky internal-error word in mapped pinned memory: kernels that detect an internal
     // consistency failure after the host has stopped waiting (the encoder's look-back) OR
     // kFlagInternal into it; every entry point reports it (ACZ_ERR_CUDA) and clears it.
@@ -184,6 +190,7 @@ struct acz_gpu_blob {
     cudaStream_t stream = nullptr;
     int invalid = 0;  // deferred decompress failure (foreign blobs), ACZ_ERR_*
     std::string invalid_msg;
+    struct AsyncPending* async = nullptr;  // an unsettled acz_gpu_compress_async
 };
 
 namespace acz_b200 {
@@ -526,6 +533,7 @@ int acz_gpu_ctx_destroy(acz_gpu_ctx* ctx) {
     for (void* p : {ctx->ws_io, ctx->ws_aux, ctx->ws_scan, (void*)ctx->d_partials})
         if (p) cudaFree(p);
     if (ctx->h_sticky) cudaFreeHost(ctx->h_sticky);
+    if (ctx->async_host) cudaFreeHost(ctx->async_host);
     for (Slot* sl : ctx->slots) free_slot(sl);
     for (auto st : ctx->pool) cudaStreamDestroy(st);
     for (auto e : ctx->pool_ev) cudaEventDestroy(e);
@@ -1243,6 +1251,171 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
     });
 }
 
+// ---------------------------------------------------- asynchronous compress (hooks) --
+// The training hooks compress one conv input at a time while the forward pass is still
+// being enqueued; a host wait per layer for its codebook drains the GPU's queue every
+// layer. acz_gpu_compress_async enqueues the whole compress (quantiser, histogram,
+// codebook, encode) with no host wait, into a blob sized from the previous compress of the
+// same (shape, eb, radius, predictor) -- the speculative encode of the batched path, whose
+// kernels write nothing unless the book fits -- and a copy of the BookInfo into a mapped
+// ring entry of the context, behind an event. acz_gpu_compress_settle later reads that
+// entry: the blob is complete (bit-identical to acz_gpu_compress), or it did not fit and
+// the caller compresses the tensor again synchronously.
+struct AsyncHead {  // the leading fields of SmallBlock
+    acz_b200::BookInfo info;
+    unsigned int flags;
+};
+static_assert(offsetof(AsyncHead, flags) == offsetof(SmallBlock, flags),
+              "AsyncHead must mirror SmallBlock's leading fields");
+constexpr uint32_t kAsyncRing = 1024;
+constexpr size_t kAsyncStride = (sizeof(AsyncHead) + 63) & ~size_t(63);
+
+struct AsyncPending {
+    acz_gpu_ctx* ctx = nullptr;
+    uint32_t ring = 0;
+    cudaEvent_t ev = nullptr;
+    Plan pl;
+    std::string key;
+};
+
+namespace {
+void async_release(acz_gpu_blob* b) {
+    AsyncPending* p = b->async;
+    if (!p) return;
+    if (p->ev) cudaEventDestroy(p->ev);
+    p->ctx->async_free.push_back(p->ring);
+    delete p;
+    b->async = nullptr;
+}
+}  // namespace
+
+int acz_gpu_compress_async(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
+                           uint32_t rank, double eb, uint32_t quant_radius, uint32_t predictor,
+                           void* stream, acz_gpu_blob** out, int* pending) {
+    return guarded(ctx, [&]() -> int {
+    if (!ctx || !out || !pending) return ACZ_ERR_INVALID;
+    *out = nullptr;
+    *pending = 0;
+    ctx->err.clear();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Slot* sl = get_slot(ctx, 0);
+    if (!sl) return fail(ctx, ACZ_ERR_NOMEM, "slot");
+    Plan pl;
+    int rc = compress_begin(ctx, sl, d_in, shape, rank, eb, quant_radius, predictor, s, &pl);
+    if (rc) return rc;
+    const std::string key = size_key(pl);
+    auto it = ctx->size_cache.find(key);
+    if (predictor == ACZ_PRED_PREV && it != ctx->size_cache.end()) {
+        if (!ctx->async_host) {
+            CK(cudaHostAlloc(&ctx->async_host, kAsyncStride * kAsyncRing, cudaHostAllocMapped));
+            CK(cudaHostGetDevicePointer(&ctx->async_dev, ctx->async_host, 0));
+            for (uint32_t i = kAsyncRing; i-- > 0;) ctx->async_free.push_back(i);
+        }
+        if (!ctx->async_free.empty()) {
+            if ((rc = spec_encode(ctx, sl, &pl, it->second, s))) return rc;
+            acz_gpu_blob* b = pl.spec;
+            pl.spec = nullptr;
+            AsyncPending* ap = new (std::nothrow) AsyncPending();
+            cudaEvent_t ev = nullptr;
+            cudaError_t e = ap ? cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)
+                               : cudaErrorMemoryAllocation;
+            const uint32_t ring = ctx->async_free.back();
+            CopyRegions cr{};
+            cr.src[0] = sl->d_small;
+            cr.dst[0] = static_cast<char*>(ctx->async_dev) + kAsyncStride * ring;
+            cr.bytes[0] = sizeof(AsyncHead);
+            cr.n = 1;
+            cr.to_host = 1;
+            if (e == cudaSuccess) e = launch_copy_regions(cr, ctx->sms, s, &ctx->launches);
+            if (e == cudaSuccess) e = cudaEventRecord(ev, s);
+            if (e != cudaSuccess) {
+                if (ev) cudaEventDestroy(ev);
+                delete ap;
+                blob_arena_free(b, s);
+                delete b;
+                return cuda_fail(ctx, e, "async compress");
+            }
+            ctx->async_free.pop_back();
+            ap->ctx = ctx;
+            ap->ring = ring;
+            ap->ev = ev;
+            ap->pl = pl;
+            ap->key = key;
+            b->async = ap;
+            b->invalid = ACZ_ERR_INVALID;
+            b->invalid_msg = "blob of an unsettled asynchronous compress";
+            *out = b;
+            *pending = 1;
+            return ACZ_OK;
+        }
+    }
+    rc = compress_end(ctx, sl, pl, s, out);
+    if (rc == ACZ_OK && predictor == ACZ_PRED_PREV) {
+        const acz_gpu_blob_info_t& in = (*out)->info;
+        ctx->size_cache[key] = {in.codebook_size, in.bit_length, in.outlier_count,
+                                in.max_code_length};
+    }
+    return rc;
+    });
+}
+
+int acz_gpu_compress_settle(acz_gpu_ctx* ctx, acz_gpu_blob* b, int wait, int* state) {
+    return guarded(ctx, [&]() -> int {
+    if (!ctx || !b || !state) return ACZ_ERR_INVALID;
+    ctx->err.clear();
+    AsyncPending* ap = b->async;
+    if (!ap) {
+        *state = b->invalid ? ACZ_ASYNC_REFIT : ACZ_ASYNC_DONE;
+        return ACZ_OK;
+    }
+    if (ap->ctx != ctx) return fail(ctx, ACZ_ERR_INVALID, "blob of another context");
+    if (!wait) {
+        const cudaError_t q = cudaEventQuery(ap->ev);
+        if (q == cudaErrorNotReady) {
+            *state = ACZ_ASYNC_PENDING;
+            return ACZ_OK;
+        }
+        if (q != cudaSuccess) return cuda_fail(ctx, q, "async settle");
+    }
+    CK(cudaEventSynchronize(ap->ev));
+    AsyncHead h;
+    std::memcpy(&h, static_cast<const char*>(ctx->async_host) + kAsyncStride * ap->ring,
+                sizeof(AsyncHead));
+    const BookInfo& bi = h.info;
+    const Plan& pl = ap->pl;
+    const unsigned flags = h.flags | bi.flags;
+    const bool fits = !flags && !bi.slow && bi.book_size >= 1 && bi.total_bits <= pl.cap_bits &&
+                      bi.n_escapes <= pl.cap_out && bi.book_size <= pl.cap_book &&
+                      bi.max_len <= pl.cap_len;
+    if (!flags && !bi.slow && bi.book_size >= 1)  // the next prediction: this book's sizes
+        ctx->size_cache[ap->key] = {bi.book_size, bi.total_bits, bi.n_escapes, bi.max_len};
+    if (fits) {
+        b->nwords = (bi.total_bits + 31) / 32;
+        b->max_len = bi.max_len;
+        acz_gpu_blob_info_t& in = b->info;
+        in.rank = pl.rank;
+        for (uint32_t i = 0; i < pl.rank; ++i) in.shape[i] = pl.shape[i];
+        in.eb = pl.eb;
+        in.quant_radius = pl.radius;
+        in.predictor = pl.predictor;
+        in.element_count = pl.n;
+        in.codebook_size = bi.book_size;
+        in.bit_length = bi.total_bits;
+        in.outlier_count = bi.n_escapes;
+        in.uncompressed_bytes = 4ull * pl.n;
+        in.compressed_bytes = acz1_size(pl.rank, bi.book_size, bi.total_bits, bi.n_escapes);
+        in.device_bytes = b->arena_bytes;
+        in.sidecar_bytes = sidecar_bytes(b->nchunks, false);
+        in.max_code_length = bi.max_len;
+        b->invalid = 0;
+        b->invalid_msg.clear();
+    }
+    async_release(b);
+    *state = fits ? ACZ_ASYNC_DONE : ACZ_ASYNC_REFIT;
+    return check_sticky(ctx);
+    });
+}
+
 int acz_gpu_compress_batch(acz_gpu_ctx* ctx, uint32_t count, const float* const* d_in,
                            const uint64_t* shapes, const uint32_t* ranks, double eb,
                            uint32_t quant_radius, uint32_t predictor, void* stream,
@@ -1491,6 +1664,7 @@ int acz_gpu_blob_info(const acz_gpu_blob* b, acz_gpu_blob_info_t* info) {
 
 int acz_gpu_blob_free(acz_gpu_blob* b) {
     if (!b) return ACZ_ERR_INVALID;
+    async_release(b);
     blob_arena_free(b, b->stream);
     delete b;
     return ACZ_OK;

@@ -15,7 +15,7 @@ lib = _native.load()
 ctx = acz.default_context()
 shapes = {"conv1": (256, 3, 227, 227, False), "config1": (64, 64, 56, 56, True),
           "conv2": (256, 96, 27, 27, True), "conv3": (256, 256, 13, 13, True),
-          "vgg_conv2": (16, 64, 224, 224, True)}
+          "vgg_conv2": (16, 64, 224, 224, True), "img128": (128, 3, 224, 224, False)}
 which = sys.argv[1:] or list(shapes)
 for nm in which:
     b, c, h, w, relu = shapes[nm]
