@@ -1382,11 +1382,11 @@ __global__ void __launch_bounds__(kRW * 32) k_spec_verify(const float* __restric
 // Serial replay of a plane from its first chunk whose recorded entry disagreed with the
 // replay (see k_spec_verify): symbols and sidecar states to the plane's end.
 template <typename SymT>
-__global__ void __launch_bounds__(128) k_spec_fixup(const float* __restrict__ x, SP p, const int* dB,
-                                                    SymT* __restrict__ sym_out,
-                                                    float* __restrict__ side_state,
-                                                    const float* __restrict__ rfix,
-                                                    const unsigned long long* __restrict__ pfirst) {
+__global__ void __launch_bounds__(32) k_spec_fixup(const float* __restrict__ x, SP p, const int* dB,
+                                                   SymT* __restrict__ sym_out,
+                                                   float* __restrict__ side_state,
+                                                   const float* __restrict__ rfix,
+                                                   const unsigned long long* __restrict__ pfirst) {
     const uint64_t plane = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (plane >= p.planes) return;
     const unsigned long long cf = pfirst[plane];
@@ -1395,7 +1395,45 @@ __global__ void __launch_bounds__(128) k_spec_fixup(const float* __restrict__ x,
     spec_params(p, qp, dB);
     const uint64_t I = p.interval, end = (plane + 1) * p.P;
     double r = (double)rfix[cf];
-    for (uint64_t flat = cf * I; flat < end; ++flat) {
+    uint64_t flat = cf * I;  // a multiple of 8 (I >= 32)
+    // blocks of 8 speculative steps (qspec, exact redo on a miss) with the next block's
+    // inputs loaded ahead: the plane's chain is the only dependency (one warp per 32 planes,
+    // one plane per lane)
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(sym_out) & 15) == 0;
+    auto load8 = [&](uint64_t f, float* v) {
+        if (vec) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(x + f));
+            const float4 b = __ldg(reinterpret_cast<const float4*>(x + f) + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(x + f + u);
+        }
+    };
+    float xv[8], xn[8];
+    if (flat + 8 <= end) load8(flat, xv);
+    for (; flat + 8 <= end; flat += 8) {
+        if (flat + 16 <= end) load8(flat + 8, xn);
+        if ((flat & (I - 1)) == 0) side_state[flat >> p.ishift] = (float)r;
+        uint32_t sy[8];
+        if (!qspec<8, false>([&](int u) { return xv[u]; },
+                             [&](int u, uint32_t sv, float) { sy[u] = sv; }, r, qp))
+            qexact<8>([&](int u) { return xv[u]; }, [&](int u, uint32_t sv, float) { sy[u] = sv; },
+                      r, qp);
+        if (vec && sizeof(SymT) == 2) {
+            *reinterpret_cast<uint4*>(sym_out + flat) =
+                make_uint4(sy[0] | (sy[1] << 16), sy[2] | (sy[3] << 16), sy[4] | (sy[5] << 16),
+                           sy[6] | (sy[7] << 16));
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sym_out[flat + u] = (SymT)sy[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = xn[u];
+    }
+    for (; flat < end; ++flat) {
         if ((flat & (I - 1)) == 0) side_state[flat >> p.ishift] = (float)r;
         const float xf = __ldg(x + flat);
         double v;
@@ -1436,15 +1474,15 @@ cudaError_t launch_spec_verify(const QuantArgs& a, const SP& p, const int* dB, f
     if (e != cudaSuccess) return e;
     const uint64_t nch = (a.g.n + a.interval - 1) / a.interval;
     const unsigned vb = (unsigned)((nch + kRW * 32 - 1) / (kRW * 32));
-    const unsigned fb = (unsigned)((a.g.planes + 127) / 128);
+    const unsigned fb = (unsigned)((a.g.planes + 31) / 32);
     if (a.sym16) {
         k_spec_verify<uint16_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix,
                                                         pfirst, fixes);
-        k_spec_fixup<uint16_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix, pfirst);
+        k_spec_fixup<uint16_t><<<fb, 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix, pfirst);
     } else {
         k_spec_verify<uint32_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix,
                                                         pfirst, fixes);
-        k_spec_fixup<uint32_t><<<fb, 128, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix, pfirst);
+        k_spec_fixup<uint32_t><<<fb, 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix, pfirst);
     }
     *launches += 2;
     return cudaGetLastError();

@@ -146,3 +146,16 @@ def test_quant_spec_decoupled_path(acz, oracle, case, monkeypatch):
     """The decoupled phase-A / walk kernel pair (opt-in) is bit-identical to the oracle."""
     monkeypatch.setenv("ACZ_SPEC_DECOUPLED", "1")
     test_quant_spec_cases(acz, oracle, case)
+
+
+@pytest.mark.parametrize("eb", [0.05, 0.1, 0.3, 1.0])
+@pytest.mark.parametrize("kind", ["dense", "relu"])
+def test_quant_spec_large_error_bounds(acz, oracle, eb, kind):
+    """Large error bounds (the controller clamps eb to [eb_min, eb_max] = [.., 0.1]) leave
+    thousands of wrong walk states per tensor: the chunk-parallel repair rounds and the
+    serial plane replay after them must give the reference's symbols exactly."""
+    rng = np.random.default_rng(int(eb * 1000) + (kind == "relu"))
+    x = rng.standard_normal((6, 3, 224, 224))
+    if kind == "relu":
+        x = np.maximum(x, 0)
+    _run(acz, oracle, x, eb)
