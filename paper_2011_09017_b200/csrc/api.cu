@@ -33,6 +33,7 @@ struct SmallBlock {
     unsigned int maxsym;
     unsigned int hist_done;  // histogram CTA arrivals (fused codebook), zero between calls
     unsigned long long binding;  // sidecar binding computed on the device (sidecar export)
+    unsigned int spec_fix;       // K2b planes the serial replay redid (read back with the book)
     CanonTables canon;
     uint32_t lut[kLutSize];
 };
@@ -105,6 +106,9 @@ struct acz_gpu_ctx {
         uint32_t max_len;
     };
     std::unordered_map<std::string, SizePred> size_cache;
+    // (shape, eb, radius) whose last K2b compress had to replay more than a quarter of its
+    // planes serially (large error bounds defeat the walk): quantised by K2a from then on
+    std::unordered_map<std::string, bool> spec_bad;
     // Asynchronous compresses awaiting their settle (acz_gpu_compress_async): a ring of
     // BookInfo + flags copies in mapped pinned memory (one entry per pending blob, written
     // by the device right behind the codebook) and its free list.
@@ -794,6 +798,28 @@ int decompress_on(acz_gpu_ctx* ctx, Slot* sl, const acz_gpu_blob* b, int zero_fi
 }
 
 
+// Key of a compress's (shape, eb, radius, predictor): size predictions and the K2b record.
+std::string params_key(const uint64_t* shape, uint32_t rank, double eb, uint32_t radius,
+                       uint32_t predictor) {
+    std::string k(reinterpret_cast<const char*>(shape), 8 * rank);
+    k.append(reinterpret_cast<const char*>(&eb), 8);
+    k.append(reinterpret_cast<const char*>(&radius), 4);
+    k.append(reinterpret_cast<const char*>(&predictor), 4);
+    return k;
+}
+
+// K2b (the speculative quantiser) unless this context saw it replay more than a quarter of
+// the planes of the same (shape, eb, radius) serially -- large error bounds (e.g. eb = 0.1
+// on unit-scale data, the controller's default eb_max) defeat its walk, and the serial
+// replay after it costs more than K2a alone (128x3x224x224 at eb = 0.1: K2b 2.9 ms + replay
+// 3.7 ms). ACZ_SPEC_QUANT=1 (tests) always takes K2b.
+bool use_k2b(acz_gpu_ctx* ctx, const std::string& key, uint32_t predictor, const PlaneGeom& g) {
+    if (!quant_spec_applicable(predictor, g.plane_size, g.planes, ctx->sms)) return false;
+    if (std::getenv("ACZ_SPEC_QUANT")) return true;
+    auto it = ctx->spec_bad.find(key);
+    return it == ctx->spec_bad.end() || !it->second;
+}
+
 // State of a compress between its asynchronous first half (quantiser, histogram, codebook)
 // and its second half (blob sizing after the BookInfo read-back, encode).
 struct Plan {
@@ -806,6 +832,7 @@ struct Plan {
     uint64_t interval = 0;
     int sym16 = 0;
     const float* d_in = nullptr;
+    bool k2b = false;  // quantised by K2b (its serial-replay count is read with the book)
     // speculative encode (spec_encode): the pre-sized blob and its capacities
     acz_gpu_blob* spec = nullptr;
     unsigned long long cap_bits = 0;
@@ -865,10 +892,14 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     qa.interval = interval;
     qa.row_scratch = static_cast<float*>(sl->ws_row);
     qa.flags = &sm->flags;
+    const bool k2b = use_k2b(ctx, params_key(shape, rank, eb, quant_radius, predictor),
+                             predictor, g);
     {
         KTimer kt(ctx, ACZ_K_QUANT, s);
-        if (quant_spec_applicable(predictor, g.plane_size, g.planes, ctx->sms)) {
+        if (k2b) {
             CK(grow(&sl->ws_qs, &sl->ws_qs_cap, quant_spec_scratch_bytes(g.planes, g.plane_size)));
+            CK(cudaMemsetAsync(&sm->spec_fix, 0, sizeof(unsigned), s));
+            qa.spec_fix = &sm->spec_fix;
             CK(launch_quant_spec(qa, sl->ws_qs, s, &ctx->launches));
         } else {
             CK(launch_quant(qa, ctx->sms, s, &ctx->launches));
@@ -887,6 +918,7 @@ int compress_begin(acz_gpu_ctx* ctx, Slot* sl, const float* d_in, const uint64_t
     pl->interval = interval;
     pl->sym16 = sym16;
     pl->d_in = d_in;
+    pl->k2b = k2b;
     return ACZ_OK;
 }
 
@@ -924,6 +956,9 @@ int book_wait(acz_gpu_ctx* ctx, Slot* sl, cudaStream_t s) {
 
 int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz_gpu_blob** out) {
     if (int rc = book_wait(ctx, sl, s)) return rc;
+    if (pl.k2b)
+        ctx->spec_bad[params_key(pl.shape, pl.rank, pl.eb, pl.radius, pl.predictor)] =
+            4ull * sl->h_small->spec_fix > pl.g.planes;
     if (int rc = check_sticky(ctx)) return rc;
     const BookInfo bi = sl->h_small->info;
     const unsigned flags = sl->h_small->flags | bi.flags;
@@ -974,11 +1009,7 @@ int compress_end(acz_gpu_ctx* ctx, Slot* sl, const Plan& pl, cudaStream_t s, acz
 // re-encodes that tensor into an exactly sized blob (spec_finish). The GPU thus never waits
 // for the host between a tensor's codebook and its encode.
 std::string size_key(const Plan& pl) {
-    std::string k(reinterpret_cast<const char*>(pl.shape), 8 * pl.rank);
-    k.append(reinterpret_cast<const char*>(&pl.eb), 8);
-    k.append(reinterpret_cast<const char*>(&pl.radius), 4);
-    k.append(reinterpret_cast<const char*>(&pl.predictor), 4);
-    return k;
+    return params_key(pl.shape, pl.rank, pl.eb, pl.radius, pl.predictor);
 }
 
 // Opt-in (ACZ_SPEC_ENCODE=1, read per batch): measured neutral on the AlexNet step and

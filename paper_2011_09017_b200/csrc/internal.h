@@ -73,6 +73,7 @@ struct QuantArgs {
     uint64_t interval;        // sidecar interval (power of two for PrevValue, plane size for Lorenzo2d)
     float* row_scratch;       // planes*cols floats (Lorenzo2d only)
     unsigned int* flags;      // kFlagNonFinite
+    unsigned int* spec_fix = nullptr;  // K2b: planes the serial replay had to redo (counted)
 };
 // Lorenzo2d planes of up to this many rows use the anti-diagonal wavefront kernels
 // (3 diagonals of floats in shared memory per warp: <= 48 KB).

@@ -1386,11 +1386,13 @@ __global__ void __launch_bounds__(32) k_spec_fixup(const float* __restrict__ x, 
                                                    SymT* __restrict__ sym_out,
                                                    float* __restrict__ side_state,
                                                    const float* __restrict__ rfix,
-                                                   const unsigned long long* __restrict__ pfirst) {
+                                                   const unsigned long long* __restrict__ pfirst,
+                                                   unsigned int* __restrict__ nfix) {
     const uint64_t plane = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (plane >= p.planes) return;
     const unsigned long long cf = pfirst[plane];
     if (cf == ~0ull) return;
+    if (nfix) atomicAdd(nfix, 1u);
     QParams qp;
     spec_params(p, qp, dB);
     const uint64_t I = p.interval, end = (plane + 1) * p.P;
@@ -1478,11 +1480,13 @@ cudaError_t launch_spec_verify(const QuantArgs& a, const SP& p, const int* dB, f
     if (a.sym16) {
         k_spec_verify<uint16_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix,
                                                         pfirst, fixes);
-        k_spec_fixup<uint16_t><<<fb, 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix, pfirst);
+        k_spec_fixup<uint16_t><<<fb, 32, 0, s>>>(a.x, p, dB, a.sym16, a.side_state, rfix, pfirst,
+                                                 a.spec_fix);
     } else {
         k_spec_verify<uint32_t><<<vb, kRW * 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix,
                                                         pfirst, fixes);
-        k_spec_fixup<uint32_t><<<fb, 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix, pfirst);
+        k_spec_fixup<uint32_t><<<fb, 32, 0, s>>>(a.x, p, dB, a.sym, a.side_state, rfix, pfirst,
+                                                 a.spec_fix);
     }
     *launches += 2;
     return cudaGetLastError();

@@ -211,3 +211,27 @@ def test_training_async_equals_sync(gpu_lib):
     assert c0.ledger.to_csv() == c1.ledger.to_csv()
     assert c1.total_stored == c0.total_stored and c1.total_stored < c1.total_in
     assert not math.isnan(l1[-1])
+
+
+def test_k2b_learned_dispatch_at_large_error_bounds(gpu_lib, oracle):
+    """Long dense planes at eb = 0.1 (the controller's default eb_max): K2b's walk leaves most
+    planes to the serial replay, so the context quantises the next compress of the same
+    (shape, eb) with K2a (fewer launches); both are bit-exact. At eb = 1e-3 K2b stays."""
+    import os
+    import torch
+    import paper_2011_09017_b200 as acz
+    assert "ACZ_SPEC_QUANT" not in os.environ and "ACZ_SERIAL_QUANT" not in os.environ
+    rng = np.random.default_rng(17)
+    ctx = acz.Context(0)
+    for eb, learns in ((0.1, True), (1e-3, False)):
+        launches = []
+        for _ in range(3):
+            x = rng.standard_normal((4, 3, 224, 224)).astype(np.float32)
+            l0 = ctx.launches
+            c = acz.compress(torch.from_numpy(x).cuda(), acz.CodecParams(eb), ctx=ctx)
+            launches.append(ctx.launches - l0)
+            assert c.to_bytes() == oracle.compress(x, eb).blob
+        if learns:
+            assert launches[1] < launches[0] and launches[2] == launches[1], launches
+        else:
+            assert launches[0] == launches[1] == launches[2], launches
