@@ -111,13 +111,14 @@ int acz_gpu_compress(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
                      acz_gpu_blob** out);
 /* Asynchronous compress (the training hooks' per-layer path): enqueues the whole compress
  * on `stream` with NO host wait when an earlier compress of the same (shape, eb, radius,
- * PrevValue predictor) on this context gives the blob's size (+ margins; *pending = 1).
+ * PrevValue predictor, size_tag -- e.g. the layer id) on this context gives the blob's size
+ * (+ margins; *pending = 1).
  * The blob may not be used until acz_gpu_compress_settle reports ACZ_ASYNC_DONE. Without a
  * size prediction (first call of a shape, Lorenzo2d) it is acz_gpu_compress (*pending = 0).
  * Same arguments, results and errors as acz_gpu_compress (ref codec.hpp:54). */
 int acz_gpu_compress_async(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
                            uint32_t rank, double eb, uint32_t quant_radius, uint32_t predictor,
-                           void* stream, acz_gpu_blob** out, int* pending);
+                           uint64_t size_tag, void* stream, acz_gpu_blob** out, int* pending);
 #define ACZ_ASYNC_PENDING 0 /* not finished yet (wait = 0)                                */
 #define ACZ_ASYNC_DONE 1    /* the blob is complete, bit-identical to acz_gpu_compress      */
 #define ACZ_ASYNC_REFIT 2   /* it did not fit its predicted size, or the compress failed:

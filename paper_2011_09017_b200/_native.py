@@ -40,8 +40,8 @@ SIGNATURES = [
     ("acz_gpu_compress", C.c_int, [_vp, _vp, _u64p, C.c_uint32, C.c_double, C.c_uint32,
                                    C.c_uint32, _vp, C.POINTER(_vp)]),
     ("acz_gpu_compress_async", C.c_int, [_vp, _vp, _u64p, C.c_uint32, C.c_double,
-                                         C.c_uint32, C.c_uint32, _vp, C.POINTER(_vp),
-                                         C.POINTER(C.c_int)]),
+                                         C.c_uint32, C.c_uint32, C.c_uint64, _vp,
+                                         C.POINTER(_vp), C.POINTER(C.c_int)]),
     ("acz_gpu_compress_settle", C.c_int, [_vp, _vp, C.c_int, C.POINTER(C.c_int)]),
     ("acz_gpu_decompress", C.c_int, [_vp, _vp, C.c_int, _vp, _vp]),
     ("acz_gpu_malloc", C.c_int, [_vp, C.c_uint64, _vp, C.POINTER(_vp)]),

@@ -348,6 +348,7 @@ class AsyncCompress:
         self._t = t if pending else None
         self.result: Optional[CompressedTensor] = None if pending else CompressedTensor(h, ctx)
         self.refits = 0
+        self.refit_reason = ""
 
     @property
     def pending(self) -> bool:
@@ -368,6 +369,9 @@ class AsyncCompress:
             self._h = self._t = None
             return self.result
         # did not fit its predicted size (or failed): free it, compress synchronously
+        if rc == 0:
+            msg = lib.acz_gpu_last_error(self._ctx.handle)
+            self.refit_reason = msg.decode() if msg else ""
         lib.acz_gpu_blob_free(self._h)
         self._h = None
         self.refits += 1
@@ -385,11 +389,12 @@ class AsyncCompress:
 
 
 def compress_async(t, p: CodecParams = CodecParams(), stream=None,
-                   ctx: Optional[Context] = None) -> AsyncCompress:
+                   ctx: Optional[Context] = None, size_tag: int = 0) -> AsyncCompress:
     """:func:`compress` without the host wait for the codebook (the training hooks' per-layer
     path): once a tensor of the same shape and parameters was compressed on this context,
     the whole compress is enqueued on the stream and the blob is sized from that earlier
-    one (acz_gpu_compress_async). Settle the result before using it."""
+    one (acz_gpu_compress_async; size_tag, e.g. a layer id, keeps the predictions of
+    equally shaped tensors apart). Settle the result before using it."""
     t = _require_cuda_f32(t)
     ctx = ctx or default_context(t.device.index)
     shape = (C.c_uint64 * max(1, t.dim()))(*t.shape)
@@ -397,8 +402,9 @@ def compress_async(t, p: CodecParams = CodecParams(), stream=None,
     pend = C.c_int(0)
     rc = _native.load().acz_gpu_compress_async(ctx.handle, _dev_ptr(t), shape, t.dim(),
                                                float(p.eb), int(p.quant_radius),
-                                               int(p.predictor), _stream_handle(stream),
-                                               C.byref(h), C.byref(pend))
+                                               int(p.predictor), int(size_tag),
+                                               _stream_handle(stream), C.byref(h),
+                                               C.byref(pend))
     _check(rc, ctx)
     return AsyncCompress(t, p, stream, ctx, h, bool(pend.value))
 

@@ -185,6 +185,7 @@ class Controller:
         self.async_compress = async_compress
         self._pending: List[ActivationHandle] = []
         self.refits = 0
+        self.refit_reasons: List[str] = []
 
     # byte accounting of the stashed activations (settles pending compresses first)
     def _settled(name):
@@ -220,6 +221,8 @@ class Controller:
                 if c is None:
                     return
             self.refits += h.pending.refits
+            if h.pending.refits:
+                self.refit_reasons.append(h.pending.refit_reason)
             self._pending.pop(0)
             h.pending = None
             if c is not None:
@@ -322,7 +325,8 @@ class Controller:
             w = self.windows[layer]
             try:
                 a = _codec.compress_async(activation, _codec.CodecParams(
-                    w.eb, self.cfg.quant_radius, self.cfg.predictor), ctx=self.ctx)
+                    w.eb, self.cfg.quant_radius, self.cfg.predictor), ctx=self.ctx,
+                    size_tag=layer + 1)
             except _codec.Error as e:
                 print(f"warning: compression failed for layer {layer} ({e}); passing through",
                       file=sys.stderr)

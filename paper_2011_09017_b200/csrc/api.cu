@@ -1322,7 +1322,7 @@ void async_release(acz_gpu_blob* b) {
 
 int acz_gpu_compress_async(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* shape,
                            uint32_t rank, double eb, uint32_t quant_radius, uint32_t predictor,
-                           void* stream, acz_gpu_blob** out, int* pending) {
+                           uint64_t size_tag, void* stream, acz_gpu_blob** out, int* pending) {
     return guarded(ctx, [&]() -> int {
     if (!ctx || !out || !pending) return ACZ_ERR_INVALID;
     *out = nullptr;
@@ -1334,7 +1334,10 @@ int acz_gpu_compress_async(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* 
     Plan pl;
     int rc = compress_begin(ctx, sl, d_in, shape, rank, eb, quant_radius, predictor, s, &pl);
     if (rc) return rc;
-    const std::string key = size_key(pl);
+    // the prediction comes from the last compress with the same parameters AND tag (the
+    // controller tags by layer: layers with equal input shapes compress to different sizes)
+    std::string key = size_key(pl);
+    key.append(reinterpret_cast<const char*>(&size_tag), 8);
     auto it = ctx->size_cache.find(key);
     if (predictor == ACZ_PRED_PREV && it != ctx->size_cache.end()) {
         if (!ctx->async_host) {
@@ -1443,6 +1446,16 @@ int acz_gpu_compress_settle(acz_gpu_ctx* ctx, acz_gpu_blob* b, int wait, int* st
     }
     async_release(b);
     *state = fits ? ACZ_ASYNC_DONE : ACZ_ASYNC_REFIT;
+    if (!fits) {  // why (acz_gpu_last_error; not an error)
+        char why[160];
+        std::snprintf(why, sizeof why,
+                      "refit: flags %u slow %u book %u/%u bits %llu/%llu outliers %llu/%llu "
+                      "len %u/%u", flags, (unsigned)bi.slow, bi.book_size, pl.cap_book,
+                      (unsigned long long)bi.total_bits, (unsigned long long)pl.cap_bits,
+                      (unsigned long long)bi.n_escapes, (unsigned long long)pl.cap_out,
+                      bi.max_len, pl.cap_len);
+        ctx->err = why;
+    }
     return check_sticky(ctx);
     });
 }

@@ -111,7 +111,7 @@ def test_async_errors_and_unsettled_blob(gpu_lib):
     h, pend = C.c_void_p(), C.c_int(0)
     shp = (C.c_uint64 * 4)(*shape)
     assert lib.acz_gpu_compress_async(ctx.handle, C.c_void_p(t.data_ptr()), shp, 4, 1e-3,
-                                      32768, 0, None, C.byref(h), C.byref(pend)) == 0
+                                      32768, 0, 0, None, C.byref(h), C.byref(pend)) == 0
     assert pend.value == 1
     out = torch.empty(shape, device="cuda")
     assert lib.acz_gpu_decompress(ctx.handle, h, 1, C.c_void_p(out.data_ptr()), None) == 8
@@ -235,3 +235,26 @@ def test_k2b_learned_dispatch_at_large_error_bounds(gpu_lib, oracle):
             assert launches[1] < launches[0] and launches[2] == launches[1], launches
         else:
             assert launches[0] == launches[1] == launches[2], launches
+
+
+def test_async_size_tags_keep_equal_shapes_apart(gpu_lib, oracle):
+    """Two layers with the same input shape but different entropy, compressed alternately:
+    tagged by layer, each predicts from its own previous blob (no refits); untagged, the
+    larger one outgrows the smaller one's prediction every time."""
+    import torch
+    import paper_2011_09017_b200 as acz
+    rng = np.random.default_rng(19)
+    ctx = acz.Context(0)
+    p = acz.CodecParams(1e-3)
+    shape = (4, 16, 40, 40)
+    lo = (0.05 * _post_relu(rng, shape)).astype(np.float32)
+    hi = _post_relu(rng, shape)
+    refits = {True: 0, False: 0}
+    for tagged in (True, False):
+        for _ in range(3):
+            for tag, x in ((1, lo), (2, hi)):
+                a = acz.compress_async(torch.from_numpy(x).cuda(), p, ctx=ctx,
+                                       size_tag=tag if tagged else 99)
+                assert a.settle().to_bytes() == oracle.compress(x, 1e-3).blob
+                refits[tagged] += a.refits
+    assert refits[True] == 0 and refits[False] >= 2, refits

@@ -57,6 +57,8 @@ for compress, asy in ((False, False), (True, False), (True, True)):
     print(f"compress={compress} async={asy}: (host ms to end of forward, step ms) per iteration:", res)
     if ac:
         print("  refits", ac.ctl.refits, "compressed", ac.hooks.compressed)
+        for r in ac.ctl.refit_reasons[:20]:
+            print("   ", r)
     if compress:
         n = 6
         print("  per step (iterations 6-11, host wall ms / calls):",
