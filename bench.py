@@ -319,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------------------ CPU reference ----
-TRAFFIC_JSON = os.path.join("profiles", "r02", "v6", "traffic.json")
+TRAFFIC_JSON = os.path.join("profiles", "r02", "v7", "traffic.json")
 ONE_THREAD_SAMPLES = 16  # 1-thread leg: the first 16 samples of every tensor (~2-3 s)
 
 

@@ -376,6 +376,10 @@ class AsyncCompress:
         self._h = None
         self.refits += 1
         self.result = compress(self._t, self._p, stream=self._stream, ctx=self._ctx)
+        if self._stream is not None:
+            # its encode reads the input on that stream; the caller may free the input and
+            # use the blob on another stream once this returns
+            self._stream.synchronize()
         self._t = None
         return self.result
 

@@ -164,11 +164,19 @@ class Controller:
 
     def __init__(self, cfg: ControllerConfig, num_layers: int,
                  reducer: Optional[Callable[[List[float]], List[float]]] = None,
-                 ctx: Optional[_codec.Context] = None, async_compress: bool = False):
+                 ctx: Optional[_codec.Context] = None, async_compress: bool = False,
+                 side_stream: bool = False, max_pending: int = 2):
         """async_compress: wrap_forward enqueues the compress without waiting for its
         codebook (codec.compress_async); the handles are settled in wrap order -- as they
         finish, and all of them before any unwrap_backward, window change or ledger write --
-        so blobs, ledger and byte accounting are those of the synchronous path."""
+        so blobs, ledger and byte accounting are those of the synchronous path.
+        side_stream (with async_compress): the compresses run on a stream of their own that
+        waits for the activation's producer, so the forward pass does not queue behind them
+        (a latency-bound quantiser of a few long planes then overlaps the next layers).
+        max_pending: a pending handle keeps its raw activation alive until it is settled, so
+        at most this many stay unsettled -- wrap_forward waits for the oldest beyond it (the
+        GPU still has the newer ones queued). Without the bound the host runs the whole
+        forward pass ahead of the GPU and every raw activation lives to the backward pass."""
         cfg.validate()
         if num_layers < 0:
             raise _codec.ParamError("controller needs a non-negative layer count")
@@ -183,6 +191,9 @@ class Controller:
         self._tin = 0
         self._tstored = 0
         self.async_compress = async_compress
+        self.side_stream = side_stream
+        self.max_pending = max(0, int(max_pending))
+        self._side = None
         self._pending: List[ActivationHandle] = []
         self.refits = 0
         self.refit_reasons: List[str] = []
@@ -204,10 +215,10 @@ class Controller:
     del _settled
 
     # ---- asynchronous compress: settling in wrap order ----------------------------------
-    def settle(self, wait: bool = True) -> None:
+    def settle(self, wait: bool = True, keep: int = 0) -> None:
         """Settles pending handles in wrap order; wait=False stops at the first one whose
-        compress has not finished."""
-        while self._pending:
+        compress has not finished; keep: leave (up to) that many of the newest pending."""
+        while len(self._pending) > keep:
             h = self._pending[0]
             try:
                 c = h.pending.settle(wait)
@@ -323,10 +334,22 @@ class Controller:
             self.settle(wait=False)
         if self.async_compress and self.layer_active(layer):
             w = self.windows[layer]
+            side = main = None
+            if self.side_stream:
+                import torch
+                main = torch.cuda.current_stream(activation.device)
+                if self._side is None:
+                    self._side = torch.cuda.Stream(device=activation.device)
+                side = self._side
+                side.wait_stream(main)  # the activation has been produced
             try:
                 a = _codec.compress_async(activation, _codec.CodecParams(
                     w.eb, self.cfg.quant_radius, self.cfg.predictor), ctx=self.ctx,
-                    size_tag=layer + 1)
+                    size_tag=layer + 1, stream=side)
+                if side is not None and not a.pending:
+                    # a synchronous compress (the first of its tag) may still be encoding on
+                    # the side stream, reading the activation: the forward waits for it
+                    main.wait_stream(side)
             except _codec.Error as e:
                 print(f"warning: compression failed for layer {layer} ({e}); passing through",
                       file=sys.stderr)
@@ -336,6 +359,8 @@ class Controller:
                 self._pending.append(h)
                 if not a.pending and len(self._pending) == 1:
                     self.settle()
+                elif len(self._pending) > self.max_pending:
+                    self.settle(wait=True, keep=self.max_pending)
                 return h
             self._account(h, in_bytes)
             return h
@@ -377,6 +402,11 @@ class Controller:
             t = _codec.decompress(h.blob, zero_filter=h.zero_filter, ctx=self.ctx)
             if h.apply_relu:
                 _codec.relu_(t, ctx=self.ctx)  # nn::recompute_relu (layers.hpp:152-157)
+            if self._side is not None:
+                # the blob's arena was allocated on the side stream and is freed there
+                # (stream-ordered): after this stream's decode has read it
+                import torch
+                self._side.wait_stream(torch.cuda.current_stream(t.device))
             h.blob = None
         else:
             raise _codec.ParamError("unwrap_backward: handle already consumed")

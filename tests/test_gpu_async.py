@@ -180,7 +180,7 @@ def test_training_async_equals_sync(gpu_lib):
     from paper_2011_09017_b200.training import AdaptiveCompression
     torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
 
-    def run(async_compress):
+    def run(async_compress, side_stream=False):
         torch.manual_seed(3)
         net = nn.Sequential(nn.Conv2d(3, 16, 3, padding=1), nn.ReLU(inplace=True),
                             nn.Conv2d(16, 32, 3, padding=1), nn.ReLU(inplace=True),
@@ -190,7 +190,7 @@ def test_training_async_equals_sync(gpu_lib):
         x = torch.randn(16, 3, 32, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
         y = torch.randint(0, 10, (16,), device="cuda", generator=torch.Generator("cuda").manual_seed(2))
         ac = AdaptiveCompression(net, opt, ControllerConfig(collect_interval=2),
-                                 async_compress=async_compress)
+                                 async_compress=async_compress, side_stream=side_stream)
         losses = []
         for it in range(7):
             opt.zero_grad(set_to_none=True)
@@ -205,10 +205,11 @@ def test_training_async_equals_sync(gpu_lib):
         return losses, [p.detach().clone() for p in net.parameters()], ac.ctl
     l0, w0, c0 = run(False)
     l1, w1, c1 = run(True)
-    assert l0 == l1
-    for a, b in zip(w0, w1):
-        assert torch.equal(a, b)
-    assert c0.ledger.to_csv() == c1.ledger.to_csv()
+    l2, w2, c2 = run(True, side_stream=True)
+    assert l0 == l1 == l2
+    for a, b, c in zip(w0, w1, w2):
+        assert torch.equal(a, b) and torch.equal(a, c)
+    assert c0.ledger.to_csv() == c1.ledger.to_csv() == c2.ledger.to_csv()
     assert c1.total_stored == c0.total_stored and c1.total_stored < c1.total_in
     assert not math.isnan(l1[-1])
 

@@ -30,19 +30,20 @@ wrap(K, "mean_abs", "stats.mean_abs")
 
 B = int(os.environ.get("B", 128))
 dev = torch.device("cuda", 0)
-for compress, asy in ((False, False), (True, False), (True, True)):
+for compress, asy, side in ((False, False, False), (True, False, False), (True, True, False),
+                            (True, True, True)):
     torch.manual_seed(0)
     model = torchvision.models.resnet18(num_classes=1000).to(dev)
     opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
     crit = nn.CrossEntropyLoss()
     x = torch.randn(B, 3, 224, 224, device=dev); y = torch.randint(0, 1000, (B,), device=dev)
     ac = AdaptiveCompression(model, opt, ControllerConfig(collect_interval=4),
-                             async_compress=asy) if compress else None
+                             async_compress=asy, side_stream=side) if compress else None
     res = []
     for it in range(12):
         if it == 6:
             acc.clear(); cnt.clear()
-        torch.cuda.synchronize(); t0 = time.perf_counter()
+        torch.cuda.synchronize(); torch.cuda.reset_peak_memory_stats(); t0 = time.perf_counter()
         opt.zero_grad(set_to_none=True)
         if ac:
             ac.begin(it)
@@ -53,8 +54,9 @@ for compress, asy in ((False, False), (True, False), (True, True)):
         else:
             loss = crit(model(x), y); t1 = time.perf_counter(); loss.backward()
         opt.step(); torch.cuda.synchronize(); t2 = time.perf_counter()
-        res.append((round((t1 - t0) * 1e3, 2), round((t2 - t0) * 1e3, 2)))
-    print(f"compress={compress} async={asy}: (host ms to end of forward, step ms) per iteration:", res)
+        res.append((round((t1 - t0) * 1e3, 2), round((t2 - t0) * 1e3, 2),
+                    round(torch.cuda.max_memory_allocated() / 2**20)))
+    print(f"compress={compress} async={asy} side_stream={side}: (host ms to end of forward, step ms, torch peak MiB) per iteration:", res)
     if ac:
         print("  refits", ac.ctl.refits, "compressed", ac.hooks.compressed)
         for r in ac.ctl.refit_reasons[:20]:
