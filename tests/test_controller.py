@@ -126,3 +126,65 @@ def test_distributed_stats_gloo():
     assert b0 == 8 and r0 == st.r
     assert math.isclose(l0, st.l_bar, rel_tol=1e-12) and math.isclose(m0, st.m_avg, rel_tol=1e-12)
     assert math.isclose(e0, single.layer_eb(0), rel_tol=1e-12)
+
+
+class _FakeBlob:
+    def __init__(self, nbytes):
+        self.compressed_bytes = nbytes
+
+
+class _FakeAsync:
+    """Stands in for codec.AsyncCompress (host logic only): done after `ready_after` polls."""
+    log = []
+
+    def __init__(self, t, nbytes, ready_after):
+        self._t, self.n, self.polls, self.ready_after = t, nbytes, 0, ready_after
+        self.pending, self.refits, self.refit_reason = True, 0, ""
+
+    def settle(self, wait=True):
+        self.polls += 1
+        if not wait and self.polls <= self.ready_after:
+            return None
+        _FakeAsync.log.append(self.n)
+        self.pending = False
+        self._t = None
+        return _FakeBlob(self.n)
+
+
+def test_controller_async_settle_order_and_bound(monkeypatch):
+    """The asynchronous path's host logic without a GPU: handles settle in wrap order (a
+    finished newer one waits for an unfinished older one), at most max_pending stay
+    unsettled (their raw activations alive), the byte accounting and window sums equal the
+    synchronous path's, and unwrap settles everything first."""
+    import torch
+    from paper_2011_09017_b200 import codec as K
+    from paper_2011_09017_b200.controller import Controller, ControllerConfig
+    sizes = [5000, 100, 3000, 700, 40, 9000]
+    ready = [3, 0, 0, 5, 0, 0]  # polls before each one reports finished (wait=False)
+    it = iter(zip(sizes, ready))
+
+    def fake_async(t, p, stream=None, ctx=None, size_tag=0):
+        n, r = next(it)
+        return _FakeAsync(t, n, r)
+    monkeypatch.setattr(K, "compress_async", fake_async)
+    monkeypatch.setattr(K, "compression_ratio", lambda c: 1.0)
+    _FakeAsync.log = []
+
+    def active(ctl):
+        for i in range(len(sizes)):
+            ctl.collect_stats_from_sums(i, [1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 8.0])
+        ctl.begin_iteration(1)
+
+    c = Controller(ControllerConfig(collect_interval=100, eb_min=1e-3, eb_max=1e-3), len(sizes),
+                   async_compress=True, max_pending=2)
+    active(c)
+    acts = [torch.zeros(1000 * (i + 1)) for i in range(len(sizes))]
+    hs = []
+    for i, a in enumerate(acts):
+        hs.append(c.wrap_forward(i, a, False))
+        assert len(c._pending) <= 2
+    assert _FakeAsync.log == sizes[:len(_FakeAsync.log)]  # settled strictly in wrap order
+    assert c.current_bytes == sum(sizes)                   # (reading it settles the rest)
+    assert _FakeAsync.log == sizes and not c._pending
+    assert c.total_in == sum(4 * a.numel() for a in acts) and c.peak_bytes == sum(sizes)
+    assert all(h.blob is not None and h.zero_filter and h.pending is None for h in hs)
