@@ -111,6 +111,8 @@ class ActivationHandle:
     pending: Optional[_codec.AsyncCompress] = None
     post_relu: bool = False
     in_bytes: int = 0
+    side: object = None  # the stream its blob was compressed (and will be freed) on
+    stored_bytes: int = 0  # held_bytes as wrapped (for the deferred accounting)
 
 
 @dataclass
@@ -165,7 +167,7 @@ class Controller:
     def __init__(self, cfg: ControllerConfig, num_layers: int,
                  reducer: Optional[Callable[[List[float]], List[float]]] = None,
                  ctx: Optional[_codec.Context] = None, async_compress: bool = False,
-                 side_stream: bool = False, max_pending: int = 2):
+                 side_stream: bool = False, max_pending: int = 4):
         """async_compress: wrap_forward enqueues the compress without waiting for its
         codebook (codec.compress_async); the handles are settled in wrap order -- as they
         finish, and all of them before any unwrap_backward, window change or ledger write --
@@ -193,7 +195,8 @@ class Controller:
         self.async_compress = async_compress
         self.side_stream = side_stream
         self.max_pending = max(0, int(max_pending))
-        self._side = None
+        self._lanes = [None, None]   # (stream, context) per compress lane (side_stream)
+        self._events = []            # ("w" | "u", handle, bytes) not yet accounted
         self._pending: List[ActivationHandle] = []
         self.refits = 0
         self.refit_reasons: List[str] = []
@@ -214,34 +217,56 @@ class Controller:
     total_stored = _settled("_tstored")
     del _settled
 
-    # ---- asynchronous compress: settling in wrap order ----------------------------------
+    # ---- asynchronous compress: settling, and the accounting in program order -----------
+    def _settle_handle(self, h: ActivationHandle, wait: bool) -> bool:
+        """Settles one pending handle; False if its compress has not finished (wait=False)."""
+        try:
+            c = h.pending.settle(wait)
+        except _codec.Error as e:
+            print(f"warning: compression failed for layer {h.layer_id} ({e}); passing "
+                  "through", file=sys.stderr)
+            c = None
+            h.raw = h.pending._t
+        else:
+            if c is None:
+                return False
+        self.refits += h.pending.refits
+        if h.pending.refits:
+            self.refit_reasons.append(h.pending.refit_reason)
+        h.pending = None
+        if c is not None:
+            self._engage_blob(h, c)
+        else:
+            h.held_bytes = h.stored_bytes = h.in_bytes
+        return True
+
     def settle(self, wait: bool = True, keep: int = 0) -> None:
         """Settles pending handles in wrap order; wait=False stops at the first one whose
         compress has not finished; keep: leave (up to) that many of the newest pending."""
         while len(self._pending) > keep:
             h = self._pending[0]
-            try:
-                c = h.pending.settle(wait)
-            except _codec.Error as e:
-                print(f"warning: compression failed for layer {h.layer_id} ({e}); passing "
-                      "through", file=sys.stderr)
-                t = h.pending._t
-                c = None
-                h.raw = t
-            else:
-                if c is None:
-                    return
-            self.refits += h.pending.refits
-            if h.pending.refits:
-                self.refit_reasons.append(h.pending.refit_reason)
+            if h.pending is not None and not self._settle_handle(h, wait):
+                break
             self._pending.pop(0)
-            h.pending = None
-            if c is not None:
-                self._engage_blob(h, c)
-            self._account(h, h.in_bytes)
+        self._flush()
+
+    def _flush(self) -> None:
+        """Applies the byte accounting of wraps and unwraps in program order, up to the
+        first wrap whose size is not known yet (so current/peak bytes and the window sums
+        are those of the synchronous path)."""
+        while self._events:
+            kind, h, nbytes = self._events[0]
+            if kind == "w" and h.pending is not None:
+                return
+            self._events.pop(0)
+            if kind == "w":
+                self._account(h, h.in_bytes)
+            else:
+                self._cur -= nbytes
 
     def _engage_blob(self, h: ActivationHandle, c) -> None:
         h.blob, h.held_bytes = c, c.compressed_bytes
+        h.stored_bytes = h.held_bytes
         h.achieved_ratio = _codec.compression_ratio(c)
         if self.cfg.zero_restoration == RELU_RECOMPUTE and h.post_relu:
             h.apply_relu = True
@@ -249,15 +274,15 @@ class Controller:
             h.zero_filter = True
 
     def _account(self, h: ActivationHandle, in_bytes: int) -> None:
-        if h.raw is not None:
-            h.held_bytes = in_bytes
+        # h.stored_bytes: what the wrap held (h.held_bytes may already be 0: a handle can be
+        # unwrapped before an older wrap settles and lets this one's accounting run)
         w = self.windows[h.layer_id]
         if w.open:
             w.bytes_in += in_bytes
-            w.bytes_stored += h.held_bytes
+            w.bytes_stored += h.stored_bytes
         self._tin += in_bytes
-        self._tstored += h.held_bytes
-        self._cur += h.held_bytes
+        self._tstored += h.stored_bytes
+        self._cur += h.stored_bytes
         self._peak = max(self._peak, self._cur)
 
     # ---- phases 1-3 ----------------------------------------------------------------
@@ -332,19 +357,27 @@ class Controller:
         h = ActivationHandle(layer_id=layer)
         if self._pending:
             self.settle(wait=False)
+        h.in_bytes = in_bytes
         if self.async_compress and self.layer_active(layer):
             w = self.windows[layer]
             side = main = None
+            ctx = self.ctx
             if self.side_stream:
                 import torch
                 main = torch.cuda.current_stream(activation.device)
-                if self._side is None:
-                    self._side = torch.cuda.Stream(device=activation.device)
-                side = self._side
+                lane = self._lane(activation)
+                if self._lanes[lane] is None:
+                    self._lanes[lane] = (torch.cuda.Stream(device=activation.device),
+                                         self.ctx if lane == 0 else
+                                         _codec.Context(activation.device.index or 0))
+                side, ctx = self._lanes[lane]
+                if lane == 0 and ctx is None:
+                    ctx = self.ctx
+                h.side = side
                 side.wait_stream(main)  # the activation has been produced
             try:
                 a = _codec.compress_async(activation, _codec.CodecParams(
-                    w.eb, self.cfg.quant_radius, self.cfg.predictor), ctx=self.ctx,
+                    w.eb, self.cfg.quant_radius, self.cfg.predictor), ctx=ctx,
                     size_tag=layer + 1, stream=side)
                 if side is not None and not a.pending:
                     # a synchronous compress (the first of its tag) may still be encoding on
@@ -355,14 +388,17 @@ class Controller:
                       file=sys.stderr)
                 h.raw = activation
             else:
-                h.pending, h.post_relu, h.in_bytes = a, is_post_relu, in_bytes
+                h.pending, h.post_relu = a, is_post_relu
                 self._pending.append(h)
+                self._events.append(("w", h, 0))
                 if not a.pending and len(self._pending) == 1:
                     self.settle()
                 elif len(self._pending) > self.max_pending:
                     self.settle(wait=True, keep=self.max_pending)
                 return h
-            self._account(h, in_bytes)
+            h.held_bytes = h.stored_bytes = in_bytes
+            self._events.append(("w", h, 0))
+            self._flush()
             return h
         if not self.layer_active(layer):
             h.raw, h.held_bytes = activation, in_bytes
@@ -382,37 +418,42 @@ class Controller:
                 print(f"warning: compression failed for layer {layer} ({e}); passing through",
                       file=sys.stderr)
                 h.raw, h.held_bytes = activation, in_bytes
-        w = self.windows[layer]
-        if w.open:
-            w.bytes_in += in_bytes
-            w.bytes_stored += h.held_bytes
-        self._tin += in_bytes
-        self._tstored += h.held_bytes
-        self._cur += h.held_bytes
-        self._peak = max(self._peak, self._cur)
+        h.stored_bytes = h.held_bytes
+        self._events.append(("w", h, 0))
+        self._flush()
         return h
 
     def unwrap_backward(self, h: ActivationHandle):
         """ref src/controller.cpp:234-249"""
-        if self._pending:
-            self.settle()
+        if h.pending is not None:
+            # only this handle: older ones may still be compressing on another lane
+            self._settle_handle(h, True)
         if h.raw is not None:
             t, h.raw = h.raw, None
         elif h.blob is not None:
             t = _codec.decompress(h.blob, zero_filter=h.zero_filter, ctx=self.ctx)
             if h.apply_relu:
                 _codec.relu_(t, ctx=self.ctx)  # nn::recompute_relu (layers.hpp:152-157)
-            if self._side is not None:
-                # the blob's arena was allocated on the side stream and is freed there
+            if h.side is not None:
+                # the blob's arena was allocated on its lane's stream and is freed there
                 # (stream-ordered): after this stream's decode has read it
                 import torch
-                self._side.wait_stream(torch.cuda.current_stream(t.device))
+                h.side.wait_stream(torch.cuda.current_stream(t.device))
             h.blob = None
         else:
             raise _codec.ParamError("unwrap_backward: handle already consumed")
-        self._cur -= h.held_bytes
+        self._events.append(("u", h, h.held_bytes))
         h.held_bytes = 0
+        self._flush()
         return t
+
+    @staticmethod
+    def _lane(activation) -> int:
+        """Compress lane of an activation: long planes (an input image, >= 128x128) get
+        their own context and stream, so their latency-bound quantiser does not hold back
+        the other layers' compresses (the backward pass starts with the last layer's)."""
+        sh = activation.shape
+        return 1 if len(sh) >= 2 and int(sh[-1]) * int(sh[-2]) >= 16384 else 0
 
     def finalize(self) -> None:
         self.settle()

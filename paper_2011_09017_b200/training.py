@@ -38,7 +38,7 @@ class AdaptiveCompression:
 
     def __init__(self, model, optimizer, cfg: ControllerConfig, reducer=None,
                  ctx: Optional[_codec.Context] = None, min_numel: int = 0,
-                 async_compress: bool = True, side_stream: bool = True):
+                 async_compress: bool = True, side_stream: bool = True, max_pending: int = 4):
         import torch.nn as nn
         self.model, self.opt = model, optimizer
         self.convs = [m for m in model.modules()
@@ -48,7 +48,8 @@ class AdaptiveCompression:
         # (side_stream: on a stream of their own, overlapping the next layers' forward)
         self.ctl = Controller(cfg, len(self.convs), reducer=reducer, ctx=ctx,
                               async_compress=async_compress,
-                              side_stream=async_compress and side_stream)
+                              side_stream=async_compress and side_stream,
+                              max_pending=max_pending)
         self.hooks = SavedActivationHooks(self.ctl, model, min_numel=min_numel)
         self._act: Dict[int, List[float]] = {}   # layer -> [nonzeros, count, batch]
         self._grad: Dict[int, List[float]] = {}  # layer -> [sum |g|, count]

@@ -188,3 +188,19 @@ def test_controller_async_settle_order_and_bound(monkeypatch):
     assert _FakeAsync.log == sizes and not c._pending
     assert c.total_in == sum(4 * a.numel() for a in acts) and c.peak_bytes == sum(sizes)
     assert all(h.blob is not None and h.zero_filter and h.pending is None for h in hs)
+
+    # unwrap settles only its own handle: the newest one is unwrapped while older ones are
+    # still compressing; the accounting still follows program order (peak after all wraps)
+    monkeypatch.setattr(K, "decompress", lambda b, zero_filter=False, ctx=None: torch.zeros(1))
+    it = iter(zip(sizes, [9, 9, 9, 9, 9, 0]))
+    _FakeAsync.log = []
+    c2 = Controller(ControllerConfig(collect_interval=100, eb_min=1e-3, eb_max=1e-3),
+                    len(sizes), async_compress=True, max_pending=len(sizes))
+    active(c2)
+    hs = [c2.wrap_forward(i, a, False) for i, a in enumerate(acts)]
+    c2.unwrap_backward(hs[-1])
+    assert _FakeAsync.log == [sizes[-1]] and c2._cur == 0  # nothing accounted yet
+    assert c2.current_bytes == sum(sizes) - sizes[-1] and c2.peak_bytes == sum(sizes)
+    for h in reversed(hs[:-1]):
+        c2.unwrap_backward(h)
+    assert c2.current_bytes == 0 and c2.total_stored == sum(sizes)

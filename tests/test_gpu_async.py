@@ -180,15 +180,17 @@ def test_training_async_equals_sync(gpu_lib):
     from paper_2011_09017_b200.training import AdaptiveCompression
     torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
 
-    def run(async_compress, side_stream=False):
+    def run(async_compress, side_stream=False, hw=32):
         torch.manual_seed(3)
         net = nn.Sequential(nn.Conv2d(3, 16, 3, padding=1), nn.ReLU(inplace=True),
                             nn.Conv2d(16, 32, 3, padding=1), nn.ReLU(inplace=True),
                             nn.MaxPool2d(2), nn.Conv2d(32, 32, 3, padding=1), nn.ReLU(),
                             nn.AdaptiveAvgPool2d(1), nn.Flatten(), nn.Linear(32, 10)).cuda()
         opt = torch.optim.SGD(net.parameters(), lr=0.05, momentum=0.9)
-        x = torch.randn(16, 3, 32, 32, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
-        y = torch.randint(0, 10, (16,), device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+        x = torch.randn(16 if hw == 32 else 2, 3, hw, hw, device="cuda",
+                        generator=torch.Generator("cuda").manual_seed(1))
+        y = torch.randint(0, 10, (x.shape[0],), device="cuda",
+                          generator=torch.Generator("cuda").manual_seed(2))
         ac = AdaptiveCompression(net, opt, ControllerConfig(collect_interval=2),
                                  async_compress=async_compress, side_stream=side_stream)
         losses = []
@@ -212,6 +214,14 @@ def test_training_async_equals_sync(gpu_lib):
     assert c0.ledger.to_csv() == c1.ledger.to_csv() == c2.ledger.to_csv()
     assert c1.total_stored == c0.total_stored and c1.total_stored < c1.total_in
     assert not math.isnan(l1[-1])
+    # 128x128 inputs: the first conv's input goes to the second compress lane (its own
+    # context and stream), the rest to the first; unwraps settle out of wrap order
+    l3, w3, c3 = run(False, hw=128)
+    l4, w4, c4 = run(True, side_stream=True, hw=128)
+    assert l3 == l4 and all(torch.equal(a, b) for a, b in zip(w3, w4))
+    assert c3.ledger.to_csv() == c4.ledger.to_csv()
+    assert c4._lanes[0] is not None and c4._lanes[1] is not None
+    assert (c3.peak_bytes, c3.total_stored) == (c4.peak_bytes, c4.total_stored)
 
 
 def test_k2b_learned_dispatch_at_large_error_bounds(gpu_lib, oracle):

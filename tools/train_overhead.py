@@ -30,15 +30,15 @@ wrap(K, "mean_abs", "stats.mean_abs")
 
 B = int(os.environ.get("B", 128))
 dev = torch.device("cuda", 0)
-for compress, asy, side in ((False, False, False), (True, False, False), (True, True, False),
-                            (True, True, True)):
+for compress, asy, side in ((False, False, False), (True, False, False), (True, True, True)):
     torch.manual_seed(0)
     model = torchvision.models.resnet18(num_classes=1000).to(dev)
     opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
     crit = nn.CrossEntropyLoss()
     x = torch.randn(B, 3, 224, 224, device=dev); y = torch.randint(0, 1000, (B,), device=dev)
     ac = AdaptiveCompression(model, opt, ControllerConfig(collect_interval=4),
-                             async_compress=asy, side_stream=side) if compress else None
+                             async_compress=asy, side_stream=side,
+                             max_pending=int(os.environ.get("MAXP", 4))) if compress else None
     res = []
     for it in range(12):
         if it == 6:
