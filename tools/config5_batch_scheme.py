@@ -77,7 +77,9 @@ def run(batch, steps, compress, W, seed=0):
     # steady state: iterations after the first non-degenerate window opened (the windows
     # collected at iteration 0 see all-zero momentum and pass through, ref
     # include/acz/controller.hpp:92-94; the next collection is at W)
-    ss = range(W + 1, steps)
+    # (and after the first of them, W + 1, whose compresses are the codec's warm-up: the
+    # first compress of every layer is synchronous and sizes the asynchronous ones)
+    ss = range(W + 2, steps)
     res = {
         "batch": batch, "compress": compress, "steps": steps, "W": W,
         "static_bytes": static,
@@ -107,7 +109,7 @@ def run(batch, steps, compress, W, seed=0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--base", type=int, default=128)
-    ap.add_argument("--steps", type=int, default=12)
+    ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--W", type=int, default=4)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
