@@ -124,7 +124,8 @@ int acz_gpu_compress_async(acz_gpu_ctx* ctx, const float* d_in, const uint64_t* 
 #define ACZ_ASYNC_REFIT 2   /* it did not fit its predicted size, or the compress failed:
                                free it and compress the tensor again (acz_gpu_compress)   */
 /* Settles an acz_gpu_compress_async blob. wait = 0 polls (*state may be
- * ACZ_ASYNC_PENDING); wait = 1 blocks until the codebook is known. */
+ * ACZ_ASYNC_PENDING); wait = 1 blocks until the codebook is known. Free (or settle) every
+ * pending blob before destroying its context. */
 int acz_gpu_compress_settle(acz_gpu_ctx* ctx, acz_gpu_blob* blob, int wait, int* state);
 /* Decompress into d_out (element_count floats). zero_filter: |v| <= eb -> 0 on output
  * (ref src/codec.cpp:162-164). Stream-ordered, no host synchronisation. */

@@ -1313,6 +1313,10 @@ namespace {
 void async_release(acz_gpu_blob* b) {
     AsyncPending* p = b->async;
     if (!p) return;
+    // an unsettled blob being freed: its BookInfo copy may still be in flight, and the ring
+    // entry must not be handed to another compress (possibly on another stream) before it
+    // has landed
+    if (p->ev) cudaEventSynchronize(p->ev);
     if (p->ev) cudaEventDestroy(p->ev);
     p->ctx->async_free.push_back(p->ring);
     delete p;
