@@ -169,12 +169,14 @@ class Controller:
                  ctx: Optional[_codec.Context] = None, async_compress: bool = False,
                  side_stream: bool = False, max_pending: int = 4):
         """async_compress: wrap_forward enqueues the compress without waiting for its
-        codebook (codec.compress_async); the handles are settled in wrap order -- as they
-        finish, and all of them before any unwrap_backward, window change or ledger write --
-        so blobs, ledger and byte accounting are those of the synchronous path.
-        side_stream (with async_compress): the compresses run on a stream of their own that
-        waits for the activation's producer, so the forward pass does not queue behind them
-        (a latency-bound quantiser of a few long planes then overlaps the next layers).
+        codebook (codec.compress_async); handles are settled as they finish (in wrap order),
+        an unwrap settles its own handle, and everything is settled before a window change,
+        a ledger write or a read of the byte counters; the byte accounting is replayed in
+        program order, so blobs, ledger and counters are those of the synchronous path.
+        side_stream (with async_compress): the compresses run on side streams that wait for
+        the activation's producer, so the forward pass does not queue behind them; long
+        planes (an input image) get a second lane (stream + context) so that their
+        latency-bound quantiser does not hold back the other layers' compresses.
         max_pending: a pending handle keeps its raw activation alive until it is settled, so
         at most this many stay unsettled -- wrap_forward waits for the oldest beyond it (the
         GPU still has the newer ones queued). Without the bound the host runs the whole
