@@ -112,6 +112,7 @@ class ActivationHandle:
     post_relu: bool = False
     in_bytes: int = 0
     side: object = None  # the stream its blob was compressed (and will be freed) on
+    prefetched: object = None  # (tensor, event) decoded ahead (Controller(prefetch=True))
     stored_bytes: int = 0  # held_bytes as wrapped (for the deferred accounting)
 
 
@@ -167,7 +168,7 @@ class Controller:
     def __init__(self, cfg: ControllerConfig, num_layers: int,
                  reducer: Optional[Callable[[List[float]], List[float]]] = None,
                  ctx: Optional[_codec.Context] = None, async_compress: bool = False,
-                 side_stream: bool = False, max_pending: int = 4):
+                 side_stream: bool = False, max_pending: int = 4, prefetch: bool = False):
         """async_compress: wrap_forward enqueues the compress without waiting for its
         codebook (codec.compress_async); handles are settled as they finish (in wrap order),
         an unwrap settles its own handle, and everything is settled before a window change,
@@ -180,7 +181,9 @@ class Controller:
         max_pending: a pending handle keeps its raw activation alive until it is settled, so
         at most this many stay unsettled -- wrap_forward waits for the oldest beyond it (the
         GPU still has the newer ones queued). Without the bound the host runs the whole
-        forward pass ahead of the GPU and every raw activation lives to the backward pass."""
+        forward pass ahead of the GPU and every raw activation lives to the backward pass.
+        prefetch: after each unwrap, the newest still-held handle is decoded ahead on a
+        stream of its own (the backward pass usually unwraps in reverse wrap order)."""
         cfg.validate()
         if num_layers < 0:
             raise _codec.ParamError("controller needs a non-negative layer count")
@@ -198,6 +201,9 @@ class Controller:
         self.side_stream = side_stream
         self.max_pending = max(0, int(max_pending))
         self._lanes = [None, None]   # (stream, context) per compress lane (side_stream)
+        self.prefetch = prefetch
+        self._pf = None              # decode-ahead stream (prefetch)
+        self._live: List[ActivationHandle] = []  # wrapped, not yet unwrapped (prefetch)
         self._events = []            # ("w" | "u", handle, bytes) not yet accounted
         self._pending: List[ActivationHandle] = []
         self.refits = 0
@@ -292,6 +298,7 @@ class Controller:
         if iteration < 0:
             raise _codec.ParamError("iteration must be >= 0")
         self.settle()
+        self._live.clear()
         self.iteration = iteration
 
     def collecting(self) -> bool:
@@ -357,6 +364,8 @@ class Controller:
             raise _codec.ParamError("wrap_forward: unknown layer id")
         in_bytes = activation.numel() * 4
         h = ActivationHandle(layer_id=layer)
+        if self.prefetch:
+            self._live.append(h)
         if self._pending:
             self.settle(wait=False)
         h.in_bytes = in_bytes
@@ -433,9 +442,18 @@ class Controller:
         if h.raw is not None:
             t, h.raw = h.raw, None
         elif h.blob is not None:
-            t = _codec.decompress(h.blob, zero_filter=h.zero_filter, ctx=self.ctx)
-            if h.apply_relu:
-                _codec.relu_(t, ctx=self.ctx)  # nn::recompute_relu (layers.hpp:152-157)
+            if h.prefetched is not None:
+                # decoded ahead on the prefetch stream (see _prefetch_next)
+                import torch
+                t, ev = h.prefetched
+                h.prefetched = None
+                main = torch.cuda.current_stream(t.device)
+                main.wait_event(ev)
+                t.record_stream(main)
+            else:
+                t = _codec.decompress(h.blob, zero_filter=h.zero_filter, ctx=self.ctx)
+                if h.apply_relu:
+                    _codec.relu_(t, ctx=self.ctx)  # nn::recompute_relu (layers.hpp:152-157)
             if h.side is not None:
                 # the blob's arena was allocated on its lane's stream and is freed there
                 # (stream-ordered): after this stream's decode has read it
@@ -447,7 +465,42 @@ class Controller:
         self._events.append(("u", h, h.held_bytes))
         h.held_bytes = 0
         self._flush()
+        if self.prefetch:
+            self._forget(h)
+            self._prefetch_next()
         return t
+
+    def _forget(self, h: ActivationHandle) -> None:
+        for i in range(len(self._live) - 1, -1, -1):
+            if self._live[i] is h:
+                del self._live[i]
+                return
+
+    def _prefetch_next(self) -> None:
+        """Decodes the handle the backward pass will most likely unwrap next (the newest
+        wrapped one still held) on a stream of its own, overlapping the current layer's
+        backward kernels; unwrap_backward then only waits for that decode."""
+        if not self._live:
+            return
+        nxt = self._live[-1]
+        if nxt.prefetched is not None or nxt.raw is not None:
+            return
+        if nxt.pending is not None and not self._settle_handle(nxt, False):
+            return  # still compressing: decoded on demand
+        if nxt.blob is None:
+            return
+        import torch
+        dev = torch.device("cuda", nxt.blob._ctx.device)
+        if self._pf is None:
+            self._pf = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(self._pf):
+            t = _codec.decompress(nxt.blob, zero_filter=nxt.zero_filter, ctx=self.ctx,
+                                  stream=self._pf)
+            if nxt.apply_relu:
+                _codec.relu_(t, stream=self._pf, ctx=self.ctx)
+        ev = torch.cuda.Event()
+        ev.record(self._pf)
+        nxt.prefetched = (t, ev)
 
     @staticmethod
     def _lane(activation) -> int:

@@ -38,7 +38,8 @@ for compress, asy, side in ((False, False, False), (True, False, False), (True, 
     x = torch.randn(B, 3, 224, 224, device=dev); y = torch.randint(0, 1000, (B,), device=dev)
     ac = AdaptiveCompression(model, opt, ControllerConfig(collect_interval=4),
                              async_compress=asy, side_stream=side,
-                             max_pending=int(os.environ.get("MAXP", 4))) if compress else None
+                             max_pending=int(os.environ.get("MAXP", 4)),
+                             prefetch=os.environ.get("PREFETCH", "0") == "1") if compress else None
     res = []
     for it in range(12):
         if it == 6:
