@@ -270,3 +270,29 @@ def test_async_size_tags_keep_equal_shapes_apart(gpu_lib, oracle):
                 assert a.settle().to_bytes() == oracle.compress(x, 1e-3).blob
                 refits[tagged] += a.refits
     assert refits[True] == 0 and refits[False] >= 2, refits
+
+
+def test_async_lorenzo_and_edge_cases(gpu_lib, oracle):
+    """Lorenzo2d has no size prediction: compress_async is the synchronous compress; empty
+    tensors raise what compress() raises; the ring of pending entries is returned on every
+    settle over many calls."""
+    import torch
+    import paper_2011_09017_b200 as acz
+    rng = np.random.default_rng(23)
+    ctx = acz.Context(0)
+    x = _post_relu(rng, (2, 4, 33, 47))
+    p = acz.CodecParams(1e-3, predictor=acz.Predictor.Lorenzo2d)
+    for _ in range(2):
+        a = acz.compress_async(torch.from_numpy(x).cuda(), p, ctx=ctx)
+        assert not a.pending
+        assert a.settle().to_bytes() == oracle.compress(x, 1e-3, predictor=1).blob
+    for bad in (torch.empty(0, device="cuda"), torch.empty(3, 0, 4, device="cuda")):
+        with pytest.raises(acz.Error) as sync_err:
+            acz.compress(bad, acz.CodecParams(1e-3), ctx=ctx)
+        with pytest.raises(type(sync_err.value)):
+            acz.compress_async(bad, acz.CodecParams(1e-3), ctx=ctx)
+    q = acz.CodecParams(1e-3)
+    t = torch.from_numpy(_post_relu(rng, (2, 8, 16, 16))).cuda()
+    for k in range(1200):  # more than the 1024-entry ring: entries are returned on settle
+        a = acz.compress_async(t, q, ctx=ctx, size_tag=k % 3)
+        a.settle()
