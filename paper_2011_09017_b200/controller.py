@@ -470,6 +470,15 @@ class Controller:
             self._prefetch_next()
         return t
 
+    def contexts(self) -> List[_codec.Context]:
+        """Every codec context this controller compresses on (memory accounting: each holds
+        its own workspace)."""
+        out = [self.ctx or _codec.default_context()]
+        for lane in self._lanes:
+            if lane is not None and lane[1] is not None and all(lane[1] is not c for c in out):
+                out.append(lane[1])
+        return out
+
     def _forget(self, h: ActivationHandle) -> None:
         for i in range(len(self._live) - 1, -1, -1):
             if self._live[i] is h:

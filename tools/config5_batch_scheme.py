@@ -70,6 +70,9 @@ def run(batch, steps, compress, W, seed=0):
         e1.record()
         torch.cuda.synchronize()
         mi = ctx.memory_info()
+        if ac:  # the workspaces of every context the controller compresses on (lanes)
+            mi["workspace_bytes"] = sum(c.memory_info()["workspace_bytes"]
+                                        for c in ac.ctl.contexts())
         times.append(e0.elapsed_time(e1))
         peaks.append(torch.cuda.max_memory_allocated())
         codec_peaks.append(mi["blob_peak_bytes"] + mi["workspace_bytes"])
@@ -101,6 +104,9 @@ def run(batch, steps, compress, W, seed=0):
         res["ledger_rows"] = len(c.ledger.records)
         ac.remove()
     del model, opt, x, y
+    if ac:
+        for c in ac.ctl.contexts():
+            c.trim()
     ctx.trim()
     torch.cuda.empty_cache()
     return res
