@@ -168,7 +168,8 @@ class Controller:
     def __init__(self, cfg: ControllerConfig, num_layers: int,
                  reducer: Optional[Callable[[List[float]], List[float]]] = None,
                  ctx: Optional[_codec.Context] = None, async_compress: bool = False,
-                 side_stream: bool = False, max_pending: int = 4, prefetch: bool = False):
+                 side_stream: bool = False, max_pending: int = 4, prefetch: bool = False,
+                 two_lanes: bool = False):
         """async_compress: wrap_forward enqueues the compress without waiting for its
         codebook (codec.compress_async); handles are settled as they finish (in wrap order),
         an unwrap settles its own handle, and everything is settled before a window change,
@@ -182,6 +183,8 @@ class Controller:
         at most this many stay unsettled -- wrap_forward waits for the oldest beyond it (the
         GPU still has the newer ones queued). Without the bound the host runs the whole
         forward pass ahead of the GPU and every raw activation lives to the backward pass.
+        two_lanes (with side_stream): long planes get the second lane; off, one side stream
+        and one context (the second lane's context holds a second workspace).
         prefetch: after each unwrap, the newest still-held handle is decoded ahead on a
         stream of its own (the backward pass usually unwraps in reverse wrap order)."""
         cfg.validate()
@@ -202,6 +205,7 @@ class Controller:
         self.max_pending = max(0, int(max_pending))
         self._lanes = [None, None]   # (stream, context) per compress lane (side_stream)
         self.prefetch = prefetch
+        self.two_lanes = two_lanes
         self._pf = None              # decode-ahead stream (prefetch)
         self._live: List[ActivationHandle] = []  # wrapped, not yet unwrapped (prefetch)
         self._events = []            # ("w" | "u", handle, bytes) not yet accounted
@@ -376,7 +380,7 @@ class Controller:
             if self.side_stream:
                 import torch
                 main = torch.cuda.current_stream(activation.device)
-                lane = self._lane(activation)
+                lane = self._lane(activation) if self.two_lanes else 0
                 if self._lanes[lane] is None:
                     self._lanes[lane] = (torch.cuda.Stream(device=activation.device),
                                          self.ctx if lane == 0 else

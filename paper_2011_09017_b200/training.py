@@ -39,7 +39,7 @@ class AdaptiveCompression:
     def __init__(self, model, optimizer, cfg: ControllerConfig, reducer=None,
                  ctx: Optional[_codec.Context] = None, min_numel: int = 0,
                  async_compress: bool = True, side_stream: bool = True, max_pending: int = 4,
-                 prefetch: bool = False):
+                 prefetch: bool = False, two_lanes: bool = True):
         import torch.nn as nn
         self.model, self.opt = model, optimizer
         self.convs = [m for m in model.modules()
@@ -53,7 +53,13 @@ class AdaptiveCompression:
                               max_pending=max_pending,
                               # decode-ahead in the backward pass: ResNet-18 B128 25.9 ->
                               # 25.5 ms per step for +49 MiB of peak (off by default)
-                              prefetch=async_compress and side_stream and prefetch)
+                              prefetch=async_compress and side_stream and prefetch,
+                              # a second compress lane (stream + context) for long-plane
+                              # inputs: ResNet-18 B128 27.9 -> 26.1 ms per step and 2379 ->
+                              # 2282 MiB torch peak (the image's latency-bound quantiser no
+                              # longer holds the other layers' raw inputs), for a second
+                              # context workspace (counted in config 5)
+                              two_lanes=two_lanes)
         self.hooks = SavedActivationHooks(self.ctl, model, min_numel=min_numel)
         self._act: Dict[int, List[float]] = {}   # layer -> [nonzeros, count, batch]
         self._grad: Dict[int, List[float]] = {}  # layer -> [sum |g|, count]

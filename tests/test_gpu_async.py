@@ -180,7 +180,7 @@ def test_training_async_equals_sync(gpu_lib):
     from paper_2011_09017_b200.training import AdaptiveCompression
     torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
 
-    def run(async_compress, side_stream=False, hw=32, prefetch=False):
+    def run(async_compress, side_stream=False, hw=32, prefetch=False, two_lanes=False):
         torch.manual_seed(3)
         net = nn.Sequential(nn.Conv2d(3, 16, 3, padding=1), nn.ReLU(inplace=True),
                             nn.Conv2d(16, 32, 3, padding=1), nn.ReLU(inplace=True),
@@ -193,7 +193,7 @@ def test_training_async_equals_sync(gpu_lib):
                           generator=torch.Generator("cuda").manual_seed(2))
         ac = AdaptiveCompression(net, opt, ControllerConfig(collect_interval=2),
                                  async_compress=async_compress, side_stream=side_stream,
-                                 prefetch=prefetch)
+                                 prefetch=prefetch, two_lanes=two_lanes)
         losses = []
         for it in range(7):
             opt.zero_grad(set_to_none=True)
@@ -218,7 +218,7 @@ def test_training_async_equals_sync(gpu_lib):
     # 128x128 inputs: the first conv's input goes to the second compress lane (its own
     # context and stream), the rest to the first; unwraps settle out of wrap order
     l3, w3, c3 = run(False, hw=128)
-    l4, w4, c4 = run(True, side_stream=True, hw=128, prefetch=True)
+    l4, w4, c4 = run(True, side_stream=True, hw=128, prefetch=True, two_lanes=True)
     assert l3 == l4 and all(torch.equal(a, b) for a, b in zip(w3, w4))
     assert c3.ledger.to_csv() == c4.ledger.to_csv()
     assert c4._lanes[0] is not None and c4._lanes[1] is not None

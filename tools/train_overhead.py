@@ -39,7 +39,8 @@ for compress, asy, side in ((False, False, False), (True, False, False), (True, 
     ac = AdaptiveCompression(model, opt, ControllerConfig(collect_interval=4),
                              async_compress=asy, side_stream=side,
                              max_pending=int(os.environ.get("MAXP", 4)),
-                             prefetch=os.environ.get("PREFETCH", "0") == "1") if compress else None
+                             prefetch=os.environ.get("PREFETCH", "0") == "1",
+                             two_lanes=os.environ.get("LANES", "2") == "2") if compress else None
     res = []
     for it in range(12):
         if it == 6:
